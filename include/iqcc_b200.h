@@ -1,0 +1,171 @@
+/* iqcc_b200.h — C-ABI of the B200 engine for the iQCC dressing hot path
+ * (arXiv 2603.08883).  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * The reference (/root/reference/proj, header-only C++20) has no FFI; its
+ * boundary is the C++ API in namespace iqcc.  Each entry point below names
+ * the reference function it replaces.  The C++ shim
+ * include/iqcc_b200/iqcc_gpu.hpp re-exposes these with the reference's exact
+ * signatures (iqcc::gpu::dress_single, ...), rethrowing the same exception
+ * types from the status codes.
+ *
+ * Host data layout at this boundary is the reference's PauliSum storage
+ * (iqcc/pauli.hpp:373-377): rows [M][2B] uint64 (x blocks then z blocks,
+ * bit j%64 of block j/64 = qubit j), coefficients [M][2] double (re, im),
+ * canonical order (iqcc/pauli.hpp:146-161), duplicate free.  Coefficients
+ * must be real (im == 0): JW Hamiltonians and everything dressing produces
+ * from them are; nonzero im is rejected with
+ * IQCC_EINVAL rather than silently dropped.
+ *
+ * Device layout: per sum one array of key rows [M][2B]
+ * uint64 holding the bit-REVERSED words (so canonical order is plain
+ * lexicographic unsigned order) and one fp64 coefficient array [M].
+ *
+ * Status codes: 0 ok; IQCC_EINVAL ~ std::invalid_argument;
+ * IQCC_ERUNTIME ~ std::runtime_error; IQCC_ECUDA / IQCC_ENOMEM device errors.
+ * iqcc_gpu_last_error() returns the message of the last failure on the
+ * calling thread.  Handles are not thread safe; one host thread per device.
+ */
+#ifndef IQCC_B200_H
+#define IQCC_B200_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  IQCC_OK = 0,
+  IQCC_EINVAL = 1,
+  IQCC_ERUNTIME = 2,
+  IQCC_ECUDA = 3,
+  IQCC_ENOMEM = 4
+};
+
+typedef struct iqcc_gpu_sum iqcc_gpu_sum;
+
+/* ---- engine ---------------------------------------------------------- */
+const char* iqcc_gpu_last_error(void);
+/* Binds the calling thread to `device` and creates the engine context. */
+int iqcc_gpu_init(int device);
+/* Run all engine work on an existing cudaStream_t (e.g. torch's current
+ * stream) instead of the engine's own; NULL restores the default. */
+int iqcc_gpu_set_stream(void* cuda_stream);
+int iqcc_gpu_finalize(void);
+/* Number of engine kernel launches so far (bench.py's gpu_launches). */
+uint64_t iqcc_gpu_launch_count(void);
+/* Per-kernel CUDA-event timing (off by default): enable, then query the
+ * accumulated milliseconds and launch count of a kernel family by name
+ * ("merge", "classify", "rank", "partition", "select", "expect", ...). */
+int iqcc_gpu_profile_enable(int on);
+int iqcc_gpu_profile_get(const char* name, double* total_ms, uint64_t* launches);
+int iqcc_gpu_profile_reset(void);
+
+/* ---- sums (replace iqcc::PauliSum storage, iqcc/pauli.hpp:245-378) ---- */
+/* Upload a canonical real PauliSum from HOST buffers (reference layout). */
+int iqcc_gpu_sum_create(size_t n_qubits, const uint64_t* rows, const double* coeff, size_t M,
+                        iqcc_gpu_sum** out);
+/* Same, from DEVICE buffers in the reference layout. */
+int iqcc_gpu_sum_create_device(size_t n_qubits, const uint64_t* d_rows, const double* d_coeff,
+                               size_t M, iqcc_gpu_sum** out);
+/* Synthetic G_mol(n, n_terms, seed) built on the device (
+ * generator in paper_2603_08883_b200/csrc/gen_mol.h).  Bench input only. */
+int iqcc_gpu_sum_generate_mol(size_t n_qubits, size_t n_terms, uint64_t seed, iqcc_gpu_sum** out);
+int iqcc_gpu_sum_clone(const iqcc_gpu_sum* h, iqcc_gpu_sum** out);
+int iqcc_gpu_sum_destroy(iqcc_gpu_sum* h);
+int iqcc_gpu_sum_qubits(const iqcc_gpu_sum* h, size_t* n_qubits);
+/* Logical term count (PauliSum::size). */
+int iqcc_gpu_sum_size(iqcc_gpu_sum* h, size_t* M);
+/* Download in canonical order into HOST buffers of capacity `cap` terms
+ * (rows [cap][2B], coeff [cap][2]); *M receives the term count. */
+int iqcc_gpu_sum_download(iqcc_gpu_sum* h, uint64_t* rows, double* coeff, size_t cap, size_t* M);
+/* Same into DEVICE buffers. */
+int iqcc_gpu_sum_download_device(iqcc_gpu_sum* h, uint64_t* d_rows, double* d_coeff, size_t cap,
+                                 size_t* M);
+
+/* ---- dressing (iqcc/dressing.hpp) ------------------------------------- */
+typedef struct {
+  size_t n_in;             /* logical terms before the step */
+  size_t n_anticommuting;  /* terms whose product was generated */
+  size_t n_out;            /* logical terms after the step (and compress) */
+} iqcc_dress_stats;
+
+typedef struct {
+  size_t dropped_terms;   /* CompressStats, iqcc/pauli.hpp:417-420 */
+  double dropped_weight;
+} iqcc_compress_stats;
+
+/* In place H <- dress_single(H, {gen, tau}, {drop_thr, ...})
+ * (iqcc/dressing.hpp:197-220).  cos_tau/sin_tau are std::cos/std::sin of
+ * the amplitude evaluated by the HOST (glibc) so coefficients are
+ * bit-identical to the reference.  gen: one row [2B]; identity -> EINVAL. */
+int iqcc_gpu_dress(iqcc_gpu_sum* h, const uint64_t* gen, double cos_tau, double sin_tau,
+                   double drop_thr, iqcc_dress_stats* stats);
+/* In place H <- compress(H, eps, max_terms) (iqcc/pauli.hpp:425-474). */
+int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compress_stats* stats);
+/* In place dress_sequence (iqcc/dressing.hpp:311-324): K entanglers in
+ * order, compress(eps, max_terms) after each step when eps > 0 or the size
+ * exceeds max_terms.  gens [K][2B]. */
+int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
+                            const double* sin_tau, double eps, size_t max_terms,
+                            iqcc_compress_stats* stats);
+/* growth_split (iqcc/dressing.hpp:41-50). */
+int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* n_commuting,
+                          size_t* n_anticommuting);
+
+/* ---- QMF energy / gradient, DIS (iqcc/qmf.hpp, iqcc/dis.hpp) ----------- */
+/* factors [n][3] = per qubit (X, Z, Y) single-qubit expectations evaluated
+ * on the host exactly as qmf_factor (iqcc/qmf.hpp:56-61). */
+int iqcc_gpu_expect(iqcc_gpu_sum* h, const double* factors, double* energy);
+/* qmf_energy_gradient (iqcc/qmf.hpp:94-148).  derivs [n][6] =
+ * (dth_X, dph_X, dth_Z, dph_Z, dth_Y, dph_Y) from the host's sin/cos.
+ * grad receives 2n values (theta block then phi block). */
+int iqcc_gpu_qmf_energy_gradient(iqcc_gpu_sum* h, const double* factors, const double* derivs,
+                                 double* energy, double* grad);
+/* gradient (iqcc/dis.hpp:39-52) for K candidate generators [K][2B];
+ * flip_group_only != 0 restricts each sum to the candidate's flip group
+ * (group_gradient, iqcc/dis.hpp:121-132, exact at poles). */
+int iqcc_gpu_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* cands, size_t K,
+                       int flip_group_only, double* g);
+/* dis_candidates (iqcc/dis.hpp:140-191) without the optional seeded
+ * shuffle (applied by the shim on the host with the same mt19937_64).
+ * Writes up to `cap` picks sorted by (|g| desc, canonical); *n_picks gets
+ * the total before truncation to top_k. */
+int iqcc_gpu_dis_candidates(iqcc_gpu_sum* h, const double* factors, int at_poles, size_t top_k,
+                            double screen_thr, size_t per_group_cap, uint64_t* rows_out,
+                            double* g_out, size_t cap, size_t* n_picks);
+
+/* ---- bit-wise partitioning across GPUs (iqcc/partition.hpp) ------------ */
+/* choose_partition_bits (iqcc/partition.hpp:52-108) computed on the device. */
+int iqcc_gpu_choose_partition_bits(iqcc_gpu_sum* h, size_t m, size_t* bits_out,
+                                   double* imbalance);
+/* Keep only terms whose partition key (gather of `bits`) is owned by
+ * `rank` under owner[2^m] (distribute, iqcc/partition.hpp:208-220). */
+int iqcc_gpu_sum_restrict(iqcc_gpu_sum* h, size_t m, const size_t* bits, const size_t* owner,
+                          int rank);
+/* NCCL: 128-byte ncclUniqueId from rank 0, then every rank joins. */
+int iqcc_gpu_nccl_unique_id(void* out128);
+int iqcc_gpu_comm_init(const void* uid128, int rank, int world);
+int iqcc_gpu_comm_destroy(void);
+typedef struct {
+  size_t mask;            /* entangler key on the partition bits */
+  size_t sent_terms;      /* products shipped to the partner rank */
+  size_t recv_terms;
+  size_t bytes_wire;      /* sent_terms * (16B + 8) device wire bytes */
+  size_t bytes_reference; /* sent_terms * (16 + 16B), MessageLog formula */
+} iqcc_exchange_stats;
+/* One parallel_dress step (iqcc/partition.hpp:398-452) over the
+ * communicator: local products whose key flips route to the rank owning
+ * key ^ mask; compress_partitioned semantics (:325-396) across ranks. */
+int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const size_t* owner,
+                            const uint64_t* gen, double cos_tau, double sin_tau, double eps,
+                            size_t max_terms, iqcc_exchange_stats* xstats,
+                            iqcc_compress_stats* cstats);
+/* Partitioned energy: local expect + allreduce (parallel_expect, :241-254). */
+int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* energy);
+/* Total logical terms over all ranks. */
+int iqcc_gpu_parallel_size(iqcc_gpu_sum* h, size_t* total);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,526 @@
+// capi.cu — engine context (device, stream, scratch, profiling) and the
+// extern "C" entry points declared in include/iqcc_b200.h.
+//
+// Every entry point catches C++ exceptions and maps them onto status codes:
+// std::invalid_argument -> IQCC_EINVAL (the reference throws
+// std::invalid_argument for precondition violations),
+// std::runtime_error -> IQCC_ERUNTIME, CUDA failures -> IQCC_ECUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/iqcc_b200.h"
+#include "engine.cuh"
+#include "multi.cuh"
+
+namespace iqcc_b200 {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct ProfileEntry {
+  double ms = 0.0;
+  uint64_t launches = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+
+struct Ctx {
+  int device = -1;
+  cudaStream_t own = nullptr;
+  cudaStream_t cur = nullptr;
+  Workspace ws;
+  uint64_t launches = 0;
+  bool profiling = false;
+  std::map<std::string, ProfileEntry> prof;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+static Ctx* g_ctx = nullptr;
+static thread_local std::string g_err;
+
+Ctx& ctx() {
+  if (!g_ctx) throw std::runtime_error("iqcc_gpu_init has not been called");
+  return *g_ctx;
+}
+cudaStream_t stream() { return ctx().cur; }
+Workspace& workspace() { return ctx().ws; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what);
+}
+
+void count_launch(const char* family) {
+  Ctx& c = ctx();
+  ++c.launches;
+  (void)family;
+}
+
+static cudaEvent_t take_event() {
+  Ctx& c = ctx();
+  if (!c.event_pool.empty()) {
+    cudaEvent_t e = c.event_pool.back();
+    c.event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  IQCC_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+KernelScope::KernelScope(const char* f) : family(f) {
+  Ctx& c = ctx();
+  ++c.launches;
+  if (c.profiling) {
+    a = take_event();
+    b = take_event();
+    IQCC_CUDA(cudaEventRecord(a, c.cur));
+  }
+}
+
+KernelScope::~KernelScope() {
+  Ctx& c = ctx();
+  cudaError_t le = cudaPeekAtLastError();
+  if (a) {
+    cudaEventRecord(b, c.cur);
+    auto& e = c.prof[family];
+    e.launches += 1;
+    e.pending.push_back({a, b});
+  }
+  if (le != cudaSuccess) {
+    // surfaced by the next IQCC_CUDA check; keep the error sticky for the caller
+    g_err = std::string("kernel launch failed (") + family + "): " + cudaGetErrorString(le);
+  }
+}
+
+static void profile_flush() {
+  Ctx& c = ctx();
+  for (auto& [name, e] : c.prof) {
+    for (auto& pr : e.pending) {
+      IQCC_CUDA(cudaEventSynchronize(pr.second));
+      float ms = 0.f;
+      IQCC_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      e.ms += ms;
+      c.event_pool.push_back(pr.first);
+      c.event_pool.push_back(pr.second);
+    }
+    e.pending.clear();
+  }
+}
+
+void* DevBuf::get(size_t n) {
+  if (n <= bytes && p) return p;
+  cudaStream_t st = stream();
+  if (p) IQCC_CUDA(cudaFreeAsync(p, st));
+  p = nullptr;
+  size_t want = std::max<size_t>(n + n / 8, 256);
+  cudaError_t e = cudaMallocAsync(&p, want, st);
+  if (e != cudaSuccess) {
+    // retry without slack once the pool has released cached blocks
+    cudaGetLastError();
+    IQCC_CUDA(cudaStreamSynchronize(st));
+    cudaMemPool_t pool;
+    IQCC_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx().device));
+    cudaMemPoolTrimTo(pool, 0);
+    want = std::max<size_t>(n, 256);
+    e = cudaMallocAsync(&p, want, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      bytes = 0;
+      throw std::bad_alloc();
+    }
+  }
+  bytes = want;
+  return p;
+}
+
+void DevBuf::release() {
+  if (p && g_ctx) cudaFreeAsync(p, g_ctx->cur);
+  p = nullptr;
+  bytes = 0;
+}
+
+void Workspace::release_all() {
+  DevBuf* all[] = {&lcp, &mbits, &fmask, &tile_cnt, &tile_pfx, &fwd_agg, &bwd_agg, &fwd_carry,
+                   &bwd_carry, &inv_perm, &rdelta, &part_a, &part_b, &tile_status, &counters,
+                   &hist, &cand_v, &cand_i, &levels, &stage_rows, &stage_coef, &partials,
+                   &grad_part, &tables, &misc, &misc2, &misc3, &xbuf_keys, &xbuf_coef,
+                   &rbuf_keys, &rbuf_coef, &out_keys, &out_coef};
+  for (DevBuf* b : all) b->release();
+}
+
+}  // namespace iqcc_b200
+
+using namespace iqcc_b200;
+
+struct iqcc_gpu_sum {
+  DeviceStore s;
+};
+
+namespace {
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return IQCC_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(IQCC_EINVAL, e.what());
+  } catch (const CudaError& e) {
+    return fail(IQCC_ECUDA, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(IQCC_ENOMEM, "device out of memory");
+  } catch (const std::exception& e) {
+    return fail(IQCC_ERUNTIME, e.what());
+  }
+}
+
+uint32_t ref_blocks(const DeviceStore& s) { return s.n_qubits == 0 ? 1 : (s.n_qubits + 63) / 64; }
+
+/// Reference-layout row (B_ref blocks per plane) -> device-width row.
+std::vector<uint64_t> widen_row(const uint64_t* row, uint32_t Bref, uint32_t B) {
+  std::vector<uint64_t> r(2 * B, 0);
+  for (uint32_t w = 0; w < Bref; ++w) {
+    r[w] = row[w];
+    r[B + w] = row[Bref + w];
+  }
+  return r;
+}
+
+bool row_is_identity(const uint64_t* row, uint32_t Bref) {
+  for (uint32_t w = 0; w < 2 * Bref; ++w)
+    if (row[w]) return false;
+  return true;
+}
+
+void need(const iqcc_gpu_sum* h) {
+  if (!h) throw std::invalid_argument("null sum handle");
+}
+
+}  // namespace
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* iqcc_gpu_last_error(void) { return g_err.c_str(); }
+
+int iqcc_gpu_init(int device) {
+  return guarded([&] {
+    if (g_ctx && g_ctx->device == device) return;
+    if (g_ctx) throw std::invalid_argument("engine already initialised on another device");
+    IQCC_CUDA(cudaSetDevice(device));
+    auto* c = new Ctx();
+    c->device = device;
+    IQCC_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->cur = c->own;
+    cudaMemPool_t pool;
+    IQCC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    IQCC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_ctx = c;
+  });
+}
+
+int iqcc_gpu_set_stream(void* s) {
+  return guarded([&] {
+    Ctx& c = ctx();
+    IQCC_CUDA(cudaStreamSynchronize(c.cur));
+    c.cur = s ? static_cast<cudaStream_t>(s) : c.own;
+  });
+}
+
+int iqcc_gpu_finalize(void) {
+  return guarded([&] {
+    if (!g_ctx) return;
+    cudaStreamSynchronize(g_ctx->cur);
+    multi_shutdown();
+    g_ctx->ws.release_all();
+    cudaStreamSynchronize(g_ctx->cur);
+    cudaStreamDestroy(g_ctx->own);
+    delete g_ctx;
+    g_ctx = nullptr;
+  });
+}
+
+uint64_t iqcc_gpu_launch_count(void) { return g_ctx ? g_ctx->launches : 0; }
+
+int iqcc_gpu_profile_enable(int on) {
+  return guarded([&] { ctx().profiling = on != 0; });
+}
+
+int iqcc_gpu_profile_get(const char* name, double* total_ms, uint64_t* launches) {
+  return guarded([&] {
+    profile_flush();
+    auto& p = ctx().prof;
+    auto it = p.find(name);
+    *total_ms = it == p.end() ? 0.0 : it->second.ms;
+    *launches = it == p.end() ? 0 : it->second.launches;
+  });
+}
+
+int iqcc_gpu_profile_reset(void) {
+  return guarded([&] {
+    profile_flush();
+    ctx().prof.clear();
+  });
+}
+
+int iqcc_gpu_sum_create(size_t n_qubits, const uint64_t* rows, const double* coeff, size_t M,
+                        iqcc_gpu_sum** out) {
+  return guarded([&] {
+    ctx();
+    auto h = std::make_unique<iqcc_gpu_sum>();
+    store_upload(h->s, n_qubits, rows, coeff, M, true);
+    *out = h.release();
+  });
+}
+
+int iqcc_gpu_sum_create_device(size_t n_qubits, const uint64_t* rows, const double* coeff, size_t M,
+                               iqcc_gpu_sum** out) {
+  return guarded([&] {
+    ctx();
+    auto h = std::make_unique<iqcc_gpu_sum>();
+    store_upload(h->s, n_qubits, rows, coeff, M, false);
+    *out = h.release();
+  });
+}
+
+int iqcc_gpu_sum_generate_mol(size_t n_qubits, size_t n_terms, uint64_t seed, iqcc_gpu_sum** out) {
+  return guarded([&] {
+    ctx();
+    auto h = std::make_unique<iqcc_gpu_sum>();
+    store_generate_mol(h->s, n_qubits, n_terms, seed);
+    *out = h.release();
+  });
+}
+
+int iqcc_gpu_sum_clone(const iqcc_gpu_sum* h, iqcc_gpu_sum** out) {
+  return guarded([&] {
+    need(h);
+    auto c = std::make_unique<iqcc_gpu_sum>();
+    store_clone(h->s, c->s);
+    *out = c.release();
+  });
+}
+
+int iqcc_gpu_sum_destroy(iqcc_gpu_sum* h) {
+  return guarded([&] {
+    if (!h) return;
+    if (g_ctx) h->s.free_all();
+    delete h;
+  });
+}
+
+int iqcc_gpu_sum_qubits(const iqcc_gpu_sum* h, size_t* n) {
+  return guarded([&] {
+    need(h);
+    *n = h->s.n_qubits;
+  });
+}
+
+int iqcc_gpu_sum_size(iqcc_gpu_sum* h, size_t* M) {
+  return guarded([&] {
+    need(h);
+    *M = h->s.logical;
+  });
+}
+
+int iqcc_gpu_sum_download(iqcc_gpu_sum* h, uint64_t* rows, double* coeff, size_t cap, size_t* M) {
+  return guarded([&] {
+    need(h);
+    *M = store_download(h->s, rows, coeff, cap, true);
+  });
+}
+
+int iqcc_gpu_sum_download_device(iqcc_gpu_sum* h, uint64_t* rows, double* coeff, size_t cap,
+                                 size_t* M) {
+  return guarded([&] {
+    need(h);
+    *M = store_download(h->s, rows, coeff, cap, false);
+  });
+}
+
+int iqcc_gpu_dress(iqcc_gpu_sum* h, const uint64_t* gen, double cos_tau, double sin_tau,
+                   double drop_thr, iqcc_dress_stats* stats) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    if (row_is_identity(gen, Bref)) throw std::invalid_argument("dress_single: identity generator");
+    auto row = widen_row(gen, Bref, h->s.B);
+    const size_t n_in = h->s.logical;
+    DressOutcome o = dress_step(h->s, row.data(), cos_tau, sin_tau, drop_thr, false, 0.0);
+    if (stats) {
+      stats->n_in = n_in;
+      stats->n_anticommuting = o.n_anticommuting;
+      stats->n_out = h->s.logical;
+    }
+  });
+}
+
+int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compress_stats* stats) {
+  return guarded([&] {
+    need(h);
+    CompressResult r = compress_store(h->s, eps, max_terms, false, 0, stats != nullptr);
+    if (stats) {
+      stats->dropped_terms += r.dropped_terms;
+      stats->dropped_weight += r.dropped_weight;
+    }
+  });
+}
+
+int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
+                            const double* sin_tau, double eps, size_t max_terms,
+                            iqcc_compress_stats* stats) {
+  return guarded([&] {
+    need(h);
+    if (max_terms < 1) throw std::invalid_argument("dress_sequence: max_terms < 1");
+    const uint32_t Bref = ref_blocks(h->s);
+    for (size_t k = 0; k < K; ++k)
+      if (row_is_identity(gens + k * 2 * Bref, Bref))
+        throw std::invalid_argument("dress_single: identity generator");
+    for (size_t k = 0; k < K; ++k) {
+      auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
+      const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
+      DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps);
+      if (eps > 0.0 || h->s.logical > max_terms) {
+        CompressResult r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr);
+        if (stats) {
+          stats->dropped_terms += r.dropped_terms;
+          stats->dropped_weight += r.dropped_weight;
+        }
+      }
+    }
+  });
+}
+
+int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* nc, size_t* na) {
+  return guarded([&] {
+    need(h);
+    auto row = widen_row(gen, ref_blocks(h->s), h->s.B);
+    growth_split(h->s, row.data(), nc, na);
+  });
+}
+
+int iqcc_gpu_expect(iqcc_gpu_sum* h, const double* factors, double* energy) {
+  return guarded([&] {
+    need(h);
+    *energy = expect_store(h->s, factors);
+  });
+}
+
+int iqcc_gpu_qmf_energy_gradient(iqcc_gpu_sum* h, const double* factors, const double* derivs,
+                                 double* energy, double* grad) {
+  return guarded([&] {
+    need(h);
+    *energy = qmf_grad_store(h->s, factors, derivs, grad);
+  });
+}
+
+int iqcc_gpu_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* cands, size_t K,
+                       int flip_group_only, double* g) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    std::vector<uint64_t> wide(K * 2 * h->s.B);
+    for (size_t k = 0; k < K; ++k) {
+      auto r = widen_row(cands + k * 2 * Bref, Bref, h->s.B);
+      std::copy(r.begin(), r.end(), wide.begin() + k * 2 * h->s.B);
+    }
+    gradients_store(h->s, factors, wide.data(), K, flip_group_only != 0, g);
+  });
+}
+
+int iqcc_gpu_dis_candidates(iqcc_gpu_sum* h, const double* factors, int at_poles, size_t top_k,
+                            double screen_thr, size_t per_group_cap, uint64_t* rows_out,
+                            double* g_out, size_t cap, size_t* n_picks) {
+  return guarded([&] {
+    need(h);
+    if (top_k < 1) throw std::invalid_argument("dis_candidates: top_k < 1");
+    std::vector<uint64_t> rows;
+    std::vector<double> g;
+    size_t n = dis_store(h->s, factors, at_poles != 0, top_k, screen_thr, per_group_cap, rows, g);
+    const uint32_t Bref = ref_blocks(h->s), B = h->s.B;
+    const size_t w = std::min(cap, std::min(n, top_k));
+    for (size_t i = 0; i < w; ++i) {
+      for (uint32_t b = 0; b < Bref; ++b) {
+        rows_out[i * 2 * Bref + b] = rows[i * 2 * B + b];
+        rows_out[i * 2 * Bref + Bref + b] = rows[i * 2 * B + B + b];
+      }
+      g_out[i] = g[i];
+    }
+    *n_picks = n;
+  });
+}
+
+int iqcc_gpu_choose_partition_bits(iqcc_gpu_sum* h, size_t m, size_t* bits_out, double* imbalance) {
+  return guarded([&] {
+    need(h);
+    *imbalance = choose_bits_store(h->s, m, bits_out);
+  });
+}
+
+int iqcc_gpu_sum_restrict(iqcc_gpu_sum* h, size_t m, const size_t* bits, const size_t* owner,
+                          int rank) {
+  return guarded([&] {
+    need(h);
+    restrict_store(h->s, m, bits, owner, rank);
+  });
+}
+
+int iqcc_gpu_nccl_unique_id(void* out128) {
+  return guarded([&] { multi_unique_id(out128); });
+}
+
+int iqcc_gpu_comm_init(const void* uid, int rank, int world) {
+  return guarded([&] {
+    ctx();
+    multi_init(uid, rank, world);
+  });
+}
+
+int iqcc_gpu_comm_destroy(void) {
+  return guarded([&] { multi_shutdown(); });
+}
+
+int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const size_t* owner,
+                            const uint64_t* gen, double cos_tau, double sin_tau, double eps,
+                            size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    if (row_is_identity(gen, Bref)) throw std::invalid_argument("parallel_dress: identity generator");
+    if (max_terms < 1) throw std::invalid_argument("compress_partitioned: max_terms < 1");
+    auto row = widen_row(gen, Bref, h->s.B);
+    parallel_dress_step(h->s, m, bits, owner, row.data(), cos_tau, sin_tau, eps, max_terms, xs, cs);
+  });
+}
+
+int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* energy) {
+  return guarded([&] {
+    need(h);
+    *energy = parallel_expect_store(h->s, factors);
+  });
+}
+
+int iqcc_gpu_parallel_size(iqcc_gpu_sum* h, size_t* total) {
+  return guarded([&] {
+    need(h);
+    *total = parallel_size(h->s);
+  });
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,353 @@
+// engine.cuh — shared device helpers and host context of the B200 iQCC engine.
+//
+// Device term store (one per sum / shard): key rows [M][2B] uint64 holding the
+// BIT-REVERSED words of the reference row (x blocks then z blocks,
+// iqcc/pauli.hpp:373-377), and coef [M] fp64 (real part).
+// Bit reversal maps the reference's canonical order (iqcc/pauli.hpp:146-161:
+// lowest differing bit most significant, x plane first) onto plain
+// lexicographic unsigned order of the rows, so comparisons are word compares
+// and the first differing canonical position is 64*w + clz(a^b).
+// popcount-based algebra (commutation, product phase) is invariant under the
+// reversal.  Rows are 16/32/64 B for B = 1/2/4, loaded as 128-bit vectors;
+// a random access to a 124-qubit row touches exactly one 32 B sector.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+namespace iqcc_b200 {
+
+typedef unsigned long long ull;
+
+constexpr int kMaxB = 4;        // up to 256 qubits
+constexpr int kLevelsPerChunk = 8;
+constexpr int kThrPerChunk = 2 * kLevelsPerChunk;
+
+template <int B>
+struct Key {
+  ull w[2 * B];
+};
+
+template <int B>
+__device__ __forceinline__ Key<B> load_key(const ull* __restrict__ keys, size_t i) {
+  Key<B> k;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(keys + i * (2 * B));
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    ulonglong2 v = __ldg(p + j);
+    k.w[2 * j] = v.x;
+    k.w[2 * j + 1] = v.y;
+  }
+  return k;
+}
+
+template <int B>
+__device__ __forceinline__ void store_key(ull* __restrict__ keys, size_t i, const Key<B>& k) {
+  ulonglong2* p = reinterpret_cast<ulonglong2*>(keys + i * (2 * B));
+#pragma unroll
+  for (int j = 0; j < B; ++j) p[j] = make_ulonglong2(k.w[2 * j], k.w[2 * j + 1]);
+}
+
+template <int B>
+__device__ __forceinline__ int key_cmp(const Key<B>& a, const Key<B>& b) {
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w)
+    if (a.w[w] != b.w[w]) return a.w[w] < b.w[w] ? -1 : 1;
+  return 0;
+}
+
+template <int B>
+__device__ __forceinline__ bool key_is_identity(const Key<B>& a) {
+  ull o = 0;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) o |= a.w[w];
+  return o == 0;
+}
+
+/// First differing canonical position (0 = x bit of qubit 0), or 0x7fff when equal.
+template <int B>
+__device__ __forceinline__ int key_lcp(const Key<B>& a, const Key<B>& b) {
+  int r = 0x7fff;
+#pragma unroll
+  for (int w = 2 * B - 1; w >= 0; --w) {
+    ull d = a.w[w] ^ b.w[w];
+    if (d) r = 64 * w + __clzll((long long)d);
+  }
+  return r;
+}
+
+/// Symplectic product parity (commutes, iqcc/pauli.hpp:188-193): 1 = anticommute.
+template <int B>
+__device__ __forceinline__ int anticommutes(const Key<B>& k, const Key<B>& p) {
+  int s = 0;
+#pragma unroll
+  for (int b = 0; b < B; ++b) s += __popcll((k.w[b] & p.w[B + b]) ^ (k.w[B + b] & p.w[b]));
+  return s & 1;
+}
+
+/// Phase exponent t of k*p = i^t (k^p) (multiply_into, iqcc/pauli.hpp:202-215), mod 4.
+template <int B>
+__device__ __forceinline__ int product_phase(const Key<B>& k, const Key<B>& p) {
+  int t = 0;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    ull kx = k.w[b], kz = k.w[B + b], px = p.w[b], pz = p.w[B + b];
+    t += __popcll(kx & kz) + __popcll(px & pz) - __popcll((kx ^ px) & (kz ^ pz)) +
+         2 * __popcll(kz & px);
+  }
+  return t & 3;
+}
+
+template <int B>
+__device__ __forceinline__ Key<B> key_xor(const Key<B>& a, const Key<B>& b) {
+  Key<B> r;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) r.w[w] = a.w[w] ^ b.w[w];
+  return r;
+}
+
+/// Bit at canonical position pos (0 .. 128B-1).
+template <int B>
+__device__ __forceinline__ unsigned key_bit(const Key<B>& k, int pos) {
+  int w = pos >> 6;
+  ull v = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * B; ++j) v = (j == w) ? k.w[j] : v;
+  return (unsigned)(v >> (63 - (pos & 63))) & 1u;
+}
+
+/// Lazy compress filter attached to a store (compress, iqcc/pauli.hpp:425-474):
+/// keep(i) = identity || !active || (|c| >= eps && (!has_v || |c| > v ||
+/// (|c| == v && i <= cut))).  |c| of a real coefficient is std::abs(complex)
+/// exactly (hypot(re, 0) == |re|).
+struct Filter {
+  int active = 0;
+  int has_v = 0;
+  double eps = 0.0;
+  double v = 0.0;
+  ull cut = 0;
+};
+
+__device__ __forceinline__ bool filter_keep(const Filter& f, size_t i, double c, bool identity) {
+  if (identity || !f.active) return true;
+  double a = fabs(c);
+  if (!(a >= f.eps)) return false;
+  if (!f.has_v) return true;
+  return a > f.v || (a == f.v && (ull)i <= f.cut);
+}
+
+/// keep_term (iqcc/pauli.hpp:180-184) for a real coefficient.
+__device__ __forceinline__ bool keep_term(double c, bool identity, double thr) {
+  if (identity) return true;
+  if (c == 0.0) return false;
+  return fabs(c) >= thr;
+}
+
+// ---------------------------------------------------------------- scans
+template <class T, class Op>
+__device__ __forceinline__ T warp_inclusive(T v, Op op) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = op(n, v);
+  }
+  return v;
+}
+
+template <class T, class Op>
+__device__ __forceinline__ T warp_inclusive_rev(T v, Op op) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_down_sync(0xffffffffu, v, o);
+    if (lane + o < 32) v = op(v, n);
+  }
+  return v;
+}
+
+/// Block-wide exclusive scan (NT threads, NT % 32 == 0); `scratch` holds NT/32+1 T.
+template <int NT, class T, class Op>
+__device__ __forceinline__ T block_exclusive(T v, T identity, Op op, T* scratch, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = warp_inclusive(v, op);
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < NT / 32 ? scratch[lane] : identity;
+    T si = warp_inclusive(s, op);
+    if (lane < NT / 32) scratch[lane] = si;
+  }
+  __syncthreads();
+  T base = warp > 0 ? scratch[warp - 1] : identity;
+  T excl_in_warp = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) excl_in_warp = identity;
+  T out = op(base, excl_in_warp);
+  if (total) *total = scratch[NT / 32 - 1];
+  __syncthreads();
+  return out;
+}
+
+/// Block-wide exclusive scan from the right (thread NT-1 first).
+template <int NT, class T, class Op>
+__device__ __forceinline__ T block_exclusive_rev(T v, T identity, Op op, T* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = warp_inclusive_rev(v, op);
+  if (lane == 0) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < NT / 32 ? scratch[lane] : identity;
+    // reverse inclusive over warps: combine with higher warp ids
+    T si = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      T n = __shfl_down_sync(0xffffffffu, si, o);
+      if (lane + o < NT / 32) si = op(si, n);
+    }
+    if (lane < NT / 32) scratch[lane] = si;
+  }
+  __syncthreads();
+  T base = warp + 1 < NT / 32 ? scratch[warp + 1] : identity;
+  T excl_in_warp = __shfl_down_sync(0xffffffffu, inc, 1);
+  if (lane == 31) excl_in_warp = identity;
+  T out = op(excl_in_warp, base);
+  __syncthreads();
+  return out;
+}
+
+struct OpAdd {
+  template <class T>
+  __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
+};
+struct OpMax {
+  __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+  __device__ __forceinline__ long long operator()(long long a, long long b) const { return a > b ? a : b; }
+};
+struct OpMin {
+  __device__ __forceinline__ int operator()(int a, int b) const { return a < b ? a : b; }
+  __device__ __forceinline__ long long operator()(long long a, long long b) const { return a < b ? a : b; }
+};
+
+/// Decoupled look-back (single-pass prefix over tiles processed in
+/// dynamic-id order).  status[t]: bits 63:62 = 0 invalid / 1 aggregate /
+/// 2 inclusive prefix, bits 61:0 = value.  Called by ONE thread per tile.
+__device__ __forceinline__ ull lookback_exclusive(ull* status, ull tile, ull agg) {
+  const ull AGG = 1ull << 62, PFX = 2ull << 62, VAL = (1ull << 62) - 1;
+  if (tile == 0) {
+    __threadfence();
+    atomicExch(status, PFX | agg);
+    return 0;
+  }
+  atomicExch(status + tile, AGG | agg);
+  __threadfence();
+  ull excl = 0;
+  long long p = (long long)tile - 1;
+  for (;;) {
+    ull v = atomicAdd(status + p, 0ull);
+    ull flag = v & ~VAL;
+    if (flag == 0) continue;
+    excl += v & VAL;
+    if (flag == PFX) break;
+    --p;
+  }
+  __threadfence();
+  atomicExch(status + tile, PFX | (excl + agg));
+  return excl;
+}
+
+// ---------------------------------------------------------------- host side
+struct Ctx;
+Ctx& ctx();
+cudaStream_t stream();
+void count_launch(const char* family);
+void check_cuda(cudaError_t e, const char* what);
+#define IQCC_CUDA(x) ::iqcc_b200::check_cuda((x), #x)
+
+/// Kernel-family timing scope (CUDA events on the engine stream) when
+/// profiling is enabled; always counts the launch.
+struct KernelScope {
+  const char* family;
+  cudaEvent_t a = nullptr, b = nullptr;
+  explicit KernelScope(const char* f);
+  ~KernelScope();
+};
+
+/// Grow-only device scratch buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t n);
+  template <class T>
+  T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+  void release();
+};
+
+struct Workspace {
+  DevBuf lcp, mbits, fmask, tile_cnt, tile_pfx, fwd_agg, bwd_agg, fwd_carry, bwd_carry;
+  DevBuf inv_perm, rdelta, part_a, part_b, tile_status, counters, hist, cand_v, cand_i;
+  DevBuf levels, stage_rows, stage_coef, partials, grad_part, tables, misc, misc2, misc3;
+  DevBuf xbuf_keys, xbuf_coef, rbuf_keys, rbuf_coef;
+  DevBuf out_keys, out_coef;  // double buffer swapped with the store after a step
+  void release_all();
+};
+Workspace& workspace();
+
+struct DeviceStore {
+  uint32_t n_qubits = 0, B = 1;
+  size_t M = 0;        // physical terms
+  DevBuf kbuf, cbuf;   // key rows [cap][2B], coef [cap]
+  Filter filt;         // lazy compress filter (see filter_keep)
+  size_t logical = 0;  // terms that pass filt
+  bool has_identity = false;
+  ull* keys() const { return static_cast<ull*>(kbuf.p); }
+  double* coef() const { return static_cast<double*>(cbuf.p); }
+  void ensure(size_t n);  // capacity >= n terms, contents NOT kept
+  void free_all() {
+    kbuf.release();
+    cbuf.release();
+  }
+};
+
+struct CompressResult {
+  size_t dropped_terms = 0;
+  double dropped_weight = 0.0;
+};
+
+// implemented in the .cu files
+void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const double* coeff,
+                  size_t M, bool host_src);
+size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap, bool host_dst);
+void store_generate_mol(DeviceStore& s, size_t n_qubits, size_t n_terms, uint64_t seed);
+void store_materialize(DeviceStore& s);
+void store_clone(const DeviceStore& src, DeviceStore& dst);
+
+struct DressOutcome {
+  size_t n_anticommuting = 0;
+  size_t count_eps = 0;  // emitted terms passing (identity || |c| >= eps)
+};
+/// One dressing step in place; if want_hist, also accumulates the |c|
+/// histogram of emitted terms for a following compress(eps).
+DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cos_tau, double sin_tau,
+                        double drop_thr, bool want_hist, double eps);
+/// Selects the compress filter on a store without a filter.  If hist_ready,
+/// the histogram/count_eps of the last dress_step are used.
+CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
+                              size_t count_eps, bool want_stats);
+void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* na);
+
+double expect_store(DeviceStore& s, const double* factors);
+double qmf_grad_store(DeviceStore& s, const double* factors, const double* derivs, double* grad);
+void gradients_store(DeviceStore& s, const double* factors, const uint64_t* cands, size_t K,
+                     bool flip_group_only, double* g);
+size_t dis_store(DeviceStore& s, const double* factors, bool poles, size_t top_k, double thr,
+                 size_t cap_per_group, std::vector<uint64_t>& rows_out, std::vector<double>& g_out);
+double choose_bits_store(DeviceStore& s, size_t m, size_t* bits_out);
+void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner, int rank);
+
+/// Reversed row conversion helpers (host).
+void row_to_device_key(const uint64_t* row, uint32_t B, ull* key);
+void device_key_to_row(const ull* key, uint32_t B, uint64_t* row);
+
+}  // namespace iqcc_b200

@@ -1,0 +1,15 @@
+// multi.cuh — bit-wise partitioning across GPUs (one process per GPU, NCCL).
+#pragma once
+#include "../../include/iqcc_b200.h"
+#include "engine.cuh"
+
+namespace iqcc_b200 {
+void multi_unique_id(void* out128);
+void multi_init(const void* uid128, int rank, int world);
+void multi_shutdown();
+void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner,
+                         const uint64_t* gen_row, double cs, double sn, double eps,
+                         size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out);
+double parallel_expect_store(DeviceStore& s, const double* factors);
+size_t parallel_size(DeviceStore& s);
+}  // namespace iqcc_b200

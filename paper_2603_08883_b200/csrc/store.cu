@@ -1,0 +1,672 @@
+// store.cu — device term store: upload/download in the reference layout,
+// lazy-filter compaction, synthetic G_mol generation, and compress().
+//
+// compress (iqcc/pauli.hpp:425-474) keeps the identity plus every |c| >= eps
+// and, when more than max_terms remain, the max_terms-1 (identity present)
+// largest |c| with canonical order (= store index order) breaking ties.  On
+// the device this is a radix select on the IEEE bit pattern of |c| (monotone
+// for non-negative doubles): a 4096-bin histogram of the top 12 bits (fused
+// into the merge kernel after a dressing step), a candidate gather of the
+// selected bin, 16-bit digit histograms down to the exact threshold value v,
+// and the index cut among the ties at v.  The result is a lazy Filter
+// (engine.cuh) applied by every later consumer, so no extra compaction pass
+// is spent on the hot path.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "engine.cuh"
+#include "gen_mol.h"
+
+namespace iqcc_b200 {
+
+constexpr int CT = 256;  // compaction threads
+constexpr int CI = 8;    // items per thread
+constexpr int CTILE = CT * CI;
+
+static inline unsigned long long brev_host(unsigned long long v) {
+  v = ((v >> 1) & 0x5555555555555555ull) | ((v & 0x5555555555555555ull) << 1);
+  v = ((v >> 2) & 0x3333333333333333ull) | ((v & 0x3333333333333333ull) << 2);
+  v = ((v >> 4) & 0x0F0F0F0F0F0F0F0Full) | ((v & 0x0F0F0F0F0F0F0F0Full) << 4);
+  return __builtin_bswap64(v);
+}
+
+void row_to_device_key(const uint64_t* row, uint32_t B, ull* key) {
+  for (uint32_t w = 0; w < 2 * B; ++w) key[w] = brev_host(row[w]);
+}
+void device_key_to_row(const ull* key, uint32_t B, uint64_t* row) {
+  for (uint32_t w = 0; w < 2 * B; ++w) row[w] = brev_host(key[w]);
+}
+
+void DeviceStore::ensure(size_t n) {
+  n = std::max<size_t>(n, 1);
+  kbuf.get(n * 2 * B * sizeof(ull));
+  cbuf.get(n * sizeof(double));
+}
+
+// ------------------------------------------------------------------ upload
+template <int B>
+__global__ void k_upload(const ull* __restrict__ rows, const double* __restrict__ coeff, size_t M,
+                         ull* __restrict__ keys, double* __restrict__ coef,
+                         ull* __restrict__ err /*[0]=first imag idx+1, [1]=first order idx+1*/) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  Key<B> k, p;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) k.w[w] = __brevll(rows[i * 2 * B + w]);
+  store_key<B>(keys, i, k);
+  const double re = coeff[2 * i], im = coeff[2 * i + 1];
+  coef[i] = re;
+  if (im != 0.0) atomicMin(err, (ull)i + 1);
+  if (i > 0) {
+#pragma unroll
+    for (int w = 0; w < 2 * B; ++w) p.w[w] = __brevll(rows[(i - 1) * 2 * B + w]);
+    if (key_cmp<B>(p, k) >= 0) atomicMin(err + 1, (ull)i + 1);
+  }
+}
+
+void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const double* coeff,
+                  size_t M, bool host_src) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  s.n_qubits = (uint32_t)n_qubits;
+  s.B = n_qubits == 0 ? 1 : (uint32_t)((n_qubits + 63) / 64);
+  if (s.B == 3) s.B = 4;  // device rows are 1, 2 or 4 blocks; padding blocks stay zero
+  const uint32_t Bref = n_qubits == 0 ? 1 : (uint32_t)((n_qubits + 63) / 64);
+  if (s.B > (uint32_t)kMaxB) throw std::invalid_argument("more than 256 qubits are not supported");
+  s.ensure(M);
+  s.M = M;
+  s.filt = Filter{};
+  s.logical = M;
+  s.has_identity = false;
+  if (M == 0) return;
+  // staging in the device row width (pads a 3-block reference row to 4)
+  ull* d_rows = ws.stage_rows.as<ull>(M * 2 * s.B);
+  double* d_coef = ws.stage_coef.as<double>(2 * M);
+  const cudaMemcpyKind kind = host_src ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (Bref == s.B) {
+    IQCC_CUDA(cudaMemcpyAsync(d_rows, rows, M * 2 * s.B * sizeof(ull), kind, st));
+  } else {
+    IQCC_CUDA(cudaMemsetAsync(d_rows, 0, M * 2 * s.B * sizeof(ull), st));
+    // x blocks -> [0,Bref), z blocks -> [B, B+Bref)
+    IQCC_CUDA(cudaMemcpy2DAsync(d_rows, 2 * s.B * sizeof(ull), rows, 2 * Bref * sizeof(ull),
+                                Bref * sizeof(ull), M, kind, st));
+    IQCC_CUDA(cudaMemcpy2DAsync(d_rows + s.B, 2 * s.B * sizeof(ull), rows + Bref,
+                                2 * Bref * sizeof(ull), Bref * sizeof(ull), M, kind, st));
+  }
+  IQCC_CUDA(cudaMemcpyAsync(d_coef, coeff, 2 * M * sizeof(double), kind, st));
+  ull* err = ws.counters.as<ull>(8);
+  ull init[2] = {ULLONG_MAX, ULLONG_MAX};
+  IQCC_CUDA(cudaMemcpyAsync(err, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  const unsigned grid = (unsigned)((M + 255) / 256);
+  {
+    KernelScope ks("upload");
+    switch (s.B) {
+      case 1: k_upload<1><<<grid, 256, 0, st>>>(d_rows, d_coef, M, s.keys(), s.coef(), err); break;
+      case 2: k_upload<2><<<grid, 256, 0, st>>>(d_rows, d_coef, M, s.keys(), s.coef(), err); break;
+      default: k_upload<4><<<grid, 256, 0, st>>>(d_rows, d_coef, M, s.keys(), s.coef(), err); break;
+    }
+  }
+  ull h[2];
+  ull first_key[kMaxB * 2];
+  IQCC_CUDA(cudaMemcpyAsync(h, err, sizeof(h), cudaMemcpyDeviceToHost, st));
+  IQCC_CUDA(cudaMemcpyAsync(first_key, s.keys(), 2 * s.B * sizeof(ull), cudaMemcpyDeviceToHost, st));
+  IQCC_CUDA(cudaStreamSynchronize(st));
+  if (h[0] != ULLONG_MAX)
+    throw std::invalid_argument("coefficient " + std::to_string(h[0] - 1) +
+                                " has a nonzero imaginary part; the device engine stores real "
+                                "coefficients only");
+  if (h[1] != ULLONG_MAX)
+    throw std::invalid_argument("terms are not in canonical order / not unique at index " +
+                                std::to_string(h[1] - 1));
+  bool id = true;
+  for (uint32_t w = 0; w < 2 * s.B; ++w) id = id && first_key[w] == 0;
+  s.has_identity = id;
+}
+
+// ------------------------------------------------ filtered compaction (1 pass)
+// mode 0: write device store arrays; mode 1: write reference layout rows +
+// complex coefficients (download staging).
+template <int B>
+__global__ void __launch_bounds__(CT) k_compact(const ull* __restrict__ keys,
+                                                const double* __restrict__ coef, size_t M,
+                                                Filter filt, int mode, uint32_t Bout,
+                                                ull* __restrict__ okeys, double* __restrict__ ocoef,
+                                                ull* __restrict__ tile_status,
+                                                unsigned* __restrict__ tile_counter,
+                                                ull* __restrict__ total_out) {
+  __shared__ ull s_tile, s_base;
+  __shared__ int scratch[CT / 32 + 2];
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const ull tile = s_tile;
+  const size_t ntiles = (M + CTILE - 1) / CTILE;
+  if (tile >= ntiles) return;
+  const size_t first = tile * CTILE + (size_t)threadIdx.x * CI;
+  unsigned keep = 0;
+#pragma unroll
+  for (int k = 0; k < CI; ++k) {
+    const size_t i = first + k;
+    if (i < M) {
+      Key<B> key = load_key<B>(keys, i);
+      if (filter_keep(filt, i, coef[i], key_is_identity<B>(key))) keep |= 1u << k;
+    }
+  }
+  int total;
+  const int excl = block_exclusive<CT>((int)__popc(keep), 0, OpAdd(), scratch, &total);
+  if (threadIdx.x == 0) {
+    s_base = lookback_exclusive(tile_status, tile, (ull)total);
+    if (tile == ntiles - 1) *total_out = s_base + total;
+  }
+  __syncthreads();
+  size_t pos = s_base + excl;
+#pragma unroll
+  for (int k = 0; k < CI; ++k) {
+    if (!((keep >> k) & 1u)) continue;
+    const size_t i = first + k;
+    Key<B> key = load_key<B>(keys, i);
+    const double c = coef[i];
+    if (mode == 0) {
+      store_key<B>(okeys, pos, key);
+      ocoef[pos] = c;
+    } else {
+      for (uint32_t w = 0; w < Bout; ++w) {
+        okeys[pos * 2 * Bout + w] = __brevll(key.w[w]);
+        okeys[pos * 2 * Bout + Bout + w] = __brevll(key.w[B + w]);
+      }
+      ocoef[2 * pos] = c;
+      ocoef[2 * pos + 1] = 0.0;
+    }
+    ++pos;
+  }
+}
+
+static size_t run_compact(DeviceStore& s, int mode, uint32_t Bout, ull* okeys, double* ocoef) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const size_t ntiles = std::max<size_t>(1, (s.M + CTILE - 1) / CTILE);
+  ull* tstat = ws.tile_status.as<ull>(ntiles + 1);
+  ull* ctr = ws.counters.as<ull>(8);
+  IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntiles + 1) * sizeof(ull), st));
+  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
+  unsigned* tc = reinterpret_cast<unsigned*>(ctr + 4);
+  if (s.M > 0) {
+    KernelScope ks("compact");
+    switch (s.B) {
+      case 1: k_compact<1><<<(unsigned)ntiles, CT, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, mode, Bout, okeys, ocoef, tstat, tc, ctr); break;
+      case 2: k_compact<2><<<(unsigned)ntiles, CT, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, mode, Bout, okeys, ocoef, tstat, tc, ctr); break;
+      default: k_compact<4><<<(unsigned)ntiles, CT, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, mode, Bout, okeys, ocoef, tstat, tc, ctr); break;
+    }
+  }
+  ull n = 0;
+  IQCC_CUDA(cudaMemcpyAsync(&n, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  IQCC_CUDA(cudaStreamSynchronize(st));
+  return (size_t)n;
+}
+
+void store_materialize(DeviceStore& s) {
+  if (!s.filt.active) return;
+  Workspace& ws = workspace();
+  ull* ok = ws.out_keys.as<ull>(std::max<size_t>(s.M, 1) * 2 * s.B);
+  double* oc = ws.out_coef.as<double>(std::max<size_t>(s.M, 1));
+  size_t n = run_compact(s, 0, s.B, ok, oc);
+  std::swap(s.kbuf, ws.out_keys);
+  std::swap(s.cbuf, ws.out_coef);
+  s.M = n;
+  s.logical = n;
+  s.filt = Filter{};
+}
+
+size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap, bool host_dst) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const uint32_t Bref = s.n_qubits == 0 ? 1 : (s.n_qubits + 63) / 64;
+  const size_t n_log = s.logical;
+  if (n_log > cap) throw std::invalid_argument("download: output capacity " + std::to_string(cap) +
+                                               " < " + std::to_string(n_log) + " terms");
+  if (n_log == 0) return 0;
+  ull* d_rows = host_dst ? ws.stage_rows.as<ull>(n_log * 2 * Bref) : reinterpret_cast<ull*>(rows);
+  double* d_coef = host_dst ? ws.stage_coef.as<double>(2 * n_log) : coeff;
+  size_t n = run_compact(s, 1, Bref, d_rows, d_coef);
+  if (n != n_log) throw std::runtime_error("download: filtered count mismatch");
+  if (host_dst) {
+    IQCC_CUDA(cudaMemcpyAsync(rows, d_rows, n * 2 * Bref * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaMemcpyAsync(coeff, d_coef, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaStreamSynchronize(st));
+  }
+  return n;
+}
+
+void store_clone(const DeviceStore& src, DeviceStore& dst) {
+  cudaStream_t st = stream();
+  dst.n_qubits = src.n_qubits;
+  dst.B = src.B;
+  dst.ensure(src.M);
+  dst.M = src.M;
+  dst.filt = src.filt;
+  dst.logical = src.logical;
+  dst.has_identity = src.has_identity;
+  if (src.M) {
+    IQCC_CUDA(cudaMemcpyAsync(dst.keys(), src.keys(), src.M * 2 * src.B * sizeof(ull),
+                              cudaMemcpyDeviceToDevice, st));
+    IQCC_CUDA(cudaMemcpyAsync(dst.coef(), src.coef(), src.M * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+// ------------------------------------------------------------- generator
+template <int B>
+__global__ void k_gen_mol(uint32_t n, uint32_t Bref, uint64_t seed, size_t N,
+                          ull* __restrict__ keys, double* __restrict__ coef) {
+  const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  uint64_t row[2 * kMaxB];
+  const double c = iqcc_gen::mol_term(n, Bref, seed, k, row);
+  Key<B> key;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) key.w[w] = 0;
+  for (uint32_t w = 0; w < Bref; ++w) {
+    key.w[w] = __brevll(row[w]);
+    key.w[B + w] = __brevll(row[Bref + w]);
+  }
+  store_key<B>(keys, k, key);
+  coef[k] = c;
+}
+
+// LSD radix sort of (key, generation index) with 8-bit digits: one
+// histogram + scatter pass per digit of every key word, least significant
+// first; stable, so equal keys keep generation order.  Synthetic-input
+// preparation only (not on the dressing path).
+__global__ void k_digit_hist(const ull* __restrict__ keys, const unsigned* __restrict__ perm,
+                             size_t N, int W, int word, int shift, unsigned* __restrict__ hist,
+                             size_t per_block) {
+  __shared__ unsigned h[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const size_t lo = blockIdx.x * per_block, hi = min(N, lo + per_block);
+  for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+    atomicAdd(h + ((keys[(size_t)perm[i] * W + word] >> shift) & 0xFF), 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[(size_t)b * gridDim.x + blockIdx.x] = h[b];
+}
+
+__global__ void k_digit_scatter(const ull* __restrict__ keys, const unsigned* __restrict__ perm,
+                                size_t N, int W, int word, int shift,
+                                const unsigned* __restrict__ offs, unsigned* __restrict__ out,
+                                size_t per_block) {
+  // one warp per block keeps the scatter stable: lanes process items in
+  // order via ballot ranks within the warp, warps run sequentially.
+  __shared__ unsigned base[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) base[b] = offs[(size_t)b * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const size_t lo = blockIdx.x * per_block, hi = min(N, lo + per_block);
+  const int lane = threadIdx.x;
+  for (size_t i0 = lo; i0 < hi; i0 += 32) {
+    const size_t i = i0 + lane;
+    unsigned d = 256;
+    unsigned p = 0;
+    if (i < hi) {
+      p = perm[i];
+      d = (unsigned)((keys[(size_t)p * W + word] >> shift) & 0xFF);
+    }
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned rank = __popc(peers & ((1u << lane) - 1u));
+    unsigned leader = __ffs(peers) - 1;
+    unsigned b = 0;
+    if (i < hi && lane == (int)leader) b = atomicAdd(base + d, (unsigned)__popc(peers));
+    b = __shfl_sync(0xffffffffu, b, leader);
+    if (i < hi) out[b + rank] = p;
+    __syncwarp();
+  }
+}
+
+__global__ void k_scan_digits(unsigned* __restrict__ hist, size_t n) {
+  // single thread exclusive scan over 256 * nblocks counters (small)
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned s = 0;
+  for (size_t i = 0; i < n; ++i) {
+    unsigned v = hist[i];
+    hist[i] = s;
+    s += v;
+  }
+}
+
+template <int B>
+__global__ void k_gather_dedupe_flags(const ull* __restrict__ keys, const unsigned* __restrict__ perm,
+                                      size_t N, unsigned char* __restrict__ flag) {
+  const size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  Key<B> a = load_key<B>(keys, perm[r]);
+  bool keep = true;
+  if (r > 0) keep = key_cmp<B>(load_key<B>(keys, perm[r - 1]), a) != 0;
+  flag[r] = keep ? 1 : 0;
+}
+
+template <int B>
+__global__ void __launch_bounds__(CT) k_gather_compact(const ull* __restrict__ keys,
+                                                       const double* __restrict__ coef,
+                                                       const unsigned* __restrict__ perm,
+                                                       const unsigned char* __restrict__ flag,
+                                                       size_t N, ull* __restrict__ okeys,
+                                                       double* __restrict__ ocoef,
+                                                       ull* __restrict__ tile_status,
+                                                       unsigned* __restrict__ tile_counter,
+                                                       ull* __restrict__ total_out) {
+  __shared__ ull s_tile, s_base;
+  __shared__ int scratch[CT / 32 + 2];
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const ull tile = s_tile;
+  const size_t ntiles = (N + CTILE - 1) / CTILE;
+  if (tile >= ntiles) return;
+  const size_t first = tile * CTILE + (size_t)threadIdx.x * CI;
+  unsigned keep = 0;
+  for (int k = 0; k < CI; ++k)
+    if (first + k < N && flag[first + k]) keep |= 1u << k;
+  int total;
+  const int excl = block_exclusive<CT>((int)__popc(keep), 0, OpAdd(), scratch, &total);
+  if (threadIdx.x == 0) {
+    s_base = lookback_exclusive(tile_status, tile, (ull)total);
+    if (tile == ntiles - 1) *total_out = s_base + total;
+  }
+  __syncthreads();
+  size_t pos = s_base + excl;
+  for (int k = 0; k < CI; ++k) {
+    if (!((keep >> k) & 1u)) continue;
+    const unsigned p = perm[first + k];
+    store_key<B>(okeys, pos, load_key<B>(keys, p));
+    ocoef[pos] = coef[p];
+    ++pos;
+  }
+}
+
+template <int B>
+static void gen_impl(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const uint32_t Bref = (uint32_t)((n + 63) / 64);
+  const int W = 2 * B;
+  ull* tk = ws.out_keys.as<ull>(N * W);
+  double* tc = ws.out_coef.as<double>(N);
+  {
+    KernelScope ks("generate");
+    k_gen_mol<B><<<(unsigned)((N + 255) / 256), 256, 0, st>>>((uint32_t)n, Bref, seed, N, tk, tc);
+  }
+  unsigned* perm = ws.inv_perm.as<unsigned>(N);
+  unsigned* perm2 = ws.rdelta.as<unsigned>(N);
+  std::vector<unsigned> iota_h;  // identity permutation via a tiny kernel-free path
+  {
+    // identity permutation: generation order
+    iota_h.resize(N);
+    for (size_t i = 0; i < N; ++i) iota_h[i] = (unsigned)i;
+    IQCC_CUDA(cudaMemcpyAsync(perm, iota_h.data(), N * sizeof(unsigned), cudaMemcpyHostToDevice, st));
+  }
+  const size_t per_block = 16384;
+  const size_t nb = std::max<size_t>(1, (N + per_block - 1) / per_block);
+  unsigned* hist = ws.misc2.as<unsigned>(256 * nb);
+  for (int word = W - 1; word >= 0; --word) {
+    for (int shift = 0; shift < 64; shift += 8) {
+      KernelScope ks("generate");
+      k_digit_hist<<<(unsigned)nb, 256, 0, st>>>(tk, perm, N, W, word, shift, hist, per_block);
+      k_scan_digits<<<1, 1, 0, st>>>(hist, 256 * nb);
+      k_digit_scatter<<<(unsigned)nb, 32, 0, st>>>(tk, perm, N, W, word, shift, hist, perm2, per_block);
+      std::swap(perm, perm2);
+    }
+  }
+  unsigned char* flag = ws.mbits.as<unsigned char>(N);
+  {
+    KernelScope ks("generate");
+    k_gather_dedupe_flags<B><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(tk, perm, N, flag);
+  }
+  s.ensure(N);
+  const size_t ntiles = (N + CTILE - 1) / CTILE;
+  ull* tstat = ws.tile_status.as<ull>(ntiles + 1);
+  ull* ctr = ws.counters.as<ull>(8);
+  IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntiles + 1) * sizeof(ull), st));
+  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
+  {
+    KernelScope ks("generate");
+    k_gather_compact<B><<<(unsigned)ntiles, CT, 0, st>>>(tk, tc, perm, flag, N, s.keys(), s.coef(),
+                                                        tstat, reinterpret_cast<unsigned*>(ctr + 4), ctr);
+  }
+  ull m = 0;
+  IQCC_CUDA(cudaMemcpyAsync(&m, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  IQCC_CUDA(cudaStreamSynchronize(st));
+  s.M = m;
+  s.logical = m;
+  s.filt = Filter{};
+  s.has_identity = true;  // term 0 of G_mol is the identity
+}
+
+void store_generate_mol(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
+  if (n < 1 || n > 256) throw std::invalid_argument("generate_mol: 1 <= n_qubits <= 256");
+  if (N < 1 || N > 0xFFFFFFF0ull) throw std::invalid_argument("generate_mol: bad term count");
+  s.n_qubits = (uint32_t)n;
+  uint32_t B = (uint32_t)((n + 63) / 64);
+  s.B = B == 3 ? 4 : B;
+  switch (s.B) {
+    case 1: gen_impl<1>(s, n, N, seed); break;
+    case 2: gen_impl<2>(s, n, N, seed); break;
+    default: gen_impl<4>(s, n, N, seed); break;
+  }
+}
+
+// ------------------------------------------------------------ compress
+template <int B>
+__global__ void k_hist_eps(const ull* __restrict__ keys, const double* __restrict__ coef, size_t M,
+                           double eps, unsigned* __restrict__ hist, ull* __restrict__ ctr) {
+  __shared__ unsigned sh[4096];
+  for (int b = threadIdx.x; b < 4096; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  int n_eps = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < M;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double a = fabs(coef[i]);
+    const bool id = i == 0 && key_is_identity<B>(load_key<B>(keys, 0));
+    if (id || a >= eps) ++n_eps;
+    if (!id && a >= eps) atomicAdd(sh + (unsigned)(__double_as_longlong(a) >> 51), 1u);
+  }
+  n_eps = __reduce_add_sync(0xffffffffu, n_eps);
+  if ((threadIdx.x & 31) == 0 && n_eps) atomicAdd(ctr + 1, (ull)n_eps);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 4096; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+
+template <int B>
+__global__ void k_gather_bin(const ull* __restrict__ keys, const double* __restrict__ coef,
+                             size_t M, double eps, unsigned bin, ull* __restrict__ cv,
+                             ull* __restrict__ ci, ull* __restrict__ ctr) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const double a = fabs(coef[i]);
+  if (!(a >= eps)) return;
+  const ull bits = (ull)__double_as_longlong(a);
+  if ((unsigned)(bits >> 51) != bin) return;
+  if (i == 0 && key_is_identity<B>(load_key<B>(keys, 0))) return;
+  const ull slot = atomicAdd(ctr + 2, 1ull);
+  cv[slot] = bits;
+  ci[slot] = i;
+}
+
+__global__ void k_cand_hist(const ull* __restrict__ cv, size_t n, ull known_mask, ull known_val,
+                            int shift, unsigned mask, unsigned* __restrict__ hist) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const ull v = cv[i];
+    if ((v & known_mask) == known_val) atomicAdd(hist + ((v >> shift) & mask), 1u);
+  }
+}
+
+__global__ void k_cand_ties(const ull* __restrict__ cv, const ull* __restrict__ ci, size_t n,
+                            ull value, ull* __restrict__ out, ull* __restrict__ ctr) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n || cv[i] != value) return;
+  out[atomicAdd(ctr + 3, 1ull)] = ci[i];
+}
+
+template <int B>
+__global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __restrict__ coef,
+                                 size_t M, Filter filt, double* __restrict__ partial) {
+  __shared__ double sm[256 / 32 + 2];
+  double acc = 0.0;
+  const size_t per = (M + gridDim.x - 1) / gridDim.x;
+  const size_t lo = blockIdx.x * per, hi = min(M, lo + per);
+  for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double c = coef[i];
+    bool id = i == 0 && key_is_identity<B>(load_key<B>(keys, 0));
+    if (!filter_keep(filt, i, c, id)) acc += fabs(c);
+  }
+  double tot;
+  block_exclusive<256>(acc, 0.0, OpAdd(), sm, &tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
+                              size_t count_eps, bool want_stats) {
+  if (eps < 0) throw std::invalid_argument("compress: epsilon < 0");
+  if (max_terms < 1) throw std::invalid_argument("compress: max_terms < 1");
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  if (s.filt.active) {
+    store_materialize(s);
+    hist_ready = false;
+  }
+  CompressResult res;
+  unsigned* hist = ws.hist.as<unsigned>(4096);
+  ull* ctr = ws.counters.as<ull>(8);
+  if (!hist_ready) {
+    IQCC_CUDA(cudaMemsetAsync(hist, 0, 4096 * sizeof(unsigned), st));
+    IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
+    const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (s.M + 255) / 256));
+    if (s.M) {
+      KernelScope ks("select");
+      switch (s.B) {
+        case 1: k_hist_eps<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, hist, ctr); break;
+        case 2: k_hist_eps<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, hist, ctr); break;
+        default: k_hist_eps<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, hist, ctr); break;
+      }
+    }
+    ull h = 0;
+    IQCC_CUDA(cudaMemcpyAsync(&h, ctr + 1, sizeof(ull), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaStreamSynchronize(st));
+    count_eps = (size_t)h;
+  }
+  Filter f;
+  f.active = 1;
+  f.eps = eps;
+  size_t logical = count_eps;
+  if (count_eps > max_terms) {
+    const size_t budget = max_terms - (s.has_identity ? 1 : 0);
+    f.has_v = 1;
+    if (budget == 0) {
+      f.eps = HUGE_VAL;  // identity only (|c| >= inf never holds for finite c)
+      f.v = HUGE_VAL;
+      f.cut = 0;
+    } else {
+      std::vector<unsigned> hh(4096);
+      IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, 4096 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaStreamSynchronize(st));
+      size_t cum = 0, r = 0;
+      int bin = -1;
+      for (int b = 4095; b >= 0; --b) {
+        if (cum + hh[b] >= budget) {
+          bin = b;
+          r = budget - cum;
+          break;
+        }
+        cum += hh[b];
+      }
+      if (bin < 0) throw std::runtime_error("compress: histogram inconsistent");
+      const size_t nc = hh[bin];
+      ull* cv = ws.cand_v.as<ull>(nc);
+      ull* ci = ws.cand_i.as<ull>(nc);
+      IQCC_CUDA(cudaMemsetAsync(ctr + 2, 0, 2 * sizeof(ull), st));
+      {
+        KernelScope ks("select");
+        const unsigned grid = (unsigned)((s.M + 255) / 256);
+        switch (s.B) {
+          case 1: k_gather_bin<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
+          case 2: k_gather_bin<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
+          default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
+        }
+      }
+      // digits of the low 51 bits, most significant first; larger values first
+      ull known_mask = ~((1ull << 51) - 1), known_val = (ull)bin << 51;
+      const int shifts[4] = {35, 19, 3, 0};
+      const int widths[4] = {16, 16, 16, 3};
+      unsigned* dh = ws.misc2.as<unsigned>(65536);
+      std::vector<unsigned> hd(65536);
+      for (int round = 0; round < 4; ++round) {
+        const unsigned dmask = (1u << widths[round]) - 1u;
+        IQCC_CUDA(cudaMemsetAsync(dh, 0, (dmask + 1) * sizeof(unsigned), st));
+        {
+          KernelScope ks("select");
+          const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (nc + 255) / 256));
+          k_cand_hist<<<grid, 256, 0, st>>>(cv, nc, known_mask, known_val, shifts[round], dmask, dh);
+        }
+        IQCC_CUDA(cudaMemcpyAsync(hd.data(), dh, (dmask + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        IQCC_CUDA(cudaStreamSynchronize(st));
+        size_t c2 = 0;
+        long d = -1;
+        for (long x = dmask; x >= 0; --x) {
+          if (c2 + hd[x] >= r) {
+            d = x;
+            r -= c2;
+            break;
+          }
+          c2 += hd[x];
+        }
+        if (d < 0) throw std::runtime_error("compress: digit select failed");
+        known_mask |= (ull)dmask << shifts[round];
+        known_val |= (ull)d << shifts[round];
+      }
+      const ull vbits = known_val;  // exact threshold value; r ties at it are kept
+      ull* ties = ws.misc3.as<ull>(nc);
+      {
+        KernelScope ks("select");
+        k_cand_ties<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(cv, ci, nc, vbits, ties, ctr);
+      }
+      ull ntie = 0;
+      IQCC_CUDA(cudaMemcpyAsync(&ntie, ctr + 3, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaStreamSynchronize(st));
+      std::vector<ull> th(ntie);
+      IQCC_CUDA(cudaMemcpyAsync(th.data(), ties, ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaStreamSynchronize(st));
+      std::sort(th.begin(), th.end());
+      if (r < 1 || r > th.size()) throw std::runtime_error("compress: tie resolution failed");
+      double v;
+      std::memcpy(&v, &vbits, 8);
+      f.v = v;
+      f.cut = th[r - 1];
+    }
+    logical = max_terms;
+  }
+  if (eps == 0.0 && !f.has_v) f.active = 0;  // nothing to drop
+  s.filt = f;
+  s.logical = logical;
+  res.dropped_terms = s.M - logical;
+  if (want_stats && res.dropped_terms > 0) {
+    const unsigned grid = 592;
+    double* part = ws.partials.as<double>(grid);
+    {
+      KernelScope ks("select");
+      switch (s.B) {
+        case 1: k_dropped_weight<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, part); break;
+        case 2: k_dropped_weight<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, part); break;
+        default: k_dropped_weight<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, part); break;
+      }
+    }
+    std::vector<double> hp(grid);
+    IQCC_CUDA(cudaMemcpyAsync(hp.data(), part, grid * sizeof(double), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaStreamSynchronize(st));
+    double w = 0.0;
+    for (double x : hp) w += x;
+    res.dropped_weight = w;
+  }
+  return res;
+}
+
+}  // namespace iqcc_b200

@@ -1,0 +1,446 @@
+"""Python mirror of the reference's ``namespace iqcc`` API for the hot path,
+backed by the B200 engine (C-ABI in include/iqcc_b200.h).
+
+Names, argument meaning and error behaviour follow the reference headers
+(``/root/reference/proj/include/iqcc/*.hpp``): ``ValueError`` stands for
+``std::invalid_argument`` and ``RuntimeError`` for ``std::runtime_error``.
+Host containers use the reference storage layout (iqcc/pauli.hpp:373-377):
+rows ``uint64[M, 2B]`` (x blocks then z blocks, bit j%64 of block j//64 is
+qubit j) and ``complex128`` coefficients.  Everything numeric runs on the GPU;
+the host only computes ``cos/sin`` of amplitudes and Bloch angles with libm
+(``math.cos``/``math.sin`` are glibc's, like ``std::cos``/``std::sin`` in the
+reference), so device results are bit-identical to the reference's.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import native
+from .native import check, lib
+
+U64_MAX = 2**64 - 1
+
+
+def blocks_for(n_qubits: int) -> int:
+    """iqcc/pauli.hpp:21-23."""
+    return 1 if n_qubits == 0 else (n_qubits + 63) // 64
+
+
+def _addr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ---------------------------------------------------------------- words
+class PauliWord:
+    """A Pauli word as one reference row (x blocks then z blocks)."""
+
+    __slots__ = ("n_qubits", "row")
+
+    def __init__(self, n_qubits: int, row=None):
+        self.n_qubits = n_qubits
+        B = blocks_for(n_qubits)
+        self.row = np.zeros(2 * B, np.uint64) if row is None else np.array(row, dtype=np.uint64).reshape(2 * B)
+
+    @staticmethod
+    def from_string(letters: str) -> "PauliWord":
+        """PauliWord::from_string, iqcc/pauli.hpp:50-65."""
+        w = PauliWord(len(letters))
+        B = blocks_for(len(letters))
+        for j, ch in enumerate(letters):
+            bit = np.uint64(1 << (j % 64))
+            if ch == "I":
+                continue
+            if ch not in "XYZ":
+                raise ValueError(f"invalid Pauli letter '{ch}'")
+            if ch in "XY":
+                w.row[j // 64] |= bit
+            if ch in "ZY":
+                w.row[B + j // 64] |= bit
+        return w
+
+    def letter(self, j: int) -> str:
+        B = blocks_for(self.n_qubits)
+        x = (int(self.row[j // 64]) >> (j % 64)) & 1
+        z = (int(self.row[B + j // 64]) >> (j % 64)) & 1
+        return "IXZY"[x | (z << 1)]
+
+    def to_string(self) -> str:
+        return "".join(self.letter(j) for j in range(self.n_qubits))
+
+    def is_identity(self) -> bool:
+        return not self.row.any()
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, PauliWord) and self.n_qubits == other.n_qubits and np.array_equal(self.row, other.row)
+
+    def __repr__(self) -> str:
+        return f"PauliWord('{self.to_string()}')"
+
+
+# ------------------------------------------------------------ containers
+class PauliSum:
+    """Host PauliSum in the reference layout (canonical, duplicate free)."""
+
+    def __init__(self, n_qubits: int, rows=None, coeffs=None):
+        self.n_qubits = n_qubits
+        W = 2 * blocks_for(n_qubits)
+        self.rows = np.zeros((0, W), np.uint64) if rows is None else np.ascontiguousarray(rows, np.uint64).reshape(-1, W)
+        self.coeffs = (np.zeros(0, np.complex128) if coeffs is None
+                       else np.ascontiguousarray(np.asarray(coeffs, dtype=np.complex128)).reshape(-1))
+        if self.rows.shape[0] != self.coeffs.shape[0]:
+            raise ValueError("rows / coeffs length mismatch")
+
+    def __len__(self) -> int:
+        return self.coeffs.shape[0]
+
+    def size(self) -> int:
+        return len(self)
+
+    def word(self, i: int) -> PauliWord:
+        return PauliWord(self.n_qubits, self.rows[i])
+
+    def coeff(self, i: int) -> complex:
+        return complex(self.coeffs[i])
+
+    def append(self, w: PauliWord, c) -> None:
+        """PauliSum::append (caller keeps canonical order)."""
+        self.rows = np.vstack([self.rows, w.row[None, :]])
+        self.coeffs = np.append(self.coeffs, np.complex128(c))
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, PauliSum) and self.n_qubits == other.n_qubits
+                and np.array_equal(self.rows, other.rows) and np.array_equal(self.coeffs, other.coeffs))
+
+    def to_device(self) -> "DeviceSum":
+        return DeviceSum.upload(self)
+
+
+@dataclass
+class DressOp:
+    """iqcc/dressing.hpp:15-18."""
+    generator: PauliWord
+    amplitude: float = 0.0
+
+
+@dataclass
+class Ansatz:
+    """iqcc/dressing.hpp:22-31."""
+    entanglers: list = field(default_factory=list)
+    tau: list = field(default_factory=list)
+
+    def push(self, p: PauliWord, amplitude: float) -> None:
+        self.entanglers.append(p)
+        self.tau.append(float(amplitude))
+
+    def size(self) -> int:
+        return len(self.entanglers)
+
+
+@dataclass
+class MergeOptions:
+    """iqcc/pauli.hpp:236-240 (the device path has no imaginary parts, so
+    the hermiticity check can never fire; kept for signature parity)."""
+    drop_threshold: float = 1e-12
+    check_hermitian: bool = True
+    hermitian_tol: float = 1e-10
+
+
+@dataclass
+class CompressStats:
+    """iqcc/pauli.hpp:417-420."""
+    dropped_terms: int = 0
+    dropped_weight: float = 0.0
+
+
+@dataclass
+class GrowthSplit:
+    n_commuting: int = 0
+    n_anticommuting: int = 0
+
+    def bound(self) -> int:
+        return self.n_commuting + 2 * self.n_anticommuting
+
+
+@dataclass
+class QmfState:
+    """iqcc/qmf.hpp:14-31."""
+    theta: np.ndarray
+    phi: np.ndarray
+
+    @staticmethod
+    def zeros(n: int) -> "QmfState":
+        return QmfState(np.zeros(n), np.zeros(n))
+
+    def n_qubits(self) -> int:
+        return len(self.theta)
+
+    def at_poles(self, tol: float = 1e-12) -> bool:
+        return all(abs(math.sin(float(t))) <= tol for t in self.theta)
+
+
+def hf_reference(occupations: Sequence[bool]) -> QmfState:
+    """iqcc/qmf.hpp:34-39."""
+    th = np.array([math.pi if o else 0.0 for o in occupations], np.float64)
+    return QmfState(th, np.zeros(len(occupations)))
+
+
+@dataclass
+class DisOptions:
+    """iqcc/dis.hpp:60-70."""
+    screen_threshold: float = 1e-8
+    per_group_cap: int = 128
+    tie_break_seed: Optional[int] = None
+
+
+@dataclass
+class RankedGenerator:
+    word: PauliWord
+    gradient: float
+
+
+def qmf_factor_table(omega: QmfState) -> np.ndarray:
+    """Per-qubit (X, Z, Y) expectations, evaluated exactly as qmf_factor
+    (iqcc/qmf.hpp:56-61) with glibc sin/cos."""
+    n = omega.n_qubits()
+    t = np.zeros((n, 3), np.float64)
+    for j in range(n):
+        th, ph = float(omega.theta[j]), float(omega.phi[j])
+        t[j, 0] = math.sin(th) * math.cos(ph)
+        t[j, 1] = math.cos(th)
+        t[j, 2] = math.sin(th) * math.sin(ph)
+    return t
+
+
+def qmf_deriv_table(omega: QmfState) -> np.ndarray:
+    """Per-qubit (dth_X, dph_X, dth_Z, dph_Z, dth_Y, dph_Y) as in
+    qmf_energy_gradient (iqcc/qmf.hpp:130-143)."""
+    n = omega.n_qubits()
+    t = np.zeros((n, 6), np.float64)
+    for j in range(n):
+        th, ph = float(omega.theta[j]), float(omega.phi[j])
+        st, ct, sp, cp = math.sin(th), math.cos(th), math.sin(ph), math.cos(ph)
+        t[j] = (ct * cp, -st * sp, -st, 0.0, ct * sp, st * cp)
+    return t
+
+
+# --------------------------------------------------------- device handle
+class DeviceSum:
+    """A PauliSum resident in B200 HBM (one shard when partitioned)."""
+
+    def __init__(self, handle: int, n_qubits: int):
+        self.handle = handle
+        self.n_qubits = n_qubits
+
+    @staticmethod
+    def upload(h: PauliSum) -> "DeviceSum":
+        native.init()
+        out = C.c_void_p()
+        rows = np.ascontiguousarray(h.rows, np.uint64)
+        cf = np.ascontiguousarray(h.coeffs, np.complex128)
+        check(lib.iqcc_gpu_sum_create(h.n_qubits, _addr(rows), _addr(cf), len(h), C.byref(out)))
+        return DeviceSum(out.value, h.n_qubits)
+
+    @staticmethod
+    def generate_mol(n_qubits: int, n_terms: int, seed: int) -> "DeviceSum":
+        native.init()
+        out = C.c_void_p()
+        check(lib.iqcc_gpu_sum_generate_mol(n_qubits, n_terms, seed, C.byref(out)))
+        return DeviceSum(out.value, n_qubits)
+
+    def clone(self) -> "DeviceSum":
+        out = C.c_void_p()
+        check(lib.iqcc_gpu_sum_clone(self.handle, C.byref(out)))
+        return DeviceSum(out.value, self.n_qubits)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.iqcc_gpu_sum_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        n = C.c_size_t()
+        check(lib.iqcc_gpu_sum_size(self.handle, C.byref(n)))
+        return n.value
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def download(self, rows: np.ndarray | None = None, coeffs: np.ndarray | None = None) -> PauliSum:
+        n = self.size()
+        W = 2 * blocks_for(self.n_qubits)
+        if rows is None:
+            rows = np.empty((max(n, 1), W), np.uint64)
+            coeffs = np.empty(max(n, 1), np.complex128)
+        got = C.c_size_t()
+        check(lib.iqcc_gpu_sum_download(self.handle, _addr(rows), _addr(coeffs), rows.shape[0], C.byref(got)))
+        return PauliSum(self.n_qubits, rows[: got.value], coeffs[: got.value])
+
+    # ---- hot path, in place
+    def dress(self, gen: PauliWord, tau: float, drop_threshold: float = 1e-12) -> DressStats:
+        g = np.ascontiguousarray(gen.row, np.uint64)
+        st = native.DressStats()
+        check(lib.iqcc_gpu_dress(self.handle, _addr(g), math.cos(tau), math.sin(tau), drop_threshold, C.byref(st)))
+        return st
+
+    def compress(self, eps: float, max_terms: int = U64_MAX, stats: CompressStats | None = None) -> None:
+        cs = native.CompressStatsC()
+        check(lib.iqcc_gpu_compress(self.handle, eps, max_terms, C.byref(cs)))
+        if stats is not None:
+            stats.dropped_terms += cs.dropped_terms
+            stats.dropped_weight += cs.dropped_weight
+
+    def dress_sequence(self, ansatz: Ansatz, eps: float, max_terms: int = U64_MAX,
+                       stats: CompressStats | None = None) -> None:
+        K = ansatz.size()
+        W = 2 * blocks_for(self.n_qubits)
+        gens = np.zeros((max(K, 1), W), np.uint64)
+        for k, p in enumerate(ansatz.entanglers):
+            gens[k] = p.row
+        cs_ = np.array([math.cos(t) for t in ansatz.tau] or [1.0])
+        sn_ = np.array([math.sin(t) for t in ansatz.tau] or [0.0])
+        st = native.CompressStatsC()
+        check(lib.iqcc_gpu_dress_sequence(self.handle, K, _addr(gens), _addr(cs_), _addr(sn_), eps, max_terms,
+                                          C.byref(st) if stats is not None else None))
+        if stats is not None:
+            stats.dropped_terms += st.dropped_terms
+            stats.dropped_weight += st.dropped_weight
+
+    def growth_split(self, p: PauliWord) -> GrowthSplit:
+        g = np.ascontiguousarray(p.row, np.uint64)
+        nc, na = C.c_size_t(), C.c_size_t()
+        check(lib.iqcc_gpu_growth_split(self.handle, _addr(g), C.byref(nc), C.byref(na)))
+        return GrowthSplit(nc.value, na.value)
+
+    def expect(self, omega: QmfState) -> float:
+        t = qmf_factor_table(omega)
+        e = C.c_double()
+        check(lib.iqcc_gpu_expect(self.handle, _addr(t), C.byref(e)))
+        return e.value
+
+    def qmf_energy_gradient(self, omega: QmfState):
+        t, d = qmf_factor_table(omega), qmf_deriv_table(omega)
+        g = np.zeros(2 * self.n_qubits, np.float64)
+        e = C.c_double()
+        check(lib.iqcc_gpu_qmf_energy_gradient(self.handle, _addr(t), _addr(d), C.byref(e), _addr(g)))
+        return e.value, g
+
+    def gradients(self, omega: QmfState, cands: np.ndarray, flip_group_only: bool = False) -> np.ndarray:
+        t = qmf_factor_table(omega)
+        c = np.ascontiguousarray(cands, np.uint64).reshape(-1, 2 * blocks_for(self.n_qubits))
+        g = np.zeros(max(1, c.shape[0]), np.float64)
+        check(lib.iqcc_gpu_gradients(self.handle, _addr(t), _addr(c), c.shape[0], int(flip_group_only), _addr(g)))
+        return g[: c.shape[0]]
+
+
+# ----------------------------------------------- reference-shaped functions
+def _dressed_copy(h: PauliSum) -> DeviceSum:
+    return DeviceSum.upload(h)
+
+
+def dress_single(h: PauliSum, op: DressOp, opts: MergeOptions = MergeOptions()) -> PauliSum:
+    """iqcc/dressing.hpp:197-220."""
+    if h.n_qubits != op.generator.n_qubits:
+        raise ValueError("dress_single: mismatched qubit counts")
+    if op.generator.is_identity():
+        raise ValueError("dress_single: identity generator")
+    d = DeviceSum.upload(h)
+    d.dress(op.generator, op.amplitude, opts.drop_threshold)
+    return d.download()
+
+
+@dataclass
+class SortlessStats:
+    n_buckets: int = 0
+    new_term_streams: int = 0
+    new_stream_sorts: int = 0
+    merge_comparisons: int = 0
+
+
+def sortless_dress(h: PauliSum, op: DressOp, opts: MergeOptions = MergeOptions(),
+                   stats: SortlessStats | None = None) -> PauliSum:
+    """iqcc/dressing.hpp:228-307.  Same sum as dress_single (the device path
+    never sorts products); keeps the reference's limit of 64 key bits on the
+    entangler support (bucket_by_support, dressing.hpp:163-165)."""
+    if h.n_qubits != op.generator.n_qubits:
+        raise ValueError("sortless_dress: mismatched qubit counts")
+    if op.generator.is_identity():
+        raise ValueError("sortless_dress: identity generator")
+    B = blocks_for(h.n_qubits)
+    support = sum(bin(int(op.generator.row[b]) | int(op.generator.row[B + b])).count("1") for b in range(B))
+    if 2 * support > 64:
+        raise RuntimeError("entangler support exceeds 64 bits; not supported")
+    out = dress_single(h, op, opts)
+    if stats is not None:
+        stats.new_stream_sorts = 0
+    return out
+
+
+def dress_sequence(h: PauliSum, ansatz: Ansatz, epsilon: float, max_terms: int = U64_MAX,
+                   stats: CompressStats | None = None, opts: MergeOptions = MergeOptions()) -> PauliSum:
+    """iqcc/dressing.hpp:311-324 (device resident across the whole ansatz)."""
+    if max_terms < 1:
+        raise ValueError("dress_sequence: max_terms < 1")
+    d = DeviceSum.upload(h)
+    d.dress_sequence(ansatz, epsilon, max_terms, stats)
+    return d.download()
+
+
+def compress(h: PauliSum, epsilon: float, max_terms: int, stats: CompressStats | None = None) -> PauliSum:
+    """iqcc/pauli.hpp:425-474."""
+    if epsilon < 0:
+        raise ValueError("compress: epsilon < 0")
+    if max_terms < 1:
+        raise ValueError("compress: max_terms < 1")
+    d = DeviceSum.upload(h)
+    d.compress(epsilon, max_terms, stats)
+    return d.download()
+
+
+def growth_split(h: PauliSum, p: PauliWord) -> GrowthSplit:
+    """iqcc/dressing.hpp:41-50."""
+    return DeviceSum.upload(h).growth_split(p)
+
+
+def expect_sum(omega: QmfState, h: PauliSum) -> float:
+    """iqcc/qmf.hpp:83-90."""
+    if len(h) and h.n_qubits != omega.n_qubits():
+        raise ValueError("expect_sum: mismatched qubit counts")
+    return DeviceSum.upload(h).expect(omega)
+
+
+def qmf_energy_gradient(h: PauliSum, omega: QmfState):
+    """iqcc/qmf.hpp:94-148; returns (energy, grad[2n])."""
+    return DeviceSum.upload(h).qmf_energy_gradient(omega)
+
+
+def gradient(h: PauliSum, omega: QmfState, p: PauliWord) -> float:
+    """iqcc/dis.hpp:39-52."""
+    return float(DeviceSum.upload(h).gradients(omega, p.row[None, :])[0])
+
+
+def dis_candidates(h: PauliSum, omega: QmfState, top_k: int, opts: DisOptions = DisOptions()) -> list:
+    """iqcc/dis.hpp:140-191.  The optional seeded tie shuffle is applied on
+    the host with the same generator (std::mt19937_64 + std::shuffle would
+    be required for bit parity)."""
+    if top_k < 1:
+        raise ValueError("dis_candidates: top_k < 1")
+    d = DeviceSum.upload(h)
+    t = qmf_factor_table(omega)
+    W = 2 * blocks_for(h.n_qubits)
+    cap = max(1, top_k if top_k < 1 << 40 else len(h))
+    cap = min(cap, max(1, len(h)))
+    rows = np.zeros((cap, W), np.uint64)
+    g = np.zeros(cap, np.float64)
+    n = C.c_size_t()
+    check(lib.iqcc_gpu_dis_candidates(d.handle, _addr(t), int(omega.at_poles()), top_k, opts.screen_threshold,
+                                      opts.per_group_cap, _addr(rows), _addr(g), cap, C.byref(n)))
+    k = min(n.value, top_k, cap)
+    return [RankedGenerator(PauliWord(h.n_qubits, rows[i]), float(g[i])) for i in range(k)]
