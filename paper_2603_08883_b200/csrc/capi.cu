@@ -120,7 +120,7 @@ void* DevBuf::get(size_t n) {
   cudaStream_t st = stream();
   if (p) IQCC_CUDA(cudaFreeAsync(p, st));
   p = nullptr;
-  size_t want = std::max<size_t>(n + n / 8, 256);
+  size_t want = std::max<size_t>(n + n / 2, 256);  // generous slack: stores grow ~1.5x per step
   cudaError_t e = cudaMallocAsync(&p, want, st);
   if (e != cudaSuccess) {
     // retry without slack once the pool has released cached blocks

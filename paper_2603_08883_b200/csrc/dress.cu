@@ -34,6 +34,7 @@
 //   k_partition     merge-path split per output tile
 //   k_merge         survivors (x) products merge, combine, drop, compact
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <stdexcept>
 
@@ -54,19 +55,25 @@ struct Thr {
 
 // ---------------------------------------------------------------- classify
 template <int B>
-__global__ void __launch_bounds__(256) k_classify(const ull* __restrict__ keys, size_t M, Key<B> P,
+__global__ void __launch_bounds__(256) k_classify(const ull* __restrict__ keys,
+                                                  const double* __restrict__ coef, Filter filt,
+                                                  size_t M, Key<B> P,
                                                   const int* __restrict__ lvl, int m,
                                                   short* __restrict__ lcp,
                                                   unsigned char* __restrict__ mbits,
-                                                  unsigned* __restrict__ fmask) {
+                                                  unsigned* __restrict__ fmask,
+                                                  unsigned* __restrict__ pmask) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  int f = 0;
+  int f = 0, pr = 0;
   if (i < M) {
     Key<B> k = load_key<B>(keys, i);
     int l = -1;
     if (i > 0) l = key_lcp<B>(load_key<B>(keys, i - 1), k);
     lcp[i] = (short)l;
-    f = anticommutes<B>(k, P);
+    // dead slots and terms dropped by a pending compress filter are absent:
+    // they emit nothing and generate no product
+    pr = filter_keep(filt, i, __ldg(coef + i), i == 0 && key_is_identity<B>(k));
+    f = pr && anticommutes<B>(k, P);
     for (int c = 0; c * kLevelsPerChunk < m; ++c) {
       unsigned byte = 0;
       for (int j = 0; j < kLevelsPerChunk && c * kLevelsPerChunk + j < m; ++j)
@@ -74,9 +81,73 @@ __global__ void __launch_bounds__(256) k_classify(const ull* __restrict__ keys, 
       mbits[(size_t)c * M + i] = (unsigned char)byte;
     }
   }
-  unsigned bal = __ballot_sync(0xffffffffu, f);
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  const unsigned pal = __ballot_sync(0xffffffffu, pr);
   const size_t i0 = i - (threadIdx.x & 31);
-  if ((threadIdx.x & 31) == 0 && i0 < M) fmask[i0 >> 5] = bal;
+  if ((threadIdx.x & 31) == 0 && i0 < M) {
+    fmask[i0 >> 5] = bal;
+    pmask[i0 >> 5] = pal;
+  }
+}
+
+// ------------------------------------------------- popcount prefix (pmask)
+constexpr int PW = 1024;  // words per block
+__global__ void __launch_bounds__(256) k_popc_blocks(const unsigned* __restrict__ words, size_t W,
+                                                     unsigned* __restrict__ bsum) {
+  __shared__ unsigned sm[256 / 32 + 2];
+  const size_t w0 = blockIdx.x * (size_t)PW + threadIdx.x * 4;
+  unsigned c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (w0 + k < W) c += __popc(words[w0 + k]);
+  unsigned tot;
+  block_exclusive<256>(c, 0u, OpAdd(), sm, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_blocks(unsigned* __restrict__ bsum, size_t nb,
+                                                      unsigned* __restrict__ total) {
+  __shared__ unsigned sm[1024 / 32 + 2];
+  const size_t per = (nb + 1023) / 1024;
+  const size_t lo = threadIdx.x * per, hi = min(nb, lo + per);
+  unsigned c = 0;
+  for (size_t k = lo; k < hi; ++k) c += bsum[k];
+  unsigned tot;
+  unsigned run = block_exclusive<1024>(c, 0u, OpAdd(), sm, &tot);
+  for (size_t k = lo; k < hi; ++k) {
+    const unsigned v = bsum[k];
+    bsum[k] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0) *total = tot;
+}
+
+__global__ void __launch_bounds__(256) k_popc_prefix(const unsigned* __restrict__ words, size_t W,
+                                                     const unsigned* __restrict__ bpfx,
+                                                     unsigned* __restrict__ pre) {
+  __shared__ unsigned sm[256 / 32 + 2];
+  const size_t w0 = blockIdx.x * (size_t)PW + threadIdx.x * 4;
+  unsigned c[4], t = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    c[k] = w0 + k < W ? __popc(words[w0 + k]) : 0u;
+    t += c[k];
+  }
+  unsigned run = block_exclusive<256>(t, 0u, OpAdd(), sm, (unsigned*)nullptr) + bpfx[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (w0 + k < W) pre[w0 + k] = run;
+    run += c[k];
+  }
+}
+
+/// # present terms before index a.
+__device__ __forceinline__ size_t present_before(const unsigned* __restrict__ pmask,
+                                                 const unsigned* __restrict__ pre, size_t W,
+                                                 unsigned total, size_t a) {
+  const size_t w = a >> 5;
+  if (w >= W) return total;
+  return (size_t)pre[w] + __popc(pmask[w] & ((1u << (a & 31)) - 1u));
 }
 
 // ------------------------------------------------------------ tile helpers
@@ -409,7 +480,10 @@ __device__ __forceinline__ Key<B> q_key(const ull* __restrict__ keys,
 template <int B>
 __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __restrict__ inv_perm,
                             size_t nS, size_t nQ, Key<B> P, size_t tile_items, size_t ntiles,
-                            ull* __restrict__ part_a, ull* __restrict__ part_b) {
+                            ull* __restrict__ part_a, ull* __restrict__ part_b,
+                            ull* __restrict__ part_o, const unsigned* __restrict__ pmask,
+                            const unsigned* __restrict__ ppre, size_t W,
+                            const unsigned* __restrict__ ptotal) {
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t > ntiles) return;
   const size_t d = min(t * tile_items, nS + nQ);
@@ -422,20 +496,17 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
       hi = mid;
   }
   size_t a = lo, b = d - lo;
-  // never split an equal (survivor, product) pair across tiles
-  if (a > 0 && b < nQ && key_cmp<B>(load_key<B>(keys, a - 1), q_key<B>(keys, inv_perm, b, P)) == 0)
-    --a;
+  // never split a run of equal survivors (live + dead slot) from its product
+  if (b < nQ) {
+    const Key<B> q = q_key<B>(keys, inv_perm, b, P);
+    while (a > 0 && key_cmp<B>(load_key<B>(keys, a - 1), q) == 0) --a;
+  }
   part_a[t] = a;
   part_b[t] = b;
+  // output slots before this tile: every present survivor and every product
+  // owns exactly one slot (live or dead)
+  part_o[t] = present_before(pmask, ppre, W, *ptotal, a) + b;
 }
-
-// ----------------------------------------------------------------- merge
-template <int B>
-struct MergeSmem {
-  static constexpr size_t bytes(int cap, int nt) {
-    return (size_t)cap * (16 * B + 8 + 1) + 2 * nt * sizeof(int) + 4096 * sizeof(unsigned) + 64;
-  }
-};
 
 template <int B>
 __device__ __forceinline__ Key<B> sm_key(const ull* sk, int e) {
@@ -445,145 +516,314 @@ __device__ __forceinline__ Key<B> sm_key(const ull* sk, int e) {
   return k;
 }
 
+// ----------------------------------------------------------------- merge
+// One output tile per CTA (dynamic tile id for the look-back).  The
+// survivor range S[a0,a1) is contiguous: it is staged into shared memory by
+// the TMA engine (cp.async.bulk, one elected thread, completion on an
+// mbarrier).  The product range Q[b0,b1) is a gather through inv_perm: each
+// row/coefficient is fetched with cp.async (LDGSTS) so every thread keeps
+// many requests in flight without staging through registers.  Outputs are
+// written to a shared staging list in merged order and stored coalesced.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* s, const void* g, unsigned bytes,
+                                         unsigned long long* mb) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(s)),
+      "l"(g), "r"(bytes), "r"(smem_u32(mb))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(mb)), "r"(phase)
+        : "memory");
+  }
+}
+
+template <int B, int NT, int IPT>
+struct MergeCfg {
+  static constexpr int TILE = NT * IPT;
+  static constexpr int CAP = TILE + 8;  // tiles absorb short runs of equal survivors
+  static constexpr size_t KEYB = (size_t)CAP * 16 * B;
+  static constexpr size_t OFF_KEYS = 0;
+  // S coefs [coff, coff+nS), Q coefs [nS+4, ...); reused as the output value
+  // staging once every walk has finished reading them
+  static constexpr size_t OFF_COEF = KEYB;
+  static constexpr size_t OFF_OUTV = OFF_COEF;
+  static constexpr size_t OFF_OUTE = (OFF_COEF + (size_t)(CAP + 4) * 8 + 15) & ~(size_t)15;
+  static constexpr size_t OFF_TA = (OFF_OUTE + (size_t)CAP * 2 + 15) & ~(size_t)15;
+  static constexpr size_t OFF_PM = OFF_TA + (size_t)2 * NT * 4;       // present bits of S
+  static constexpr int PMW = (CAP + 31) / 32;
+  static constexpr size_t OFF_PP = OFF_PM + (size_t)PMW * 4;          // their prefix
+  static constexpr size_t OFF_HIST = (OFF_PP + (size_t)PMW * 4 + 15) & ~(size_t)15;
+  static constexpr int HBINS = 2048;  // |c| exponent histogram (u16 per tile) for compress
+  static constexpr size_t bytes(bool hist) { return OFF_HIST + (hist ? HBINS * 2 : 0); }
+};
+
+template <int B>
+__device__ __forceinline__ Key<B> sm_key16(const ull* sk, int e) {
+  Key<B> k;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(sk + (size_t)e * 2 * B);
+#pragma unroll
+  for (int h = 0; h < B; ++h) {
+    ulonglong2 v = p[h];
+    k.w[2 * h] = v.x;
+    k.w[2 * h + 1] = v.y;
+  }
+  return k;
+}
+
+// Output slot rule (no look-back needed): every present survivor and every
+// product owns one slot, in merged order.  A survivor/product pair writes
+// the combined value into the survivor's slot and a dead slot after it;
+// a value failing keep_term leaves a dead slot.  So the tile's output
+// offset is present_before(a0) + b0, known before the tile runs.
 template <int B, int NT, int IPT>
 __global__ void __launch_bounds__(NT) k_merge(
     const ull* __restrict__ keys, const double* __restrict__ coef, Filter filt,
     const unsigned* __restrict__ inv_perm, const ull* __restrict__ part_a,
-    const ull* __restrict__ part_b, size_t ntiles, Key<B> P, double cs, double sn, double drop,
-    ull* __restrict__ out_keys, double* __restrict__ out_coef, ull* __restrict__ tile_status,
-    unsigned* __restrict__ tile_counter, ull* __restrict__ counters, int want_hist, double eps,
-    unsigned* __restrict__ hist) {
-  constexpr int CAP = NT * IPT + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ull* sk = reinterpret_cast<ull*>(smem_raw);
-  double* sv = reinterpret_cast<double*>(sk + (size_t)CAP * 2 * B);
-  int* s_ta = reinterpret_cast<int*>(sv + CAP);
+    const ull* __restrict__ part_b, const ull* __restrict__ part_o, Key<B> P, double cs,
+    double sn, double drop, ull* __restrict__ out_keys, double* __restrict__ out_coef,
+    ull* __restrict__ counters, int want_hist, double eps, unsigned* __restrict__ hist) {
+  using Cfg = MergeCfg<B, NT, IPT>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ull* sk = reinterpret_cast<ull*>(smem_raw + Cfg::OFF_KEYS);
+  double* sc = reinterpret_cast<double*>(smem_raw + Cfg::OFF_COEF);
+  double* outv = reinterpret_cast<double*>(smem_raw + Cfg::OFF_OUTV);
+  unsigned short* oute = reinterpret_cast<unsigned short*>(smem_raw + Cfg::OFF_OUTE);
+  int* s_ta = reinterpret_cast<int*>(smem_raw + Cfg::OFF_TA);
   int* s_tb = s_ta + NT;
-  unsigned* shist = reinterpret_cast<unsigned*>(s_tb + NT);
-  unsigned char* sf = reinterpret_cast<unsigned char*>(shist + 4096);
-  __shared__ ull s_tile, s_base;
-  __shared__ int scratch[NT / 32 + 2];
+  unsigned* spm = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PM);
+  unsigned* spp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PP);
+  unsigned short* shist = reinterpret_cast<unsigned short*>(smem_raw + Cfg::OFF_HIST);
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ int s_cnt[2];
 
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-  if (want_hist)
-    for (int b = threadIdx.x; b < 4096; b += NT) shist[b] = 0;
-  __syncthreads();
-  const ull tile = s_tile;
-  if (tile >= ntiles) return;
+  const size_t tile = blockIdx.x;
   const size_t a0 = part_a[tile], a1 = part_a[tile + 1];
   const size_t b0 = part_b[tile], b1 = part_b[tile + 1];
+  const size_t o0 = part_o[tile], o1 = part_o[tile + 1];
   const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0), n = nS + nQ;
+  const int nslots = (int)(o1 - o0);
+  const int coff = (int)(a0 & 1);
+  const int qc0 = nS + 4;
 
-  for (int e = threadIdx.x; e < nS; e += NT) {
-    const size_t i = a0 + e;
-    Key<B> k = load_key<B>(keys, i);
-    const double c = __ldg(coef + i);
-    const bool id = key_is_identity<B>(k);
-    const double v = anticommutes<B>(k, P) ? __dmul_rn(c, cs) : c;
-#pragma unroll
-    for (int w = 0; w < 2 * B; ++w) sk[(size_t)e * 2 * B + w] = k.w[w];
-    sv[e] = v;
-    sf[e] = (unsigned char)((filter_keep(filt, i, c, id) ? 1 : 0) | (id ? 2 : 0));
+  // ---- stage: survivors by TMA bulk copy, products by cp.async gathers
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    if (nS > 0) {
+      const unsigned kb = (unsigned)nS * 16u * B;
+      const size_t c0 = a0 & ~(size_t)1, c1 = (a1 + 1) & ~(size_t)1;
+      const unsigned cb = (unsigned)((c1 - c0) * 8);
+      mbar_expect_tx(&mbar, kb + cb);
+      bulk_g2s(sk, keys + a0 * 2 * B, kb, &mbar);
+      bulk_g2s(sc, coef + c0, cb, &mbar);
+    }
+    s_cnt[0] = s_cnt[1] = 0;
   }
-  for (int e = threadIdx.x; e < nQ; e += NT) {
-    const size_t src = __ldg(inv_perm + b0 + e);
-    Key<B> k = load_key<B>(keys, src);
-    const double c = __ldg(coef + src);
-    const double pr = __dmul_rn(c, sn);
-    const double v = product_phase<B>(k, P) == 1 ? pr : -pr;
-    Key<B> q = key_xor<B>(k, P);
-    const int e2 = nS + e;
+  if (want_hist)
+    for (int b = threadIdx.x; b < Cfg::HBINS / 2; b += NT) reinterpret_cast<unsigned*>(shist)[b] = 0;
+  __syncthreads();  // mbarrier initialised before anyone waits on it
+  for (int j = threadIdx.x; j < nQ; j += NT) {
+    const size_t src = __ldg(inv_perm + b0 + j);
+    const ull* g = keys + src * 2 * B;
+    ull* s = sk + (size_t)(nS + j) * 2 * B;
 #pragma unroll
-    for (int w = 0; w < 2 * B; ++w) sk[(size_t)e2 * 2 * B + w] = q.w[w];
-    sv[e2] = v;
-    sf[e2] = (unsigned char)(filter_keep(filt, src, c, false) ? 1 : 0);
+    for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, g + 2 * h);
+    cp_async8(sc + qc0 + j, coef + src);
   }
+  cp_async_wait_all();
+  if (nS > 0) mbar_wait(&mbar, 0);
   __syncthreads();
+  if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar)) : "memory");
 
-  // per-thread merge-path split inside the tile (pairs never split)
+  // ---- present bits of the survivors (+ their prefix) for slot offsets
+  {
+    const int lane = threadIdx.x & 31;
+    for (int e0 = (threadIdx.x & ~31); e0 < nS; e0 += NT) {
+      const int e = e0 + lane;
+      bool pr = false;
+      if (e < nS) {
+        const Key<B> k = sm_key16<B>(sk, e);
+        pr = filter_keep(filt, a0 + e, sc[coff + e], a0 + e == 0 && key_is_identity<B>(k));
+      }
+      const unsigned word = __ballot_sync(0xffffffffu, pr);
+      if (lane == 0) spm[e0 >> 5] = word;
+    }
+  }
+  // Q rows stay raw in shared memory; their product key is row ^ P (on the fly)
+  auto qkey = [&](int j) { return key_xor<B>(sm_key16<B>(sk, nS + j), P); };
+
+  // ---- per-thread merge-path split (runs of equal survivors stay with their product)
   {
     const int d = min((int)threadIdx.x * IPT, n);
     int lo = max(0, d - nQ), hi = min(d, nS);
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (key_cmp<B>(sm_key<B>(sk, mid), sm_key<B>(sk, nS + d - 1 - mid)) <= 0)
+      const int mid = (lo + hi) >> 1;
+      if (key_cmp<B>(sm_key16<B>(sk, mid), qkey(d - 1 - mid)) <= 0)
         lo = mid + 1;
       else
         hi = mid;
     }
-    int a = lo, b = d - lo;
-    if (a > 0 && b < nQ && key_cmp<B>(sm_key<B>(sk, a - 1), sm_key<B>(sk, nS + b)) == 0) --a;
+    int a = lo;
+    const int b = d - lo;
+    if (b < nQ) {
+      const Key<B> q = qkey(b);
+      while (a > 0 && key_cmp<B>(sm_key16<B>(sk, a - 1), q) == 0) --a;
+    }
     s_ta[threadIdx.x] = a;
     s_tb[threadIdx.x] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive prefix of the present-bit words
+    const int nw = (nS + 31) >> 5;
+    unsigned carry = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int w = w0 + threadIdx.x;
+      const unsigned c = w < nw ? __popc(spm[w]) : 0u;
+      const unsigned inc = warp_inclusive(c, OpAdd());
+      if (w < nw) spp[w] = carry + inc - c;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
   }
   __syncthreads();
   const int ia0 = s_ta[threadIdx.x], ib0 = s_tb[threadIdx.x];
   const int ia1 = threadIdx.x + 1 < NT ? s_ta[threadIdx.x + 1] : nS;
   const int ib1 = threadIdx.x + 1 < NT ? s_tb[threadIdx.x + 1] : nQ;
+  auto present = [&](int e) { return (spm[e >> 5] >> (e & 31)) & 1u; };
+  int slot = (ia0 < nS ? (int)(spp[ia0 >> 5] + __popc(spm[ia0 >> 5] & ((1u << (ia0 & 31)) - 1u)))
+                       : (int)(spp[(nS - 1) >> 5] + __popc(spm[(nS - 1) >> 5] & (0xffffffffu >> (31 - ((nS - 1) & 31))))));
+  if (nS == 0) slot = 0;
+  slot += ib0;
 
-  // walk: calls emit(entry index for the key, value) for every surviving output
-  auto walk = [&](auto&& emit) {
+  // ---- single walk; slot values held in registers until the staging is free
+  double ov[IPT + 2];
+  unsigned short oe[IPT + 2];
+  int cnt = 0;
+  {
     int i = ia0, j = ib0;
+    Key<B> ks, kq;
+    if (i < ia1) ks = sm_key16<B>(sk, i);
+    if (j < ib1) kq = qkey(j);
+#pragma unroll 1
     while (i < ia1 || j < ib1) {
-      int c;
-      if (j >= ib1)
-        c = -1;
-      else if (i >= ia1)
-        c = 1;
-      else
-        c = key_cmp<B>(sm_key<B>(sk, i), sm_key<B>(sk, nS + j));
-      if (c < 0) {
-        const unsigned char f = sf[i];
-        if ((f & 1) && keep_term(sv[i], f & 2, drop)) emit(i, sv[i], (f & 2) != 0);
-        ++i;
-      } else if (c > 0) {
-        const unsigned char f = sf[nS + j];
-        if ((f & 1) && keep_term(sv[nS + j], false, drop)) emit(nS + j, sv[nS + j], false);
-        ++j;
-      } else {
-        const unsigned char fs = sf[i], fq = sf[nS + j];
-        const bool ps = fs & 1, pq = fq & 1;
-        if (ps || pq) {
-          double v = ps && pq ? __dadd_rn(sv[i], sv[nS + j]) : (ps ? sv[i] : sv[nS + j]);
-          if (keep_term(v, fs & 2, drop)) emit(i, v, (fs & 2) != 0);
+      const int c = j >= ib1 ? -1 : (i >= ia1 ? 1 : key_cmp<B>(ks, kq));
+      if (c <= 0) {
+        const bool pres = present(i);
+        const size_t gi = a0 + i;
+        const bool id = gi == 0 && key_is_identity<B>(ks);
+        double v = 0.0;
+        if (pres) {
+          const double cv = sc[coff + i];
+          v = anticommutes<B>(ks, P) ? __dmul_rn(cv, cs) : cv;
         }
+        if (c == 0) {
+          const double pr = __dmul_rn(sc[qc0 + j], sn);
+          const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
+          if (pres) {
+            const double sum = __dadd_rn(v, qv);
+            ov[cnt] = keep_term(sum, id, drop) ? sum : dead_value();
+            oe[cnt++] = (unsigned short)i;
+            ov[cnt] = dead_value();  // the product's slot
+            oe[cnt++] = (unsigned short)(nS + j);
+          } else {
+            ov[cnt] = keep_term(qv, false, drop) ? qv : dead_value();
+            oe[cnt++] = (unsigned short)(nS + j);
+          }
+        } else if (pres) {
+          ov[cnt] = keep_term(v, id, drop) ? v : dead_value();
+          oe[cnt++] = (unsigned short)i;
+        }
+      } else {
+        const double pr = __dmul_rn(sc[qc0 + j], sn);
+        const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
+        ov[cnt] = keep_term(qv, false, drop) ? qv : dead_value();
+        oe[cnt++] = (unsigned short)(nS + j);
+      }
+      if (c <= 0) {
+        // a dead duplicate of this key (previous step's pair) follows: skip it
         ++i;
-        ++j;
+        while (i < ia1 && !present(i) && key_cmp<B>(sm_key16<B>(sk, i), ks) == 0) ++i;
+        if (i < ia1) ks = sm_key16<B>(sk, i);
+      }
+      if (c >= 0 && ++j < ib1) kq = qkey(j);
+    }
+  }
+  __syncthreads();  // every walk has finished reading the coefficient area
+#pragma unroll
+  for (int k = 0; k < IPT + 2; ++k)
+    if (k < cnt) {
+      outv[slot + k] = ov[k];
+      oute[slot + k] = oe[k];
+    }
+  __syncthreads();
+  int n_eps = 0, n_dead = 0;
+  for (int q = threadIdx.x; q < nslots; q += NT) {
+    const int e = oute[q];
+    const double v = outv[q];
+    const Key<B> k = e < nS ? sm_key16<B>(sk, e) : qkey(e - nS);
+    store_key<B>(out_keys, o0 + q, k);
+    out_coef[o0 + q] = v;
+    if (is_dead(v)) {
+      ++n_dead;
+    } else if (want_hist) {
+      const double a = fabs(v);
+      const bool id = o0 + q == 0 && key_is_identity<B>(k);
+      if (id || a >= eps) ++n_eps;
+      if (!id && a >= eps) {
+        const unsigned bin = (unsigned)(__double_as_longlong(a) >> 52);
+        atomicAdd(reinterpret_cast<unsigned*>(shist) + (bin >> 1), (bin & 1u) ? 0x10000u : 1u);
       }
     }
-  };
-
-  int cnt = 0;
-  walk([&](int, double, bool) { ++cnt; });
-  int total;
-  const int excl = block_exclusive<NT>(cnt, 0, OpAdd(), scratch, &total);
-  if (threadIdx.x == 0) {
-    s_base = lookback_exclusive(tile_status, tile, (ull)total);
-    if (tile == ntiles - 1) counters[0] = s_base + total;
+  }
+  n_dead = __reduce_add_sync(0xffffffffu, n_dead);
+  n_eps = __reduce_add_sync(0xffffffffu, n_eps);
+  if ((threadIdx.x & 31) == 0) {
+    if (n_dead) atomicAdd(&s_cnt[0], n_dead);
+    if (n_eps) atomicAdd(&s_cnt[1], n_eps);
   }
   __syncthreads();
-  size_t pos = s_base + excl;
-  int n_eps = 0;
-  walk([&](int e, double v, bool id) {
-    Key<B> k = sm_key<B>(sk, e);
-    store_key<B>(out_keys, pos, k);
-    out_coef[pos] = v;
-    ++pos;
-    if (want_hist) {
-      const double a = fabs(v);
-      if (id || a >= eps) ++n_eps;
-      if (!id && a >= eps) atomicAdd(shist + (unsigned)(__double_as_longlong(a) >> 51), 1u);
-    }
-  });
-  if (want_hist) {
-    int tot_eps;
-    block_exclusive<NT>(n_eps, 0, OpAdd(), scratch, &tot_eps);
-    if (threadIdx.x == 0 && tot_eps) atomicAdd(counters + 1, (ull)tot_eps);
-    __syncthreads();
-    for (int b = threadIdx.x; b < 4096; b += NT)
-      if (shist[b]) atomicAdd(hist + b, shist[b]);
+  if (threadIdx.x == 0) {
+    if (s_cnt[0]) atomicAdd(counters + 2, (ull)s_cnt[0]);
+    if (s_cnt[1]) atomicAdd(counters + 1, (ull)s_cnt[1]);
   }
+  if (want_hist)
+    for (int b = threadIdx.x; b < Cfg::HBINS / 2; b += NT) {
+      const unsigned w = reinterpret_cast<unsigned*>(shist)[b];
+      if (w & 0xFFFFu) atomicAdd(hist + 2 * b, w & 0xFFFFu);
+      if (w >> 16) atomicAdd(hist + 2 * b + 1, w >> 16);
+    }
 }
+
+/// Merge tile shapes (NT threads x IPT items); the default per block count
+/// can be overridden for tuning with IQCC_MERGE_CFG=<index>.
+struct MergeShape {
+  int nt, ipt;
+};
+constexpr MergeShape kMergeShapes[] = {{256, 4}, {128, 4}, {128, 8}, {256, 2}, {512, 2}, {64, 8}};
 
 // ------------------------------------------------------------- host side
 namespace {
@@ -604,8 +844,46 @@ std::vector<int> level_positions(const Key<B>& P) {
   return pos;  // ascending canonical positions
 }
 
-template <int B>
-constexpr int merge_threads() { return B >= 4 ? 128 : 256; }
+
+template <int B, int NT, int IPT>
+size_t launch_merge(DeviceStore& s, const unsigned* inv_perm, size_t M, size_t A, const Key<B>& P,
+                    double cs, double sn, double drop, bool want_hist, double eps,
+                    const unsigned* pmask, const unsigned* ppre, size_t W, const unsigned* ptotal) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  constexpr int TILEM = NT * IPT;
+  const size_t total = M + A;
+  const size_t ntm = std::max<size_t>(1, (total + TILEM - 1) / TILEM);
+  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1));
+  ull* pb = pa + (ntm + 1);
+  ull* po = pb + (ntm + 1);
+  {
+    KernelScope ks("partition");
+    k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
+        s.keys(), inv_perm, M, A, P, TILEM, ntm, pa, pb, po, pmask, ppre, W, ptotal);
+  }
+  ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
+  double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
+  ull* ctr = ws.counters.as<ull>(8);
+  unsigned* hist = ws.hist.as<unsigned>(4096);  // first 2048 bins used (exponent of |c|)
+  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
+  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), st));
+  const size_t smem = MergeCfg<B, NT, IPT>::bytes(want_hist);
+  static bool attr = false;
+  if (!attr) {
+    IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)MergeCfg<B, NT, IPT>::bytes(true)));
+    attr = true;
+  }
+  {
+    KernelScope ks("merge");
+    k_merge<B, NT, IPT><<<(unsigned)ntm, NT, smem, st>>>(s.keys(), s.coef(), s.filt, inv_perm, pa,
+                                                        pb, po, P, cs, sn, drop, out_keys, out_coef,
+                                                        ctr, want_hist ? 1 : 0, eps, hist);
+  }
+  IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
+  return ntm;
+}
 
 template <int B>
 DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
@@ -617,20 +895,39 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
   DressOutcome out;
   size_t A = 0;
   unsigned* inv_perm = nullptr;
-  if (sn != 0.0 && M > 0) {
-    const std::vector<int> pos = level_positions<B>(P);
-    const int m = (int)pos.size();
-    const int nch = (m + kLevelsPerChunk - 1) / kLevelsPerChunk;
+  const std::vector<int> pos = level_positions<B>(P);
+  const int m = (int)pos.size();
+  const int nch = (m + kLevelsPerChunk - 1) / kLevelsPerChunk;
+  const size_t W = (M + 31) / 32;
+  unsigned* fmask = ws.fmask.as<unsigned>(2 * std::max<size_t>(W, 1) + 64);
+  unsigned* pmask = fmask + std::max<size_t>(W, 1);
+  unsigned* ppre = ws.tables.as<unsigned>(std::max<size_t>(W, 1) + (W + PW - 1) / PW + 8);
+  unsigned* bsum = ppre + std::max<size_t>(W, 1);
+  unsigned* ptotal = bsum + (W + PW - 1) / PW + 4;
+  IQCC_CUDA(cudaMemsetAsync(ptotal, 0, sizeof(unsigned), st));
+  short* lcp = nullptr;
+  unsigned char* mb = nullptr;
+  if (M > 0) {
     int* d_lvl = ws.levels.as<int>(m);
     IQCC_CUDA(cudaMemcpyAsync(d_lvl, pos.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
-    short* lcp = ws.lcp.as<short>(M);
-    unsigned char* mb = ws.mbits.as<unsigned char>((size_t)nch * M);
-    unsigned* fmask = ws.fmask.as<unsigned>((M + 31) / 32);
+    lcp = ws.lcp.as<short>(M);
+    mb = ws.mbits.as<unsigned char>((size_t)nch * M);
     {
       KernelScope ks("classify");
-      k_classify<B><<<(unsigned)((M + 255) / 256), 256, 0, st>>>(s.keys(), M, P, d_lvl, m, lcp, mb,
-                                                                  fmask);
+      k_classify<B><<<(unsigned)((M + 255) / 256), 256, 0, st>>>(s.keys(), s.coef(), s.filt, M,
+                                                                  P, d_lvl, m, lcp, mb, fmask, pmask);
     }
+    const size_t nb = (W + PW - 1) / PW;
+    {
+      KernelScope ks("present");
+      k_popc_blocks<<<(unsigned)nb, 256, 0, st>>>(pmask, W, bsum);
+      k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, ptotal);
+      k_popc_prefix<<<(unsigned)nb, 256, 0, st>>>(pmask, W, bsum, ppre);
+      count_launch("present");
+      count_launch("present");
+    }
+  }
+  if (sn != 0.0 && M > 0) {
     const size_t ntiles = (M + TILE - 1) / TILE;
     const size_t ngroups = (ntiles + GROUP - 1) / GROUP;
     if (ngroups > 1024) throw std::runtime_error("dress: more than 2^31 terms on one device");
@@ -658,14 +955,22 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
         thr.t[2 * lv + 1] = b;  // child split: lcp <= b
       }
       {
-        KernelScope ks("rank");
+        KernelScope ks("tile_agg");
         k_tile_agg<<<(unsigned)ntiles, TT, 0, st>>>(lcp, fmask, M, thr, tile_cnt, fwd_agg, bwd_agg);
+      }
+      {
+        KernelScope ks("carry");
         k_group_agg<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
                                                          g_cnt, g_fwd, g_bwd);
         k_group_scan<<<1, 1024, 0, st>>>(ngroups, thr.n, g_cnt, g_fwd, g_bwd, a_total);
         k_tile_carry<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
                                                           g_cnt, g_fwd, g_bwd, a_total, tile_pfx,
                                                           fwd_carry, bwd_carry);
+        count_launch("carry");
+        count_launch("carry");
+      }
+      {
+        KernelScope ks("rank");
         if (c == nch - 1)
           k_rank<true><<<(unsigned)ntiles, TT, 0, st>>>(lcp, mb + (size_t)c * M, fmask, M, thr,
                                                         tile_pfx, fwd_carry, bwd_carry, rdelta,
@@ -674,10 +979,6 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
           k_rank<false><<<(unsigned)ntiles, TT, 0, st>>>(lcp, mb + (size_t)c * M, fmask, M, thr,
                                                          tile_pfx, fwd_carry, bwd_carry, rdelta,
                                                          c > 0, inv_perm);
-        count_launch("rank");
-        count_launch("rank");
-        count_launch("rank");
-        count_launch("rank");
       }
     }
     long long a_host = 0;
@@ -687,46 +988,29 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
   }
   out.n_anticommuting = A;
 
-  constexpr int NT = merge_threads<B>(), IPT = 8, TILEM = NT * IPT;
-  const size_t total = M + A;
-  const size_t ntm = std::max<size_t>(1, (total + TILEM - 1) / TILEM);
-  ull* pa = ws.part_a.as<ull>(ntm + 1);
-  ull* pb = ws.part_b.as<ull>(ntm + 1);
-  {
-    KernelScope ks("partition");
-    k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(s.keys(), inv_perm, M, A, P,
-                                                                      TILEM, ntm, pa, pb);
+  static int shape = -1;
+  if (shape < 0) {
+    const char* env = getenv("IQCC_MERGE_CFG");
+    shape = env ? atoi(env) : (B >= 4 ? 3 : 1);
+    if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 1;
   }
-  ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
-  double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
-  ull* tstat = ws.tile_status.as<ull>(ntm + 1);
+  switch (shape) {
+    case 0: launch_merge<B, 256, 4>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+    case 1: launch_merge<B, 128, 4>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+    case 2: launch_merge<B, 128, 8>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+    case 3: launch_merge<B, 256, 2>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+    case 4: launch_merge<B, 512, 2>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+    default: launch_merge<B, 64, 8>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+  }
   ull* ctr = ws.counters.as<ull>(8);
-  unsigned* hist = ws.hist.as<unsigned>(4096);
-  IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntm + 1) * sizeof(ull), st));
-  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
-  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, 4096 * sizeof(unsigned), st));
-  unsigned* tile_counter = reinterpret_cast<unsigned*>(ctr + 4);
-  const size_t smem = MergeSmem<B>::bytes(TILEM + 1, NT);
-  static bool attr = false;
-  if (!attr) {
-    IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    attr = true;
-  }
-  {
-    KernelScope ks("merge");
-    k_merge<B, NT, IPT><<<(unsigned)ntm, NT, smem, st>>>(
-        s.keys(), s.coef(), s.filt, inv_perm, pa, pb, ntm, P, cs, sn, drop, out_keys, out_coef,
-        tstat, tile_counter, ctr, want_hist ? 1 : 0, eps, hist);
-  }
-  ull hc[2] = {0, 0};
-  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 2 * sizeof(ull), cudaMemcpyDeviceToHost, st));
+  ull hc[4] = {0, 0, 0, 0};
+  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 4 * sizeof(ull), cudaMemcpyDeviceToHost, st));
   IQCC_CUDA(cudaStreamSynchronize(st));
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
-  s.M = hc[0];
+  s.M = hc[3];              // physical slots (live + dead)
   s.filt = Filter{};
-  s.logical = s.M;
+  s.logical = hc[3] - hc[2];  // minus dead slots
   out.count_eps = hc[1];
   return out;
 }

@@ -131,7 +131,19 @@ struct Filter {
   ull cut = 0;
 };
 
+/// Dead slot: a term removed by a dressing step (cancelled partner or below
+/// the drop threshold) whose slot was kept so that every output tile's
+/// offset is known before the merge runs.  Encoded as a NaN payload that a
+/// live coefficient never carries (uploads reject NaN); the next step skips
+/// dead slots and does not re-emit them.
+constexpr ull kDeadBits = 0x7FF4DEAD0000DEADull;
+__device__ __forceinline__ bool is_dead(double c) {
+  return (ull)__double_as_longlong(c) == kDeadBits;
+}
+__device__ __forceinline__ double dead_value() { return __longlong_as_double((long long)kDeadBits); }
+
 __device__ __forceinline__ bool filter_keep(const Filter& f, size_t i, double c, bool identity) {
+  if (is_dead(c)) return false;
   if (identity || !f.active) return true;
   double a = fabs(c);
   if (!(a >= f.eps)) return false;
@@ -232,28 +244,48 @@ struct OpMin {
 
 /// Decoupled look-back (single-pass prefix over tiles processed in
 /// dynamic-id order).  status[t]: bits 63:62 = 0 invalid / 1 aggregate /
-/// 2 inclusive prefix, bits 61:0 = value.  Called by ONE thread per tile.
-__device__ __forceinline__ ull lookback_exclusive(ull* status, ull tile, ull agg) {
+/// 2 inclusive prefix, bits 61:0 = value.  Called by ALL 32 lanes of ONE
+/// warp per tile: each probe reads 32 predecessors in parallel and stops at
+/// the nearest one carrying an inclusive prefix.  Returns the exclusive
+/// prefix to every lane.
+__device__ __forceinline__ ull ld_acquire(const ull* p) {
+  ull v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(ull* p, ull v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ ull lookback_warp(ull* status, ull tile, ull agg) {
   const ull AGG = 1ull << 62, PFX = 2ull << 62, VAL = (1ull << 62) - 1;
+  const int lane = threadIdx.x & 31;
   if (tile == 0) {
-    __threadfence();
-    atomicExch(status, PFX | agg);
+    if (lane == 0) st_release(status, PFX | agg);
     return 0;
   }
-  atomicExch(status + tile, AGG | agg);
-  __threadfence();
+  if (lane == 0) st_release(status + tile, AGG | agg);
   ull excl = 0;
-  long long p = (long long)tile - 1;
+  long long end = (long long)tile - 1;
   for (;;) {
-    ull v = atomicAdd(status + p, 0ull);
-    ull flag = v & ~VAL;
-    if (flag == 0) continue;
-    excl += v & VAL;
-    if (flag == PFX) break;
-    --p;
+    const long long idx = end - lane;
+    ull v = idx >= 0 ? ld_acquire(status + idx) : PFX;
+    while (__any_sync(0xffffffffu, (v & ~VAL) == 0)) {
+      if ((v & ~VAL) == 0) v = ld_acquire(status + idx);
+    }
+    const unsigned pm = __ballot_sync(0xffffffffu, (v & ~VAL) == PFX);
+    ull part = v & VAL;
+    if (pm) {
+      const int first = __ffs(pm) - 1;
+      if (lane > first) part = 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    excl += part;
+    if (pm) break;
+    end -= 32;
   }
-  __threadfence();
-  atomicExch(status + tile, PFX | (excl + agg));
+  if (lane == 0) st_release(status + tile, PFX | (excl + agg));
   return excl;
 }
 

@@ -5,7 +5,7 @@
 // and, when more than max_terms remain, the max_terms-1 (identity present)
 // largest |c| with canonical order (= store index order) breaking ties.  On
 // the device this is a radix select on the IEEE bit pattern of |c| (monotone
-// for non-negative doubles): a 4096-bin histogram of the top 12 bits (fused
+// for non-negative doubles): a 2048-bin histogram of the exponent (fused
 // into the merge kernel after a dressing step), a candidate gather of the
 // selected bin, 16-bit digit histograms down to the exact threshold value v,
 // and the index cut among the ties at v.  The result is a lazy Filter
@@ -59,7 +59,7 @@ __global__ void k_upload(const ull* __restrict__ rows, const double* __restrict_
   store_key<B>(keys, i, k);
   const double re = coeff[2 * i], im = coeff[2 * i + 1];
   coef[i] = re;
-  if (im != 0.0) atomicMin(err, (ull)i + 1);
+  if (im != 0.0 || re != re) atomicMin(err, (ull)i + 1);  // complex or NaN
   if (i > 0) {
 #pragma unroll
     for (int w = 0; w < 2 * B; ++w) p.w[w] = __brevll(rows[(i - 1) * 2 * B + w]);
@@ -116,8 +116,8 @@ void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const d
   IQCC_CUDA(cudaStreamSynchronize(st));
   if (h[0] != ULLONG_MAX)
     throw std::invalid_argument("coefficient " + std::to_string(h[0] - 1) +
-                                " has a nonzero imaginary part; the device engine stores real "
-                                "coefficients only");
+                                " is NaN or has a nonzero imaginary part; the device engine stores "
+                                "real, finite-or-infinite coefficients only");
   if (h[1] != ULLONG_MAX)
     throw std::invalid_argument("terms are not in canonical order / not unique at index " +
                                 std::to_string(h[1] - 1));
@@ -156,9 +156,12 @@ __global__ void __launch_bounds__(CT) k_compact(const ull* __restrict__ keys,
   }
   int total;
   const int excl = block_exclusive<CT>((int)__popc(keep), 0, OpAdd(), scratch, &total);
-  if (threadIdx.x == 0) {
-    s_base = lookback_exclusive(tile_status, tile, (ull)total);
-    if (tile == ntiles - 1) *total_out = s_base + total;
+  if (threadIdx.x < 32) {
+    const ull bse = lookback_warp(tile_status, tile, (ull)total);
+    if (threadIdx.x == 0) {
+      s_base = bse;
+      if (tile == ntiles - 1) *total_out = bse + total;
+    }
   }
   __syncthreads();
   size_t pos = s_base + excl;
@@ -207,7 +210,7 @@ static size_t run_compact(DeviceStore& s, int mode, uint32_t Bout, ull* okeys, d
 }
 
 void store_materialize(DeviceStore& s) {
-  if (!s.filt.active) return;
+  if (!s.filt.active && s.M == s.logical) return;  // no filter, no dead slots
   Workspace& ws = workspace();
   ull* ok = ws.out_keys.as<ull>(std::max<size_t>(s.M, 1) * 2 * s.B);
   double* oc = ws.out_coef.as<double>(std::max<size_t>(s.M, 1));
@@ -367,9 +370,12 @@ __global__ void __launch_bounds__(CT) k_gather_compact(const ull* __restrict__ k
     if (first + k < N && flag[first + k]) keep |= 1u << k;
   int total;
   const int excl = block_exclusive<CT>((int)__popc(keep), 0, OpAdd(), scratch, &total);
-  if (threadIdx.x == 0) {
-    s_base = lookback_exclusive(tile_status, tile, (ull)total);
-    if (tile == ntiles - 1) *total_out = s_base + total;
+  if (threadIdx.x < 32) {
+    const ull bse = lookback_warp(tile_status, tile, (ull)total);
+    if (threadIdx.x == 0) {
+      s_base = bse;
+      if (tile == ntiles - 1) *total_out = bse + total;
+    }
   }
   __syncthreads();
   size_t pos = s_base + excl;
@@ -457,8 +463,8 @@ void store_generate_mol(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
 template <int B>
 __global__ void k_hist_eps(const ull* __restrict__ keys, const double* __restrict__ coef, size_t M,
                            double eps, unsigned* __restrict__ hist, ull* __restrict__ ctr) {
-  __shared__ unsigned sh[4096];
-  for (int b = threadIdx.x; b < 4096; b += blockDim.x) sh[b] = 0;
+  __shared__ unsigned sh[2048];
+  for (int b = threadIdx.x; b < 2048; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   int n_eps = 0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < M;
@@ -466,12 +472,12 @@ __global__ void k_hist_eps(const ull* __restrict__ keys, const double* __restric
     const double a = fabs(coef[i]);
     const bool id = i == 0 && key_is_identity<B>(load_key<B>(keys, 0));
     if (id || a >= eps) ++n_eps;
-    if (!id && a >= eps) atomicAdd(sh + (unsigned)(__double_as_longlong(a) >> 51), 1u);
+    if (!id && a >= eps) atomicAdd(sh + (unsigned)(__double_as_longlong(a) >> 52), 1u);
   }
   n_eps = __reduce_add_sync(0xffffffffu, n_eps);
   if ((threadIdx.x & 31) == 0 && n_eps) atomicAdd(ctr + 1, (ull)n_eps);
   __syncthreads();
-  for (int b = threadIdx.x; b < 4096; b += blockDim.x)
+  for (int b = threadIdx.x; b < 2048; b += blockDim.x)
     if (sh[b]) atomicAdd(hist + b, sh[b]);
 }
 
@@ -484,9 +490,15 @@ __global__ void k_gather_bin(const ull* __restrict__ keys, const double* __restr
   const double a = fabs(coef[i]);
   if (!(a >= eps)) return;
   const ull bits = (ull)__double_as_longlong(a);
-  if ((unsigned)(bits >> 51) != bin) return;
+  if ((unsigned)(bits >> 52) != bin) return;
   if (i == 0 && key_is_identity<B>(load_key<B>(keys, 0))) return;
-  const ull slot = atomicAdd(ctr + 2, 1ull);
+  // warp-aggregated slot allocation (one atomic per warp, not per candidate)
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+  ull base = 0;
+  if (lane == leader) base = atomicAdd(ctr + 2, (ull)__popc(act));
+  base = __shfl_sync(act, base, leader);
+  const ull slot = base + __popc(act & ((1u << lane) - 1u));
   cv[slot] = bits;
   ci[slot] = i;
 }
@@ -504,7 +516,12 @@ __global__ void k_cand_ties(const ull* __restrict__ cv, const ull* __restrict__ 
                             ull value, ull* __restrict__ out, ull* __restrict__ ctr) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= n || cv[i] != value) return;
-  out[atomicAdd(ctr + 3, 1ull)] = ci[i];
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+  ull base = 0;
+  if (lane == leader) base = atomicAdd(ctr + 3, (ull)__popc(act));
+  base = __shfl_sync(act, base, leader);
+  out[base + __popc(act & ((1u << lane) - 1u))] = ci[i];
 }
 
 template <int B>
@@ -517,7 +534,7 @@ __global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __r
   for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const double c = coef[i];
     bool id = i == 0 && key_is_identity<B>(load_key<B>(keys, 0));
-    if (!filter_keep(filt, i, c, id)) acc += fabs(c);
+    if (!is_dead(c) && !filter_keep(filt, i, c, id)) acc += fabs(c);
   }
   double tot;
   block_exclusive<256>(acc, 0.0, OpAdd(), sm, &tot);
@@ -535,10 +552,11 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
     hist_ready = false;
   }
   CompressResult res;
+  const size_t logical_before = s.logical;
   unsigned* hist = ws.hist.as<unsigned>(4096);
   ull* ctr = ws.counters.as<ull>(8);
   if (!hist_ready) {
-    IQCC_CUDA(cudaMemsetAsync(hist, 0, 4096 * sizeof(unsigned), st));
+    IQCC_CUDA(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), st));
     IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
     const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (s.M + 255) / 256));
     if (s.M) {
@@ -566,12 +584,12 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       f.v = HUGE_VAL;
       f.cut = 0;
     } else {
-      std::vector<unsigned> hh(4096);
-      IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, 4096 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      std::vector<unsigned> hh(2048);
+      IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, 2048 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
       size_t cum = 0, r = 0;
       int bin = -1;
-      for (int b = 4095; b >= 0; --b) {
+      for (int b = 2047; b >= 0; --b) {
         if (cum + hh[b] >= budget) {
           bin = b;
           r = budget - cum;
@@ -593,10 +611,10 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
           default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
         }
       }
-      // digits of the low 51 bits, most significant first; larger values first
-      ull known_mask = ~((1ull << 51) - 1), known_val = (ull)bin << 51;
-      const int shifts[4] = {35, 19, 3, 0};
-      const int widths[4] = {16, 16, 16, 3};
+      // digits of the 52 mantissa bits, most significant first; larger values first
+      ull known_mask = ~((1ull << 52) - 1), known_val = (ull)bin << 52;
+      const int shifts[4] = {36, 20, 4, 0};
+      const int widths[4] = {16, 16, 16, 4};
       unsigned* dh = ws.misc2.as<unsigned>(65536);
       std::vector<unsigned> hd(65536);
       for (int round = 0; round < 4; ++round) {
@@ -647,7 +665,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
   if (eps == 0.0 && !f.has_v) f.active = 0;  // nothing to drop
   s.filt = f;
   s.logical = logical;
-  res.dropped_terms = s.M - logical;
+  res.dropped_terms = logical_before - logical;
   if (want_stats && res.dropped_terms > 0) {
     const unsigned grid = 592;
     double* part = ws.partials.as<double>(grid);
