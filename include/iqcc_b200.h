@@ -82,6 +82,10 @@ int iqcc_gpu_sum_download(iqcc_gpu_sum* h, uint64_t* rows, double* coeff, size_t
 int iqcc_gpu_sum_download_device(iqcc_gpu_sum* h, uint64_t* d_rows, double* d_coeff, size_t cap,
                                  size_t* M);
 
+/* Inspection: copy the PHYSICAL device store (bit-reversed key rows [M][2B'],
+ * B' in {1,2,4}; raw coefficients incl. dead-slot NaNs) to host buffers. */
+int iqcc_gpu_sum_raw(iqcc_gpu_sum* h, uint64_t* keys, double* coeff, size_t cap, size_t* M);
+
 /* ---- dressing (iqcc/dressing.hpp) ------------------------------------- */
 typedef struct {
   size_t n_in;             /* logical terms before the step */

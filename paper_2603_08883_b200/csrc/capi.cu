@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -51,6 +53,25 @@ Ctx& ctx() {
 }
 cudaStream_t stream() { return ctx().cur; }
 Workspace& workspace() { return ctx().ws; }
+
+ull* debug_buffer() {
+  Workspace& ws = ctx().ws;
+  if (!ws.dbg.p) {
+    ws.dbg.get(4 * sizeof(ull));
+    IQCC_CUDA(cudaMemsetAsync(ws.dbg.p, 0, 4 * sizeof(ull), stream()));
+  }
+  return static_cast<ull*>(ws.dbg.p);
+}
+
+void debug_check(const char* where) {
+  ull h[3];
+  IQCC_CUDA(cudaMemcpyAsync(h, debug_buffer(), sizeof(h), cudaMemcpyDeviceToHost, stream()));
+  IQCC_CUDA(cudaStreamSynchronize(stream()));
+  if (h[0])
+    throw std::runtime_error(std::string("bounds check failed after ") + where + ": site " +
+                             std::to_string(h[0]) + " index " + std::to_string(h[1]) + " bound " +
+                             std::to_string(h[2]));
+}
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -97,6 +118,11 @@ KernelScope::~KernelScope() {
   if (le != cudaSuccess) {
     // surfaced by the next IQCC_CUDA check; keep the error sticky for the caller
     g_err = std::string("kernel launch failed (") + family + "): " + cudaGetErrorString(le);
+  }
+  static const bool dbg = getenv("IQCC_DEBUG") != nullptr;
+  if (dbg) {
+    cudaError_t e = cudaStreamSynchronize(c.cur);
+    if (e != cudaSuccess) fprintf(stderr, "[iqcc debug] kernel family '%s' failed: %s\n", family, cudaGetErrorString(e));
   }
 }
 
@@ -153,7 +179,7 @@ void Workspace::release_all() {
                    &bwd_carry, &inv_perm, &rdelta, &part_a, &part_b, &tile_status, &counters,
                    &hist, &cand_v, &cand_i, &levels, &stage_rows, &stage_coef, &partials,
                    &grad_part, &tables, &misc, &misc2, &misc3, &xbuf_keys, &xbuf_coef,
-                   &rbuf_keys, &rbuf_coef, &out_keys, &out_coef};
+                   &rbuf_keys, &rbuf_coef, &out_keys, &out_coef, &dbg};
   for (DevBuf* b : all) b->release();
 }
 
@@ -350,6 +376,21 @@ int iqcc_gpu_sum_download_device(iqcc_gpu_sum* h, uint64_t* rows, double* coeff,
   return guarded([&] {
     need(h);
     *M = store_download(h->s, rows, coeff, cap, false);
+  });
+}
+
+/* Debug/inspection: the physical device store (bit-reversed key rows, raw
+ * coefficients including dead-slot NaNs), no filtering. */
+int iqcc_gpu_sum_raw(iqcc_gpu_sum* h, uint64_t* keys, double* coef, size_t cap, size_t* M) {
+  return guarded([&] {
+    need(h);
+    *M = h->s.M;
+    const size_t n = std::min(cap, h->s.M);
+    if (n) {
+      IQCC_CUDA(cudaMemcpyAsync(keys, h->s.keys(), n * 2 * h->s.B * sizeof(ull), cudaMemcpyDeviceToHost, stream()));
+      IQCC_CUDA(cudaMemcpyAsync(coef, h->s.coef(), n * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    }
+    IQCC_CUDA(cudaStreamSynchronize(stream()));
   });
 }
 

@@ -54,39 +54,48 @@ struct Thr {
 };
 
 // ---------------------------------------------------------------- classify
-template <int B>
+template <int B, int IT>
 __global__ void __launch_bounds__(256) k_classify(const ull* __restrict__ keys,
                                                   const double* __restrict__ coef, Filter filt,
-                                                  size_t M, Key<B> P,
-                                                  const int* __restrict__ lvl, int m,
-                                                  short* __restrict__ lcp,
-                                                  unsigned char* __restrict__ mbits,
+                                                  size_t M, Key<B> P, short* __restrict__ lcp,
                                                   unsigned* __restrict__ fmask,
                                                   unsigned* __restrict__ pmask) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  int f = 0, pr = 0;
-  if (i < M) {
-    Key<B> k = load_key<B>(keys, i);
-    int l = -1;
-    if (i > 0) l = key_lcp<B>(load_key<B>(keys, i - 1), k);
-    lcp[i] = (short)l;
-    // dead slots and terms dropped by a pending compress filter are absent:
-    // they emit nothing and generate no product
-    pr = filter_keep(filt, i, __ldg(coef + i), i == 0 && key_is_identity<B>(k));
-    f = pr && anticommutes<B>(k, P);
-    for (int c = 0; c * kLevelsPerChunk < m; ++c) {
-      unsigned byte = 0;
-      for (int j = 0; j < kLevelsPerChunk && c * kLevelsPerChunk + j < m; ++j)
-        byte |= key_bit<B>(k, __ldg(lvl + c * kLevelsPerChunk + j)) << j;
-      mbits[(size_t)c * M + i] = (unsigned char)byte;
+  const int lane = threadIdx.x & 31;
+  const size_t base = blockIdx.x * (size_t)(256 * IT);
+  Key<B> k[IT], pk[IT];
+  double c[IT];
+#pragma unroll
+  for (int j = 0; j < IT; ++j) {  // issue every load first
+    const size_t i = base + (size_t)j * 256 + threadIdx.x;
+    if (i < M) {
+      k[j] = load_key<B>(keys, i);
+      c[j] = __ldg(coef + i);
     }
+    if (lane == 0 && i > 0 && i - 1 < M) pk[j] = load_key<B>(keys, i - 1);
   }
-  const unsigned bal = __ballot_sync(0xffffffffu, f);
-  const unsigned pal = __ballot_sync(0xffffffffu, pr);
-  const size_t i0 = i - (threadIdx.x & 31);
-  if ((threadIdx.x & 31) == 0 && i0 < M) {
-    fmask[i0 >> 5] = bal;
-    pmask[i0 >> 5] = pal;
+#pragma unroll
+  for (int j = 0; j < IT; ++j) {
+    const size_t i = base + (size_t)j * 256 + threadIdx.x;
+#pragma unroll
+    for (int w = 0; w < 2 * B; ++w) {
+      const ull up = __shfl_up_sync(0xffffffffu, k[j].w[w], 1);
+      if (lane > 0) pk[j].w[w] = up;
+    }
+    int f = 0, pr = 0;
+    if (i < M) {
+      lcp[i] = (short)(i > 0 ? key_lcp<B>(pk[j], k[j]) : -1);
+      // dead slots and terms dropped by a pending compress filter are absent:
+      // they emit nothing and generate no product
+      pr = filter_keep(filt, i, c[j], i == 0 && key_is_identity<B>(k[j]));
+      f = pr && anticommutes<B>(k[j], P);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    const unsigned pal = __ballot_sync(0xffffffffu, pr);
+    const size_t i0 = i - lane;
+    if (lane == 0 && i0 < M) {
+      fmask[i0 >> 5] = bal;
+      pmask[i0 >> 5] = pal;
+    }
   }
 }
 
@@ -148,130 +157,6 @@ __device__ __forceinline__ size_t present_before(const unsigned* __restrict__ pm
   const size_t w = a >> 5;
   if (w >= W) return total;
   return (size_t)pre[w] + __popc(pmask[w] & ((1u << (a & 31)) - 1u));
-}
-
-// ------------------------------------------------------------ tile helpers
-struct TileItems {
-  int l[TI];
-  unsigned bits;  // anticommute bits of the thread's TI terms
-};
-
-__device__ __forceinline__ TileItems load_items(const short* __restrict__ lcp,
-                                                const unsigned* __restrict__ fmask, size_t M,
-                                                size_t first) {
-  TileItems it;
-#pragma unroll
-  for (int k = 0; k < TI; ++k) it.l[k] = (first + k < M) ? (int)lcp[first + k] : INT_MAX;
-  it.bits = 0;
-  if (first < M) it.bits = (fmask[first >> 5] >> (first & 31)) & 0xFFu;
-  return it;
-}
-
-template <int NV>
-__device__ __forceinline__ void block_excl_max_vec(int (&v)[NV], int* sm /*[TT/32][NV]*/) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int inc[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) inc[j] = warp_inclusive(v[j], OpMax());
-  if (lane == 31)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) sm[warp * NV + j] = inc[j];
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    int base = -1;
-    for (int w = 0; w < warp; ++w) base = max(base, sm[w * NV + j]);
-    int ex = __shfl_up_sync(0xffffffffu, inc[j], 1);
-    if (lane == 0) ex = -1;
-    v[j] = max(base, ex);
-  }
-  __syncthreads();
-}
-
-template <int NV>
-__device__ __forceinline__ void block_excl_min_rev_vec(int (&v)[NV], int* sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = TT / 32;
-  int inc[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) inc[j] = warp_inclusive_rev(v[j], OpMin());
-  if (lane == 0)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) sm[warp * NV + j] = inc[j];
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    int base = INT_MAX;
-    for (int w = warp + 1; w < NW; ++w) base = min(base, sm[w * NV + j]);
-    int ex = __shfl_down_sync(0xffffffffu, inc[j], 1);
-    if (lane == 31) ex = INT_MAX;
-    v[j] = min(base, ex);
-  }
-  __syncthreads();
-}
-
-// -------------------------------------------------------- tile aggregates
-// fwd_agg[tile][j]: tile-local C of the LAST term with lcp <= thr j (or -1);
-// bwd_agg[tile][j]: tile-local C of the FIRST such term (or -1).
-__global__ void __launch_bounds__(TT) k_tile_agg(const short* __restrict__ lcp,
-                                                 const unsigned* __restrict__ fmask, size_t M,
-                                                 Thr thr, int* __restrict__ tile_cnt,
-                                                 int* __restrict__ fwd_agg,
-                                                 int* __restrict__ bwd_agg) {
-  __shared__ int sm[TT / 32 * kThrPerChunk + 8];
-  __shared__ int s_total;
-  const size_t tile = blockIdx.x;
-  const size_t first = tile * TILE + (size_t)threadIdx.x * TI;
-  TileItems it = load_items(lcp, fmask, M, first);
-  int total;
-  int cl = block_exclusive<TT>((int)__popc(it.bits), 0, OpAdd(), sm, &total);
-  if (threadIdx.x == 0) s_total = total;
-  int fa[kThrPerChunk], ba[kThrPerChunk];
-#pragma unroll
-  for (int j = 0; j < kThrPerChunk; ++j) {
-    fa[j] = -1;
-    ba[j] = INT_MAX;
-  }
-#pragma unroll
-  for (int k = 0; k < TI; ++k) {
-    int ck = cl + __popc(it.bits & ((1u << k) - 1u));
-#pragma unroll
-    for (int j = 0; j < kThrPerChunk; ++j)
-      if (j < thr.n && it.l[k] <= thr.t[j]) {
-        fa[j] = ck;
-        ba[j] = min(ba[j], ck);
-      }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j < kThrPerChunk; ++j) {
-    int a = fa[j], b = ba[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a = max(a, __shfl_xor_sync(0xffffffffu, a, o));
-      b = min(b, __shfl_xor_sync(0xffffffffu, b, o));
-    }
-    fa[j] = a;
-    ba[j] = b;
-  }
-  __shared__ int sf[TT / 32][kThrPerChunk], sb[TT / 32][kThrPerChunk];
-  if (lane == 0)
-#pragma unroll
-    for (int j = 0; j < kThrPerChunk; ++j) {
-      sf[warp][j] = fa[j];
-      sb[warp][j] = ba[j];
-    }
-  __syncthreads();
-  if (threadIdx.x < kThrPerChunk) {
-    int j = threadIdx.x, a = -1, b = INT_MAX;
-    for (int w = 0; w < TT / 32; ++w) {
-      a = max(a, sf[w][j]);
-      b = min(b, sb[w][j]);
-    }
-    fwd_agg[tile * kThrPerChunk + j] = a;
-    bwd_agg[tile * kThrPerChunk + j] = b == INT_MAX ? -1 : b;
-  }
-  if (threadIdx.x == 0) tile_cnt[tile] = s_total;
 }
 
 // ---------------------------------------------------------- carry scans
@@ -386,87 +271,185 @@ __global__ void __launch_bounds__(GROUP) k_tile_carry(const int* __restrict__ ti
   }
 }
 
-// ----------------------------------------------------------------- rank
-template <bool FINAL>
-__global__ void __launch_bounds__(TT) k_rank(const short* __restrict__ lcp,
-                                             const unsigned char* __restrict__ mb,
-                                             const unsigned* __restrict__ fmask, size_t M, Thr thr,
-                                             const int* __restrict__ tile_pfx,
-                                             const int* __restrict__ fwd_carry,
-                                             const int* __restrict__ bwd_carry,
-                                             int* __restrict__ rdelta, int has_rdelta,
-                                             unsigned* __restrict__ inv_perm) {
-  __shared__ int sm[(TT / 32) * kThrPerChunk + 8];
-  const size_t tile = blockIdx.x;
-  const size_t first = tile * TILE + (size_t)threadIdx.x * TI;
-  TileItems it = load_items(lcp, fmask, M, first);
-  unsigned char mbk[TI];
+// ------------------------------------------------- warp-tile rank kernels
+// One warp owns a tile of WT = 32*WI consecutive terms (lane l: terms
+// [WI*l, WI*l+WI)); all scans are warp shuffles, no shared memory or block
+// barriers.  NTHR thresholds per chunk (rounded up to a multiple of 4).
+constexpr int WI = 16;
+constexpr int WT = 32 * WI;
+
+struct WarpItems {
+  int l[WI];
+  unsigned bits;
+};
+
+__device__ __forceinline__ WarpItems load_witems(const short* __restrict__ lcp,
+                                                 const unsigned* __restrict__ fmask, size_t M,
+                                                 size_t first) {
+  WarpItems it;
+  if (first + WI <= M) {
+    const int4* p = reinterpret_cast<const int4*>(lcp + first);
+    int4 v0 = __ldg(p), v1 = __ldg(p + 1);
+    const short* s0 = reinterpret_cast<const short*>(&v0);
+    const short* s1 = reinterpret_cast<const short*>(&v1);
 #pragma unroll
-  for (int k = 0; k < TI; ++k) mbk[k] = (first + k < M) ? mb[first + k] : 0;
-  int cl = block_exclusive<TT>((int)__popc(it.bits), 0, OpAdd(), sm, (int*)nullptr) + tile_pfx[tile];
-  int C[TI], delta[TI];
+    for (int k = 0; k < 8; ++k) {
+      it.l[k] = s0[k];
+      it.l[8 + k] = s1[k];
+    }
+  } else {
 #pragma unroll
-  for (int k = 0; k < TI; ++k) {
+    for (int k = 0; k < WI; ++k) it.l[k] = first + k < M ? (int)lcp[first + k] : INT_MAX;
+  }
+  it.bits = first < M ? (fmask[first >> 5] >> (first & 31)) & 0xFFFFu : 0u;
+  return it;
+}
+
+template <int NTHR>
+__global__ void __launch_bounds__(256) k_tile_agg_w(const short* __restrict__ lcp,
+                                                    const unsigned* __restrict__ fmask, size_t M,
+                                                    size_t ntiles, Thr thr,
+                                                    int* __restrict__ tile_cnt,
+                                                    int* __restrict__ fwd_agg,
+                                                    int* __restrict__ bwd_agg) {
+  const size_t wt = blockIdx.x * (size_t)8 + (threadIdx.x >> 5);
+  if (wt >= ntiles) return;
+  const int lane = threadIdx.x & 31;
+  const size_t first = wt * WT + (size_t)lane * WI;
+  const WarpItems it = load_witems(lcp, fmask, M, first);
+  const int cnt = __popc(it.bits);
+  const int inc = warp_inclusive(cnt, OpAdd());
+  const int cl = inc - cnt;
+#pragma unroll
+  for (int j = 0; j < NTHR; ++j) {
+    const int T = thr.t[j];
+    int fa = -1, ba = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < WI; ++k)
+      if (it.l[k] <= T) fa = cl + __popc(it.bits & ((1u << k) - 1u));
+#pragma unroll
+    for (int k = WI - 1; k >= 0; --k)
+      if (it.l[k] <= T) ba = cl + __popc(it.bits & ((1u << k) - 1u));
+    fa = __reduce_max_sync(0xffffffffu, fa);
+    ba = __reduce_min_sync(0xffffffffu, ba);
+    if (lane == 0) {
+      fwd_agg[wt * kThrPerChunk + j] = fa;
+      bwd_agg[wt * kThrPerChunk + j] = ba == INT_MAX ? -1 : ba;
+    }
+  }
+  if (lane == 31) tile_cnt[wt] = inc;
+}
+
+// A term's side of the split at level l need not be stored: inside its node
+// a split boundary (lcp == b_l) precedes the term iff its bit b_l is 1 and
+// the node's 0-child is non-empty, i.e. iff D = st[le] - st[lt] > 0 in the
+// forward scan.  When the bit is 1 but the 0-child is empty both formulas
+// give 0, so  delta_l = D > 0 ? -D : (bwd[lt] - bwd[le]).
+template <int NTHR, bool FINAL>
+__global__ void __launch_bounds__(256) k_rank_w(const short* __restrict__ lcp,
+                                                const unsigned* __restrict__ fmask, size_t M,
+                                                size_t ntiles, Thr thr,
+                                                const int* __restrict__ tile_pfx,
+                                                const int* __restrict__ fwd_carry,
+                                                const int* __restrict__ bwd_carry,
+                                                int* __restrict__ rdelta, int has_rdelta,
+                                                unsigned* __restrict__ inv_perm,
+                                                const long long* __restrict__ a_total,
+                                                ull* __restrict__ dbg) {
+  const size_t wt = blockIdx.x * (size_t)8 + (threadIdx.x >> 5);
+  if (wt >= ntiles) return;
+  const int lane = threadIdx.x & 31;
+  const size_t first = wt * WT + (size_t)lane * WI;
+  const WarpItems it = load_witems(lcp, fmask, M, first);
+  const int cnt = __popc(it.bits);
+  const int inc = warp_inclusive(cnt, OpAdd());
+  const int cl = inc - cnt + tile_pfx[wt];
+  int C[WI], delta[WI];
+  unsigned used[WI];
+#pragma unroll
+  for (int k = 0; k < WI; ++k) {
     C[k] = cl + __popc(it.bits & ((1u << k) - 1u));
     delta[k] = 0;
+    used[k] = 0;
   }
+  int st[NTHR];
   // forward: last boundary at or before the term
-  int st[kThrPerChunk];
 #pragma unroll
-  for (int j = 0; j < kThrPerChunk; ++j) {
+  for (int j = 0; j < NTHR; ++j) {
     int a = -1;
 #pragma unroll
-    for (int k = 0; k < TI; ++k)
+    for (int k = 0; k < WI; ++k)
       if (it.l[k] <= thr.t[j]) a = C[k];
-    st[j] = a;
+    a = warp_inclusive(a, OpMax());
+    int ex = __shfl_up_sync(0xffffffffu, a, 1);
+    if (lane == 0) ex = -1;
+    st[j] = max(ex, fwd_carry[wt * kThrPerChunk + j]);
   }
-  block_excl_max_vec<kThrPerChunk>(st, sm);
 #pragma unroll
-  for (int j = 0; j < kThrPerChunk; ++j) st[j] = max(st[j], fwd_carry[tile * kThrPerChunk + j]);
+  for (int k = 0; k < WI; ++k) {
 #pragma unroll
-  for (int k = 0; k < TI; ++k) {
-#pragma unroll
-    for (int j = 0; j < kThrPerChunk; ++j)
+    for (int j = 0; j < NTHR; ++j)
       if (it.l[k] <= thr.t[j]) st[j] = C[k];
     if ((it.bits >> k) & 1u) {
 #pragma unroll
-      for (int lv = 0; lv < kLevelsPerChunk; ++lv)
-        if (lv < thr.nlev && ((mbk[k] >> lv) & 1u)) delta[k] -= st[2 * lv + 1] - st[2 * lv];
+      for (int lv = 0; lv < NTHR / 2; ++lv) {
+        const int D = st[2 * lv + 1] - st[2 * lv];
+        if (D > 0) {
+          delta[k] -= D;
+          used[k] |= 1u << lv;
+        }
+      }
     }
   }
   // backward: first boundary strictly after the term
 #pragma unroll
-  for (int j = 0; j < kThrPerChunk; ++j) {
+  for (int j = 0; j < NTHR; ++j) {
     int b = INT_MAX;
 #pragma unroll
-    for (int k = TI - 1; k >= 0; --k)
+    for (int k = WI - 1; k >= 0; --k)
       if (it.l[k] <= thr.t[j]) b = C[k];
-    st[j] = b;
+    b = warp_inclusive_rev(b, OpMin());
+    int ex = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == 31) ex = INT_MAX;
+    st[j] = min(ex, bwd_carry[wt * kThrPerChunk + j]);
   }
-  block_excl_min_rev_vec<kThrPerChunk>(st, sm);
 #pragma unroll
-  for (int j = 0; j < kThrPerChunk; ++j) st[j] = min(st[j], bwd_carry[tile * kThrPerChunk + j]);
-#pragma unroll
-  for (int k = TI - 1; k >= 0; --k) {
+  for (int k = WI - 1; k >= 0; --k) {
     if ((it.bits >> k) & 1u) {
 #pragma unroll
-      for (int lv = 0; lv < kLevelsPerChunk; ++lv)
-        if (lv < thr.nlev && !((mbk[k] >> lv) & 1u)) delta[k] += st[2 * lv] - st[2 * lv + 1];
+      for (int lv = 0; lv < NTHR / 2; ++lv)
+        if (!((used[k] >> lv) & 1u)) delta[k] += st[2 * lv] - st[2 * lv + 1];
     }
 #pragma unroll
-    for (int j = 0; j < kThrPerChunk; ++j)
+    for (int j = 0; j < NTHR; ++j)
       if (it.l[k] <= thr.t[j]) st[j] = C[k];
   }
 #pragma unroll
-  for (int k = 0; k < TI; ++k) {
+  for (int k = 0; k < WI; ++k) {
     if (!((it.bits >> k) & 1u)) continue;
     const size_t g = first + k;
-    int d = delta[k] + (has_rdelta ? rdelta[g] : 0);
-    if (FINAL)
-      inv_perm[C[k] + d] = (unsigned)g;
-    else
+    const int d = delta[k] + (has_rdelta ? rdelta[g] : 0);
+    if (FINAL) {
+      if (dbg_ok(dbg, 1, (ull)(long long)(C[k] + d), (ull)*a_total)) inv_perm[C[k] + d] = (unsigned)g;
+    } else {
       rdelta[g] = d;
+    }
   }
+}
+
+// Debug: inv_perm must be a bijection onto the present anticommuting terms.
+__global__ void k_check_perm(const unsigned* __restrict__ inv_perm, size_t A, size_t M,
+                             const unsigned* __restrict__ fmask, unsigned* __restrict__ seen,
+                             ull* __restrict__ dbg) {
+  const size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (r >= A) return;
+  const unsigned g = inv_perm[r];
+  if (!dbg_ok(dbg, 10, g, M)) return;
+  if (!((fmask[g >> 5] >> (g & 31)) & 1u)) {
+    dbg_ok(dbg, 11, r, 0);
+    return;
+  }
+  if (atomicAdd(seen + g, 1u) != 0) dbg_ok(dbg, 12, r, 0);
 }
 
 // ------------------------------------------------------------- partition
@@ -572,14 +555,14 @@ struct MergeCfg {
   // S coefs [coff, coff+nS), Q coefs [nS+4, ...); reused as the output value
   // staging once every walk has finished reading them
   static constexpr size_t OFF_COEF = KEYB;
-  static constexpr size_t OFF_OUTV = OFF_COEF;
-  static constexpr size_t OFF_OUTE = (OFF_COEF + (size_t)(CAP + 4) * 8 + 15) & ~(size_t)15;
+  static constexpr size_t OFF_OUTV = (OFF_COEF + (size_t)(CAP + 4) * 8 + 15) & ~(size_t)15;
+  static constexpr size_t OFF_OUTE = OFF_OUTV + (size_t)CAP * 8;
   static constexpr size_t OFF_TA = (OFF_OUTE + (size_t)CAP * 2 + 15) & ~(size_t)15;
   static constexpr size_t OFF_PM = OFF_TA + (size_t)2 * NT * 4;       // present bits of S
   static constexpr int PMW = (CAP + 31) / 32;
   static constexpr size_t OFF_PP = OFF_PM + (size_t)PMW * 4;          // their prefix
   static constexpr size_t OFF_HIST = (OFF_PP + (size_t)PMW * 4 + 15) & ~(size_t)15;
-  static constexpr int HBINS = 2048;  // |c| exponent histogram (u16 per tile) for compress
+  static constexpr int HBINS = kHistBins;  // |c| histogram (u16 per tile) for compress
   static constexpr size_t bytes(bool hist) { return OFF_HIST + (hist ? HBINS * 2 : 0); }
 };
 
@@ -607,7 +590,8 @@ __global__ void __launch_bounds__(NT) k_merge(
     const unsigned* __restrict__ inv_perm, const ull* __restrict__ part_a,
     const ull* __restrict__ part_b, const ull* __restrict__ part_o, Key<B> P, double cs,
     double sn, double drop, ull* __restrict__ out_keys, double* __restrict__ out_coef,
-    ull* __restrict__ counters, int want_hist, double eps, unsigned* __restrict__ hist) {
+    ull* __restrict__ counters, int want_hist, double eps, unsigned* __restrict__ hist,
+    ull* __restrict__ dbg) {
   using Cfg = MergeCfg<B, NT, IPT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   ull* sk = reinterpret_cast<ull*>(smem_raw + Cfg::OFF_KEYS);
@@ -719,22 +703,25 @@ __global__ void __launch_bounds__(NT) k_merge(
   if (nS == 0) slot = 0;
   slot += ib0;
 
-  // ---- single walk; slot values held in registers until the staging is free
-  double ov[IPT + 2];
-  unsigned short oe[IPT + 2];
-  int cnt = 0;
+  // ---- single walk; every slot value goes straight to the staging list
   {
     int i = ia0, j = ib0;
     Key<B> ks, kq;
     if (i < ia1) ks = sm_key16<B>(sk, i);
     if (j < ib1) kq = qkey(j);
+    auto put = [&](double v, int e) {
+      if (dbg_ok(dbg, 2, (ull)slot, (ull)nslots)) {
+        outv[slot] = v;
+        oute[slot] = (unsigned short)e;
+      }
+      ++slot;
+    };
 #pragma unroll 1
     while (i < ia1 || j < ib1) {
       const int c = j >= ib1 ? -1 : (i >= ia1 ? 1 : key_cmp<B>(ks, kq));
       if (c <= 0) {
         const bool pres = present(i);
-        const size_t gi = a0 + i;
-        const bool id = gi == 0 && key_is_identity<B>(ks);
+        const bool id = a0 + i == 0 && key_is_identity<B>(ks);
         double v = 0.0;
         if (pres) {
           const double cv = sc[coff + i];
@@ -745,40 +732,23 @@ __global__ void __launch_bounds__(NT) k_merge(
           const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
           if (pres) {
             const double sum = __dadd_rn(v, qv);
-            ov[cnt] = keep_term(sum, id, drop) ? sum : dead_value();
-            oe[cnt++] = (unsigned short)i;
-            ov[cnt] = dead_value();  // the product's slot
-            oe[cnt++] = (unsigned short)(nS + j);
+            put(keep_term(sum, id, drop) ? sum : dead_value(), i);
+            put(dead_value(), nS + j);  // the product's slot
           } else {
-            ov[cnt] = keep_term(qv, false, drop) ? qv : dead_value();
-            oe[cnt++] = (unsigned short)(nS + j);
+            put(keep_term(qv, false, drop) ? qv : dead_value(), nS + j);
           }
         } else if (pres) {
-          ov[cnt] = keep_term(v, id, drop) ? v : dead_value();
-          oe[cnt++] = (unsigned short)i;
+          put(keep_term(v, id, drop) ? v : dead_value(), i);
         }
       } else {
         const double pr = __dmul_rn(sc[qc0 + j], sn);
         const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
-        ov[cnt] = keep_term(qv, false, drop) ? qv : dead_value();
-        oe[cnt++] = (unsigned short)(nS + j);
+        put(keep_term(qv, false, drop) ? qv : dead_value(), nS + j);
       }
-      if (c <= 0) {
-        // a dead duplicate of this key (previous step's pair) follows: skip it
-        ++i;
-        while (i < ia1 && !present(i) && key_cmp<B>(sm_key16<B>(sk, i), ks) == 0) ++i;
-        if (i < ia1) ks = sm_key16<B>(sk, i);
-      }
+      if (c <= 0 && ++i < ia1) ks = sm_key16<B>(sk, i);
       if (c >= 0 && ++j < ib1) kq = qkey(j);
     }
   }
-  __syncthreads();  // every walk has finished reading the coefficient area
-#pragma unroll
-  for (int k = 0; k < IPT + 2; ++k)
-    if (k < cnt) {
-      outv[slot + k] = ov[k];
-      oute[slot + k] = oe[k];
-    }
   __syncthreads();
   int n_eps = 0, n_dead = 0;
   for (int q = threadIdx.x; q < nslots; q += NT) {
@@ -794,7 +764,7 @@ __global__ void __launch_bounds__(NT) k_merge(
       const bool id = o0 + q == 0 && key_is_identity<B>(k);
       if (id || a >= eps) ++n_eps;
       if (!id && a >= eps) {
-        const unsigned bin = (unsigned)(__double_as_longlong(a) >> 52);
+        const unsigned bin = hist_bin(a);
         atomicAdd(reinterpret_cast<unsigned*>(shist) + (bin >> 1), (bin & 1u) ? 0x10000u : 1u);
       }
     }
@@ -837,12 +807,15 @@ Key<B> make_key(const uint64_t* row) {
 
 template <int B>
 std::vector<int> level_positions(const Key<B>& P) {
+  // level order: word ascending, then bit index ascending (matches the pext
+  // in k_classify); any order works for the rank sum
   std::vector<int> pos;
   for (int w = 0; w < 2 * B; ++w)
-    for (int b = 63; b >= 0; --b)
+    for (int b = 0; b < 64; ++b)
       if ((P.w[w] >> b) & 1ull) pos.push_back(64 * w + (63 - b));
-  return pos;  // ascending canonical positions
+  return pos;
 }
+
 
 
 template <int B, int NT, int IPT>
@@ -865,9 +838,9 @@ size_t launch_merge(DeviceStore& s, const unsigned* inv_perm, size_t M, size_t A
   ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
   double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
   ull* ctr = ws.counters.as<ull>(8);
-  unsigned* hist = ws.hist.as<unsigned>(4096);  // first 2048 bins used (exponent of |c|)
+  unsigned* hist = ws.hist.as<unsigned>(kHistBins);
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
-  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), st));
+  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
   const size_t smem = MergeCfg<B, NT, IPT>::bytes(want_hist);
   static bool attr = false;
   if (!attr) {
@@ -879,9 +852,11 @@ size_t launch_merge(DeviceStore& s, const unsigned* inv_perm, size_t M, size_t A
     KernelScope ks("merge");
     k_merge<B, NT, IPT><<<(unsigned)ntm, NT, smem, st>>>(s.keys(), s.coef(), s.filt, inv_perm, pa,
                                                         pb, po, P, cs, sn, drop, out_keys, out_coef,
-                                                        ctr, want_hist ? 1 : 0, eps, hist);
+                                                        ctr, want_hist ? 1 : 0, eps, hist,
+                                                        debug_buffer());
   }
   IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
+  if (getenv("IQCC_DEBUG")) debug_check("merge");
   return ntm;
 }
 
@@ -906,18 +881,16 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
   unsigned* ptotal = bsum + (W + PW - 1) / PW + 4;
   IQCC_CUDA(cudaMemsetAsync(ptotal, 0, sizeof(unsigned), st));
   short* lcp = nullptr;
-  unsigned char* mb = nullptr;
   if (M > 0) {
-    int* d_lvl = ws.levels.as<int>(m);
-    IQCC_CUDA(cudaMemcpyAsync(d_lvl, pos.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
     lcp = ws.lcp.as<short>(M);
-    mb = ws.mbits.as<unsigned char>((size_t)nch * M);
     {
       KernelScope ks("classify");
-      k_classify<B><<<(unsigned)((M + 255) / 256), 256, 0, st>>>(s.keys(), s.coef(), s.filt, M,
-                                                                  P, d_lvl, m, lcp, mb, fmask, pmask);
+      constexpr int IT = B >= 4 ? 2 : 4;
+      k_classify<B, IT><<<(unsigned)((M + 256 * IT - 1) / (256 * IT)), 256, 0, st>>>(
+          s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pmask);
     }
     const size_t nb = (W + PW - 1) / PW;
+    if (getenv("IQCC_DEBUG")) debug_check("classify");
     {
       KernelScope ks("present");
       k_popc_blocks<<<(unsigned)nb, 256, 0, st>>>(pmask, W, bsum);
@@ -927,10 +900,11 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
       count_launch("present");
     }
   }
+  if (getenv("IQCC_DEBUG") && M > 0) debug_check("present");
   if (sn != 0.0 && M > 0) {
-    const size_t ntiles = (M + TILE - 1) / TILE;
+    const size_t ntiles = (M + WT - 1) / WT;
     const size_t ngroups = (ntiles + GROUP - 1) / GROUP;
-    if (ngroups > 1024) throw std::runtime_error("dress: more than 2^31 terms on one device");
+    if (ngroups > 1024) throw std::runtime_error("dress: more than 2^28 terms per device shard");
     int* tile_cnt = ws.tile_cnt.as<int>(ntiles);
     int* fwd_agg = ws.fwd_agg.as<int>(ntiles * kThrPerChunk);
     int* bwd_agg = ws.bwd_agg.as<int>(ntiles * kThrPerChunk);
@@ -944,6 +918,8 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
     long long* a_total = g_bwd + ngroups * kThrPerChunk;
     int* rdelta = nch > 1 ? ws.rdelta.as<int>(M) : nullptr;
     inv_perm = ws.inv_perm.as<unsigned>(M);
+    ull* dbg = debug_buffer();
+    const unsigned wblocks = (unsigned)((ntiles + 7) / 8);
     for (int c = 0; c < nch; ++c) {
       Thr thr;
       thr.nlev = std::min(kLevelsPerChunk, m - c * kLevelsPerChunk);
@@ -954,10 +930,19 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
         thr.t[2 * lv] = b - 1;  // node start: lcp < b
         thr.t[2 * lv + 1] = b;  // child split: lcp <= b
       }
+      const int nthr4 = (thr.n + 3) & ~3;
+      thr.n = nthr4;  // padded thresholds (t = -2) flow through every kernel
+      const bool last = c == nch - 1;
       {
         KernelScope ks("tile_agg");
-        k_tile_agg<<<(unsigned)ntiles, TT, 0, st>>>(lcp, fmask, M, thr, tile_cnt, fwd_agg, bwd_agg);
+        switch (nthr4) {
+          case 4: k_tile_agg_w<4><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
+          case 8: k_tile_agg_w<8><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
+          case 12: k_tile_agg_w<12><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
+          default: k_tile_agg_w<16><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
+        }
       }
+      if (getenv("IQCC_DEBUG")) debug_check("tile_agg");
       {
         KernelScope ks("carry");
         k_group_agg<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
@@ -969,22 +954,39 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
         count_launch("carry");
         count_launch("carry");
       }
+      if (getenv("IQCC_DEBUG")) debug_check("carry");
       {
         KernelScope ks("rank");
-        if (c == nch - 1)
-          k_rank<true><<<(unsigned)ntiles, TT, 0, st>>>(lcp, mb + (size_t)c * M, fmask, M, thr,
-                                                        tile_pfx, fwd_carry, bwd_carry, rdelta,
-                                                        c > 0, inv_perm);
-        else
-          k_rank<false><<<(unsigned)ntiles, TT, 0, st>>>(lcp, mb + (size_t)c * M, fmask, M, thr,
-                                                         tile_pfx, fwd_carry, bwd_carry, rdelta,
-                                                         c > 0, inv_perm);
+#define IQCC_RANK(NT_, F_) k_rank_w<NT_, F_><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_pfx, fwd_carry, bwd_carry, rdelta, c > 0, inv_perm, a_total, dbg)
+        if (last) {
+          switch (nthr4) {
+            case 4: IQCC_RANK(4, true); break;
+            case 8: IQCC_RANK(8, true); break;
+            case 12: IQCC_RANK(12, true); break;
+            default: IQCC_RANK(16, true); break;
+          }
+        } else {
+          switch (nthr4) {
+            case 4: IQCC_RANK(4, false); break;
+            case 8: IQCC_RANK(8, false); break;
+            case 12: IQCC_RANK(12, false); break;
+            default: IQCC_RANK(16, false); break;
+          }
+        }
+#undef IQCC_RANK
       }
     }
+    if (getenv("IQCC_DEBUG")) debug_check("rank");
     long long a_host = 0;
     IQCC_CUDA(cudaMemcpyAsync(&a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     IQCC_CUDA(cudaStreamSynchronize(st));
     A = (size_t)a_host;
+    if (getenv("IQCC_DEBUG") && A > 0) {
+      unsigned* seen = ws.misc2.as<unsigned>(M);
+      IQCC_CUDA(cudaMemsetAsync(seen, 0, M * sizeof(unsigned), st));
+      k_check_perm<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(inv_perm, A, M, fmask, seen, dbg);
+      debug_check("perm check");
+    }
   }
   out.n_anticommuting = A;
 

@@ -151,6 +151,15 @@ __device__ __forceinline__ bool filter_keep(const Filter& f, size_t i, double c,
   return a > f.v || (a == f.v && (ull)i <= f.cut);
 }
 
+/// Coarse |c| histogram bin for compress(): the IEEE exponent of |c|
+/// offset so 2^-192 .. 2^63 map to bins 1..254; smaller/larger values
+/// collect in bins 0/255 (the select then refines over all 63 bits).
+constexpr int kHistBins = 256;
+__device__ __forceinline__ unsigned hist_bin(double a) {
+  const int e = (int)((ull)__double_as_longlong(a) >> 52) - (1023 - 192);
+  return (unsigned)min(max(e, 0), kHistBins - 1);
+}
+
 /// keep_term (iqcc/pauli.hpp:180-184) for a real coefficient.
 __device__ __forceinline__ bool keep_term(double c, bool identity, double thr) {
   if (identity) return true;
@@ -289,6 +298,18 @@ __device__ __forceinline__ ull lookback_warp(ull* status, ull tile, ull agg) {
   return excl;
 }
 
+// ---------------------------------------------------------------- debug
+// Bounds checks on scattered writes: a violation records (site, index,
+// bound) in dbg[0..2] and the write is skipped (see iqcc_gpu debug_check).
+__device__ __forceinline__ bool dbg_ok(ull* dbg, unsigned site, ull idx, ull bound) {
+  if (idx < bound) return true;
+  if (atomicCAS(dbg, 0ull, (ull)site) == 0ull) {
+    dbg[1] = idx;
+    dbg[2] = bound;
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------- host side
 struct Ctx;
 Ctx& ctx();
@@ -322,9 +343,12 @@ struct Workspace {
   DevBuf levels, stage_rows, stage_coef, partials, grad_part, tables, misc, misc2, misc3;
   DevBuf xbuf_keys, xbuf_coef, rbuf_keys, rbuf_coef;
   DevBuf out_keys, out_coef;  // double buffer swapped with the store after a step
+  DevBuf dbg;                 // 4 x u64 bounds-check record
   void release_all();
 };
 Workspace& workspace();
+ull* debug_buffer();          // device dbg record (zeroed at init)
+void debug_check(const char* where);  // throws if a bounds check fired
 
 struct DeviceStore {
   uint32_t n_qubits = 0, B = 1;

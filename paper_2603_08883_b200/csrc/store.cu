@@ -13,6 +13,7 @@
 // is spent on the hot path.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -463,8 +464,8 @@ void store_generate_mol(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
 template <int B>
 __global__ void k_hist_eps(const ull* __restrict__ keys, const double* __restrict__ coef, size_t M,
                            double eps, unsigned* __restrict__ hist, ull* __restrict__ ctr) {
-  __shared__ unsigned sh[2048];
-  for (int b = threadIdx.x; b < 2048; b += blockDim.x) sh[b] = 0;
+  __shared__ unsigned sh[kHistBins];
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   int n_eps = 0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < M;
@@ -472,35 +473,64 @@ __global__ void k_hist_eps(const ull* __restrict__ keys, const double* __restric
     const double a = fabs(coef[i]);
     const bool id = i == 0 && key_is_identity<B>(load_key<B>(keys, 0));
     if (id || a >= eps) ++n_eps;
-    if (!id && a >= eps) atomicAdd(sh + (unsigned)(__double_as_longlong(a) >> 52), 1u);
+    if (!id && a >= eps) atomicAdd(sh + hist_bin(a), 1u);
   }
   n_eps = __reduce_add_sync(0xffffffffu, n_eps);
   if ((threadIdx.x & 31) == 0 && n_eps) atomicAdd(ctr + 1, (ull)n_eps);
   __syncthreads();
-  for (int b = threadIdx.x; b < 2048; b += blockDim.x)
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
     if (sh[b]) atomicAdd(hist + b, sh[b]);
 }
 
 template <int B>
-__global__ void k_gather_bin(const ull* __restrict__ keys, const double* __restrict__ coef,
-                             size_t M, double eps, unsigned bin, ull* __restrict__ cv,
-                             ull* __restrict__ ci, ull* __restrict__ ctr) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  const double a = fabs(coef[i]);
-  if (!(a >= eps)) return;
-  const ull bits = (ull)__double_as_longlong(a);
-  if ((unsigned)(bits >> 52) != bin) return;
-  if (i == 0 && key_is_identity<B>(load_key<B>(keys, 0))) return;
-  // warp-aggregated slot allocation (one atomic per warp, not per candidate)
-  const unsigned act = __activemask();
-  const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-  ull base = 0;
-  if (lane == leader) base = atomicAdd(ctr + 2, (ull)__popc(act));
-  base = __shfl_sync(act, base, leader);
-  const ull slot = base + __popc(act & ((1u << lane) - 1u));
-  cv[slot] = bits;
-  ci[slot] = i;
+__global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys,
+                                                    const double* __restrict__ coef, size_t M,
+                                                    double eps, unsigned bin, ull* __restrict__ cv,
+                                                    ull* __restrict__ ci, ull* __restrict__ ctr) {
+  // 8 coefficients per thread per iteration (4 x 16 B loads in flight)
+  const int lane = threadIdx.x & 31;
+  const bool has_id = key_is_identity<B>(load_key<B>(keys, 0));
+  // warp-uniform trip count: the warp's chunk is 256 consecutive coefficients
+  const size_t warp_id = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t n_warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t wbase = warp_id * 256; wbase < M; wbase += n_warps * 256) {
+    const size_t base = wbase + (size_t)lane * 8;
+    double v[8];
+    if (base + 8 <= M) {
+      const double2* p = reinterpret_cast<const double2*>(coef + base);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 t = __ldg(p + h);
+        v[2 * h] = t.x;
+        v[2 * h + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = base + k < M ? coef[base + k] : 0.0;
+    }
+    unsigned hit = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double a = fabs(v[k]);
+      if (base + k < M && a >= eps && hist_bin(a) == bin && !(base + k == 0 && has_id))
+        hit |= 1u << k;
+    }
+    // warp-aggregated slot allocation (one atomic per warp)
+    const unsigned n = __popc(hit);
+    const unsigned inc = warp_inclusive(n, OpAdd());
+    const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
+    ull slot = 0;
+    if (tot) {
+      if (lane == 31) slot = atomicAdd(ctr + 2, (ull)tot);
+      slot = __shfl_sync(0xffffffffu, slot, 31) + inc - n;
+    }
+    for (int k = 0; k < 8; ++k)
+      if ((hit >> k) & 1u) {
+        cv[slot] = (ull)__double_as_longlong(fabs(v[k]));
+        ci[slot] = base + k;
+        ++slot;
+      }
+  }
 }
 
 __global__ void k_cand_hist(const ull* __restrict__ cv, size_t n, ull known_mask, ull known_val,
@@ -553,10 +583,10 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
   }
   CompressResult res;
   const size_t logical_before = s.logical;
-  unsigned* hist = ws.hist.as<unsigned>(4096);
+  unsigned* hist = ws.hist.as<unsigned>(kHistBins);
   ull* ctr = ws.counters.as<ull>(8);
   if (!hist_ready) {
-    IQCC_CUDA(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), st));
+    IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
     IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
     const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (s.M + 255) / 256));
     if (s.M) {
@@ -584,12 +614,12 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       f.v = HUGE_VAL;
       f.cut = 0;
     } else {
-      std::vector<unsigned> hh(2048);
-      IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, 2048 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      std::vector<unsigned> hh(kHistBins);
+      IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, kHistBins * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
       size_t cum = 0, r = 0;
       int bin = -1;
-      for (int b = 2047; b >= 0; --b) {
+      for (int b = kHistBins - 1; b >= 0; --b) {
         if (cum + hh[b] >= budget) {
           bin = b;
           r = budget - cum;
@@ -603,25 +633,27 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       ull* ci = ws.cand_i.as<ull>(nc);
       IQCC_CUDA(cudaMemsetAsync(ctr + 2, 0, 2 * sizeof(ull), st));
       {
-        KernelScope ks("select");
-        const unsigned grid = (unsigned)((s.M + 255) / 256);
+        KernelScope ks("select_gather");
+        const unsigned grid = (unsigned)std::min<size_t>(148 * 16, std::max<size_t>(1, (s.M + 2047) / 2048));
         switch (s.B) {
           case 1: k_gather_bin<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
           case 2: k_gather_bin<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
           default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
         }
       }
-      // digits of the 52 mantissa bits, most significant first; larger values first
-      ull known_mask = ~((1ull << 52) - 1), known_val = (ull)bin << 52;
-      const int shifts[4] = {36, 20, 4, 0};
-      const int widths[4] = {16, 16, 16, 4};
+      if (getenv("IQCC_DEBUG")) debug_check("select gather");
+      // 16-bit digits of the 63 magnitude bits, most significant first;
+      // larger values first (the coarse bin only narrowed the candidates)
+      ull known_mask = 1ull << 63, known_val = 0;
+      const int shifts[4] = {47, 31, 15, 0};
+      const int widths[4] = {16, 16, 16, 15};
       unsigned* dh = ws.misc2.as<unsigned>(65536);
       std::vector<unsigned> hd(65536);
       for (int round = 0; round < 4; ++round) {
         const unsigned dmask = (1u << widths[round]) - 1u;
         IQCC_CUDA(cudaMemsetAsync(dh, 0, (dmask + 1) * sizeof(unsigned), st));
         {
-          KernelScope ks("select");
+          KernelScope ks("select_digits");
           const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (nc + 255) / 256));
           k_cand_hist<<<grid, 256, 0, st>>>(cv, nc, known_mask, known_val, shifts[round], dmask, dh);
         }
@@ -641,10 +673,11 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         known_mask |= (ull)dmask << shifts[round];
         known_val |= (ull)d << shifts[round];
       }
+      if (getenv("IQCC_DEBUG")) debug_check("select digits");
       const ull vbits = known_val;  // exact threshold value; r ties at it are kept
       ull* ties = ws.misc3.as<ull>(nc);
       {
-        KernelScope ks("select");
+        KernelScope ks("select_ties");
         k_cand_ties<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(cv, ci, nc, vbits, ties, ctr);
       }
       ull ntie = 0;

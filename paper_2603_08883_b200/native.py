@@ -61,6 +61,7 @@ _SIGS = {
     "iqcc_gpu_sum_size": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_sum_download": (C.c_int, [_vp, _u64p, _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_sum_download_device": (C.c_int, [_vp, _u64p, _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_sum_raw": (C.c_int, [_vp, _u64p, _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_dress": (C.c_int, [_vp, _u64p, C.c_double, C.c_double, C.c_double, C.POINTER(DressStats)]),
     "iqcc_gpu_compress": (C.c_int, [_vp, C.c_double, C.c_size_t, C.POINTER(CompressStatsC)]),
     "iqcc_gpu_dress_sequence": (C.c_int, [_vp, C.c_size_t, _u64p, _f64p, _f64p, C.c_double, C.c_size_t,

@@ -1,0 +1,122 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref).
+
+Run here (needs /root/reference and oracle/_ref/libiqcc_ref.so):
+    python tests/golden/make_golden.py
+The GPU box has no /root/reference; the committed fixtures carry what the
+parity tests need there.
+
+Fixtures
+--------
+c1_<name>.npz   SURVEY.md §8(d) config C1: the Jordan-Wigner Hamiltonian of
+                proj/data/<name>.fcidump (io.hpp:154-310), its HF energy, the
+                full DIS at HF (dis.hpp:140), the FCI energy (oracle.hpp:365)
+                and an iQCC trace composed as in SURVEY.md §3.6: per
+                iteration the picked entanglers, the optimized amplitudes
+                (optimizer.hpp:96), the dressed term count, the energy and a
+                SHA-256 of the dressed sum's canonical bytes; the final
+                dressed sum is stored in full.
+small.npz       random cases from the reference test seeds (dress_single,
+                compress, dress_sequence outputs with checksums).
+"""
+import hashlib
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+from oracle.oracle import Oracle  # noqa: E402
+
+DATA = "/root/reference/proj/data"
+
+
+def digest(rows, coeffs):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(rows, np.uint64).tobytes())
+    h.update(np.ascontiguousarray(coeffs, np.complex128).tobytes())
+    return h.hexdigest()
+
+
+def c1(ref, name, iters, k_per_iter):
+    h, ne = ref.jordan_wigner_fcidump(os.path.join(DATA, f"{name}.fcidump"))
+    n = h.n_qubits
+    theta = np.array([math.pi if j < ne else 0.0 for j in range(n)])
+    phi = np.zeros(n)
+    rows0, c0 = h.export()
+    e_hf = ref.expect_sum(theta, phi, h)
+    dis_rows, dis_g = ref.dis_candidates(h, theta, phi, 1 << 20)
+    e_fci = ref.ground_energy(h) if n <= 12 else float("nan")
+    trace = {"gens": [], "taus": [], "iter": [], "energy": [], "terms": [], "sha": []}
+    cur = h
+    for it in range(iters):
+        nxt, gens, taus, e = ref.iqcc_iteration(cur, theta, phi, k_per_iter)
+        if len(taus) == 0:
+            break
+        r, c = nxt.export()
+        for g, t in zip(gens, taus):
+            trace["gens"].append(g)
+            trace["taus"].append(t)
+            trace["iter"].append(it)
+        trace["energy"].append(e)
+        trace["terms"].append(len(nxt))
+        trace["sha"].append(digest(r, c))
+        cur = nxt
+    rf, cf = cur.export()
+    W = rows0.shape[1]
+    out = dict(
+        n_qubits=n, n_electrons=ne, rows0=rows0, coeffs0=c0, e_hf=e_hf, e_fci=e_fci,
+        dis_rows=dis_rows, dis_g=dis_g,
+        gens=np.array(trace["gens"], np.uint64).reshape(-1, W), taus=np.array(trace["taus"]),
+        gen_iter=np.array(trace["iter"], np.int64), energies=np.array(trace["energy"]),
+        terms=np.array(trace["terms"], np.int64), shas=np.array(trace["sha"]),
+        rows_final=rf, coeffs_final=cf,
+    )
+    np.savez_compressed(os.path.join(HERE, f"c1_{name}.npz"), **out)
+    print(name, "terms", len(h), "->", trace["terms"], "E", trace["energy"], "DIS", len(dis_g))
+
+
+def small(ref):
+    """Reference outputs for the seeds of tests/test_dressing.cpp:177-196
+    (seed 557) and tests/test_partition.cpp:180-208 (seed 631)."""
+    cases = {}
+    rng = ref.rng(557)
+    shas = []
+    for t in range(120):
+        n = 2 + t % 7
+        h = rng.sum(n, 12 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.0, 3.0)
+        r, c = ref.dress_single(h, g, tau).export()
+        shas.append(digest(r, c))
+    cases["dress557_sha"] = np.array(shas)
+    rng = ref.rng(631)
+    shas = []
+    for t in range(40):
+        n = 3 + t % 4
+        h = rng.sum(n, 25 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.0, 3.0)
+        eps = 1e-3 if t % 3 == 0 else 0.0
+        mt = 40 if t % 4 == 0 else 100000
+        d = ref.dress_single(h, g, tau)
+        if eps > 0 or len(d) > mt:
+            d, _ = ref.compress(d, eps, mt)
+        r, c = d.export()
+        shas.append(digest(r, c))
+    cases["pipeline631_sha"] = np.array(shas)
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **cases)
+    print("small fixtures", {k: len(v) for k, v in cases.items()})
+
+
+def main():
+    ref = Oracle("reference")
+    c1(ref, "h2_sto3g", 5, 1)
+    c1(ref, "h2_ccpvdz", 5, 1)
+    small(ref)
+
+
+if __name__ == "__main__":
+    main()
