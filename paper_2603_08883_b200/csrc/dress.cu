@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(GROUP) k_tile_carry(const int* __restrict__ ti
 // One warp owns a tile of WT = 32*WI consecutive terms (lane l: terms
 // [WI*l, WI*l+WI)); all scans are warp shuffles, no shared memory or block
 // barriers.  NTHR thresholds per chunk (rounded up to a multiple of 4).
-constexpr int WI = 16;
+#ifndef IQCC_WI
+#define IQCC_WI 8
+#endif
+constexpr int WI = IQCC_WI;  // terms per lane
 constexpr int WT = 32 * WI;
 
 struct WarpItems {
@@ -289,19 +292,18 @@ __device__ __forceinline__ WarpItems load_witems(const short* __restrict__ lcp,
   WarpItems it;
   if (first + WI <= M) {
     const int4* p = reinterpret_cast<const int4*>(lcp + first);
-    int4 v0 = __ldg(p), v1 = __ldg(p + 1);
-    const short* s0 = reinterpret_cast<const short*>(&v0);
-    const short* s1 = reinterpret_cast<const short*>(&v1);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      it.l[k] = s0[k];
-      it.l[8 + k] = s1[k];
+    for (int h = 0; h < WI / 8; ++h) {
+      const int4 v = __ldg(p + h);
+      const short* s = reinterpret_cast<const short*>(&v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) it.l[8 * h + k] = s[k];
     }
   } else {
 #pragma unroll
     for (int k = 0; k < WI; ++k) it.l[k] = first + k < M ? (int)lcp[first + k] : INT_MAX;
   }
-  it.bits = first < M ? (fmask[first >> 5] >> (first & 31)) & 0xFFFFu : 0u;
+  it.bits = first < M ? (fmask[first >> 5] >> (first & 31)) & ((1u << WI) - 1u) : 0u;
   return it;
 }
 

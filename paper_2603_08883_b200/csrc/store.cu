@@ -533,13 +533,21 @@ __global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys
   }
 }
 
-__global__ void k_cand_hist(const ull* __restrict__ cv, size_t n, ull known_mask, ull known_val,
-                            int shift, unsigned mask, unsigned* __restrict__ hist) {
+constexpr int kDigitBits = 12;  // digit histogram privatized in shared memory
+__global__ void __launch_bounds__(256) k_cand_hist(const ull* __restrict__ cv, size_t n,
+                                                   ull known_mask, ull known_val, int shift,
+                                                   unsigned mask, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[1 << kDigitBits];
+  for (int b = threadIdx.x; b <= (int)mask; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     const ull v = cv[i];
-    if ((v & known_mask) == known_val) atomicAdd(hist + ((v >> shift) & mask), 1u);
+    if ((v & known_mask) == known_val) atomicAdd(sh + ((v >> shift) & mask), 1u);
   }
+  __syncthreads();
+  for (int b = threadIdx.x; b <= (int)mask; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
 }
 
 __global__ void k_cand_ties(const ull* __restrict__ cv, const ull* __restrict__ ci, size_t n,
@@ -642,20 +650,27 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         }
       }
       if (getenv("IQCC_DEBUG")) debug_check("select gather");
-      // 16-bit digits of the 63 magnitude bits, most significant first;
-      // larger values first (the coarse bin only narrowed the candidates)
+      // digits below what the coarse bin fixed, most significant first;
+      // larger values first.  An interior bin fixes the exponent (bits
+      // 62..52); the clamped end bins leave all 63 magnitude bits open.
       ull known_mask = 1ull << 63, known_val = 0;
-      const int shifts[4] = {47, 31, 15, 0};
-      const int widths[4] = {16, 16, 16, 15};
-      unsigned* dh = ws.misc2.as<unsigned>(65536);
-      std::vector<unsigned> hd(65536);
-      for (int round = 0; round < 4; ++round) {
-        const unsigned dmask = (1u << widths[round]) - 1u;
+      int top = 62;
+      if (bin > 0 && bin < kHistBins - 1) {
+        known_mask |= 0x7FFull << 52;
+        known_val = (ull)(bin + (1023 - 192)) << 52;
+        top = 51;
+      }
+      unsigned* dh = ws.misc2.as<unsigned>(1 << kDigitBits);
+      std::vector<unsigned> hd(1 << kDigitBits);
+      while (top >= 0) {
+        const int width = std::min(kDigitBits, top + 1);
+        const int shift = top + 1 - width;
+        const unsigned dmask = (1u << width) - 1u;
         IQCC_CUDA(cudaMemsetAsync(dh, 0, (dmask + 1) * sizeof(unsigned), st));
         {
           KernelScope ks("select_digits");
-          const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (nc + 255) / 256));
-          k_cand_hist<<<grid, 256, 0, st>>>(cv, nc, known_mask, known_val, shifts[round], dmask, dh);
+          const unsigned grid = (unsigned)std::min<size_t>(592, std::max<size_t>(1, (nc + 1023) / 1024));
+          k_cand_hist<<<grid, 256, 0, st>>>(cv, nc, known_mask, known_val, shift, dmask, dh);
         }
         IQCC_CUDA(cudaMemcpyAsync(hd.data(), dh, (dmask + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         IQCC_CUDA(cudaStreamSynchronize(st));
@@ -670,8 +685,9 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
           c2 += hd[x];
         }
         if (d < 0) throw std::runtime_error("compress: digit select failed");
-        known_mask |= (ull)dmask << shifts[round];
-        known_val |= (ull)d << shifts[round];
+        known_mask |= (ull)dmask << shift;
+        known_val |= (ull)d << shift;
+        top = shift - 1;
       }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
       const ull vbits = known_val;  // exact threshold value; r ties at it are kept
