@@ -553,19 +553,20 @@ struct MergeCfg {
   static constexpr int TILE = NT * IPT;
   static constexpr int CAP = TILE + 8;  // tiles absorb short runs of equal survivors
   static constexpr size_t KEYB = (size_t)CAP * 16 * B;
-  static constexpr size_t OFF_KEYS = 0;
-  // S coefs [coff, coff+nS), Q coefs [nS+4, ...); reused as the output value
-  // staging once every walk has finished reading them
-  static constexpr size_t OFF_COEF = KEYB;
-  static constexpr size_t OFF_OUTV = (OFF_COEF + (size_t)(CAP + 4) * 8 + 15) & ~(size_t)15;
+  // one input stage: survivor rows [0,nS) then product rows [nS, nS+nQ);
+  // S coefs [coff, coff+nS), Q coefs [nS+4, ...)
+  static constexpr size_t STAGE = (KEYB + (size_t)(CAP + 4) * 8 + 127) & ~(size_t)127;
+  static constexpr size_t OFF_OUTV = 2 * STAGE;
   static constexpr size_t OFF_OUTE = OFF_OUTV + (size_t)CAP * 8;
   static constexpr size_t OFF_TA = (OFF_OUTE + (size_t)CAP * 2 + 15) & ~(size_t)15;
-  static constexpr size_t OFF_PM = OFF_TA + (size_t)2 * NT * 4;       // present bits of S
+  static constexpr size_t OFF_PM = OFF_TA + (size_t)2 * NT * 4;  // present bits of S
   static constexpr int PMW = (CAP + 31) / 32;
-  static constexpr size_t OFF_PP = OFF_PM + (size_t)PMW * 4;          // their prefix
+  static constexpr size_t OFF_PP = OFF_PM + (size_t)PMW * 4;     // their prefix
   static constexpr size_t OFF_HIST = (OFF_PP + (size_t)PMW * 4 + 15) & ~(size_t)15;
-  static constexpr int HBINS = kHistBins;  // |c| histogram (u16 per tile) for compress
-  static constexpr size_t bytes(bool hist) { return OFF_HIST + (hist ? HBINS * 2 : 0); }
+  static constexpr int HBINS = kHistBins;  // |c| histogram (u32, per CTA) for compress
+  static constexpr size_t bytes(bool hist, int stages) {
+    return OFF_HIST - (2 - stages) * STAGE + (hist ? HBINS * 4 : 0);
+  }
 };
 
 template <int B>
@@ -581,90 +582,94 @@ __device__ __forceinline__ Key<B> sm_key16(const ull* sk, int e) {
   return k;
 }
 
+struct MergeArgs {
+  const ull* keys;
+  const double* coef;
+  Filter filt;
+  const unsigned* inv_perm;
+  const ull* part_a;
+  const ull* part_b;
+  const ull* part_o;
+  size_t ntiles;
+  double cs, sn, drop, eps;
+  ull* out_keys;
+  double* out_coef;
+  ull* counters;
+  unsigned* hist;
+  int want_hist;
+  ull* dbg;
+};
+
+/// Issue the loads of one tile into one stage: survivors by the TMA bulk
+/// engine (thread 0, completion on *mb), products by per-thread cp.async
+/// gathers (one commit group).
+template <int B, int NT>
+__device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull* sk, double* sc,
+                                            unsigned long long* mb) {
+  const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
+  const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
+  const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0);
+  if (threadIdx.x == 0 && nS > 0) {
+    const unsigned kb = (unsigned)nS * 16u * B;
+    const size_t c0 = a0 & ~(size_t)1, c1 = (a1 + 1) & ~(size_t)1;
+    const unsigned cb = (unsigned)((c1 - c0) * 8);
+    mbar_expect_tx(mb, kb + cb);
+    bulk_g2s(sk, g.keys + a0 * 2 * B, kb, mb);
+    bulk_g2s(sc, g.coef + c0, cb, mb);
+  }
+  const int qc0 = nS + 4;
+  for (int j = threadIdx.x; j < nQ; j += NT) {
+    const size_t src = __ldg(g.inv_perm + b0 + j);
+    const ull* gk = g.keys + src * 2 * B;
+    ull* s = sk + (size_t)(nS + j) * 2 * B;
+#pragma unroll
+    for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, gk + 2 * h);
+    cp_async8(sc + qc0 + j, g.coef + src);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 // Output slot rule (no look-back needed): every present survivor and every
 // product owns one slot, in merged order.  A survivor/product pair writes
 // the combined value into the survivor's slot and a dead slot after it;
 // a value failing keep_term leaves a dead slot.  So the tile's output
 // offset is present_before(a0) + b0, known before the tile runs.
 template <int B, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_merge(
-    const ull* __restrict__ keys, const double* __restrict__ coef, Filter filt,
-    const unsigned* __restrict__ inv_perm, const ull* __restrict__ part_a,
-    const ull* __restrict__ part_b, const ull* __restrict__ part_o, Key<B> P, double cs,
-    double sn, double drop, ull* __restrict__ out_keys, double* __restrict__ out_coef,
-    ull* __restrict__ counters, int want_hist, double eps, unsigned* __restrict__ hist,
-    ull* __restrict__ dbg) {
+__device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, const Key<B>& P,
+                                              ull* sk, double* sc, unsigned char* smem_raw,
+                                              int& n_eps, int& n_dead) {
   using Cfg = MergeCfg<B, NT, IPT>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  ull* sk = reinterpret_cast<ull*>(smem_raw + Cfg::OFF_KEYS);
-  double* sc = reinterpret_cast<double*>(smem_raw + Cfg::OFF_COEF);
   double* outv = reinterpret_cast<double*>(smem_raw + Cfg::OFF_OUTV);
   unsigned short* oute = reinterpret_cast<unsigned short*>(smem_raw + Cfg::OFF_OUTE);
   int* s_ta = reinterpret_cast<int*>(smem_raw + Cfg::OFF_TA);
   int* s_tb = s_ta + NT;
   unsigned* spm = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PM);
   unsigned* spp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PP);
-  unsigned short* shist = reinterpret_cast<unsigned short*>(smem_raw + Cfg::OFF_HIST);
-  __shared__ __align__(8) unsigned long long mbar;
-  __shared__ int s_cnt[2];
-
-  const size_t tile = blockIdx.x;
-  const size_t a0 = part_a[tile], a1 = part_a[tile + 1];
-  const size_t b0 = part_b[tile], b1 = part_b[tile + 1];
-  const size_t o0 = part_o[tile], o1 = part_o[tile + 1];
+  unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
+  const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
+  const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
+  const size_t o0 = g.part_o[tile], o1 = g.part_o[tile + 1];
   const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0), n = nS + nQ;
   const int nslots = (int)(o1 - o0);
   const int coff = (int)(a0 & 1);
   const int qc0 = nS + 4;
 
-  // ---- stage: survivors by TMA bulk copy, products by cp.async gathers
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar, 1);
-    if (nS > 0) {
-      const unsigned kb = (unsigned)nS * 16u * B;
-      const size_t c0 = a0 & ~(size_t)1, c1 = (a1 + 1) & ~(size_t)1;
-      const unsigned cb = (unsigned)((c1 - c0) * 8);
-      mbar_expect_tx(&mbar, kb + cb);
-      bulk_g2s(sk, keys + a0 * 2 * B, kb, &mbar);
-      bulk_g2s(sc, coef + c0, cb, &mbar);
-    }
-    s_cnt[0] = s_cnt[1] = 0;
-  }
-  if (want_hist)
-    for (int b = threadIdx.x; b < Cfg::HBINS / 2; b += NT) reinterpret_cast<unsigned*>(shist)[b] = 0;
-  __syncthreads();  // mbarrier initialised before anyone waits on it
-  for (int j = threadIdx.x; j < nQ; j += NT) {
-    const size_t src = __ldg(inv_perm + b0 + j);
-    const ull* g = keys + src * 2 * B;
-    ull* s = sk + (size_t)(nS + j) * 2 * B;
-#pragma unroll
-    for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, g + 2 * h);
-    cp_async8(sc + qc0 + j, coef + src);
-  }
-  cp_async_wait_all();
-  if (nS > 0) mbar_wait(&mbar, 0);
-  __syncthreads();
-  if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar)) : "memory");
-
-  // ---- present bits of the survivors (+ their prefix) for slot offsets
+  // present bits of the survivors (dead slots / compress-filtered are absent)
   {
     const int lane = threadIdx.x & 31;
     for (int e0 = (threadIdx.x & ~31); e0 < nS; e0 += NT) {
       const int e = e0 + lane;
       bool pr = false;
-      if (e < nS) {
-        const Key<B> k = sm_key16<B>(sk, e);
-        pr = filter_keep(filt, a0 + e, sc[coff + e], a0 + e == 0 && key_is_identity<B>(k));
-      }
+      if (e < nS)
+        pr = filter_keep(g.filt, a0 + e, sc[coff + e],
+                         a0 + e == 0 && key_is_identity<B>(sm_key16<B>(sk, e)));
       const unsigned word = __ballot_sync(0xffffffffu, pr);
       if (lane == 0) spm[e0 >> 5] = word;
     }
   }
   // Q rows stay raw in shared memory; their product key is row ^ P (on the fly)
   auto qkey = [&](int j) { return key_xor<B>(sm_key16<B>(sk, nS + j), P); };
-
-  // ---- per-thread merge-path split (runs of equal survivors stay with their product)
-  {
+  {  // per-thread merge-path split (runs of equal survivors stay with their product)
     const int d = min((int)threadIdx.x * IPT, n);
     int lo = max(0, d - nQ), hi = min(d, nS);
     while (lo < hi) {
@@ -700,19 +705,23 @@ __global__ void __launch_bounds__(NT) k_merge(
   const int ia1 = threadIdx.x + 1 < NT ? s_ta[threadIdx.x + 1] : nS;
   const int ib1 = threadIdx.x + 1 < NT ? s_tb[threadIdx.x + 1] : nQ;
   auto present = [&](int e) { return (spm[e >> 5] >> (e & 31)) & 1u; };
-  int slot = (ia0 < nS ? (int)(spp[ia0 >> 5] + __popc(spm[ia0 >> 5] & ((1u << (ia0 & 31)) - 1u)))
-                       : (int)(spp[(nS - 1) >> 5] + __popc(spm[(nS - 1) >> 5] & (0xffffffffu >> (31 - ((nS - 1) & 31))))));
-  if (nS == 0) slot = 0;
+  int slot = 0;
+  if (nS > 0) {
+    const int x = min(ia0, nS);
+    const int w = min(x, nS - 1) >> 5;
+    const unsigned m = x >= nS ? (0xffffffffu >> (31 - ((nS - 1) & 31))) : ((1u << (x & 31)) - 1u);
+    slot = (int)(spp[w] + __popc(spm[w] & m));
+  }
   slot += ib0;
 
-  // ---- single walk; every slot value goes straight to the staging list
+  // single walk; every slot value goes straight to the staging list
   {
     int i = ia0, j = ib0;
     Key<B> ks, kq;
     if (i < ia1) ks = sm_key16<B>(sk, i);
     if (j < ib1) kq = qkey(j);
     auto put = [&](double v, int e) {
-      if (dbg_ok(dbg, 2, (ull)slot, (ull)nslots)) {
+      if (dbg_ok(g.dbg, 2, (ull)slot, (ull)nslots)) {
         outv[slot] = v;
         oute[slot] = (unsigned short)e;
       }
@@ -727,50 +736,51 @@ __global__ void __launch_bounds__(NT) k_merge(
         double v = 0.0;
         if (pres) {
           const double cv = sc[coff + i];
-          v = anticommutes<B>(ks, P) ? __dmul_rn(cv, cs) : cv;
+          v = anticommutes<B>(ks, P) ? __dmul_rn(cv, g.cs) : cv;
         }
         if (c == 0) {
-          const double pr = __dmul_rn(sc[qc0 + j], sn);
+          const double pr = __dmul_rn(sc[qc0 + j], g.sn);
           const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
           if (pres) {
             const double sum = __dadd_rn(v, qv);
-            put(keep_term(sum, id, drop) ? sum : dead_value(), i);
+            put(keep_term(sum, id, g.drop) ? sum : dead_value(), i);
             put(dead_value(), nS + j);  // the product's slot
           } else {
-            put(keep_term(qv, false, drop) ? qv : dead_value(), nS + j);
+            put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
           }
         } else if (pres) {
-          put(keep_term(v, id, drop) ? v : dead_value(), i);
+          put(keep_term(v, id, g.drop) ? v : dead_value(), i);
         }
       } else {
-        const double pr = __dmul_rn(sc[qc0 + j], sn);
+        const double pr = __dmul_rn(sc[qc0 + j], g.sn);
         const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
-        put(keep_term(qv, false, drop) ? qv : dead_value(), nS + j);
+        put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
       }
       if (c <= 0 && ++i < ia1) ks = sm_key16<B>(sk, i);
       if (c >= 0 && ++j < ib1) kq = qkey(j);
     }
   }
   __syncthreads();
-  int n_eps = 0, n_dead = 0;
   for (int q = threadIdx.x; q < nslots; q += NT) {
     const int e = oute[q];
     const double v = outv[q];
     const Key<B> k = e < nS ? sm_key16<B>(sk, e) : qkey(e - nS);
-    store_key<B>(out_keys, o0 + q, k);
-    out_coef[o0 + q] = v;
+    store_key<B>(g.out_keys, o0 + q, k);
+    g.out_coef[o0 + q] = v;
     if (is_dead(v)) {
       ++n_dead;
-    } else if (want_hist) {
+    } else if (g.want_hist) {
       const double a = fabs(v);
       const bool id = o0 + q == 0 && key_is_identity<B>(k);
-      if (id || a >= eps) ++n_eps;
-      if (!id && a >= eps) {
-        const unsigned bin = hist_bin(a);
-        atomicAdd(reinterpret_cast<unsigned*>(shist) + (bin >> 1), (bin & 1u) ? 0x10000u : 1u);
-      }
+      if (id || a >= g.eps) ++n_eps;
+      if (!id && a >= g.eps) atomicAdd(shist + hist_bin(a), 1u);
     }
   }
+}
+
+template <int B, int NT>
+__device__ __forceinline__ void merge_flush(const MergeArgs& g, unsigned* shist, int n_eps,
+                                            int n_dead, int* s_cnt) {
   n_dead = __reduce_add_sync(0xffffffffu, n_dead);
   n_eps = __reduce_add_sync(0xffffffffu, n_eps);
   if ((threadIdx.x & 31) == 0) {
@@ -779,15 +789,88 @@ __global__ void __launch_bounds__(NT) k_merge(
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (s_cnt[0]) atomicAdd(counters + 2, (ull)s_cnt[0]);
-    if (s_cnt[1]) atomicAdd(counters + 1, (ull)s_cnt[1]);
+    if (s_cnt[0]) atomicAdd(g.counters + 2, (ull)s_cnt[0]);
+    if (s_cnt[1]) atomicAdd(g.counters + 1, (ull)s_cnt[1]);
   }
-  if (want_hist)
-    for (int b = threadIdx.x; b < Cfg::HBINS / 2; b += NT) {
-      const unsigned w = reinterpret_cast<unsigned*>(shist)[b];
-      if (w & 0xFFFFu) atomicAdd(hist + 2 * b, w & 0xFFFFu);
-      if (w >> 16) atomicAdd(hist + 2 * b + 1, w >> 16);
+  if (g.want_hist)
+    for (int b = threadIdx.x; b < kHistBins; b += NT)
+      if (shist[b]) atomicAdd(g.hist + b, shist[b]);
+}
+
+/// One tile per CTA (single input stage): the default; enough CTAs stay
+/// resident that load latency of one hides behind the merge of others.
+template <int B, int NT, int IPT>
+__global__ void __launch_bounds__(NT) k_merge1(MergeArgs g, Key<B> P) {
+  using Cfg = MergeCfg<B, NT, IPT>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST - Cfg::STAGE);
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ int s_cnt[2];
+  const size_t tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    s_cnt[0] = s_cnt[1] = 0;
+  }
+  if (g.want_hist)
+    for (int b = threadIdx.x; b < Cfg::HBINS; b += NT) shist[b] = 0;
+  __syncthreads();
+  ull* sk = reinterpret_cast<ull*>(smem_raw);
+  double* sc = reinterpret_cast<double*>(smem_raw + Cfg::KEYB);
+  merge_issue<B, NT>(g, tile, sk, sc, &mbar);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (g.part_a[tile + 1] > g.part_a[tile]) mbar_wait(&mbar, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar)) : "memory");
+  int n_eps = 0, n_dead = 0;
+  // shared layout past the single stage is shifted down by one STAGE
+  merge_compute<B, NT, IPT>(g, tile, P, sk, sc, smem_raw - Cfg::STAGE, n_eps, n_dead);
+  merge_flush<B, NT>(g, shist, n_eps, n_dead, s_cnt);
+}
+
+/// Persistent merge: each CTA walks tiles blockIdx.x, +gridDim.x, ... with a
+/// two-stage pipeline: the next tile's TMA bulk copy and cp.async gathers
+/// are in flight while the current tile is merged and stored.
+template <int B, int NT, int IPT>
+__global__ void __launch_bounds__(NT) k_merge(MergeArgs g, Key<B> P) {
+  using Cfg = MergeCfg<B, NT, IPT>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
+  __shared__ __align__(8) unsigned long long mbar[2];
+  __shared__ int s_cnt[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    s_cnt[0] = s_cnt[1] = 0;
+  }
+  if (g.want_hist)
+    for (int b = threadIdx.x; b < Cfg::HBINS; b += NT) shist[b] = 0;
+  __syncthreads();
+  auto stage_k = [&](int st) { return reinterpret_cast<ull*>(smem_raw + st * Cfg::STAGE); };
+  auto stage_c = [&](int st) {
+    return reinterpret_cast<double*>(smem_raw + st * Cfg::STAGE + Cfg::KEYB);
+  };
+  size_t tile = blockIdx.x;
+  if (tile < g.ntiles) merge_issue<B, NT>(g, tile, stage_k(0), stage_c(0), &mbar[0]);
+  unsigned phase[2] = {0u, 0u};
+  int n_eps = 0, n_dead = 0;
+  for (int it = 0; tile < g.ntiles; ++it, tile += gridDim.x) {
+    const int cur = it & 1;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (g.part_a[tile + 1] > g.part_a[tile]) {
+      mbar_wait(&mbar[cur], phase[cur]);
+      phase[cur] ^= 1u;
     }
+    __syncthreads();
+    const size_t next = tile + gridDim.x;
+    if (next < g.ntiles) merge_issue<B, NT>(g, next, stage_k(cur ^ 1), stage_c(cur ^ 1), &mbar[cur ^ 1]);
+    merge_compute<B, NT, IPT>(g, tile, P, stage_k(cur), stage_c(cur), smem_raw, n_eps, n_dead);
+    __syncthreads();  // stage `cur` and the staging list are free again
+  }
+  merge_flush<B, NT>(g, shist, n_eps, n_dead, s_cnt);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[0])) : "memory");
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[1])) : "memory");
+  }
 }
 
 /// Merge tile shapes (NT threads x IPT items); the default per block count
@@ -843,19 +926,52 @@ size_t launch_merge(DeviceStore& s, const unsigned* inv_perm, size_t M, size_t A
   unsigned* hist = ws.hist.as<unsigned>(kHistBins);
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
   if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
-  const size_t smem = MergeCfg<B, NT, IPT>::bytes(want_hist);
-  static bool attr = false;
-  if (!attr) {
+  using Cfg = MergeCfg<B, NT, IPT>;
+  const size_t smem = Cfg::bytes(want_hist, 2);
+  static int ctas_per_sm = 0;
+  static int n_sm = 0;
+  if (!ctas_per_sm) {
     IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)MergeCfg<B, NT, IPT>::bytes(true)));
-    attr = true;
+                                   (int)Cfg::bytes(true, 2)));
+    IQCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_merge<B, NT, IPT>, NT,
+                                                            Cfg::bytes(true, 2)));
+    IQCC_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0));
+    ctas_per_sm = std::max(ctas_per_sm, 1);
   }
-  {
+  MergeArgs g;
+  g.keys = s.keys();
+  g.coef = s.coef();
+  g.filt = s.filt;
+  g.inv_perm = inv_perm;
+  g.part_a = pa;
+  g.part_b = pb;
+  g.part_o = po;
+  g.ntiles = ntm;
+  g.cs = cs;
+  g.sn = sn;
+  g.drop = drop;
+  g.eps = eps;
+  g.out_keys = out_keys;
+  g.out_coef = out_coef;
+  g.counters = ctr;
+  g.hist = hist;
+  g.want_hist = want_hist ? 1 : 0;
+  g.dbg = debug_buffer();
+  static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
+  if (persistent) {
     KernelScope ks("merge");
-    k_merge<B, NT, IPT><<<(unsigned)ntm, NT, smem, st>>>(s.keys(), s.coef(), s.filt, inv_perm, pa,
-                                                        pb, po, P, cs, sn, drop, out_keys, out_coef,
-                                                        ctr, want_hist ? 1 : 0, eps, hist,
-                                                        debug_buffer());
+    const unsigned grid = (unsigned)std::min<size_t>(ntm, (size_t)n_sm * ctas_per_sm);
+    k_merge<B, NT, IPT><<<grid, NT, smem, st>>>(g, P);
+  } else {
+    static bool attr1 = false;
+    if (!attr1) {
+      IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)Cfg::bytes(true, 1)));
+      attr1 = true;
+    }
+    KernelScope ks("merge");
+    k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
   }
   IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
   if (getenv("IQCC_DEBUG")) debug_check("merge");
@@ -995,7 +1111,7 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
   static int shape = -1;
   if (shape < 0) {
     const char* env = getenv("IQCC_MERGE_CFG");
-    shape = env ? atoi(env) : (B >= 4 ? 3 : 1);
+    shape = env ? atoi(env) : 3;
     if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 1;
   }
   switch (shape) {
