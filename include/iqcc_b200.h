@@ -59,6 +59,9 @@ uint64_t iqcc_gpu_launch_count(void);
 int iqcc_gpu_profile_enable(int on);
 int iqcc_gpu_profile_get(const char* name, double* total_ms, uint64_t* launches);
 int iqcc_gpu_profile_reset(void);
+/* Algorithmic bytes attributed to a family while profiling is enabled
+ * ("merge": (M_in + M_out) * (16B + 8) per dressing step). */
+int iqcc_gpu_profile_bytes(const char* name, double* bytes);
 
 /* ---- sums (replace iqcc::PauliSum storage, iqcc/pauli.hpp:245-378) ---- */
 /* Upload a canonical real PauliSum from HOST buffers (reference layout). */
@@ -108,10 +111,11 @@ int iqcc_gpu_dress(iqcc_gpu_sum* h, const uint64_t* gen, double cos_tau, double 
 int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compress_stats* stats);
 /* In place dress_sequence (iqcc/dressing.hpp:311-324): K entanglers in
  * order, compress(eps, max_terms) after each step when eps > 0 or the size
- * exceeds max_terms.  gens [K][2B]. */
+ * exceeds max_terms.  gens [K][2B].  *terms_in_total (optional) receives
+ * the sum of the logical input sizes of the K steps. */
 int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
                             const double* sin_tau, double eps, size_t max_terms,
-                            iqcc_compress_stats* stats);
+                            iqcc_compress_stats* stats, size_t* terms_in_total /* nullable */);
 /* growth_split (iqcc/dressing.hpp:41-50). */
 int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* n_commuting,
                           size_t* n_anticommuting);

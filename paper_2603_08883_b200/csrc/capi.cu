@@ -29,6 +29,7 @@ struct CudaError : std::runtime_error {
 
 struct ProfileEntry {
   double ms = 0.0;
+  double alg_bytes = 0.0;  // algorithmic bytes attributed to the family
   uint64_t launches = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
 };
@@ -82,6 +83,11 @@ void count_launch(const char* family) {
   Ctx& c = ctx();
   ++c.launches;
   (void)family;
+}
+
+void add_alg_bytes(const char* family, double bytes) {
+  Ctx& c = ctx();
+  if (c.profiling) c.prof[family].alg_bytes += bytes;
 }
 
 static cudaEvent_t take_event() {
@@ -297,6 +303,14 @@ int iqcc_gpu_profile_get(const char* name, double* total_ms, uint64_t* launches)
   });
 }
 
+int iqcc_gpu_profile_bytes(const char* name, double* bytes) {
+  return guarded([&] {
+    auto& p = ctx().prof;
+    auto it = p.find(name);
+    *bytes = it == p.end() ? 0.0 : it->second.alg_bytes;
+  });
+}
+
 int iqcc_gpu_profile_reset(void) {
   return guarded([&] {
     profile_flush();
@@ -424,7 +438,7 @@ int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compre
 
 int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
                             const double* sin_tau, double eps, size_t max_terms,
-                            iqcc_compress_stats* stats) {
+                            iqcc_compress_stats* stats, size_t* terms_in_total) {
   return guarded([&] {
     need(h);
     if (max_terms < 1) throw std::invalid_argument("dress_sequence: max_terms < 1");
@@ -432,8 +446,10 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
     for (size_t k = 0; k < K; ++k)
       if (row_is_identity(gens + k * 2 * Bref, Bref))
         throw std::invalid_argument("dress_single: identity generator");
+    if (terms_in_total) *terms_in_total = 0;
     for (size_t k = 0; k < K; ++k) {
       auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
+      if (terms_in_total) *terms_in_total += h->s.logical;
       const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
       DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps);
       if (eps > 0.0 || h->s.logical > max_terms) {

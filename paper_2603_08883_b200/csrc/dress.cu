@@ -1128,9 +1128,12 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
   IQCC_CUDA(cudaStreamSynchronize(st));
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
+  // algorithmic bytes of the step: (M_in + M_out) * (16B + 8)
+  const size_t logical_in = s.logical;
   s.M = hc[3];              // physical slots (live + dead)
   s.filt = Filter{};
   s.logical = hc[3] - hc[2];  // minus dead slots
+  add_alg_bytes("merge", (double)(logical_in + s.logical) * (16.0 * B + 8.0));
   out.count_eps = hc[1];
   return out;
 }

@@ -315,6 +315,7 @@ struct Ctx;
 Ctx& ctx();
 cudaStream_t stream();
 void count_launch(const char* family);
+void add_alg_bytes(const char* family, double bytes);
 void check_cuda(cudaError_t e, const char* what);
 #define IQCC_CUDA(x) ::iqcc_b200::check_cuda((x), #x)
 

@@ -298,7 +298,9 @@ class DeviceSum:
             stats.dropped_weight += cs.dropped_weight
 
     def dress_sequence(self, ansatz: Ansatz, eps: float, max_terms: int = U64_MAX,
-                       stats: CompressStats | None = None) -> None:
+                       stats: CompressStats | None = None) -> int:
+        """In place dress_sequence; returns the summed logical input size of
+        the K dressing steps (the bench metric's unit of work)."""
         K = ansatz.size()
         W = 2 * blocks_for(self.n_qubits)
         gens = np.zeros((max(K, 1), W), np.uint64)
@@ -307,11 +309,18 @@ class DeviceSum:
         cs_ = np.array([math.cos(t) for t in ansatz.tau] or [1.0])
         sn_ = np.array([math.sin(t) for t in ansatz.tau] or [0.0])
         st = native.CompressStatsC()
+        tin = C.c_size_t(0)
         check(lib.iqcc_gpu_dress_sequence(self.handle, K, _addr(gens), _addr(cs_), _addr(sn_), eps, max_terms,
-                                          C.byref(st) if stats is not None else None))
+                                          C.byref(st) if stats is not None else None, C.byref(tin)))
         if stats is not None:
             stats.dropped_terms += st.dropped_terms
             stats.dropped_weight += st.dropped_weight
+        return tin.value
+
+    def download_pinned(self) -> PauliSum:
+        """Download into page-locked host memory (fast DMA; bench e2e input)."""
+        rows, coeffs = pinned_buffers(self.n_qubits, self.size())
+        return self.download(rows, coeffs)
 
     def growth_split(self, p: PauliWord) -> GrowthSplit:
         g = np.ascontiguousarray(p.row, np.uint64)
@@ -338,6 +347,16 @@ class DeviceSum:
         g = np.zeros(max(1, c.shape[0]), np.float64)
         check(lib.iqcc_gpu_gradients(self.handle, _addr(t), _addr(c), c.shape[0], int(flip_group_only), _addr(g)))
         return g[: c.shape[0]]
+
+
+def pinned_buffers(n_qubits: int, n_terms: int):
+    """Page-locked host arrays (rows uint64[n, 2B], coeffs complex128[n])."""
+    import torch
+    W = 2 * blocks_for(n_qubits)
+    n = max(1, n_terms)
+    r = torch.empty((n, W), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+    c = torch.empty((n, 2), dtype=torch.float64, pin_memory=True).numpy().view(np.complex128).reshape(n)
+    return r, c
 
 
 # ----------------------------------------------- reference-shaped functions
@@ -384,13 +403,34 @@ def sortless_dress(h: PauliSum, op: DressOp, opts: MergeOptions = MergeOptions()
 
 
 def dress_sequence(h: PauliSum, ansatz: Ansatz, epsilon: float, max_terms: int = U64_MAX,
-                   stats: CompressStats | None = None, opts: MergeOptions = MergeOptions()) -> PauliSum:
-    """iqcc/dressing.hpp:311-324 (device resident across the whole ansatz)."""
+                   stats: CompressStats | None = None, opts: MergeOptions = MergeOptions(),
+                   out: tuple | None = None) -> PauliSum:
+    """iqcc/dressing.hpp:311-324 (device resident across the whole ansatz).
+    `out` optionally supplies host (rows, coeffs) buffers for the result."""
+    return dress_sequence_counted(h, ansatz, epsilon, max_terms, stats, out)[0]
+
+
+def dress_sequence_counted(h: PauliSum, ansatz: Ansatz, epsilon: float, max_terms: int = U64_MAX,
+                           stats: CompressStats | None = None, out: tuple | None = None):
+    """dress_sequence that also returns the summed logical input size."""
     if max_terms < 1:
         raise ValueError("dress_sequence: max_terms < 1")
     d = DeviceSum.upload(h)
-    d.dress_sequence(ansatz, epsilon, max_terms, stats)
-    return d.download()
+    tin = d.dress_sequence(ansatz, epsilon, max_terms, stats)
+    if out is None:
+        n = d.size()
+        rows, coeffs = (pinned_buffers(h.n_qubits, n) if _is_pinned(h) else (None, None))
+    else:
+        rows, coeffs = out
+    return d.download(rows, coeffs), tin
+
+
+def _is_pinned(h: PauliSum) -> bool:
+    try:
+        import torch
+        return torch.from_numpy(h.rows.view(np.int64)).is_pinned()
+    except Exception:
+        return False
 
 
 def compress(h: PauliSum, epsilon: float, max_terms: int, stats: CompressStats | None = None) -> PauliSum:

@@ -52,6 +52,7 @@ _SIGS = {
     "iqcc_gpu_profile_enable": (C.c_int, [C.c_int]),
     "iqcc_gpu_profile_get": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "iqcc_gpu_profile_reset": (C.c_int, []),
+    "iqcc_gpu_profile_bytes": (C.c_int, [C.c_char_p, C.POINTER(C.c_double)]),
     "iqcc_gpu_sum_create": (C.c_int, [C.c_size_t, _u64p, _f64p, C.c_size_t, C.POINTER(_vp)]),
     "iqcc_gpu_sum_create_device": (C.c_int, [C.c_size_t, _u64p, _f64p, C.c_size_t, C.POINTER(_vp)]),
     "iqcc_gpu_sum_generate_mol": (C.c_int, [C.c_size_t, C.c_size_t, C.c_uint64, C.POINTER(_vp)]),
@@ -65,7 +66,7 @@ _SIGS = {
     "iqcc_gpu_dress": (C.c_int, [_vp, _u64p, C.c_double, C.c_double, C.c_double, C.POINTER(DressStats)]),
     "iqcc_gpu_compress": (C.c_int, [_vp, C.c_double, C.c_size_t, C.POINTER(CompressStatsC)]),
     "iqcc_gpu_dress_sequence": (C.c_int, [_vp, C.c_size_t, _u64p, _f64p, _f64p, C.c_double, C.c_size_t,
-                                          C.POINTER(CompressStatsC)]),
+                                          C.POINTER(CompressStatsC), C.POINTER(C.c_size_t)]),
     "iqcc_gpu_growth_split": (C.c_int, [_vp, _u64p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "iqcc_gpu_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
     "iqcc_gpu_qmf_energy_gradient": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(C.c_double), _f64p]),
@@ -141,6 +142,12 @@ def profile_get(name: str):
     ms, n = C.c_double(0), C.c_uint64(0)
     check(lib.iqcc_gpu_profile_get(name.encode(), C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def profile_bytes(name: str) -> float:
+    b = C.c_double(0)
+    check(lib.iqcc_gpu_profile_bytes(name.encode(), C.byref(b)))
+    return b.value
 
 
 def profile_reset() -> None:
