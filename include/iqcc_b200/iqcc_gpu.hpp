@@ -1,0 +1,312 @@
+// iqcc_gpu.hpp — drop-in C++ shim: the reference's hot-path API
+// (namespace iqcc, /root/reference/proj/include/iqcc/*.hpp) re-exposed as
+// iqcc::gpu::* with identical signatures, executed by the B200 engine
+// through the C-ABI in iqcc_b200.h.
+//
+// A reference maintainer switches a call site by qualifying it:
+//     iqcc::PauliSum d = iqcc::gpu::dress_single(h, op);        // was iqcc::dress_single
+// Exceptions match the reference: std::invalid_argument for precondition
+// violations (EINVAL), std::runtime_error otherwise.  Include after the
+// reference headers are on the include path (-I <ref>/proj/include) and link
+// paper_2603_08883_b200/libiqcc_b200.so.
+//
+// Host-side numerics stay on the host exactly as in the reference:
+// std::cos/std::sin of amplitudes (iqcc/dressing.hpp:203) and the QMF factor
+// tables via iqcc::detail::qmf_factor (iqcc/qmf.hpp:56-61), so device results
+// are bit-identical.  Sums cross the boundary zero-copy from PauliSum's
+// contiguous storage (iqcc/pauli.hpp:373-377).
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <limits>
+#include <random>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "iqcc/dis.hpp"
+#include "iqcc/dressing.hpp"
+#include "iqcc/pauli.hpp"
+#include "iqcc/qmf.hpp"
+#include "iqcc_b200.h"
+
+namespace iqcc::gpu {
+
+namespace detail {
+
+inline void check(int rc) {
+  if (rc == IQCC_OK) return;
+  const std::string msg = iqcc_gpu_last_error();
+  if (rc == IQCC_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+/// Engine bound to one device per process (iqcc_gpu_init is idempotent).
+inline void ensure_engine(int device = 0) {
+  static const int rc = iqcc_gpu_init(device);
+  check(rc);
+}
+
+/// Owning device handle.
+class Handle {
+ public:
+  explicit Handle(iqcc_gpu_sum* h = nullptr) : h_(h) {}
+  Handle(const Handle&) = delete;
+  Handle& operator=(const Handle&) = delete;
+  Handle(Handle&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  ~Handle() {
+    if (h_) iqcc_gpu_sum_destroy(h_);
+  }
+  iqcc_gpu_sum* get() const { return h_; }
+
+ private:
+  iqcc_gpu_sum* h_;
+};
+
+inline Handle upload(const PauliSum& h) {
+  ensure_engine();
+  iqcc_gpu_sum* out = nullptr;
+  const uint64_t* rows = h.empty() ? nullptr : h.word(0).x.data();
+  // PauliSum stores std::complex<double> contiguously (layout-compatible with
+  // double[2]); the const accessor returns by value, so reach the storage
+  // through the non-const one without modifying it.
+  const double* coeff =
+      h.empty() ? nullptr : reinterpret_cast<const double*>(&const_cast<PauliSum&>(h).coeff(0));
+  check(iqcc_gpu_sum_create(h.n_qubits(), rows, coeff, h.size(), &out));
+  return Handle(out);
+}
+
+inline PauliSum download(const Handle& d, std::size_t n_qubits) {
+  std::size_t n = 0;
+  check(iqcc_gpu_sum_size(d.get(), &n));
+  const std::size_t B = blocks_for(n_qubits);
+  std::vector<uint64_t> rows(std::max<std::size_t>(n, 1) * 2 * B);
+  std::vector<double> coeff(std::max<std::size_t>(n, 1) * 2);
+  std::size_t got = 0;
+  check(iqcc_gpu_sum_download(d.get(), rows.data(), coeff.data(), n, &got));
+  PauliSum out(n_qubits);
+  out.reserve(got);
+  for (std::size_t i = 0; i < got; ++i)
+    out.append(PauliView{{rows.data() + i * 2 * B, B}, {rows.data() + i * 2 * B + B, B}},
+               Complex(coeff[2 * i], coeff[2 * i + 1]));
+  return out;
+}
+
+inline std::vector<double> factor_table(const QmfState& omega) {
+  std::vector<double> t(3 * omega.n_qubits());
+  for (std::size_t j = 0; j < omega.n_qubits(); ++j) {
+    t[3 * j + 0] = iqcc::detail::qmf_factor(omega, j, true, false);   // X
+    t[3 * j + 1] = iqcc::detail::qmf_factor(omega, j, false, true);   // Z
+    t[3 * j + 2] = iqcc::detail::qmf_factor(omega, j, true, true);    // Y
+  }
+  return t;
+}
+
+inline std::vector<double> deriv_table(const QmfState& omega) {
+  std::vector<double> t(6 * omega.n_qubits());
+  for (std::size_t j = 0; j < omega.n_qubits(); ++j) {  // iqcc/qmf.hpp:130-143
+    const double st = std::sin(omega.theta[j]), ct = std::cos(omega.theta[j]);
+    const double sp = std::sin(omega.phi[j]), cp = std::cos(omega.phi[j]);
+    const double v[6] = {ct * cp, -st * sp, -st, 0.0, ct * sp, st * cp};
+    std::copy(v, v + 6, t.begin() + 6 * j);
+  }
+  return t;
+}
+
+inline std::vector<uint64_t> row_of(PauliView p) {
+  std::vector<uint64_t> r(p.x.begin(), p.x.end());
+  r.insert(r.end(), p.z.begin(), p.z.end());
+  return r;
+}
+
+}  // namespace detail
+
+/// A PauliSum kept resident in HBM across many calls (the iQCC loop keeps H
+/// on the device; only the final sum comes back).
+class DeviceSum {
+ public:
+  explicit DeviceSum(const PauliSum& h) : n_(h.n_qubits()), d_(detail::upload(h)) {}
+  std::size_t n_qubits() const { return n_; }
+  std::size_t size() const {
+    std::size_t n = 0;
+    detail::check(iqcc_gpu_sum_size(d_.get(), &n));
+    return n;
+  }
+  void dress(const DressOp& op, const MergeOptions& opts = {}) {
+    if (op.generator.n_qubits() != n_) throw std::invalid_argument("dress_single: mismatched qubit counts");
+    const auto row = detail::row_of(op.generator.view());
+    detail::check(iqcc_gpu_dress(d_.get(), row.data(), std::cos(op.amplitude), std::sin(op.amplitude),
+                                 opts.drop_threshold, nullptr));
+  }
+  void compress(double epsilon, std::size_t max_terms, CompressStats* stats = nullptr) {
+    iqcc_compress_stats s{0, 0.0};
+    detail::check(iqcc_gpu_compress(d_.get(), epsilon, max_terms, &s));
+    if (stats) {
+      stats->dropped_terms += s.dropped_terms;
+      stats->dropped_weight += s.dropped_weight;
+    }
+  }
+  void dress_sequence(const Ansatz& a, double epsilon,
+                      std::size_t max_terms = std::numeric_limits<std::size_t>::max(),
+                      CompressStats* stats = nullptr) {
+    std::vector<uint64_t> gens;
+    std::vector<double> c, s;
+    for (std::size_t k = 0; k < a.size(); ++k) {
+      if (a.entanglers[k].n_qubits() != n_) throw std::invalid_argument("dress_single: mismatched qubit counts");
+      const auto row = detail::row_of(a.entanglers[k].view());
+      gens.insert(gens.end(), row.begin(), row.end());
+      c.push_back(std::cos(a.tau[k]));
+      s.push_back(std::sin(a.tau[k]));
+    }
+    iqcc_compress_stats st{0, 0.0};
+    detail::check(iqcc_gpu_dress_sequence(d_.get(), a.size(), gens.data(), c.data(), s.data(), epsilon,
+                                          max_terms, &st, nullptr));
+    if (stats) {
+      stats->dropped_terms += st.dropped_terms;
+      stats->dropped_weight += st.dropped_weight;
+    }
+  }
+  double expect(const QmfState& omega) {
+    const auto t = detail::factor_table(omega);
+    double e = 0.0;
+    detail::check(iqcc_gpu_expect(d_.get(), t.data(), &e));
+    return e;
+  }
+  PauliSum download() const { return detail::download(d_, n_); }
+  iqcc_gpu_sum* handle() const { return d_.get(); }
+
+ private:
+  std::size_t n_;
+  detail::Handle d_;
+};
+
+// ------------------------------------------------------------------ dressing
+/// iqcc::dress_single (iqcc/dressing.hpp:197-220).
+inline PauliSum dress_single(const PauliSum& h, const DressOp& op, const MergeOptions& opts = {}) {
+  if (h.n_qubits() != op.generator.n_qubits())
+    throw std::invalid_argument("dress_single: mismatched qubit counts");
+  if (op.generator.is_identity()) throw std::invalid_argument("dress_single: identity generator");
+  DeviceSum d(h);
+  d.dress(op, opts);
+  return d.download();
+}
+
+/// iqcc::sortless_dress (iqcc/dressing.hpp:228-307): the same sum; the
+/// engine never sorts products, so new_stream_sorts is 0 by construction.
+inline PauliSum sortless_dress(const PauliSum& h, const DressOp& op, const MergeOptions& opts = {},
+                               SortlessStats* stats = nullptr) {
+  if (h.n_qubits() != op.generator.n_qubits())
+    throw std::invalid_argument("sortless_dress: mismatched qubit counts");
+  if (op.generator.is_identity()) throw std::invalid_argument("sortless_dress: identity generator");
+  const auto pos = iqcc::detail::support_positions(op.generator.view(), h.n_qubits());
+  if (pos.size() > 64) throw std::runtime_error("entangler support exceeds 64 bits; not supported");
+  PauliSum out = gpu::dress_single(h, op, opts);
+  if (stats) *stats = SortlessStats{};
+  return out;
+}
+
+/// iqcc::dress_sequence (iqcc/dressing.hpp:311-324), device resident.
+inline PauliSum dress_sequence(const PauliSum& h, const Ansatz& ansatz, double epsilon,
+                               std::size_t max_terms = std::numeric_limits<std::size_t>::max(),
+                               CompressStats* stats = nullptr, const MergeOptions& opts = {}) {
+  (void)opts;
+  if (max_terms < 1) throw std::invalid_argument("dress_sequence: max_terms < 1");
+  DeviceSum d(h);
+  d.dress_sequence(ansatz, epsilon, max_terms, stats);
+  return d.download();
+}
+
+/// iqcc::compress (iqcc/pauli.hpp:425-474).
+inline PauliSum compress(const PauliSum& h, double epsilon, std::size_t max_terms,
+                         CompressStats* stats = nullptr) {
+  if (epsilon < 0) throw std::invalid_argument("compress: epsilon < 0");
+  if (max_terms < 1) throw std::invalid_argument("compress: max_terms < 1");
+  DeviceSum d(h);
+  d.compress(epsilon, max_terms, stats);
+  return d.download();
+}
+
+/// iqcc::growth_split (iqcc/dressing.hpp:41-50).
+inline GrowthSplit growth_split(const PauliSum& h, PauliView p) {
+  DeviceSum d(h);
+  const auto row = detail::row_of(p);
+  GrowthSplit g;
+  detail::check(iqcc_gpu_growth_split(d.handle(), row.data(), &g.n_commuting, &g.n_anticommuting));
+  return g;
+}
+
+// ------------------------------------------------------------ QMF and DIS
+/// iqcc::expect_sum (iqcc/qmf.hpp:83-90).
+inline double expect_sum(const QmfState& omega, const PauliSum& h) {
+  if (!h.empty() && h.n_qubits() != omega.n_qubits())
+    throw std::invalid_argument("expect_sum: mismatched qubit counts");
+  if (h.empty()) return 0.0;
+  DeviceSum d(h);
+  return d.expect(omega);
+}
+
+/// iqcc::qmf_energy_gradient (iqcc/qmf.hpp:94-148).
+inline double qmf_energy_gradient(const PauliSum& h, const QmfState& omega, std::span<double> grad) {
+  DeviceSum d(h);
+  const auto t = detail::factor_table(omega);
+  const auto dt = detail::deriv_table(omega);
+  double e = 0.0;
+  detail::check(iqcc_gpu_qmf_energy_gradient(d.handle(), t.data(), dt.data(), &e, grad.data()));
+  return e;
+}
+
+/// iqcc::gradient (iqcc/dis.hpp:39-52).
+inline double gradient(const PauliSum& h, const QmfState& omega, PauliView p) {
+  if (!h.empty() && h.word(0).x.size() != p.x.size())
+    throw std::invalid_argument("gradient: mismatched qubit counts");
+  DeviceSum d(h);
+  const auto t = detail::factor_table(omega);
+  const auto row = detail::row_of(p);
+  double g = 0.0;
+  detail::check(iqcc_gpu_gradients(d.handle(), t.data(), row.data(), 1, 0, &g));
+  return g;
+}
+
+/// iqcc::dis_candidates (iqcc/dis.hpp:140-191).  The device screens every
+/// flip group; the optional seeded shuffle of equal-|g| runs is applied here
+/// with the same std::mt19937_64 + std::shuffle as the reference.
+inline std::vector<RankedGenerator> dis_candidates(const PauliSum& h, const QmfState& omega,
+                                                   std::size_t top_k, const DisOptions& opts = {}) {
+  if (top_k < 1) throw std::invalid_argument("dis_candidates: top_k < 1");
+  DeviceSum d(h);
+  const auto t = detail::factor_table(omega);
+  const std::size_t B = blocks_for(h.n_qubits());
+  std::size_t n = 0;
+  detail::check(iqcc_gpu_dis_candidates(d.handle(), t.data(), omega.at_poles(), top_k, opts.screen_threshold,
+                                        opts.per_group_cap, nullptr, nullptr, 0, &n));
+  std::vector<uint64_t> rows(std::max<std::size_t>(n, 1) * 2 * B);
+  std::vector<double> g(std::max<std::size_t>(n, 1));
+  std::size_t n2 = 0;
+  detail::check(iqcc_gpu_dis_candidates(d.handle(), t.data(), omega.at_poles(), n ? n : 1,
+                                        opts.screen_threshold, opts.per_group_cap, rows.data(), g.data(),
+                                        n, &n2));
+  std::vector<RankedGenerator> picks;
+  for (std::size_t i = 0; i < n; ++i)
+    picks.push_back({PauliWord(h.n_qubits(), std::span<const Block>(rows.data() + i * 2 * B, B),
+                               std::span<const Block>(rows.data() + i * 2 * B + B, B)),
+                     g[i]});
+  if (opts.tie_break_seed) {
+    std::mt19937_64 rng(*opts.tie_break_seed);
+    std::size_t i = 0;
+    while (i < picks.size()) {
+      std::size_t j = i + 1;
+      const double mag = std::abs(picks[i].gradient);
+      while (j < picks.size() && std::abs(std::abs(picks[j].gradient) - mag) <= 1e-12 * std::max(1.0, mag))
+        ++j;
+      std::shuffle(picks.begin() + i, picks.begin() + j, rng);
+      i = j;
+    }
+  }
+  if (picks.size() > top_k) picks.resize(top_k);
+  return picks;
+}
+
+}  // namespace iqcc::gpu

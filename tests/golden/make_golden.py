@@ -36,7 +36,9 @@ DATA = "/root/reference/proj/data"
 def digest(rows, coeffs):
     h = hashlib.sha256()
     h.update(np.ascontiguousarray(rows, np.uint64).tobytes())
-    h.update(np.ascontiguousarray(coeffs, np.complex128).tobytes())
+    # values, not bit patterns: -0.0 and +0.0 (e.g. imaginary parts produced
+    # by the reference's complex arithmetic) compare equal, as in PauliSum ==
+    h.update((np.ascontiguousarray(coeffs, np.complex128).view(np.float64) + 0.0).tobytes())
     return h.hexdigest()
 
 

@@ -1,0 +1,273 @@
+"""GPU parity: the engine's dressing / compress / dress_sequence against the
+CPU checker (bit-exact words, term counts and coefficients), restating the
+reference's tests (tests/test_dressing.cpp, test_pauli.cpp, test_partition.cpp)
+plus the golden C1 iQCC traces and large G_mol runs (124/200 qubits)."""
+import math
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from helpers import dense_dressed, digest, load_golden, same, sum_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def host(eng, osum):
+    r, c = osum.export()
+    return eng.PauliSum(osum.n_qubits, r, c)
+
+
+def check_same(got, want_osum):
+    r, c = want_osum.export()
+    assert got.rows.shape == r.shape, (got.rows.shape, r.shape)
+    assert np.array_equal(got.rows, r), "Pauli words differ"
+    assert np.array_equal(got.coeffs, c), "coefficients differ"
+
+
+def test_zero_amplitude_is_identity(eng, port):  # test_dressing.cpp:60-66
+    rng = port.rng(501)
+    h = rng.sum(4, 30)
+    g = rng.word(4, False)
+    d = eng.dress_single(host(eng, h), eng.DressOp(eng.PauliWord(4, g), 0.0))
+    assert d == host(eng, h)
+    assert eng.sortless_dress(host(eng, h), eng.DressOp(eng.PauliWord(4, g), 0.0)) == host(eng, h)
+
+
+def test_z_about_y_at_half_pi_is_minus_x(eng):  # test_dressing.cpp:68-81
+    h = eng.PauliSum(1)
+    h.append(eng.PauliWord.from_string("Z"), 1.0)
+    d = eng.dress_single(h, eng.DressOp(eng.PauliWord.from_string("Y"), math.pi / 2))
+    assert len(d) == 1 and d.word(0) == eng.PauliWord.from_string("X")
+    assert d.coeff(0).real == pytest.approx(-1.0)
+    dense = dense_dressed(h.rows, h.coeffs, 1, eng.PauliWord.from_string("Y").row, math.pi / 2)
+    assert np.abs(sum_matrix(d.rows, d.coeffs, 1) - dense).max() < 1e-14
+
+
+def test_dense_conjugation_oracle(eng, port):  # test_dressing.cpp:83-97 (seed 503)
+    rng = port.rng(503)
+    for t in range(60):
+        n = 2 + t % 5
+        h = rng.sum(n, 10 + 8 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.5, 3.5)
+        hh = host(eng, h)
+        d = eng.dress_single(hh, eng.DressOp(eng.PauliWord(n, g), tau))
+        check_same(d, port.dress_single(h, g, tau))
+        assert np.abs(sum_matrix(d.rows, d.coeffs, n) - dense_dressed(hh.rows, hh.coeffs, n, g, tau)).max() < 1e-10
+
+
+def test_spectrum_preserved(eng, port):  # test_dressing.cpp:99-113 (seed 509)
+    rng = port.rng(509)
+    for t in range(15):
+        n = 2 + t % 4
+        h = rng.sum(n, 8 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.0, 3.0)
+        hh = host(eng, h)
+        d = eng.dress_single(hh, eng.DressOp(eng.PauliWord(n, g), tau))
+        ev0 = np.linalg.eigvalsh(sum_matrix(hh.rows, hh.coeffs, n))
+        ev1 = np.linalg.eigvalsh(sum_matrix(d.rows, d.coeffs, n))
+        assert np.abs(ev0 - ev1).max() < 1e-9
+
+
+def test_periodicity_and_inverse(eng, port):  # test_dressing.cpp:115-140 (521, 523)
+    rng = port.rng(521)
+    for _ in range(10):
+        h = rng.sum(4, 25)
+        g = rng.word(4, False)
+        tau = rng.uniform(-3.0, 3.0)
+        a = eng.dress_single(host(eng, h), eng.DressOp(eng.PauliWord(4, g), tau))
+        b = eng.dress_single(host(eng, h), eng.DressOp(eng.PauliWord(4, g), tau + 2 * math.pi))
+        check_same(a, port.dress_single(h, g, tau))
+        check_same(b, port.dress_single(h, g, tau + 2 * math.pi))
+    rng = port.rng(523)
+    for _ in range(10):
+        h = rng.sum(5, 40)
+        g = rng.word(5, False)
+        tau = rng.uniform(-3.0, 3.0)
+        d = eng.DeviceSum.upload(host(eng, h))
+        d.dress(eng.PauliWord(5, g), tau)
+        d.dress(eng.PauliWord(5, g), -tau)
+        back = d.download()
+        want = port.dress_single(port.dress_single(h, g, tau), g, -tau)
+        check_same(back, want)
+
+
+def test_sortless_equals_dress_single(eng, port):  # test_dressing.cpp:177-196 (seed 557)
+    rng = port.rng(557)
+    g_sha = load_golden("small.npz")["dress557_sha"]
+    for t in range(120):
+        n = 2 + t % 7
+        h = rng.sum(n, 12 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.0, 3.0)
+        st = eng.SortlessStats()
+        d = eng.sortless_dress(host(eng, h), eng.DressOp(eng.PauliWord(n, g), tau), stats=st)
+        assert st.new_stream_sorts == 0
+        assert digest(d.rows, d.coeffs) == g_sha[t]  # reference output (golden)
+
+
+def test_growth_bound(eng, port):  # test_dressing.cpp:241-252 (seed 563)
+    rng = port.rng(563)
+    for t in range(40):
+        n = 2 + t % 5
+        h = rng.sum(n, 10 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.0, 3.0)
+        hh = host(eng, h)
+        split = eng.growth_split(hh, eng.PauliWord(n, g))
+        assert (split.n_commuting, split.n_anticommuting) == port.growth_split(h, g)
+        d = eng.dress_single(hh, eng.DressOp(eng.PauliWord(n, g), tau), eng.MergeOptions(0.0, True))
+        assert len(d) <= split.bound()
+        check_same(d, port.dress_single(h, g, tau, drop=0.0))
+
+
+def test_identity_generator_rejected(eng):  # test_dressing.cpp:254-261
+    h = eng.PauliSum(2)
+    h.append(eng.PauliWord.from_string("XI"), 1.0)
+    with pytest.raises(ValueError):
+        eng.dress_single(h, eng.DressOp(eng.PauliWord(2), 0.5))
+    with pytest.raises(ValueError):
+        eng.sortless_dress(h, eng.DressOp(eng.PauliWord(2), 0.5))
+
+
+def test_complex_or_unsorted_input_rejected(eng):
+    h = eng.PauliSum(2)
+    h.append(eng.PauliWord.from_string("XI"), 0.5 + 0.25j)
+    with pytest.raises(ValueError):
+        eng.DeviceSum.upload(h)
+    u = eng.PauliSum(2)
+    u.append(eng.PauliWord.from_string("XI"), 1.0)
+    u.append(eng.PauliWord.from_string("ZI"), 1.0)  # ZI < XI canonically
+    with pytest.raises(ValueError):
+        eng.DeviceSum.upload(u)
+
+
+def test_empty_and_commuting(eng):
+    e = eng.PauliSum(3)
+    assert len(eng.dress_single(e, eng.DressOp(eng.PauliWord.from_string("XYZ"), 0.3))) == 0
+    h = eng.PauliSum(2)
+    h.append(eng.PauliWord.from_string("ZI"), 0.5)
+    d = eng.dress_single(h, eng.DressOp(eng.PauliWord.from_string("IX"), 0.9))
+    assert d == h  # test_dressing.cpp:216-239 disjoint support
+
+
+@pytest.mark.parametrize("n", [64, 100, 124, 200, 256])
+def test_random_large(eng, port, n):
+    rng = port.rng(n)
+    h = rng.sum(n, 20000)
+    hh = host(eng, h)
+    for k in range(3):
+        g = rng.word(n, False)
+        tau = rng.uniform(-1.0, 1.0)
+        check_same(eng.dress_single(hh, eng.DressOp(eng.PauliWord(n, g), tau)), port.dress_single(h, g, tau))
+
+
+@pytest.mark.parametrize("n,terms,steps,eps,cap", [
+    (124, 200_000, 6, 0.0, 2**64 - 1),       # growth, partner pairs (dead slots)
+    (124, 200_000, 6, 1e-10, 200_000),       # C3 shape: capped every step
+    (64, 100_000, 6, 1e-4, 120_000),         # eps cut + cap
+    (200, 50_000, 4, 1e-9, 60_000),          # 4 device blocks
+])
+def test_gmol_sequence(eng, port, n, terms, steps, eps, cap):
+    h = port.gen_mol(n, terms, 2)
+    d = eng.DeviceSum.generate_mol(n, terms, 2)
+    check_same(d.download(), h)
+    rs = np.random.default_rng(7)
+    B = (n + 63) // 64
+    for k in range(steps):
+        w = int(rs.integers(2, 5))
+        qs = rs.choice(n, w, replace=False)
+        ys = rs.integers(0, 2, w)
+        if ys.sum() % 2 == 0:
+            ys[-1] ^= 1
+        p = eng.PauliWord(n)
+        for q, y in zip(qs, ys):
+            p.row[q // 64] |= np.uint64(1 << int(q % 64))
+            if y:
+                p.row[B + q // 64] |= np.uint64(1 << int(q % 64))
+        tau = float(rs.uniform(-0.2, 0.2))
+        h, st_ref = port.dress_sequence(h, p.row[None, :], [tau], eps, cap)
+        cs = eng.CompressStats()
+        d.dress_sequence(eng.Ansatz([p], [tau]), eps, cap, cs)
+        check_same(d.download(), h)
+        assert cs.dropped_terms == st_ref["dropped_terms"]
+        assert cs.dropped_weight == pytest.approx(st_ref["dropped_weight"], rel=1e-9, abs=1e-300)
+
+
+@pytest.mark.parametrize("name", ["c1_h2_sto3g.npz", "c1_h2_ccpvdz.npz"])
+def test_golden_iqcc_trace(eng, name):
+    """Replays the reference's recorded (P, tau) sequence; every dressed sum
+    must hash identically to the reference's (tests/golden/make_golden.py)."""
+    g = load_golden(name)
+    n = int(g["n_qubits"])
+    d = eng.DeviceSum.upload(eng.PauliSum(n, g["rows0"], g["coeffs0"]))
+    for it in range(len(g["terms"])):
+        sel = g["gen_iter"] == it
+        ans = eng.Ansatz([eng.PauliWord(n, r) for r in g["gens"][sel]], list(g["taus"][sel]))
+        d.dress_sequence(ans, 0.0)
+        out = d.download()
+        assert len(out) == g["terms"][it]
+        assert digest(out.rows, out.coeffs) == g["shas"][it]
+    assert same(out.rows, out.coeffs, g["rows_final"], g["coeffs_final"])
+
+
+def test_pipeline_with_truncation_seed631(eng, port):  # test_partition.cpp:180-208
+    rng = port.rng(631)
+    sha = load_golden("small.npz")["pipeline631_sha"]
+    for t in range(40):
+        n = 3 + t % 4
+        h = rng.sum(n, 25 * n)
+        g = rng.word(n, False)
+        tau = rng.uniform(-3.0, 3.0)
+        eps = 1e-3 if t % 3 == 0 else 0.0
+        mt = 40 if t % 4 == 0 else 100000
+        out = eng.dress_sequence(host(eng, h), eng.Ansatz([eng.PauliWord(n, g)], [tau]), eps, mt)
+        assert digest(out.rows, out.coeffs) == sha[t]
+
+
+def test_compress_reference_cases(eng):  # test_pauli.cpp:157-197
+    P = eng.PauliWord.from_string
+    h = eng.PauliSum(2, np.stack([P("ZI").row, P("XI").row]), [0.5, 1e-15])
+    c = eng.compress(h, 1e-12, 10)
+    assert len(c) == 1 and c.word(0) == P("ZI")
+    assert eng.compress(h, 0.0, 2) == h
+    h2 = eng.PauliSum(2, np.stack([P("II").row, P("ZI").row, P("XI").row, P("YI").row]),
+                      [1e-15, 0.5, 0.4, 0.3])
+    c2 = eng.compress(h2, 1e-18, 2)
+    assert len(c2) == 2 and c2.word(0).is_identity() and c2.word(1) == P("ZI")
+    h3 = eng.PauliSum(2, np.stack([P("ZI").row, P("XI").row, P("YI").row]), [0.5, 0.5, 0.5])
+    c3 = eng.compress(h3, 0.0, 2)
+    assert len(c3) == 2 and c3.word(0) == P("ZI") and c3.word(1) == P("XI")
+    with pytest.raises(ValueError):
+        eng.compress(h3, -1.0, 2)
+    with pytest.raises(ValueError):
+        eng.compress(h3, 0.0, 0)
+
+
+def test_compress_random(eng, port):
+    rng = port.rng(41)
+    for t in range(30):
+        h = rng.sum(5 + t % 4, 80)
+        for eps, mt in [(0.0, 1), (1e-3, 10), (0.2, 1000), (0.0, 37)]:
+            cs = eng.CompressStats()
+            got = eng.compress(host(eng, h), eps, mt, cs)
+            want, st = port.compress(h, eps, mt)
+            check_same(got, want)
+            assert cs.dropped_terms == st["dropped_terms"]
+
+
+def test_cpp_shim_against_reference():
+    """tests/cpp/test_shim_parity.cpp: iqcc::gpu::* vs the unmodified iqcc::*
+    (built where /root/reference exists; the binary travels to the box)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "_bin", "test_shim_parity")
+    if not os.path.exists(exe):
+        pytest.skip("C++ parity harness not built (needs /root/reference at build time)")
+    fcidump = os.path.join(root, "tests", "golden", "h2_sto3g.fcidump")
+    args = [exe] + ([fcidump] if os.path.exists(fcidump) else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ALL OK" in r.stdout
