@@ -134,13 +134,13 @@ int iqcc_gpu_qmf_energy_gradient(iqcc_gpu_sum* h, const double* factors, const d
  * (group_gradient, iqcc/dis.hpp:121-132, exact at poles). */
 int iqcc_gpu_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* cands, size_t K,
                        int flip_group_only, double* g);
-/* dis_candidates (iqcc/dis.hpp:140-191) without the optional seeded
- * shuffle (applied by the shim on the host with the same mt19937_64).
- * Writes up to `cap` picks sorted by (|g| desc, canonical); *n_picks gets
- * the total before truncation to top_k. */
+/* dis_candidates (iqcc/dis.hpp:140-191).  Picks are ranked by (|g| desc,
+ * canonical); when has_seed, runs of equal |g| are reshuffled with
+ * std::mt19937_64(seed) + std::shuffle exactly as the reference does.
+ * Writes min(top_k, cap) picks; *n_picks gets the count before truncation. */
 int iqcc_gpu_dis_candidates(iqcc_gpu_sum* h, const double* factors, int at_poles, size_t top_k,
-                            double screen_thr, size_t per_group_cap, uint64_t* rows_out,
-                            double* g_out, size_t cap, size_t* n_picks);
+                            double screen_thr, size_t per_group_cap, int has_seed, uint64_t seed,
+                            uint64_t* rows_out, double* g_out, size_t cap, size_t* n_picks);
 
 /* ---- bit-wise partitioning across GPUs (iqcc/partition.hpp) ------------ */
 /* choose_partition_bits (iqcc/partition.hpp:52-108) computed on the device. */

@@ -271,41 +271,29 @@ inline double gradient(const PauliSum& h, const QmfState& omega, PauliView p) {
 }
 
 /// iqcc::dis_candidates (iqcc/dis.hpp:140-191).  The device screens every
-/// flip group; the optional seeded shuffle of equal-|g| runs is applied here
-/// with the same std::mt19937_64 + std::shuffle as the reference.
+/// flip group; the seeded shuffle of equal-|g| runs uses the same
+/// std::mt19937_64 + std::shuffle as the reference (inside the engine).
 inline std::vector<RankedGenerator> dis_candidates(const PauliSum& h, const QmfState& omega,
                                                    std::size_t top_k, const DisOptions& opts = {}) {
   if (top_k < 1) throw std::invalid_argument("dis_candidates: top_k < 1");
   DeviceSum d(h);
   const auto t = detail::factor_table(omega);
   const std::size_t B = blocks_for(h.n_qubits());
+  const int has_seed = opts.tie_break_seed ? 1 : 0;
+  const uint64_t seed = opts.tie_break_seed ? *opts.tie_break_seed : 0;
   std::size_t n = 0;
   detail::check(iqcc_gpu_dis_candidates(d.handle(), t.data(), omega.at_poles(), top_k, opts.screen_threshold,
-                                        opts.per_group_cap, nullptr, nullptr, 0, &n));
-  std::vector<uint64_t> rows(std::max<std::size_t>(n, 1) * 2 * B);
-  std::vector<double> g(std::max<std::size_t>(n, 1));
-  std::size_t n2 = 0;
-  detail::check(iqcc_gpu_dis_candidates(d.handle(), t.data(), omega.at_poles(), n ? n : 1,
-                                        opts.screen_threshold, opts.per_group_cap, rows.data(), g.data(),
-                                        n, &n2));
+                                        opts.per_group_cap, has_seed, seed, nullptr, nullptr, 0, &n));
+  const std::size_t k = std::min(n, top_k);
+  std::vector<uint64_t> rows(std::max<std::size_t>(k, 1) * 2 * B);
+  std::vector<double> g(std::max<std::size_t>(k, 1));
+  detail::check(iqcc_gpu_dis_candidates(d.handle(), t.data(), omega.at_poles(), top_k, opts.screen_threshold,
+                                        opts.per_group_cap, has_seed, seed, rows.data(), g.data(), k, &n));
   std::vector<RankedGenerator> picks;
-  for (std::size_t i = 0; i < n; ++i)
+  for (std::size_t i = 0; i < k; ++i)
     picks.push_back({PauliWord(h.n_qubits(), std::span<const Block>(rows.data() + i * 2 * B, B),
                                std::span<const Block>(rows.data() + i * 2 * B + B, B)),
                      g[i]});
-  if (opts.tie_break_seed) {
-    std::mt19937_64 rng(*opts.tie_break_seed);
-    std::size_t i = 0;
-    while (i < picks.size()) {
-      std::size_t j = i + 1;
-      const double mag = std::abs(picks[i].gradient);
-      while (j < picks.size() && std::abs(std::abs(picks[j].gradient) - mag) <= 1e-12 * std::max(1.0, mag))
-        ++j;
-      std::shuffle(picks.begin() + i, picks.begin() + j, rng);
-      i = j;
-    }
-  }
-  if (picks.size() > top_k) picks.resize(top_k);
   return picks;
 }
 

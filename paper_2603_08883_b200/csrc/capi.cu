@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <random>
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -501,22 +503,36 @@ int iqcc_gpu_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* c
 }
 
 int iqcc_gpu_dis_candidates(iqcc_gpu_sum* h, const double* factors, int at_poles, size_t top_k,
-                            double screen_thr, size_t per_group_cap, uint64_t* rows_out,
-                            double* g_out, size_t cap, size_t* n_picks) {
+                            double screen_thr, size_t per_group_cap, int has_seed, uint64_t seed,
+                            uint64_t* rows_out, double* g_out, size_t cap, size_t* n_picks) {
   return guarded([&] {
     need(h);
     if (top_k < 1) throw std::invalid_argument("dis_candidates: top_k < 1");
     std::vector<uint64_t> rows;
     std::vector<double> g;
     size_t n = dis_store(h->s, factors, at_poles != 0, top_k, screen_thr, per_group_cap, rows, g);
+    std::vector<size_t> order(n);
+    for (size_t i = 0; i < n; ++i) order[i] = i;
+    if (has_seed) {  // iqcc/dis.hpp:172-188: reshuffle runs of equal magnitude
+      std::mt19937_64 rng(seed);
+      size_t i = 0;
+      while (i < n) {
+        size_t j = i + 1;
+        const double mag = std::abs(g[order[i]]);
+        while (j < n && std::abs(std::abs(g[order[j]]) - mag) <= 1e-12 * std::max(1.0, mag)) ++j;
+        std::shuffle(order.begin() + i, order.begin() + j, rng);
+        i = j;
+      }
+    }
     const uint32_t Bref = ref_blocks(h->s), B = h->s.B;
     const size_t w = std::min(cap, std::min(n, top_k));
     for (size_t i = 0; i < w; ++i) {
+      const size_t o = order[i];
       for (uint32_t b = 0; b < Bref; ++b) {
-        rows_out[i * 2 * Bref + b] = rows[i * 2 * B + b];
-        rows_out[i * 2 * Bref + Bref + b] = rows[i * 2 * B + B + b];
+        rows_out[i * 2 * Bref + b] = rows[o * 2 * B + b];
+        rows_out[i * 2 * Bref + Bref + b] = rows[o * 2 * B + B + b];
       }
-      g_out[i] = g[i];
+      g_out[i] = g[o];
     }
     *n_picks = n;
   });

@@ -403,6 +403,14 @@ size_t dis_store(DeviceStore& s, const double* factors, bool poles, size_t top_k
 double choose_bits_store(DeviceStore& s, size_t m, size_t* bits_out);
 void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner, int rank);
 
+/// Partition bits as (device word, bit) pairs (iqcc/partition.hpp:40-42).
+struct PartSpecHost {
+  int m = 0;
+  int word[16] = {};
+  int bit[16] = {};
+};
+PartSpecHost make_part_spec(const DeviceStore& s, size_t m, const size_t* bits);
+
 /// Reversed row conversion helpers (host).
 void row_to_device_key(const uint64_t* row, uint32_t B, ull* key);
 void device_key_to_row(const ull* key, uint32_t B, uint64_t* row);

@@ -260,6 +260,132 @@ void store_clone(const DeviceStore& src, DeviceStore& dst) {
   }
 }
 
+// ------------------------------------------------- shard restriction
+// distribute (iqcc/partition.hpp:208-220) on one rank: keep the live terms
+// whose partition key (gather of the partition bits, partition.hpp:40-42)
+// is owned by `rank`.
+struct PartSpec {
+  int m;
+  int word[16];
+  int bit[16];
+};
+
+template <int B>
+__device__ __forceinline__ unsigned part_key(const Key<B>& k, const PartSpec& ps) {
+  unsigned key = 0;
+  for (int b = 0; b < ps.m; ++b) {
+    ull v = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * B; ++j) v = (j == ps.word[b]) ? k.w[j] : v;
+    key |= (unsigned)((v >> ps.bit[b]) & 1ull) << b;
+  }
+  return key;
+}
+
+template <int B>
+__global__ void __launch_bounds__(CT) k_compact_part(const ull* __restrict__ keys,
+                                                     const double* __restrict__ coef, size_t M,
+                                                     Filter filt, PartSpec ps,
+                                                     const unsigned* __restrict__ owner, int rank,
+                                                     ull* __restrict__ okeys, double* __restrict__ ocoef,
+                                                     ull* __restrict__ tile_status,
+                                                     unsigned* __restrict__ tile_counter,
+                                                     ull* __restrict__ total_out) {
+  __shared__ ull s_tile, s_base;
+  __shared__ int scratch[CT / 32 + 2];
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const ull tile = s_tile;
+  const size_t ntiles = (M + CTILE - 1) / CTILE;
+  if (tile >= ntiles) return;
+  const size_t first = tile * CTILE + (size_t)threadIdx.x * CI;
+  unsigned keep = 0;
+#pragma unroll
+  for (int k = 0; k < CI; ++k) {
+    const size_t i = first + k;
+    if (i < M) {
+      const Key<B> key = load_key<B>(keys, i);
+      if (filter_keep(filt, i, coef[i], i == 0 && key_is_identity<B>(key)) &&
+          owner[part_key<B>(key, ps)] == (unsigned)rank)
+        keep |= 1u << k;
+    }
+  }
+  int total;
+  const int excl = block_exclusive<CT>((int)__popc(keep), 0, OpAdd(), scratch, &total);
+  if (threadIdx.x < 32) {
+    const ull bse = lookback_warp(tile_status, tile, (ull)total);
+    if (threadIdx.x == 0) {
+      s_base = bse;
+      if (tile == ntiles - 1) *total_out = bse + total;
+    }
+  }
+  __syncthreads();
+  size_t pos = s_base + excl;
+#pragma unroll
+  for (int k = 0; k < CI; ++k) {
+    if (!((keep >> k) & 1u)) continue;
+    store_key<B>(okeys, pos, load_key<B>(keys, first + k));
+    ocoef[pos] = coef[first + k];
+    ++pos;
+  }
+}
+
+PartSpecHost make_part_spec(const DeviceStore& s, size_t m, const size_t* bits) {
+  if (m > 16) throw std::invalid_argument("partition: at most 16 partition bits");
+  PartSpecHost ps;
+  ps.m = (int)m;
+  const size_t n = s.n_qubits;
+  for (size_t b = 0; b < m; ++b) {
+    if (bits[b] >= 2 * n) throw std::invalid_argument("PartitionMap: bit position out of range");
+    const size_t q = bits[b] < n ? bits[b] : bits[b] - n;
+    ps.word[b] = (int)((bits[b] < n ? 0 : s.B) + q / 64);
+    ps.bit[b] = (int)(63 - q % 64);
+  }
+  return ps;
+}
+
+void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner, int rank) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const PartSpecHost h = make_part_spec(s, m, bits);
+  PartSpec ps;
+  ps.m = h.m;
+  for (int b = 0; b < 16; ++b) {
+    ps.word[b] = h.word[b];
+    ps.bit[b] = h.bit[b];
+  }
+  std::vector<unsigned> own((size_t)1 << m);
+  for (size_t p = 0; p < own.size(); ++p) own[p] = (unsigned)owner[p];
+  unsigned* down = ws.misc3.as<unsigned>(own.size());
+  IQCC_CUDA(cudaMemcpyAsync(down, own.data(), own.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
+  ull* ok = ws.out_keys.as<ull>(std::max<size_t>(s.M, 1) * 2 * s.B);
+  double* oc = ws.out_coef.as<double>(std::max<size_t>(s.M, 1));
+  const size_t ntiles = std::max<size_t>(1, (s.M + CTILE - 1) / CTILE);
+  ull* tstat = ws.tile_status.as<ull>(ntiles + 1);
+  ull* ctr = ws.counters.as<ull>(8);
+  IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntiles + 1) * sizeof(ull), st));
+  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
+  unsigned* tc = reinterpret_cast<unsigned*>(ctr + 4);
+  if (s.M > 0) {
+    KernelScope ks("restrict");
+    switch (s.B) {
+      case 1: k_compact_part<1><<<(unsigned)ntiles, CT, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, ps, down, rank, ok, oc, tstat, tc, ctr); break;
+      case 2: k_compact_part<2><<<(unsigned)ntiles, CT, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, ps, down, rank, ok, oc, tstat, tc, ctr); break;
+      default: k_compact_part<4><<<(unsigned)ntiles, CT, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, ps, down, rank, ok, oc, tstat, tc, ctr); break;
+    }
+  }
+  ull n = 0;
+  IQCC_CUDA(cudaMemcpyAsync(&n, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  IQCC_CUDA(cudaStreamSynchronize(st));
+  std::swap(s.kbuf, ws.out_keys);
+  std::swap(s.cbuf, ws.out_coef);
+  // the identity lives in the all-zero-key shard (partition.hpp:364-366)
+  s.has_identity = s.has_identity && owner[0] == (size_t)rank;
+  s.M = n;
+  s.logical = n;
+  s.filt = Filter{};
+}
+
 // ------------------------------------------------------------- generator
 template <int B>
 __global__ void k_gen_mol(uint32_t n, uint32_t Bref, uint64_t seed, size_t N,

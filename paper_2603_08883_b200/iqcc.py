@@ -467,20 +467,35 @@ def gradient(h: PauliSum, omega: QmfState, p: PauliWord) -> float:
 
 
 def dis_candidates(h: PauliSum, omega: QmfState, top_k: int, opts: DisOptions = DisOptions()) -> list:
-    """iqcc/dis.hpp:140-191.  The optional seeded tie shuffle is applied on
-    the host with the same generator (std::mt19937_64 + std::shuffle would
-    be required for bit parity)."""
+    """iqcc/dis.hpp:140-191 (seeded tie shuffle included, same generator)."""
     if top_k < 1:
         raise ValueError("dis_candidates: top_k < 1")
-    d = DeviceSum.upload(h)
+    return DeviceSum.upload(h).dis_candidates(omega, top_k, opts)
+
+
+def _dis_on(d: "DeviceSum", omega: QmfState, top_k: int, opts: DisOptions) -> list:
     t = qmf_factor_table(omega)
-    W = 2 * blocks_for(h.n_qubits)
-    cap = max(1, top_k if top_k < 1 << 40 else len(h))
-    cap = min(cap, max(1, len(h)))
+    W = 2 * blocks_for(d.n_qubits)
+    n = C.c_size_t()
+    seed = opts.tie_break_seed
+    args = (d.handle, _addr(t), int(omega.at_poles()), top_k, opts.screen_threshold, opts.per_group_cap,
+            int(seed is not None), seed or 0)
+    check(lib.iqcc_gpu_dis_candidates(*args, None, None, 0, C.byref(n)))
+    cap = max(1, min(n.value, top_k))
     rows = np.zeros((cap, W), np.uint64)
     g = np.zeros(cap, np.float64)
-    n = C.c_size_t()
-    check(lib.iqcc_gpu_dis_candidates(d.handle, _addr(t), int(omega.at_poles()), top_k, opts.screen_threshold,
-                                      opts.per_group_cap, _addr(rows), _addr(g), cap, C.byref(n)))
-    k = min(n.value, top_k, cap)
-    return [RankedGenerator(PauliWord(h.n_qubits, rows[i]), float(g[i])) for i in range(k)]
+    check(lib.iqcc_gpu_dis_candidates(*args, _addr(rows), _addr(g), cap, C.byref(n)))
+    k = min(n.value, top_k)
+    return [RankedGenerator(PauliWord(d.n_qubits, rows[i]), float(g[i])) for i in range(k)]
+
+
+DeviceSum.dis_candidates = lambda self, omega, top_k, opts=DisOptions(): _dis_on(self, omega, top_k, opts)
+
+
+def choose_partition_bits(h, m: int):
+    """iqcc/partition.hpp:52-108 on the device; returns (bits, imbalance)."""
+    d = h if isinstance(h, DeviceSum) else DeviceSum.upload(h)
+    bits = np.zeros(max(1, m), np.uintp)
+    imb = C.c_double()
+    check(lib.iqcc_gpu_choose_partition_bits(d.handle, m, _addr(bits), C.byref(imb)))
+    return [int(b) for b in bits[:m]], imb.value

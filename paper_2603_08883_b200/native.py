@@ -71,8 +71,8 @@ _SIGS = {
     "iqcc_gpu_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
     "iqcc_gpu_qmf_energy_gradient": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(C.c_double), _f64p]),
     "iqcc_gpu_gradients": (C.c_int, [_vp, _f64p, _u64p, C.c_size_t, C.c_int, _f64p]),
-    "iqcc_gpu_dis_candidates": (C.c_int, [_vp, _f64p, C.c_int, C.c_size_t, C.c_double, C.c_size_t, _u64p,
-                                          _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_dis_candidates": (C.c_int, [_vp, _f64p, C.c_int, C.c_size_t, C.c_double, C.c_size_t, C.c_int,
+                                          C.c_uint64, _u64p, _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_choose_partition_bits": (C.c_int, [_vp, C.c_size_t, _szp, C.POINTER(C.c_double)]),
     "iqcc_gpu_sum_restrict": (C.c_int, [_vp, C.c_size_t, _szp, _szp, C.c_int]),
     "iqcc_gpu_nccl_unique_id": (C.c_int, [_vp]),

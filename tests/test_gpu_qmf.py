@@ -1,0 +1,156 @@
+"""GPU parity for the energy / gradient / DIS rows:
+expect_sum, qmf_energy_gradient, gradient, dis_candidates and
+choose_partition_bits against the CPU checker, restating tests/test_qmf.cpp
+and tests/test_dis.cpp.  Tolerances: per-term values of expect_word and the
+DIS gradients are summed in the reference's order and compared bit-exactly;
+energies and QMF gradients are sums in a different order, compared at
+1e-10 relative (north_star's fp64 tolerance)."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import load_golden
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+
+
+def host(eng, osum):
+    r, c = osum.export()
+    return eng.PauliSum(osum.n_qubits, r, c)
+
+
+def close(a, b, rel=REL):
+    return abs(a - b) <= rel * max(1.0, abs(b))
+
+
+def test_expect_word_axes(eng):  # test_qmf.cpp:21-27
+    om = eng.QmfState.zeros(1)
+    h = eng.PauliSum(1)
+    h.append(eng.PauliWord.from_string("Z"), 1.0)
+    assert eng.expect_sum(om, h) == 1.0
+    om.theta[0] = math.pi / 2
+    hx = eng.PauliSum(1)
+    hx.append(eng.PauliWord.from_string("X"), 1.0)
+    assert eng.expect_sum(om, hx) == pytest.approx(1.0)
+
+
+def test_expect_sum_random(eng, port):
+    rng = port.rng(201)
+    for t in range(40):
+        n = 2 + t % 30
+        h = rng.sum(n, 200)
+        th, ph = rng.qmf(n)
+        got = eng.expect_sum(eng.QmfState(th, ph), host(eng, h))
+        assert close(got, port.expect_sum(th, ph, h))
+    # per-term values are bit-exact: one-term sums
+    for t in range(100):
+        n = 1 + t % 70
+        w = rng.word(n)
+        h = port.sum(n, w[None, :], [1.0])
+        th, ph = rng.qmf(n)
+        assert eng.expect_sum(eng.QmfState(th, ph), host(eng, h)) == port.expect_word(n, th, ph, w)
+
+
+def test_h2_hf_energy(eng):  # test_qmf.cpp:54-66
+    g = load_golden("c1_h2_sto3g.npz")
+    h = eng.PauliSum(4, g["rows0"], g["coeffs0"])
+    e = eng.expect_sum(eng.hf_reference([True, True, False, False]), h)
+    assert e == pytest.approx(-1.11615145, abs=1e-6)
+    assert close(e, float(g["e_hf"]), 1e-14)
+
+
+@pytest.mark.parametrize("n", [6, 40, 124, 200])
+def test_qmf_energy_gradient(eng, port, n):
+    rng = port.rng(211 + n)
+    h = rng.sum(n, 3000)
+    th, ph = rng.qmf(n)
+    e, g = eng.qmf_energy_gradient(host(eng, h), eng.QmfState(th, ph))
+    er, gr = port.qmf_energy_gradient(h, th, ph)
+    assert close(e, er)
+    scale = max(1.0, np.abs(gr).max())
+    assert np.abs(g - gr).max() <= REL * scale
+
+
+def test_qmf_gradient_finite_difference(eng, port):  # test_qmf.cpp:68-87
+    rng = port.rng(211)
+    for _ in range(5):
+        h = rng.sum(6, 60)
+        th, ph = rng.qmf(6)
+        _, g = eng.qmf_energy_gradient(host(eng, h), eng.QmfState(th, ph))
+        step = 1e-5
+        for j in range(12):
+            lo_t, hi_t = th.copy(), th.copy()
+            lo_p, hi_p = ph.copy(), ph.copy()
+            if j < 6:
+                lo_t[j] -= step
+                hi_t[j] += step
+            else:
+                lo_p[j - 6] -= step
+                hi_p[j - 6] += step
+            fd = (port.expect_sum(hi_t, hi_p, h) - port.expect_sum(lo_t, lo_p, h)) / (2 * step)
+            assert abs(g[j] - fd) / max(1.0, abs(fd), abs(g[j])) < 1e-6
+
+
+def test_gradient_known_answer(eng):  # test_dis.cpp:108-114
+    h = eng.PauliSum(1)
+    h.append(eng.PauliWord.from_string("X"), 1.0)
+    assert eng.gradient(h, eng.QmfState.zeros(1), eng.PauliWord.from_string("Y")) == pytest.approx(1.0)
+
+
+@pytest.mark.parametrize("n", [5, 64, 124])
+def test_gradient_bit_exact(eng, port, n):
+    rng = port.rng(419 + n)
+    h = rng.sum(n, 2000)
+    th, ph = rng.qmf(n)
+    d = eng.DeviceSum.upload(host(eng, h))
+    cands = np.stack([rng.word(n, False) for _ in range(64)])
+    g = d.gradients(eng.QmfState(th, ph), cands)
+    for k in range(len(cands)):
+        assert g[k] == port.gradient(h, th, ph, cands[k])
+
+
+def test_dis_candidates_random(eng, port):  # test_dis.cpp:231-263 shapes
+    rng = port.rng(443)
+    for t in range(12):
+        n = 4 + t % 5
+        h = rng.sum(n, 80)
+        th, ph = rng.qmf(n)
+        occ = np.where(np.arange(n) % 2 == 0, math.pi, 0.0)
+        for thx in (th, occ):
+            for k, seed in ((4, None), (100, None), (100, 7)):
+                want_rows, want_g = port.dis_candidates(h, thx, ph, k, seed=seed)
+                got = eng.dis_candidates(host(eng, h), eng.QmfState(thx, ph), k,
+                                         eng.DisOptions(tie_break_seed=seed))
+                assert len(got) == len(want_g)
+                for p, wr, wg in zip(got, want_rows, want_g):
+                    assert np.array_equal(p.word.row, wr) and p.gradient == wg
+
+
+@pytest.mark.parametrize("name", ["c1_h2_sto3g.npz", "c1_h2_ccpvdz.npz"])
+def test_dis_at_hf_golden(eng, name):
+    g = load_golden(name)
+    n, ne = int(g["n_qubits"]), int(g["n_electrons"])
+    h = eng.PauliSum(n, g["rows0"], g["coeffs0"])
+    picks = eng.dis_candidates(h, eng.hf_reference([j < ne for j in range(n)]), 1 << 20)
+    assert len(picks) == len(g["dis_g"])
+    for p, wr, wg in zip(picks, g["dis_rows"], g["dis_g"]):
+        assert np.array_equal(p.word.row, wr) and p.gradient == wg
+
+
+def test_choose_partition_bits(eng, port):  # test_partition.cpp:79-134
+    rng = port.rng(607)
+    for t in range(6):
+        h = rng.sum(8, 150)
+        for m in (1, 2, 3):
+            bits, imb = eng.choose_partition_bits(host(eng, h), m)
+            wb, wi = port.choose_partition_bits(h, m)
+            assert bits == list(wb) and imb == pytest.approx(wi, rel=1e-15)
+    hm = port.gen_mol(124, 50000, 2)
+    d = eng.DeviceSum.generate_mol(124, 50000, 2)
+    for m in (1, 2, 3):
+        bits, imb = eng.choose_partition_bits(d, m)
+        wb, wi = port.choose_partition_bits(hm, m)
+        assert bits == list(wb) and imb == pytest.approx(wi, rel=1e-15)
