@@ -52,15 +52,25 @@ def blocks_for(n):
     return 1 if n == 0 else (n + 63) // 64
 
 
-def entangler(n_qubits: int, index: int, flip_qubit: int | None = None):
-    """DIS-like generator #index (odd-Y X/Y word of weight 2-4) and tau."""
+def entangler(n_qubits: int, index: int, flip=None):
+    """DIS-like generator #index (odd-Y X/Y word of weight 2-4) and tau.
+    flip = (qubit, plane) forces the letter on `qubit` to set that plane's
+    bit, so the entangler flips that partition bit."""
     rs = np.random.default_rng([4, index])
     w = int(rs.integers(2, 5))
     qs = [int(q) for q in rs.choice(n_qubits, w, replace=False)]
-    if flip_qubit is not None and flip_qubit not in qs:
-        qs[0] = flip_qubit
     ys = [int(y) for y in rs.integers(0, 2, w)]
-    if sum(ys) % 2 == 0:
+    if flip is not None:
+        fq, plane = flip
+        if fq not in qs:
+            qs[0] = fq
+        i = qs.index(fq)
+        if plane == "z":
+            ys[i] = 1
+        if sum(ys) % 2 == 0:  # restore odd #Y on another position
+            j = (i + 1) % w
+            ys[j] ^= 1
+    elif sum(ys) % 2 == 0:
         ys[-1] ^= 1
     B = blocks_for(n_qubits)
     row = np.zeros(2 * B, np.uint64)
@@ -72,11 +82,12 @@ def entangler(n_qubits: int, index: int, flip_qubit: int | None = None):
     return row, tau
 
 
-def step_entanglers(n_qubits, step, flip_qubit=None):
+def step_entanglers(n_qubits, step, flip=None):
+    """10 entanglers; #0, #3, #6 (and #9) flip the first partition bit."""
     out = []
     for k in range(ENTANGLERS_PER_STEP):
-        fq = flip_qubit if (flip_qubit is not None and k % 3 == 0) else None
-        out.append(entangler(n_qubits, step * ENTANGLERS_PER_STEP + k, fq))
+        f = flip if (flip is not None and k % 3 == 0) else None
+        out.append(entangler(n_qubits, step * ENTANGLERS_PER_STEP + k, f))
     return out
 
 
@@ -207,15 +218,19 @@ def run_gpu_arm(args, rank, world, local_rank):
 
     # ---- input (setup, not timed)
     d = iqcc.DeviceSum.generate_mol(N_QUBITS, n_terms, SEED_H)
-    flip_qubit = None
+    # the 8-GPU partition bits (greedy, prefix-consistent for m = 1, 2, 3)
+    # fix which entanglers flip a partition bit, identically at every N
+    bits8, _ = iqcc.choose_partition_bits(d, 3)
+    b0 = bits8[0]
+    flip = (b0, "x") if b0 < N_QUBITS else (b0 - N_QUBITS, "z")
     part = None
     if world > 1:
-        part = iqcc.Partition.setup(d, world, rank)  # choose bits, restrict to own shard, NCCL
-        flip_qubit = part.flip_qubit
+        part = iqcc.Partition.setup(d, world, rank)  # restrict to own shard, join NCCL
+        assert (part.flip_qubit, part.flip_plane) == flip
     torch.cuda.synchronize()
 
     def dress_step(store, s):
-        ents = step_entanglers(N_QUBITS, s, flip_qubit)
+        ents = step_entanglers(N_QUBITS, s, flip)
         if part:
             tin = 0
             for row, tau in ents:

@@ -455,15 +455,19 @@ __global__ void k_check_perm(const unsigned* __restrict__ inv_perm, size_t A, si
 }
 
 // ------------------------------------------------------------- partition
+/// Product j in sorted order: gathered through inv_perm (local products) or
+/// read from a materialized buffer q_keys (products received from a peer).
 template <int B>
 __device__ __forceinline__ Key<B> q_key(const ull* __restrict__ keys,
-                                        const unsigned* __restrict__ inv_perm, size_t j,
-                                        const Key<B>& P) {
+                                        const unsigned* __restrict__ inv_perm,
+                                        const ull* __restrict__ q_keys, size_t j, const Key<B>& P) {
+  if (q_keys) return load_key<B>(q_keys, j);
   return key_xor<B>(load_key<B>(keys, inv_perm[j]), P);
 }
 
 template <int B>
 __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __restrict__ inv_perm,
+                            const ull* __restrict__ q_keys,
                             size_t nS, size_t nQ, Key<B> P, size_t tile_items, size_t ntiles,
                             ull* __restrict__ part_a, ull* __restrict__ part_b,
                             ull* __restrict__ part_o, const unsigned* __restrict__ pmask,
@@ -475,7 +479,7 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
   size_t lo = d > nQ ? d - nQ : 0, hi = min(d, nS);
   while (lo < hi) {
     size_t mid = (lo + hi) >> 1;
-    if (key_cmp<B>(load_key<B>(keys, mid), q_key<B>(keys, inv_perm, d - 1 - mid, P)) <= 0)
+    if (key_cmp<B>(load_key<B>(keys, mid), q_key<B>(keys, inv_perm, q_keys, d - 1 - mid, P)) <= 0)
       lo = mid + 1;
     else
       hi = mid;
@@ -483,7 +487,7 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
   size_t a = lo, b = d - lo;
   // never split a run of equal survivors (live + dead slot) from its product
   if (b < nQ) {
-    const Key<B> q = q_key<B>(keys, inv_perm, b, P);
+    const Key<B> q = q_key<B>(keys, inv_perm, q_keys, b, P);
     while (a > 0 && key_cmp<B>(load_key<B>(keys, a - 1), q) == 0) --a;
   }
   part_a[t] = a;
@@ -587,6 +591,8 @@ struct MergeArgs {
   const double* coef;
   Filter filt;
   const unsigned* inv_perm;
+  const ull* q_keys;    // non-null: products already materialized (key ^ P, value)
+  const double* q_vals;
   const ull* part_a;
   const ull* part_b;
   const ull* part_o;
@@ -618,13 +624,23 @@ __device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull
     bulk_g2s(sc, g.coef + c0, cb, mb);
   }
   const int qc0 = nS + 4;
-  for (int j = threadIdx.x; j < nQ; j += NT) {
-    const size_t src = __ldg(g.inv_perm + b0 + j);
-    const ull* gk = g.keys + src * 2 * B;
-    ull* s = sk + (size_t)(nS + j) * 2 * B;
+  if (g.q_keys) {  // contiguous received products
+    for (int j = threadIdx.x; j < nQ; j += NT) {
+      const ull* gk = g.q_keys + (b0 + j) * 2 * B;
+      ull* s = sk + (size_t)(nS + j) * 2 * B;
 #pragma unroll
-    for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, gk + 2 * h);
-    cp_async8(sc + qc0 + j, g.coef + src);
+      for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, gk + 2 * h);
+      cp_async8(sc + qc0 + j, g.q_vals + b0 + j);
+    }
+  } else {
+    for (int j = threadIdx.x; j < nQ; j += NT) {
+      const size_t src = __ldg(g.inv_perm + b0 + j);
+      const ull* gk = g.keys + src * 2 * B;
+      ull* s = sk + (size_t)(nS + j) * 2 * B;
+#pragma unroll
+      for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, gk + 2 * h);
+      cp_async8(sc + qc0 + j, g.coef + src);
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -667,8 +683,16 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
       if (lane == 0) spm[e0 >> 5] = word;
     }
   }
-  // Q rows stay raw in shared memory; their product key is row ^ P (on the fly)
-  auto qkey = [&](int j) { return key_xor<B>(sm_key16<B>(sk, nS + j), P); };
+  // local products stay raw in shared memory (key = row ^ P on the fly);
+  // received products arrive as final keys and values
+  const bool qdirect = g.q_keys != nullptr;
+  const Key<B> PX = qdirect ? Key<B>{} : P;
+  auto qkey = [&](int j) { return key_xor<B>(sm_key16<B>(sk, nS + j), PX); };
+  auto qval = [&](int j, const Key<B>& kq) {
+    if (qdirect) return sc[qc0 + j];
+    const double pr = __dmul_rn(sc[qc0 + j], g.sn);
+    return product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
+  };
   {  // per-thread merge-path split (runs of equal survivors stay with their product)
     const int d = min((int)threadIdx.x * IPT, n);
     int lo = max(0, d - nQ), hi = min(d, nS);
@@ -739,8 +763,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
           v = anticommutes<B>(ks, P) ? __dmul_rn(cv, g.cs) : cv;
         }
         if (c == 0) {
-          const double pr = __dmul_rn(sc[qc0 + j], g.sn);
-          const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
+          const double qv = qval(j, kq);
           if (pres) {
             const double sum = __dadd_rn(v, qv);
             put(keep_term(sum, id, g.drop) ? sum : dead_value(), i);
@@ -752,8 +775,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
           put(keep_term(v, id, g.drop) ? v : dead_value(), i);
         }
       } else {
-        const double pr = __dmul_rn(sc[qc0 + j], g.sn);
-        const double qv = product_phase<B>(key_xor<B>(kq, P), P) == 1 ? pr : -pr;
+        const double qv = qval(j, kq);
         put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
       }
       if (c <= 0 && ++i < ia1) ks = sm_key16<B>(sk, i);
@@ -903,101 +925,35 @@ std::vector<int> level_positions(const Key<B>& P) {
 
 
 
-template <int B, int NT, int IPT>
-size_t launch_merge(DeviceStore& s, const unsigned* inv_perm, size_t M, size_t A, const Key<B>& P,
-                    double cs, double sn, double drop, bool want_hist, double eps,
-                    const unsigned* pmask, const unsigned* ppre, size_t W, const unsigned* ptotal) {
-  Workspace& ws = workspace();
-  cudaStream_t st = stream();
-  constexpr int TILEM = NT * IPT;
-  const size_t total = M + A;
-  const size_t ntm = std::max<size_t>(1, (total + TILEM - 1) / TILEM);
-  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1));
-  ull* pb = pa + (ntm + 1);
-  ull* po = pb + (ntm + 1);
-  {
-    KernelScope ks("partition");
-    k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
-        s.keys(), inv_perm, M, A, P, TILEM, ntm, pa, pb, po, pmask, ppre, W, ptotal);
-  }
-  ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
-  double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
-  ull* ctr = ws.counters.as<ull>(8);
-  unsigned* hist = ws.hist.as<unsigned>(kHistBins);
-  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
-  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
-  using Cfg = MergeCfg<B, NT, IPT>;
-  const size_t smem = Cfg::bytes(want_hist, 2);
-  static int ctas_per_sm = 0;
-  static int n_sm = 0;
-  if (!ctas_per_sm) {
-    IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Cfg::bytes(true, 2)));
-    IQCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_merge<B, NT, IPT>, NT,
-                                                            Cfg::bytes(true, 2)));
-    IQCC_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0));
-    ctas_per_sm = std::max(ctas_per_sm, 1);
-  }
-  MergeArgs g;
-  g.keys = s.keys();
-  g.coef = s.coef();
-  g.filt = s.filt;
-  g.inv_perm = inv_perm;
-  g.part_a = pa;
-  g.part_b = pb;
-  g.part_o = po;
-  g.ntiles = ntm;
-  g.cs = cs;
-  g.sn = sn;
-  g.drop = drop;
-  g.eps = eps;
-  g.out_keys = out_keys;
-  g.out_coef = out_coef;
-  g.counters = ctr;
-  g.hist = hist;
-  g.want_hist = want_hist ? 1 : 0;
-  g.dbg = debug_buffer();
-  static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
-  if (persistent) {
-    KernelScope ks("merge");
-    const unsigned grid = (unsigned)std::min<size_t>(ntm, (size_t)n_sm * ctas_per_sm);
-    k_merge<B, NT, IPT><<<grid, NT, smem, st>>>(g, P);
-  } else {
-    static bool attr1 = false;
-    if (!attr1) {
-      IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)Cfg::bytes(true, 1)));
-      attr1 = true;
-    }
-    KernelScope ks("merge");
-    k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
-  }
-  IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
-  if (getenv("IQCC_DEBUG")) debug_check("merge");
-  return ntm;
-}
+/// Device state of one planned step (classify + present prefix + product
+/// order), shared by the local dressing step and the partitioned one.
+struct PlanState {
+  size_t M = 0, A = 0, W = 0;
+  unsigned* inv_perm = nullptr;
+  unsigned* pmask = nullptr;
+  unsigned* ppre = nullptr;
+  unsigned* ptotal = nullptr;
+};
+PlanState g_plan;
 
 template <int B>
-DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps) {
+void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
+  PlanState pl;
   const size_t M = s.M;
-  const Key<B> P = make_key<B>(gen_row);
-  DressOutcome out;
-  size_t A = 0;
-  unsigned* inv_perm = nullptr;
+  pl.M = M;
   const std::vector<int> pos = level_positions<B>(P);
   const int m = (int)pos.size();
   const int nch = (m + kLevelsPerChunk - 1) / kLevelsPerChunk;
   const size_t W = (M + 31) / 32;
+  pl.W = W;
   unsigned* fmask = ws.fmask.as<unsigned>(2 * std::max<size_t>(W, 1) + 64);
-  unsigned* pmask = fmask + std::max<size_t>(W, 1);
-  unsigned* ppre = ws.tables.as<unsigned>(std::max<size_t>(W, 1) + (W + PW - 1) / PW + 8);
-  unsigned* bsum = ppre + std::max<size_t>(W, 1);
-  unsigned* ptotal = bsum + (W + PW - 1) / PW + 4;
-  IQCC_CUDA(cudaMemsetAsync(ptotal, 0, sizeof(unsigned), st));
+  pl.pmask = fmask + std::max<size_t>(W, 1);
+  pl.ppre = ws.tables.as<unsigned>(std::max<size_t>(W, 1) + (W + PW - 1) / PW + 8);
+  unsigned* bsum = pl.ppre + std::max<size_t>(W, 1);
+  pl.ptotal = bsum + (W + PW - 1) / PW + 4;
+  IQCC_CUDA(cudaMemsetAsync(pl.ptotal, 0, sizeof(unsigned), st));
   short* lcp = nullptr;
   if (M > 0) {
     lcp = ws.lcp.as<short>(M);
@@ -1005,21 +961,21 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
       KernelScope ks("classify");
       constexpr int IT = B >= 4 ? 2 : 4;
       k_classify<B, IT><<<(unsigned)((M + 256 * IT - 1) / (256 * IT)), 256, 0, st>>>(
-          s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pmask);
+          s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pl.pmask);
     }
-    const size_t nb = (W + PW - 1) / PW;
     if (getenv("IQCC_DEBUG")) debug_check("classify");
+    const size_t nb = (W + PW - 1) / PW;
     {
       KernelScope ks("present");
-      k_popc_blocks<<<(unsigned)nb, 256, 0, st>>>(pmask, W, bsum);
-      k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, ptotal);
-      k_popc_prefix<<<(unsigned)nb, 256, 0, st>>>(pmask, W, bsum, ppre);
+      k_popc_blocks<<<(unsigned)nb, 256, 0, st>>>(pl.pmask, W, bsum);
+      k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, pl.ptotal);
+      k_popc_prefix<<<(unsigned)nb, 256, 0, st>>>(pl.pmask, W, bsum, pl.ppre);
       count_launch("present");
       count_launch("present");
     }
   }
   if (getenv("IQCC_DEBUG") && M > 0) debug_check("present");
-  if (sn != 0.0 && M > 0) {
+  if (products && M > 0) {
     const size_t ntiles = (M + WT - 1) / WT;
     const size_t ngroups = (ntiles + GROUP - 1) / GROUP;
     if (ngroups > 1024) throw std::runtime_error("dress: more than 2^28 terms per device shard");
@@ -1035,7 +991,7 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
     long long* g_bwd = g_fwd + ngroups * kThrPerChunk;
     long long* a_total = g_bwd + ngroups * kThrPerChunk;
     int* rdelta = nch > 1 ? ws.rdelta.as<int>(M) : nullptr;
-    inv_perm = ws.inv_perm.as<unsigned>(M);
+    pl.inv_perm = ws.inv_perm.as<unsigned>(M);
     ull* dbg = debug_buffer();
     const unsigned wblocks = (unsigned)((ntiles + 7) / 8);
     for (int c = 0; c < nch; ++c) {
@@ -1060,7 +1016,6 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
           default: k_tile_agg_w<16><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
         }
       }
-      if (getenv("IQCC_DEBUG")) debug_check("tile_agg");
       {
         KernelScope ks("carry");
         k_group_agg<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
@@ -1072,10 +1027,9 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
         count_launch("carry");
         count_launch("carry");
       }
-      if (getenv("IQCC_DEBUG")) debug_check("carry");
       {
         KernelScope ks("rank");
-#define IQCC_RANK(NT_, F_) k_rank_w<NT_, F_><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_pfx, fwd_carry, bwd_carry, rdelta, c > 0, inv_perm, a_total, dbg)
+#define IQCC_RANK(NT_, F_) k_rank_w<NT_, F_><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_pfx, fwd_carry, bwd_carry, rdelta, c > 0, pl.inv_perm, a_total, dbg)
         if (last) {
           switch (nthr4) {
             case 4: IQCC_RANK(4, true); break;
@@ -1098,30 +1052,114 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
     long long a_host = 0;
     IQCC_CUDA(cudaMemcpyAsync(&a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     IQCC_CUDA(cudaStreamSynchronize(st));
-    A = (size_t)a_host;
-    if (getenv("IQCC_DEBUG") && A > 0) {
+    pl.A = (size_t)a_host;
+    if (getenv("IQCC_DEBUG") && pl.A > 0) {
       unsigned* seen = ws.misc2.as<unsigned>(M);
       IQCC_CUDA(cudaMemsetAsync(seen, 0, M * sizeof(unsigned), st));
-      k_check_perm<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(inv_perm, A, M, fmask, seen, dbg);
+      k_check_perm<<<(unsigned)((pl.A + 255) / 256), 256, 0, st>>>(pl.inv_perm, pl.A, M, fmask, seen, dbg);
       debug_check("perm check");
     }
   }
-  out.n_anticommuting = A;
+  g_plan = pl;
+}
 
+template <int B, int NT, int IPT>
+void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys, const double* q_vals,
+                    double cs, double sn, double drop, bool want_hist, double eps) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const PlanState& pl = g_plan;
+  constexpr int TILEM = NT * IPT;
+  const size_t M = s.M;
+  const size_t total = M + nQ;
+  const size_t ntm = std::max<size_t>(1, (total + TILEM - 1) / TILEM);
+  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1));
+  ull* pb = pa + (ntm + 1);
+  ull* po = pb + (ntm + 1);
+  {
+    KernelScope ks("partition");
+    k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
+        s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
+        pl.ptotal);
+  }
+  ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
+  double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
+  ull* ctr = ws.counters.as<ull>(8);
+  unsigned* hist = ws.hist.as<unsigned>(kHistBins);
+  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
+  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
+  using Cfg = MergeCfg<B, NT, IPT>;
+  MergeArgs g;
+  g.keys = s.keys();
+  g.coef = s.coef();
+  g.filt = s.filt;
+  g.inv_perm = pl.inv_perm;
+  g.q_keys = q_keys;
+  g.q_vals = q_vals;
+  g.part_a = pa;
+  g.part_b = pb;
+  g.part_o = po;
+  g.ntiles = ntm;
+  g.cs = cs;
+  g.sn = sn;
+  g.drop = drop;
+  g.eps = eps;
+  g.out_keys = out_keys;
+  g.out_coef = out_coef;
+  g.counters = ctr;
+  g.hist = hist;
+  g.want_hist = want_hist ? 1 : 0;
+  g.dbg = debug_buffer();
+  static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
+  if (persistent) {
+    static int ctas_per_sm = 0, n_sm = 0;
+    if (!ctas_per_sm) {
+      IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)Cfg::bytes(true, 2)));
+      IQCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_merge<B, NT, IPT>, NT,
+                                                              Cfg::bytes(true, 2)));
+      IQCC_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0));
+      ctas_per_sm = std::max(ctas_per_sm, 1);
+    }
+    KernelScope ks("merge");
+    const unsigned grid = (unsigned)std::min<size_t>(ntm, (size_t)n_sm * ctas_per_sm);
+    k_merge<B, NT, IPT><<<grid, NT, Cfg::bytes(want_hist, 2), st>>>(g, P);
+  } else {
+    static bool attr1 = false;
+    if (!attr1) {
+      IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)Cfg::bytes(true, 1)));
+      attr1 = true;
+    }
+    KernelScope ks("merge");
+    k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
+  }
+  IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
+  if (getenv("IQCC_DEBUG")) debug_check("merge");
+}
+
+template <int B>
+DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys,
+                        const double* q_vals, double cs, double sn, double drop, bool want_hist,
+                        double eps) {
   static int shape = -1;
   if (shape < 0) {
     const char* env = getenv("IQCC_MERGE_CFG");
     shape = env ? atoi(env) : 3;
-    if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 1;
+    if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 3;
   }
+#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps)
   switch (shape) {
-    case 0: launch_merge<B, 256, 4>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
-    case 1: launch_merge<B, 128, 4>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
-    case 2: launch_merge<B, 128, 8>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
-    case 3: launch_merge<B, 256, 2>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
-    case 4: launch_merge<B, 512, 2>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
-    default: launch_merge<B, 64, 8>(s, inv_perm, M, A, P, cs, sn, drop, want_hist, eps, pmask, ppre, W, ptotal); break;
+    case 0: IQCC_MERGE(256, 4); break;
+    case 1: IQCC_MERGE(128, 4); break;
+    case 2: IQCC_MERGE(128, 8); break;
+    case 3: IQCC_MERGE(256, 2); break;
+    case 4: IQCC_MERGE(512, 2); break;
+    default: IQCC_MERGE(64, 8); break;
   }
+#undef IQCC_MERGE
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
   ull* ctr = ws.counters.as<ull>(8);
   ull hc[4] = {0, 0, 0, 0};
   IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 4 * sizeof(ull), cudaMemcpyDeviceToHost, st));
@@ -1130,15 +1168,72 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
   std::swap(s.cbuf, ws.out_coef);
   // algorithmic bytes of the step: (M_in + M_out) * (16B + 8)
   const size_t logical_in = s.logical;
-  s.M = hc[3];              // physical slots (live + dead)
+  s.M = hc[3];                // physical slots (live + dead)
   s.filt = Filter{};
   s.logical = hc[3] - hc[2];  // minus dead slots
   add_alg_bytes("merge", (double)(logical_in + s.logical) * (16.0 * B + 8.0));
+  DressOutcome out;
   out.count_eps = hc[1];
+  out.n_anticommuting = g_plan.A;
   return out;
 }
 
+template <int B>
+DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
+                        bool want_hist, double eps) {
+  const Key<B> P = make_key<B>(gen_row);
+  plan_impl<B>(s, P, sn != 0.0);
+  return merge_impl<B>(s, P, g_plan.A, nullptr, nullptr, cs, sn, drop, want_hist, eps);
+}
+
+// Sorted products as a contiguous buffer (keys ^ P, +-fl(c*sin)) for a peer.
+template <int B>
+__global__ void k_materialize(const ull* __restrict__ keys, const double* __restrict__ coef,
+                              const unsigned* __restrict__ inv_perm, size_t A, Key<B> P, double sn,
+                              ull* __restrict__ okeys, double* __restrict__ ovals) {
+  const size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (r >= A) return;
+  const unsigned src = inv_perm[r];
+  const Key<B> k = load_key<B>(keys, src);
+  const double pr = __dmul_rn(coef[src], sn);
+  store_key<B>(okeys, r, key_xor<B>(k, P));
+  ovals[r] = product_phase<B>(k, P) == 1 ? pr : -pr;
+}
+
 }  // namespace
+
+size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products) {
+  switch (s.B) {
+    case 1: plan_impl<1>(s, make_key<1>(gen_row), products); break;
+    case 2: plan_impl<2>(s, make_key<2>(gen_row), products); break;
+    default: plan_impl<4>(s, make_key<4>(gen_row), products); break;
+  }
+  return g_plan.A;
+}
+
+void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
+                          double* ovals) {
+  const size_t A = g_plan.A;
+  if (A == 0) return;
+  cudaStream_t st = stream();
+  KernelScope ks("materialize");
+  const unsigned grid = (unsigned)((A + 255) / 256);
+  switch (s.B) {
+    case 1: k_materialize<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<1>(gen_row), sn, okeys, ovals); break;
+    case 2: k_materialize<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<2>(gen_row), sn, okeys, ovals); break;
+    default: k_materialize<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<4>(gen_row), sn, okeys, ovals); break;
+  }
+}
+
+DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
+                            double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
+                            const double* q_vals) {
+  switch (s.B) {
+    case 1: return merge_impl<1>(s, make_key<1>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps);
+    case 2: return merge_impl<2>(s, make_key<2>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps);
+    default: return merge_impl<4>(s, make_key<4>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps);
+  }
+}
 
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
                         bool want_hist, double eps) {

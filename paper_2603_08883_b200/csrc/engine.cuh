@@ -128,7 +128,7 @@ struct Filter {
   int has_v = 0;
   double eps = 0.0;
   double v = 0.0;
-  ull cut = 0;
+  long long cut = 0;  // last kept index among |c| == v (-1: none)
 };
 
 /// Dead slot: a term removed by a dressing step (cancelled partner or below
@@ -148,7 +148,7 @@ __device__ __forceinline__ bool filter_keep(const Filter& f, size_t i, double c,
   double a = fabs(c);
   if (!(a >= f.eps)) return false;
   if (!f.has_v) return true;
-  return a > f.v || (a == f.v && (ull)i <= f.cut);
+  return a > f.v || (a == f.v && (long long)i <= f.cut);
 }
 
 /// Coarse |c| histogram bin for compress(): the IEEE exponent of |c|
@@ -388,10 +388,31 @@ struct DressOutcome {
 /// histogram of emitted terms for a following compress(eps).
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cos_tau, double sin_tau,
                         double drop_thr, bool want_hist, double eps);
+/// Phases of a step for the partitioned path: plan (classify, present
+/// prefix, product order; returns the product count A), materialize the
+/// sorted products (keys ^ P, values) into a buffer, and merge the store's
+/// survivors with products given as a buffer (q_keys != nullptr) or the
+/// planned local products.
+size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products);
+void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
+                          double* ovals);
+DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
+                            double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
+                            const double* q_vals);
 /// Selects the compress filter on a store without a filter.  If hist_ready,
 /// the histogram/count_eps of the last dress_step are used.
+/// Cross-rank hooks for compress_partitioned (iqcc/partition.hpp:325-396);
+/// nullptr = single device.
+struct Reducer {
+  virtual ~Reducer() = default;
+  virtual void sum(ull* vals, size_t n) = 0;  // in place, host buffers
+  /// all ranks' tied keys (device rows, 2B words each), concatenated in rank
+  /// order; *mine_offset receives where this rank's keys start.
+  virtual std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t words_per_key,
+                                       size_t* mine_offset) = 0;
+};
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
-                              size_t count_eps, bool want_stats);
+                              size_t count_eps, bool want_stats, Reducer* red = nullptr);
 void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* na);
 
 double expect_store(DeviceStore& s, const double* factors);

@@ -1,0 +1,234 @@
+// multi.cu — bit-wise partitioning across GPUs (one process per GPU, NCCL).
+//
+// parallel_dress (iqcc/partition.hpp:398-452) with one partition per rank
+// (2^m == world, owner a permutation): a term's partition key is the gather
+// of its bits at the partition positions (partition.hpp:40-42); survivors
+// never move and every product of partition p has key p ^ mask, mask = the
+// entangler's key.  So:
+//   mask == 0  -> purely local dressing step, no communication;
+//   mask != 0  -> each rank orders its products locally (same trie-rank
+//                 pipeline), materializes them, swaps them with the rank
+//                 owning p ^ mask (pairwise ncclSend/ncclRecv on the engine
+//                 stream), and merges its survivors with the received,
+//                 already sorted products.
+// compress_partitioned (partition.hpp:325-396) runs with allreduced
+// histograms and an allgather of the (few) tied words for the canonical
+// tie-break.  Energies: per-rank partial sums allgathered and added in rank
+// order (reduce_scalar, partition.hpp:233-237).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "multi.cuh"
+
+namespace iqcc_b200 {
+
+namespace {
+
+struct Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  ull* dev = nullptr;  // small device scratch for collectives
+};
+Comm g_comm;
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw std::runtime_error(std::string("NCCL error ") + ncclGetErrorString(r) + " at " + what);
+}
+#define IQCC_NCCL(x) nccl_check((x), #x)
+
+Comm& comm() {
+  if (!g_comm.comm) throw std::runtime_error("iqcc_gpu_comm_init has not been called");
+  return g_comm;
+}
+
+ull* scratch(size_t n) {
+  Workspace& ws = workspace();
+  return ws.misc3.as<ull>(n);
+}
+
+struct NcclReducer : Reducer {
+  void sum(ull* vals, size_t n) override {
+    Comm& c = comm();
+    cudaStream_t st = stream();
+    ull* d = workspace().partials.as<ull>(n);
+    IQCC_CUDA(cudaMemcpyAsync(d, vals, n * sizeof(ull), cudaMemcpyHostToDevice, st));
+    IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, c.comm, st));
+    IQCC_CUDA(cudaMemcpyAsync(vals, d, n * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaStreamSynchronize(st));
+  }
+  std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t W, size_t* mine_off) override {
+    Comm& c = comm();
+    cudaStream_t st = stream();
+    std::vector<ull> counts(c.world, 0);
+    counts[c.rank] = mine.size() / W;
+    sum(counts.data(), counts.size());
+    size_t mx = 0, off = 0;
+    for (int r = 0; r < c.world; ++r) {
+      mx = std::max<size_t>(mx, counts[r]);
+      if (r < c.rank) off += counts[r];
+    }
+    *mine_off = off;
+    std::vector<ull> all;
+    if (mx == 0) return all;
+    ull* d = workspace().rbuf_keys.as<ull>((size_t)mx * W * (c.world + 1));
+    ull* dm = d + (size_t)mx * W * c.world;
+    IQCC_CUDA(cudaMemsetAsync(dm, 0, mx * W * sizeof(ull), st));
+    if (!mine.empty())
+      IQCC_CUDA(cudaMemcpyAsync(dm, mine.data(), mine.size() * sizeof(ull), cudaMemcpyHostToDevice, st));
+    IQCC_NCCL(ncclAllGather(dm, d, mx * W, ncclUint64, c.comm, st));
+    std::vector<ull> padded((size_t)mx * W * c.world);
+    IQCC_CUDA(cudaMemcpyAsync(padded.data(), d, padded.size() * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < c.world; ++r)
+      all.insert(all.end(), padded.begin() + (size_t)r * mx * W,
+                 padded.begin() + (size_t)r * mx * W + counts[r] * W);
+    return all;
+  }
+};
+
+size_t key_of_row(const uint64_t* row, uint32_t B, size_t n, size_t m, const size_t* bits) {
+  size_t key = 0;
+  for (size_t b = 0; b < m; ++b) {
+    const size_t p = bits[b];
+    const size_t q = p < n ? p : p - n;
+    const uint64_t w = row[(p < n ? 0 : B) + q / 64];
+    key |= (size_t)((w >> (q % 64)) & 1u) << b;
+  }
+  return key;
+}
+
+}  // namespace
+
+void multi_unique_id(void* out128) {
+  ncclUniqueId id;
+  IQCC_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+}
+
+void multi_init(const void* uid128, int rank, int world) {
+  if (g_comm.comm) throw std::invalid_argument("communicator already initialised");
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("comm_init: bad rank/world");
+  ncclUniqueId id;
+  std::memcpy(&id, uid128, 128);
+  IQCC_NCCL(ncclCommInitRank(&g_comm.comm, world, id, rank));
+  g_comm.rank = rank;
+  g_comm.world = world;
+}
+
+void multi_shutdown() {
+  if (g_comm.comm) {
+    ncclCommDestroy(g_comm.comm);
+    g_comm = Comm{};
+  }
+}
+
+void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner,
+                         const uint64_t* gen_row, double cs, double sn, double eps,
+                         size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out) {
+  Comm& c = comm();
+  if (((size_t)1 << m) != (size_t)c.world)
+    throw std::invalid_argument("parallel_dress: one partition per rank (2^m == world) required");
+  size_t mine = SIZE_MAX;
+  for (size_t p = 0; p < ((size_t)1 << m); ++p) {
+    if (owner[p] >= (size_t)c.world) throw std::invalid_argument("PartitionMap: owner out of range");
+    if (owner[p] == (size_t)c.rank) mine = p;
+  }
+  if (mine == SIZE_MAX) throw std::invalid_argument("parallel_dress: rank owns no partition");
+  const uint32_t Bref = s.n_qubits == 0 ? 1 : (s.n_qubits + 63) / 64;
+  std::vector<uint64_t> ref_row(2 * Bref);
+  for (uint32_t w = 0; w < Bref; ++w) {
+    ref_row[w] = gen_row[w];
+    ref_row[Bref + w] = gen_row[s.B + w];
+  }
+  const size_t mask = key_of_row(ref_row.data(), Bref, s.n_qubits, m, bits);
+  const bool want_hist = eps > 0.0 || max_terms != SIZE_MAX;
+  DressOutcome o;
+  iqcc_exchange_stats x{mask, 0, 0, 0, 0};
+  if (mask == 0 || sn == 0.0) {
+    o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps);
+  } else {
+    cudaStream_t st = stream();
+    Workspace& ws = workspace();
+    const size_t A = plan_products(s, gen_row, true);
+    const size_t W = 2 * s.B;
+    ull* sk = ws.xbuf_keys.as<ull>(std::max<size_t>(A, 1) * W);
+    double* sv = ws.xbuf_coef.as<double>(std::max<size_t>(A, 1));
+    materialize_products(s, gen_row, sn, sk, sv);
+    const int peer = (int)owner[mine ^ mask];
+    ull* cnt = scratch(4);
+    IQCC_CUDA(cudaMemcpyAsync(cnt, &A, sizeof(ull), cudaMemcpyHostToDevice, st));
+    {
+      KernelScope ks("exchange");
+      IQCC_NCCL(ncclGroupStart());
+      IQCC_NCCL(ncclSend(cnt, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclRecv(cnt + 1, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclGroupEnd());
+    }
+    ull nrecv = 0;
+    IQCC_CUDA(cudaMemcpyAsync(&nrecv, cnt + 1, sizeof(ull), cudaMemcpyDeviceToHost, st));
+    IQCC_CUDA(cudaStreamSynchronize(st));
+    ull* rk = ws.rbuf_keys.as<ull>(std::max<size_t>(nrecv, 1) * W);
+    double* rv = ws.rbuf_coef.as<double>(std::max<size_t>(nrecv, 1));
+    {
+      KernelScope ks("exchange");
+      IQCC_NCCL(ncclGroupStart());
+      if (A) {
+        IQCC_NCCL(ncclSend(sk, A * W, ncclUint64, peer, c.comm, st));
+        IQCC_NCCL(ncclSend(sv, A, ncclFloat64, peer, c.comm, st));
+      }
+      if (nrecv) {
+        IQCC_NCCL(ncclRecv(rk, nrecv * W, ncclUint64, peer, c.comm, st));
+        IQCC_NCCL(ncclRecv(rv, nrecv, ncclFloat64, peer, c.comm, st));
+      }
+      IQCC_NCCL(ncclGroupEnd());
+    }
+    x.sent_terms = A;
+    x.recv_terms = nrecv;
+    x.bytes_wire = A * (W * 8 + 8);
+    x.bytes_reference = A * (16 + Bref * 16);  // MessageLog formula, partition.hpp:420-422
+    o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv);
+  }
+  if (xs) *xs = x;
+  ull tot[1] = {(ull)s.logical};
+  NcclReducer red;
+  red.sum(tot, 1);
+  if (eps > 0.0 || tot[0] > max_terms) {
+    CompressResult r = compress_store(s, eps, max_terms, want_hist, o.count_eps, cs_out != nullptr, &red);
+    if (cs_out) {
+      cs_out->dropped_terms += r.dropped_terms;
+      cs_out->dropped_weight += r.dropped_weight;
+    }
+  }
+}
+
+double parallel_expect_store(DeviceStore& s, const double* factors) {
+  Comm& c = comm();
+  const double local = expect_store(s, factors);
+  cudaStream_t st = stream();
+  double* d = workspace().partials.as<double>(c.world + 1);
+  IQCC_CUDA(cudaMemcpyAsync(d + c.world, &local, sizeof(double), cudaMemcpyHostToDevice, st));
+  IQCC_NCCL(ncclAllGather(d + c.world, d, 1, ncclFloat64, c.comm, st));
+  std::vector<double> parts(c.world);
+  IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, c.world * sizeof(double), cudaMemcpyDeviceToHost, st));
+  IQCC_CUDA(cudaStreamSynchronize(st));
+  double e = 0.0;
+  for (double v : parts) e += v;  // worker order (reduce_scalar)
+  return e;
+}
+
+size_t parallel_size(DeviceStore& s) {
+  ull v[1] = {(ull)s.logical};
+  NcclReducer red;
+  red.sum(v, 1);
+  return (size_t)v[0];
+}
+
+}  // namespace iqcc_b200

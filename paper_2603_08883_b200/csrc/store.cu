@@ -706,7 +706,7 @@ __global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __r
 }
 
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
-                              size_t count_eps, bool want_stats) {
+                              size_t count_eps, bool want_stats, Reducer* red) {
   if (eps < 0) throw std::invalid_argument("compress: epsilon < 0");
   if (max_terms < 1) throw std::invalid_argument("compress: max_terms < 1");
   Workspace& ws = workspace();
@@ -736,37 +736,44 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
     IQCC_CUDA(cudaStreamSynchronize(st));
     count_eps = (size_t)h;
   }
+  // global view (compress_partitioned: per-shard eps cut, one global budget)
+  ull glob[2] = {(ull)count_eps, (ull)(s.has_identity ? 1 : 0)};
+  if (red) red->sum(glob, 2);
   Filter f;
   f.active = 1;
   f.eps = eps;
-  size_t logical = count_eps;
-  if (count_eps > max_terms) {
-    const size_t budget = max_terms - (s.has_identity ? 1 : 0);
+  size_t logical = count_eps;  // local kept
+  if (glob[0] > max_terms) {
+    const size_t budget = max_terms - (glob[1] ? 1 : 0);  // identity kept first
     f.has_v = 1;
     if (budget == 0) {
       f.eps = HUGE_VAL;  // identity only (|c| >= inf never holds for finite c)
       f.v = HUGE_VAL;
-      f.cut = 0;
+      f.cut = -1;
+      logical = s.has_identity ? 1 : 0;
     } else {
       std::vector<unsigned> hh(kHistBins);
       IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, kHistBins * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
-      size_t cum = 0, r = 0;
+      std::vector<ull> hg(hh.begin(), hh.end());
+      if (red) red->sum(hg.data(), hg.size());
+      size_t cum = 0, r = 0, local_above = 0;
       int bin = -1;
       for (int b = kHistBins - 1; b >= 0; --b) {
-        if (cum + hh[b] >= budget) {
+        if (cum + hg[b] >= budget) {
           bin = b;
           r = budget - cum;
           break;
         }
-        cum += hh[b];
+        cum += hg[b];
+        local_above += hh[b];
       }
       if (bin < 0) throw std::runtime_error("compress: histogram inconsistent");
-      const size_t nc = hh[bin];
-      ull* cv = ws.cand_v.as<ull>(nc);
-      ull* ci = ws.cand_i.as<ull>(nc);
+      const size_t nc = hh[bin];  // local candidates
+      ull* cv = ws.cand_v.as<ull>(std::max<size_t>(nc, 1));
+      ull* ci = ws.cand_i.as<ull>(std::max<size_t>(nc, 1));
       IQCC_CUDA(cudaMemsetAsync(ctr + 2, 0, 2 * sizeof(ull), st));
-      {
+      if (nc) {
         KernelScope ks("select_gather");
         const unsigned grid = (unsigned)std::min<size_t>(148 * 16, std::max<size_t>(1, (s.M + 2047) / 2048));
         switch (s.B) {
@@ -788,27 +795,31 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       }
       unsigned* dh = ws.misc2.as<unsigned>(1 << kDigitBits);
       std::vector<unsigned> hd(1 << kDigitBits);
+      std::vector<ull> hdg(1 << kDigitBits);
       while (top >= 0) {
         const int width = std::min(kDigitBits, top + 1);
         const int shift = top + 1 - width;
         const unsigned dmask = (1u << width) - 1u;
         IQCC_CUDA(cudaMemsetAsync(dh, 0, (dmask + 1) * sizeof(unsigned), st));
-        {
+        if (nc) {
           KernelScope ks("select_digits");
           const unsigned grid = (unsigned)std::min<size_t>(592, std::max<size_t>(1, (nc + 1023) / 1024));
           k_cand_hist<<<grid, 256, 0, st>>>(cv, nc, known_mask, known_val, shift, dmask, dh);
         }
         IQCC_CUDA(cudaMemcpyAsync(hd.data(), dh, (dmask + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         IQCC_CUDA(cudaStreamSynchronize(st));
+        for (unsigned x = 0; x <= dmask; ++x) hdg[x] = hd[x];
+        if (red) red->sum(hdg.data(), dmask + 1);
         size_t c2 = 0;
         long d = -1;
         for (long x = dmask; x >= 0; --x) {
-          if (c2 + hd[x] >= r) {
+          if (c2 + hdg[x] >= r) {
             d = x;
             r -= c2;
             break;
           }
-          c2 += hd[x];
+          c2 += hdg[x];
+          local_above += hd[x];
         }
         if (d < 0) throw std::runtime_error("compress: digit select failed");
         known_mask |= (ull)dmask << shift;
@@ -816,9 +827,9 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         top = shift - 1;
       }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
-      const ull vbits = known_val;  // exact threshold value; r ties at it are kept
-      ull* ties = ws.misc3.as<ull>(nc);
-      {
+      const ull vbits = known_val;  // exact threshold value; r ties at it are kept (globally)
+      ull* ties = ws.misc3.as<ull>(std::max<size_t>(nc, 1));
+      if (nc) {
         KernelScope ks("select_ties");
         k_cand_ties<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(cv, ci, nc, vbits, ties, ctr);
       }
@@ -826,16 +837,41 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       IQCC_CUDA(cudaMemcpyAsync(&ntie, ctr + 3, sizeof(ull), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
       std::vector<ull> th(ntie);
-      IQCC_CUDA(cudaMemcpyAsync(th.data(), ties, ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
+      if (ntie)
+        IQCC_CUDA(cudaMemcpyAsync(th.data(), ties, ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
-      std::sort(th.begin(), th.end());
-      if (r < 1 || r > th.size()) throw std::runtime_error("compress: tie resolution failed");
+      std::sort(th.begin(), th.end());  // local index order = canonical order
+      size_t keep_ties = r;
+      if (red) {
+        // canonical tie-break across shards (partition.hpp:350-361): the
+        // globally first r tied words are kept
+        const size_t W = 2 * s.B;
+        std::vector<ull> mine(th.size() * W);
+        for (size_t i = 0; i < th.size(); ++i)
+          IQCC_CUDA(cudaMemcpyAsync(mine.data() + i * W, s.keys() + th[i] * W, W * sizeof(ull),
+                                    cudaMemcpyDeviceToHost, st));
+        IQCC_CUDA(cudaStreamSynchronize(st));
+        size_t off = 0;
+        std::vector<ull> all = red->gather_keys(mine, W, &off);
+        const size_t nall = all.size() / W;
+        std::vector<size_t> ord(nall);
+        for (size_t i = 0; i < nall; ++i) ord[i] = i;
+        std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+          return std::lexicographical_compare(all.begin() + a * W, all.begin() + (a + 1) * W,
+                                              all.begin() + b * W, all.begin() + (b + 1) * W);
+        });
+        keep_ties = 0;
+        for (size_t k = 0; k < std::min(r, nall); ++k)
+          if (ord[k] >= off && ord[k] < off + th.size()) ++keep_ties;
+      } else if (r < 1 || r > th.size()) {
+        throw std::runtime_error("compress: tie resolution failed");
+      }
       double v;
       std::memcpy(&v, &vbits, 8);
       f.v = v;
-      f.cut = th[r - 1];
+      f.cut = keep_ties ? (long long)th[keep_ties - 1] : -1;
+      logical = local_above + keep_ties + (s.has_identity ? 1 : 0);
     }
-    logical = max_terms;
   }
   if (eps == 0.0 && !f.has_v) f.active = 0;  // nothing to drop
   s.filt = f;

@@ -122,8 +122,18 @@ def check(status: int) -> None:
 _initialised_device = None
 
 
-def init(device: int = 0) -> None:
+def init(device: int | None = None) -> None:
+    """Bind the engine to a device (once per process).  With no argument an
+    already initialised engine is kept; otherwise torch's current device."""
     global _initialised_device
+    if device is None:
+        if _initialised_device is not None:
+            return
+        try:
+            import torch
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        except Exception:
+            device = 0
     if _initialised_device == device:
         return
     check(lib.iqcc_gpu_init(device))

@@ -1,0 +1,86 @@
+"""torchrun worker for the multi-GPU parity test (tests/test_gpu_multi.py).
+
+Every rank builds the same G_mol, keeps its bit-wise partition shard, and
+runs parallel_dress steps (some entanglers flip the first partition bit, so
+products are exchanged over NCCL).  Rank 0 gathers the shards and compares
+their union with the CPU checker's serial pipeline, bit for bit, plus the
+partitioned energy."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def main():
+    n, N, steps = int(sys.argv[1]), int(float(sys.argv[2])), int(sys.argv[3])
+    eps, cap = float(sys.argv[4]), int(float(sys.argv[5]))
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    from paper_2603_08883_b200 import iqcc, native
+    native.init(local)
+    d = iqcc.DeviceSum.generate_mol(n, N, 2)
+    part = iqcc.Partition.setup(d, world, rank)
+    B = iqcc.blocks_for(n)
+    rs = np.random.default_rng(11)
+    gens, taus, exch = [], [], 0
+    for k in range(steps):
+        w = int(rs.integers(2, 5))
+        qs = [int(q) for q in rs.choice(n, w, replace=False)]
+        ys = [int(y) for y in rs.integers(0, 2, w)]
+        if k % 2 == 0:  # flip the first partition bit
+            if part.flip_qubit not in qs:
+                qs[0] = part.flip_qubit
+            i = qs.index(part.flip_qubit)
+            if part.flip_plane == "z":
+                ys[i] = 1
+            if sum(ys) % 2 == 0:
+                ys[(i + 1) % w] ^= 1
+        elif sum(ys) % 2 == 0:
+            ys[-1] ^= 1
+        p = iqcc.PauliWord(n)
+        for q, y in zip(qs, ys):
+            p.row[q // 64] |= np.uint64(1 << (q % 64))
+            if y:
+                p.row[B + q // 64] |= np.uint64(1 << (q % 64))
+        tau = float(rs.uniform(-0.2, 0.2))
+        xs = part.dress(d, p, tau, eps, cap)
+        exch += xs.sent_terms
+        gens.append(p.row.copy())
+        taus.append(tau)
+    shard = d.download()
+    th = np.where(np.arange(n) < n // 3, np.pi, 0.0)
+    ph = np.zeros(n)
+    e_par = part.expect(d, iqcc.QmfState(th, ph))
+    objs = [None] * world
+    dist.all_gather_object(objs, (shard.rows, shard.coeffs, exch))
+    if rank == 0:
+        from oracle.oracle import Oracle
+        port = Oracle("port")
+        h = port.gen_mol(n, N, 2)
+        h, _ = port.dress_sequence(h, np.stack(gens), taus, eps, cap)
+        r, c = h.export()
+        rows = np.concatenate([o[0] for o in objs])
+        coeffs = np.concatenate([o[1] for o in objs])
+        # gather (partition.hpp:224-230): canonical merge of disjoint shards
+        rows, coeffs = port.from_terms(n, rows, coeffs, drop=0.0, check=False).export()
+        ok = rows.shape == r.shape and np.array_equal(rows, r) and np.array_equal(coeffs, c)
+        e_ref = port.expect_sum(th, ph, h)
+        e_ok = abs(e_par - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
+        print(f"MULTI world={world} terms={len(r)} exchanged={sum(o[2] for o in objs)} "
+              f"bitexact={ok} energy_ok={e_ok}", flush=True)
+        if not (ok and e_ok):
+            sys.exit(1)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

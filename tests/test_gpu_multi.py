@@ -1,0 +1,30 @@
+"""Multi-GPU parity: bit-wise partitioned dressing with the
+NCCL pairwise product exchange equals the serial reference pipeline bit for
+bit (tests/test_partition.cpp:180-208 at the process level).  Needs >= 2
+visible GPUs; launched with torchrun."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def n_gpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("args", [("124", "2e5", "6", "1e-10", "2e5"), ("64", "1e5", "5", "0", "1e18")])
+def test_partitioned_dressing_matches_serial(world, args):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "multi_worker.py"),
+           *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "bitexact=True" in r.stdout and "energy_ok=True" in r.stdout
