@@ -340,7 +340,7 @@ struct DevBuf {
 
 struct Workspace {
   DevBuf lcp, mbits, fmask, tile_cnt, tile_pfx, fwd_agg, bwd_agg, fwd_carry, bwd_carry;
-  DevBuf inv_perm, rdelta, part_a, part_b, tile_status, counters, hist, cand_v, cand_i;
+  DevBuf inv_perm, rdelta, part_a, part_b, tile_status, counters, hist, cand_v, cand_i, cand_v2, cand_i2;
   DevBuf levels, stage_rows, stage_coef, partials, grad_part, tables, misc, misc2, misc3;
   DevBuf xbuf_keys, xbuf_coef, rbuf_keys, rbuf_coef;
   DevBuf out_keys, out_coef;  // double buffer swapped with the store after a step
@@ -405,7 +405,8 @@ DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, 
 /// nullptr = single device.
 struct Reducer {
   virtual ~Reducer() = default;
-  virtual void sum(ull* vals, size_t n) = 0;  // in place, host buffers
+  virtual void sum(ull* vals, size_t n) = 0;         // in place, host buffers
+  virtual void sum_device(ull* dvals, size_t n) = 0;  // in place on the stream
   /// all ranks' tied keys (device rows, 2B words each), concatenated in rank
   /// order; *mine_offset receives where this rank's keys start.
   virtual std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t words_per_key,

@@ -63,6 +63,9 @@ struct NcclReducer : Reducer {
     IQCC_CUDA(cudaMemcpyAsync(vals, d, n * sizeof(ull), cudaMemcpyDeviceToHost, st));
     IQCC_CUDA(cudaStreamSynchronize(st));
   }
+  void sum_device(ull* d, size_t n) override {
+    IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, comm().comm, stream()));
+  }
   std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t W, size_t* mine_off) override {
     Comm& c = comm();
     cudaStream_t st = stream();

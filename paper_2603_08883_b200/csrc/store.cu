@@ -608,84 +608,276 @@ __global__ void k_hist_eps(const ull* __restrict__ keys, const double* __restric
     if (sh[b]) atomicAdd(hist + b, sh[b]);
 }
 
+// Device-resident radix select.  SelState lives in device memory; pick
+// kernels (one warp) consume the (optionally allreduced) histograms, so the
+// whole select runs on the stream with a single host read at the end.
+struct SelState {
+  ull known_mask, known_val;  // magnitude bits fixed so far
+  ull r;                      // rank still to take inside the current prefix
+  ull local_above;            // local terms strictly above the prefix
+  ull ntie;                   // local candidates equal to the final value
+  int bin;
+  int fail;
+  int top;                    // highest magnitude bit not fixed yet (-1: done)
+};
+
+__device__ __forceinline__ void next_digit(const SelState* st, int& shift, unsigned& dmask) {
+  const int width = min(12, st->top + 1);
+  shift = st->top + 1 - width;
+  dmask = (1u << width) - 1u;
+}
+
+// Parallel pick over a histogram, largest values first: find the bin x
+// (scanning from the top) where the running global count reaches r.
+// 256 threads, each owning a contiguous run of bins from the top.
+__device__ __forceinline__ bool block_pick(const ull* __restrict__ hg, const unsigned* __restrict__ hl,
+                                           int nbins, ull r, int* x_out, ull* before_g,
+                                           ull* before_l) {
+  __shared__ ull sg[256], sl[256];
+  __shared__ int s_x;
+  __shared__ ull s_bg, s_bl;
+  const int per = (nbins + 255) / 256;
+  const int hi = nbins - 1 - threadIdx.x * per;  // this thread's bins: hi, hi-1, ...
+  ull tg = 0, tl = 0;
+  for (int k = 0; k < per; ++k) {
+    const int x = hi - k;
+    if (x >= 0) {
+      tg += hg[x];
+      tl += hl[x];
+    }
+  }
+  sg[threadIdx.x] = tg;
+  sl[threadIdx.x] = tl;
+  if (threadIdx.x == 0) s_x = -1;
+  __syncthreads();
+  // exclusive prefix over threads (thread 0 holds the top bins)
+  for (int o = 1; o < 256; o <<= 1) {
+    ull vg = threadIdx.x >= o ? sg[threadIdx.x - o] : 0, vl = threadIdx.x >= o ? sl[threadIdx.x - o] : 0;
+    __syncthreads();
+    sg[threadIdx.x] += vg;
+    sl[threadIdx.x] += vl;
+    __syncthreads();
+  }
+  const ull eg = sg[threadIdx.x] - tg, el = sl[threadIdx.x] - tl;
+  if (eg < r && eg + tg >= r) {  // the crossing lies in this thread's run
+    ull cg = eg, cl = el;
+    for (int k = 0; k < per; ++k) {
+      const int x = hi - k;
+      if (x < 0) break;
+      if (cg + hg[x] >= r) {
+        s_x = x;
+        s_bg = cg;
+        s_bl = cl;
+        break;
+      }
+      cg += hg[x];
+      cl += hl[x];
+    }
+  }
+  __syncthreads();
+  *x_out = s_x;
+  *before_g = s_bg;
+  *before_l = s_bl;
+  return s_x >= 0;
+}
+
+// hist_g[256] (global counts, u64) / hist_l[256] (local, u32): pick the
+// coarse bin holding the budget-th largest |c|.
+__global__ void __launch_bounds__(256) k_pick_bin(const ull* __restrict__ hist_g,
+                                                  const unsigned* __restrict__ hist_l, ull budget,
+                                                  SelState* __restrict__ st) {
+  int b;
+  ull bg, bl;
+  const bool ok = block_pick(hist_g, hist_l, kHistBins, budget, &b, &bg, &bl);
+  if (threadIdx.x != 0) return;
+  st->fail = ok ? 0 : 1;
+  if (!ok) return;
+  st->bin = b;
+  st->r = budget - bg;
+  st->local_above = bl;
+  st->known_mask = 1ull << 63;
+  st->known_val = 0;
+  st->top = 62;
+  if (b > 0 && b < kHistBins - 1) {  // interior bin: the exponent is fixed
+    st->known_mask |= 0x7FFull << 52;
+    st->known_val = (ull)(b + (1023 - 192)) << 52;
+    st->top = 51;
+  }
+  st->ntie = 0;
+}
+
+__global__ void __launch_bounds__(256) k_pick_digit(const ull* __restrict__ dh_g,
+                                                    const unsigned* __restrict__ dh_l,
+                                                    SelState* __restrict__ st) {
+  if (st->fail || st->top < 0) return;  // uniform across the block
+  int shift;
+  unsigned dmask;
+  next_digit(st, shift, dmask);
+  int x;
+  ull bg, bl;
+  const bool ok = block_pick(dh_g, dh_l, (int)dmask + 1, st->r, &x, &bg, &bl);
+  if (threadIdx.x != 0) return;
+  if (!ok) {
+    st->fail = 2;
+    return;
+  }
+  st->r -= bg;
+  st->local_above += bl;
+  st->known_mask |= (ull)dmask << shift;
+  st->known_val |= (ull)x << shift;
+  st->top = shift - 1;
+}
+
+__global__ void k_widen(const unsigned* __restrict__ in, ull* __restrict__ out, int n) {
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x) out[i] = in[i];
+}
+
+__global__ void k_gather_rows(const ull* __restrict__ keys, const ull* __restrict__ idx, size_t n,
+                              size_t W, ull* __restrict__ out) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t < n * W) out[t] = keys[idx[t / W] * W + t % W];
+}
+
+constexpr int kDigitBits = 12;  // digit histograms privatized in shared memory
+
+// Append the hit lanes of one 2048-element chunk (8 per thread) to (ov, oi)
+// with one global atomic per block, and histogram their next digit in
+// shared memory (warp-aggregated: magnitudes repeat a lot, G_mol
+// coefficients carry few mantissa bits).
+__device__ __forceinline__ void chunk_emit(const ull (&v)[8], unsigned hit, size_t first,
+                                           const ull* __restrict__ ci, ull* __restrict__ ov,
+                                           ull* __restrict__ oi, ull* __restrict__ n_out, bool do_hist,
+                                           int shift, unsigned dmask, unsigned* sh, int* scratch,
+                                           ull* s_base) {
+  int total;
+  const int excl = block_exclusive<256>((int)__popc(hit), 0, OpAdd(), scratch, &total);
+  if (threadIdx.x == 0 && total) *s_base = atomicAdd(n_out, (ull)total);
+  __syncthreads();
+  if (total) {
+    ull slot = *s_base + excl;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool h = (hit >> k) & 1u;
+      if (h) {
+        ov[slot] = v[k];
+        oi[slot] = ci ? ci[first + k] : first + k;
+        ++slot;
+      }
+      if (do_hist) {
+        const unsigned d = h ? (unsigned)((v[k] >> shift) & dmask) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        if (h && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(sh + d, (unsigned)__popc(peers));
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void hist_begin(const SelState* sel, bool& do_hist, int& shift,
+                                           unsigned& dmask, unsigned* sh) {
+  do_hist = sel->top >= 0;
+  shift = 0;
+  dmask = 0;
+  if (do_hist) {
+    next_digit(sel, shift, dmask);
+    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x) sh[b] = 0;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void hist_end(bool do_hist, unsigned dmask, const unsigned* sh,
+                                         unsigned* __restrict__ hist) {
+  __syncthreads();
+  if (do_hist)
+    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
+      if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+
+// candidates of the selected coarse bin (|c| bits, index), plus the
+// histogram of their first digit
 template <int B>
 __global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys,
                                                     const double* __restrict__ coef, size_t M,
-                                                    double eps, unsigned bin, ull* __restrict__ cv,
-                                                    ull* __restrict__ ci, ull* __restrict__ ctr) {
-  // 8 coefficients per thread per iteration (4 x 16 B loads in flight)
-  const int lane = threadIdx.x & 31;
+                                                    double eps, const SelState* __restrict__ sel,
+                                                    ull* __restrict__ cv, ull* __restrict__ ci,
+                                                    ull* __restrict__ n_out, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[1 << kDigitBits];
+  __shared__ int scratch[256 / 32 + 2];
+  __shared__ ull s_base;
+  if (sel->fail) return;
+  bool do_hist;
+  int shift;
+  unsigned dmask;
+  hist_begin(sel, do_hist, shift, dmask, sh);
+  const unsigned bin = (unsigned)sel->bin;
   const bool has_id = key_is_identity<B>(load_key<B>(keys, 0));
-  // warp-uniform trip count: the warp's chunk is 256 consecutive coefficients
-  const size_t warp_id = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
-  const size_t n_warps = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t wbase = warp_id * 256; wbase < M; wbase += n_warps * 256) {
-    const size_t base = wbase + (size_t)lane * 8;
-    double v[8];
-    if (base + 8 <= M) {
-      const double2* p = reinterpret_cast<const double2*>(coef + base);
+  for (size_t base = blockIdx.x * (size_t)2048; base < M; base += (size_t)gridDim.x * 2048) {
+    const size_t first = base + (size_t)threadIdx.x * 8;
+    double c[8];
+    if (first + 8 <= M) {
+      const double2* p = reinterpret_cast<const double2*>(coef + first);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const double2 t = __ldg(p + h);
+        c[2 * h] = t.x;
+        c[2 * h + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = first + k < M ? coef[first + k] : 0.0;
+    }
+    unsigned hit = 0;
+    ull v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double a = fabs(c[k]);
+      v[k] = (ull)__double_as_longlong(a);
+      if (first + k < M && a >= eps && hist_bin(a) == bin && !(first + k == 0 && has_id)) hit |= 1u << k;
+    }
+    chunk_emit(v, hit, first, nullptr, cv, ci, n_out, do_hist, shift, dmask, sh, scratch, &s_base);
+  }
+  hist_end(do_hist, dmask, sh, hist);
+}
+
+// keep the candidates matching the prefix fixed so far, and histogram the
+// next digit over them; once every bit is fixed this yields the ties
+__global__ void __launch_bounds__(256) k_cand_filter(const ull* __restrict__ cv, const ull* __restrict__ ci,
+                                                     const ull* __restrict__ n_in,
+                                                     const SelState* __restrict__ sel,
+                                                     ull* __restrict__ ov, ull* __restrict__ oi,
+                                                     ull* __restrict__ n_out, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[1 << kDigitBits];
+  __shared__ int scratch[256 / 32 + 2];
+  __shared__ ull s_base;
+  if (sel->fail) return;
+  bool do_hist;
+  int shift;
+  unsigned dmask;
+  hist_begin(sel, do_hist, shift, dmask, sh);
+  const size_t n = *n_in;
+  const ull km = sel->known_mask, kv = sel->known_val;
+  for (size_t base = blockIdx.x * (size_t)2048; base < n; base += (size_t)gridDim.x * 2048) {
+    const size_t first = base + (size_t)threadIdx.x * 8;
+    ull v[8];
+    if (first + 8 <= n) {
+      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cv + first);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const ulonglong2 t = __ldg(p + h);
         v[2 * h] = t.x;
         v[2 * h + 1] = t.y;
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = base + k < M ? coef[base + k] : 0.0;
+      for (int k = 0; k < 8; ++k) v[k] = first + k < n ? cv[first + k] : ~0ull;
     }
     unsigned hit = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double a = fabs(v[k]);
-      if (base + k < M && a >= eps && hist_bin(a) == bin && !(base + k == 0 && has_id))
-        hit |= 1u << k;
-    }
-    // warp-aggregated slot allocation (one atomic per warp)
-    const unsigned n = __popc(hit);
-    const unsigned inc = warp_inclusive(n, OpAdd());
-    const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
-    ull slot = 0;
-    if (tot) {
-      if (lane == 31) slot = atomicAdd(ctr + 2, (ull)tot);
-      slot = __shfl_sync(0xffffffffu, slot, 31) + inc - n;
-    }
     for (int k = 0; k < 8; ++k)
-      if ((hit >> k) & 1u) {
-        cv[slot] = (ull)__double_as_longlong(fabs(v[k]));
-        ci[slot] = base + k;
-        ++slot;
-      }
+      if (first + k < n && (v[k] & km) == kv) hit |= 1u << k;
+    chunk_emit(v, hit, first, ci, ov, oi, n_out, do_hist, shift, dmask, sh, scratch, &s_base);
   }
-}
-
-constexpr int kDigitBits = 12;  // digit histogram privatized in shared memory
-__global__ void __launch_bounds__(256) k_cand_hist(const ull* __restrict__ cv, size_t n,
-                                                   ull known_mask, ull known_val, int shift,
-                                                   unsigned mask, unsigned* __restrict__ hist) {
-  __shared__ unsigned sh[1 << kDigitBits];
-  for (int b = threadIdx.x; b <= (int)mask; b += blockDim.x) sh[b] = 0;
-  __syncthreads();
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const ull v = cv[i];
-    if ((v & known_mask) == known_val) atomicAdd(sh + ((v >> shift) & mask), 1u);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b <= (int)mask; b += blockDim.x)
-    if (sh[b]) atomicAdd(hist + b, sh[b]);
-}
-
-__global__ void k_cand_ties(const ull* __restrict__ cv, const ull* __restrict__ ci, size_t n,
-                            ull value, ull* __restrict__ out, ull* __restrict__ ctr) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= n || cv[i] != value) return;
-  const unsigned act = __activemask();
-  const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-  ull base = 0;
-  if (lane == leader) base = atomicAdd(ctr + 3, (ull)__popc(act));
-  base = __shfl_sync(act, base, leader);
-  out[base + __popc(act & ((1u << lane) - 1u))] = ci[i];
+  hist_end(do_hist, dmask, sh, hist);
 }
 
 template <int B>
@@ -752,105 +944,100 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       f.cut = -1;
       logical = s.has_identity ? 1 : 0;
     } else {
+      SelState* sel = reinterpret_cast<SelState*>(ws.misc.as<ull>(16));
+      ull* hist_g = ws.misc.as<ull>(16) + 8;  // placeholder, resized below
+      ull* gbuf = ws.partials.as<ull>(kHistBins + (1 << kDigitBits));
+      hist_g = gbuf;
+      ull* dh_g = gbuf + kHistBins;
+      k_widen<<<1, 256, 0, st>>>(hist, hist_g, kHistBins);
+      if (red) red->sum_device(hist_g, kHistBins);
+      k_pick_bin<<<1, 256, 0, st>>>(hist_g, hist, (ull)budget, sel);
+      count_launch("select");
+      count_launch("select");
+      // candidate upper bound: the largest local coarse bin count
       std::vector<unsigned> hh(kHistBins);
       IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, kHistBins * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
-      std::vector<ull> hg(hh.begin(), hh.end());
-      if (red) red->sum(hg.data(), hg.size());
-      size_t cum = 0, r = 0, local_above = 0;
-      int bin = -1;
-      for (int b = kHistBins - 1; b >= 0; --b) {
-        if (cum + hg[b] >= budget) {
-          bin = b;
-          r = budget - cum;
-          break;
-        }
-        cum += hg[b];
-        local_above += hh[b];
-      }
-      if (bin < 0) throw std::runtime_error("compress: histogram inconsistent");
-      const size_t nc = hh[bin];  // local candidates
-      ull* cv = ws.cand_v.as<ull>(std::max<size_t>(nc, 1));
-      ull* ci = ws.cand_i.as<ull>(std::max<size_t>(nc, 1));
-      IQCC_CUDA(cudaMemsetAsync(ctr + 2, 0, 2 * sizeof(ull), st));
-      if (nc) {
+      const size_t ncap = std::max<size_t>(1, *std::max_element(hh.begin(), hh.end()));
+      // ping-pong candidate arrays: A0 = the bin, A_k = A_{k-1} matching
+      // the prefix after k picks; 8-aligned so chunks load as 16-byte pairs
+      const size_t ncap8 = (ncap + 7) & ~(size_t)7;
+      ull* av[3] = {ws.cand_v.as<ull>(ncap8), ws.cand_v2.as<ull>(ncap8), nullptr};
+      ull* ai[3] = {ws.cand_i.as<ull>(ncap8), ws.cand_i2.as<ull>(ncap8), nullptr};
+      // digit rounds: the device tracks the next unfixed bit (interior bins
+      // start below the exponent); spare rounds only re-compact the ties
+      const int rounds = (63 + kDigitBits - 1) / kDigitBits;
+      const size_t hsz = (size_t)1 << kDigitBits;
+      unsigned* dh = ws.misc2.as<unsigned>(hsz * rounds);
+      ull* cnt = ctr + 2;  // cnt[k] = |A_k|
+      IQCC_CUDA(cudaMemsetAsync(dh, 0, hsz * rounds * sizeof(unsigned), st));
+      IQCC_CUDA(cudaMemsetAsync(cnt, 0, (rounds + 1) * sizeof(ull), st));
+      {
         KernelScope ks("select_gather");
-        const unsigned grid = (unsigned)std::min<size_t>(148 * 16, std::max<size_t>(1, (s.M + 2047) / 2048));
+        const unsigned grid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (s.M + 2047) / 2048));
         switch (s.B) {
-          case 1: k_gather_bin<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
-          case 2: k_gather_bin<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
-          default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, (unsigned)bin, cv, ci, ctr); break;
+          case 1: k_gather_bin<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, sel, av[0], ai[0], cnt, dh); break;
+          case 2: k_gather_bin<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, sel, av[0], ai[0], cnt, dh); break;
+          default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, sel, av[0], ai[0], cnt, dh); break;
         }
       }
       if (getenv("IQCC_DEBUG")) debug_check("select gather");
-      // digits below what the coarse bin fixed, most significant first;
-      // larger values first.  An interior bin fixes the exponent (bits
-      // 62..52); the clamped end bins leave all 63 magnitude bits open.
-      ull known_mask = 1ull << 63, known_val = 0;
-      int top = 62;
-      if (bin > 0 && bin < kHistBins - 1) {
-        known_mask |= 0x7FFull << 52;
-        known_val = (ull)(bin + (1023 - 192)) << 52;
-        top = 51;
-      }
-      unsigned* dh = ws.misc2.as<unsigned>(1 << kDigitBits);
-      std::vector<unsigned> hd(1 << kDigitBits);
-      std::vector<ull> hdg(1 << kDigitBits);
-      while (top >= 0) {
-        const int width = std::min(kDigitBits, top + 1);
-        const int shift = top + 1 - width;
-        const unsigned dmask = (1u << width) - 1u;
-        IQCC_CUDA(cudaMemsetAsync(dh, 0, (dmask + 1) * sizeof(unsigned), st));
-        if (nc) {
-          KernelScope ks("select_digits");
-          const unsigned grid = (unsigned)std::min<size_t>(592, std::max<size_t>(1, (nc + 1023) / 1024));
-          k_cand_hist<<<grid, 256, 0, st>>>(cv, nc, known_mask, known_val, shift, dmask, dh);
-        }
-        IQCC_CUDA(cudaMemcpyAsync(hd.data(), dh, (dmask + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        IQCC_CUDA(cudaStreamSynchronize(st));
-        for (unsigned x = 0; x <= dmask; ++x) hdg[x] = hd[x];
-        if (red) red->sum(hdg.data(), dmask + 1);
-        size_t c2 = 0;
-        long d = -1;
-        for (long x = dmask; x >= 0; --x) {
-          if (c2 + hdg[x] >= r) {
-            d = x;
-            r -= c2;
-            break;
-          }
-          c2 += hdg[x];
-          local_above += hd[x];
-        }
-        if (d < 0) throw std::runtime_error("compress: digit select failed");
-        known_mask |= (ull)dmask << shift;
-        known_val |= (ull)d << shift;
-        top = shift - 1;
+      const unsigned cgrid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (ncap + 2047) / 2048));
+      int cur = 0;
+      for (int round = 0; round < rounds; ++round) {
+        KernelScope ks("select_digits");
+        unsigned* h = dh + hsz * round;
+        k_widen<<<4, 256, 0, st>>>(h, dh_g, (int)hsz);
+        if (red) red->sum_device(dh_g, hsz);
+        k_pick_digit<<<1, 256, 0, st>>>(dh_g, h, sel);
+        const int nxt = cur ^ 1;
+        k_cand_filter<<<cgrid, 256, 0, st>>>(av[cur], ai[cur], cnt + round, sel, av[nxt], ai[nxt],
+                                             cnt + round + 1, round + 1 < rounds ? h + hsz : h);
+        count_launch("select_digits");
+        count_launch("select_digits");
+        cur = nxt;
       }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
-      const ull vbits = known_val;  // exact threshold value; r ties at it are kept (globally)
-      ull* ties = ws.misc3.as<ull>(std::max<size_t>(nc, 1));
-      if (nc) {
-        KernelScope ks("select_ties");
-        k_cand_ties<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(cv, ci, nc, vbits, ties, ctr);
-      }
+      ull* ties = ai[cur];  // A_rounds: every bit fixed -> exactly the ties
+      SelState hs;
       ull ntie = 0;
-      IQCC_CUDA(cudaMemcpyAsync(&ntie, ctr + 3, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaMemcpyAsync(&hs, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaMemcpyAsync(&ntie, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
-      std::vector<ull> th(ntie);
-      if (ntie)
-        IQCC_CUDA(cudaMemcpyAsync(th.data(), ties, ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
+      if (hs.fail) throw std::runtime_error("compress: device select failed");
+      hs.ntie = ntie;
+      const ull vbits = hs.known_val;  // exact threshold value; hs.r ties at it are kept (globally)
+      size_t r = hs.r;
+      size_t local_above = hs.local_above;
+      std::vector<ull> th(hs.ntie);
+      if (hs.ntie)
+        IQCC_CUDA(cudaMemcpyAsync(th.data(), ties, hs.ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaStreamSynchronize(st));
-      std::sort(th.begin(), th.end());  // local index order = canonical order
+      if (getenv("IQCC_VERBOSE"))
+        fprintf(stderr, "[compress] M=%zu ncap=%zu ntie=%llu r=%zu above=%llu\n", s.M, ncap,
+                (unsigned long long)hs.ntie, r, (unsigned long long)local_above);
       size_t keep_ties = r;
       if (red) {
         // canonical tie-break across shards (partition.hpp:350-361): the
-        // globally first r tied words are kept
+        // globally first r tied words are kept; local index order is
+        // canonical order
+        std::sort(th.begin(), th.end());
         const size_t W = 2 * s.B;
         std::vector<ull> mine(th.size() * W);
-        for (size_t i = 0; i < th.size(); ++i)
-          IQCC_CUDA(cudaMemcpyAsync(mine.data() + i * W, s.keys() + th[i] * W, W * sizeof(ull),
-                                    cudaMemcpyDeviceToHost, st));
-        IQCC_CUDA(cudaStreamSynchronize(st));
+        if (!th.empty()) {
+          ull* d_idx = ai[cur ^ 1];  // free ping-pong buffer
+          ull* d_rows = av[cur ^ 1];
+          if (th.size() * (W + 1) > ncap8) {
+            d_idx = ws.misc3.as<ull>(th.size() * (W + 1));
+            d_rows = d_idx + th.size();
+          }
+          IQCC_CUDA(cudaMemcpyAsync(d_idx, th.data(), th.size() * sizeof(ull), cudaMemcpyHostToDevice, st));
+          k_gather_rows<<<(unsigned)((th.size() * W + 255) / 256), 256, 0, st>>>(s.keys(), d_idx, th.size(), W,
+                                                                                   d_rows);
+          count_launch("select");
+          IQCC_CUDA(cudaMemcpyAsync(mine.data(), d_rows, mine.size() * sizeof(ull), cudaMemcpyDeviceToHost, st));
+          IQCC_CUDA(cudaStreamSynchronize(st));
+        }
         size_t off = 0;
         std::vector<ull> all = red->gather_keys(mine, W, &off);
         const size_t nall = all.size() / W;
@@ -865,6 +1052,9 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
           if (ord[k] >= off && ord[k] < off + th.size()) ++keep_ties;
       } else if (r < 1 || r > th.size()) {
         throw std::runtime_error("compress: tie resolution failed");
+      } else {
+        // single store: the first r ties in index order are kept
+        std::nth_element(th.begin(), th.begin() + (r - 1), th.end());
       }
       double v;
       std::memcpy(&v, &vbits, 8);
