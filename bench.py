@@ -256,16 +256,18 @@ def run_gpu_arm(args, rank, world, local_rank):
         time.sleep(0.6)  # let nvidia-smi start sampling before the timed region
         torch.cuda.synchronize()
         e0.record(stream)
+        w0 = time.perf_counter()
         for s in range(args.steps):
             tin_total += dress_step(d, args.warmup + s)
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    print(f"[bench] wall {1e3 * (time.perf_counter() - w0):.1f} ms for {args.steps} steps", file=sys.stderr)
     launches = native.launch_count() - launches0
     merge_ms, merge_n = native.profile_get("merge")
     fam = {f: native.profile_get(f)[0] for f in
            ["classify", "present", "tile_agg", "carry", "rank", "partition", "merge",
-            "select_gather", "select_digits", "select_ties", "exchange"]}
+            "select_gather", "select_digits", "exchange", "host_wait", "host_dress", "host_compress", "span_dress", "span_compress", "host_alloc", "host_compress_inner"]}
     native.profile(False)
     if dist:
         t = torch.tensor([ms], device="cuda")

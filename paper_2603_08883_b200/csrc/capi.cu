@@ -5,6 +5,7 @@
 // std::invalid_argument -> IQCC_EINVAL (the reference throws
 // std::invalid_argument for precondition violations),
 // std::runtime_error -> IQCC_ERUNTIME, CUDA failures -> IQCC_ECUDA.
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -45,6 +46,8 @@ struct Ctx {
   bool profiling = false;
   std::map<std::string, ProfileEntry> prof;
   std::vector<cudaEvent_t> event_pool;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
 
 static Ctx* g_ctx = nullptr;
@@ -134,6 +137,61 @@ KernelScope::~KernelScope() {
   }
 }
 
+void* host_pinned(size_t bytes) {
+  Ctx& c = ctx();
+  if (bytes > c.pinned_bytes) {
+    if (c.pinned) IQCC_CUDA(cudaFreeHost(c.pinned));
+    c.pinned = nullptr;
+    c.pinned_bytes = std::max<size_t>(bytes, 8192);
+    IQCC_CUDA(cudaMallocHost(&c.pinned, c.pinned_bytes));
+  }
+  return c.pinned;
+}
+
+// Busy-wait: a blocking/yielding synchronize can leave the GPU idle for a
+// scheduler quantum after every step boundary.
+static void spin_sync(cudaStream_t st) {
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) IQCC_CUDA(e);
+  }
+}
+
+void host_sync(cudaStream_t st) {
+  Ctx& c = ctx();
+  if (!c.profiling) {
+    spin_sync(st);
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  spin_sync(st);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  auto& e = c.prof["host_wait"];
+  e.ms += ms;
+  e.launches += 1;
+}
+
+static void host_ms(const char* fam, std::chrono::steady_clock::time_point t0) {
+  Ctx& c = ctx();
+  if (!c.profiling) return;
+  auto& e = c.prof[fam];
+  e.ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  e.launches += 1;
+}
+
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+HostScope::HostScope(const char* f) : family(f), t0(now_ms()) {}
+HostScope::~HostScope() {
+  Ctx& c = ctx();
+  if (!c.profiling) return;
+  auto& e = c.prof[family];
+  e.ms += now_ms() - t0;
+  e.launches += 1;
+}
+
 static void profile_flush() {
   Ctx& c = ctx();
   for (auto& [name, e] : c.prof) {
@@ -151,7 +209,14 @@ static void profile_flush() {
 
 void* DevBuf::get(size_t n) {
   if (n <= bytes && p) return p;
+  HostScope hs("host_alloc");
   cudaStream_t st = stream();
+  static const bool verbose = getenv("IQCC_VERBOSE") != nullptr;
+  if (verbose) {
+    const Workspace& w = ctx().ws;
+    fprintf(stderr, "[alloc] buf@ws+%td n=%zu had=%zu\n",
+            (const char*)this - (const char*)&w, n, bytes);
+  }
   if (p) IQCC_CUDA(cudaFreeAsync(p, st));
   p = nullptr;
   size_t want = std::max<size_t>(n + n / 2, 256);  // generous slack: stores grow ~1.5x per step
@@ -283,6 +348,7 @@ int iqcc_gpu_finalize(void) {
     multi_shutdown();
     g_ctx->ws.release_all();
     cudaStreamSynchronize(g_ctx->cur);
+    if (g_ctx->pinned) cudaFreeHost(g_ctx->pinned);
     cudaStreamDestroy(g_ctx->own);
     delete g_ctx;
     g_ctx = nullptr;
@@ -453,9 +519,17 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
       if (terms_in_total) *terms_in_total += h->s.logical;
       const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
+      const auto t0 = std::chrono::steady_clock::now();
+      KernelScope* outer = new KernelScope("span_dress");
       DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps);
+      delete outer;
+      host_ms("host_dress", t0);
       if (eps > 0.0 || h->s.logical > max_terms) {
+        const auto t1 = std::chrono::steady_clock::now();
+        KernelScope* outer2 = new KernelScope("span_compress");
         CompressResult r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr);
+        delete outer2;
+        host_ms("host_compress", t1);
         if (stats) {
           stats->dropped_terms += r.dropped_terms;
           stats->dropped_weight += r.dropped_weight;

@@ -1049,10 +1049,10 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
       }
     }
     if (getenv("IQCC_DEBUG")) debug_check("rank");
-    long long a_host = 0;
-    IQCC_CUDA(cudaMemcpyAsync(&a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
-    pl.A = (size_t)a_host;
+    long long* a_host = static_cast<long long*>(host_pinned(sizeof(long long)));
+    IQCC_CUDA(cudaMemcpyAsync(a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    host_sync(st);
+    pl.A = (size_t)*a_host;
     if (getenv("IQCC_DEBUG") && pl.A > 0) {
       unsigned* seen = ws.misc2.as<unsigned>(M);
       IQCC_CUDA(cudaMemsetAsync(seen, 0, M * sizeof(unsigned), st));
@@ -1161,9 +1161,9 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   ull* ctr = ws.counters.as<ull>(8);
-  ull hc[4] = {0, 0, 0, 0};
+  ull* hc = static_cast<ull*>(host_pinned(4 * sizeof(ull)));
   IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 4 * sizeof(ull), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
   // algorithmic bytes of the step: (M_in + M_out) * (16B + 8)
@@ -1282,7 +1282,7 @@ void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* n
   }
   ull h[2];
   IQCC_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   *na = h[0];
   *nc = h[1];
 }

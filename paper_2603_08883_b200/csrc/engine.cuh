@@ -321,6 +321,21 @@ void check_cuda(cudaError_t e, const char* what);
 
 /// Kernel-family timing scope (CUDA events on the engine stream) when
 /// profiling is enabled; always counts the launch.
+/// cudaStreamSynchronize that books the host's blocked time under the
+/// profile family "host_wait" (launch-bound vs GPU-bound diagnosis).
+void host_sync(cudaStream_t st);
+/// Page-locked host scratch (>= 8 KiB) for small device->host reads, so the
+/// copies stay asynchronous; valid until the next call.
+void* host_pinned(size_t bytes);
+
+/// Host wall time of a region, booked under a profile family (profiling on).
+struct HostScope {
+  const char* family;
+  double t0;
+  explicit HostScope(const char* f);
+  ~HostScope();
+};
+
 struct KernelScope {
   const char* family;
   cudaEvent_t a = nullptr, b = nullptr;

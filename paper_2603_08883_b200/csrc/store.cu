@@ -114,7 +114,7 @@ void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const d
   ull first_key[kMaxB * 2];
   IQCC_CUDA(cudaMemcpyAsync(h, err, sizeof(h), cudaMemcpyDeviceToHost, st));
   IQCC_CUDA(cudaMemcpyAsync(first_key, s.keys(), 2 * s.B * sizeof(ull), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   if (h[0] != ULLONG_MAX)
     throw std::invalid_argument("coefficient " + std::to_string(h[0] - 1) +
                                 " is NaN or has a nonzero imaginary part; the device engine stores "
@@ -206,7 +206,7 @@ static size_t run_compact(DeviceStore& s, int mode, uint32_t Bout, ull* okeys, d
   }
   ull n = 0;
   IQCC_CUDA(cudaMemcpyAsync(&n, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   return (size_t)n;
 }
 
@@ -238,7 +238,7 @@ size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap,
   if (host_dst) {
     IQCC_CUDA(cudaMemcpyAsync(rows, d_rows, n * 2 * Bref * sizeof(ull), cudaMemcpyDeviceToHost, st));
     IQCC_CUDA(cudaMemcpyAsync(coeff, d_coef, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
+    host_sync(st);
   }
   return n;
 }
@@ -376,7 +376,7 @@ void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* 
   }
   ull n = 0;
   IQCC_CUDA(cudaMemcpyAsync(&n, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
   // the identity lives in the all-zero-key shard (partition.hpp:364-366)
@@ -566,7 +566,7 @@ static void gen_impl(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
   }
   ull m = 0;
   IQCC_CUDA(cudaMemcpyAsync(&m, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   s.M = m;
   s.logical = m;
   s.filt = Filter{};
@@ -899,6 +899,7 @@ __global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __r
 
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
                               size_t count_eps, bool want_stats, Reducer* red) {
+  HostScope hscope("host_compress_inner");
   if (eps < 0) throw std::invalid_argument("compress: epsilon < 0");
   if (max_terms < 1) throw std::invalid_argument("compress: max_terms < 1");
   Workspace& ws = workspace();
@@ -923,10 +924,10 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         default: k_hist_eps<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, hist, ctr); break;
       }
     }
-    ull h = 0;
-    IQCC_CUDA(cudaMemcpyAsync(&h, ctr + 1, sizeof(ull), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
-    count_eps = (size_t)h;
+    ull* h = static_cast<ull*>(host_pinned(sizeof(ull)));
+    IQCC_CUDA(cudaMemcpyAsync(h, ctr + 1, sizeof(ull), cudaMemcpyDeviceToHost, st));
+    host_sync(st);
+    count_eps = (size_t)*h;
   }
   // global view (compress_partitioned: per-shard eps cut, one global budget)
   ull glob[2] = {(ull)count_eps, (ull)(s.has_identity ? 1 : 0)};
@@ -954,11 +955,9 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       k_pick_bin<<<1, 256, 0, st>>>(hist_g, hist, (ull)budget, sel);
       count_launch("select");
       count_launch("select");
-      // candidate upper bound: the largest local coarse bin count
-      std::vector<unsigned> hh(kHistBins);
-      IQCC_CUDA(cudaMemcpyAsync(hh.data(), hist, kHistBins * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaStreamSynchronize(st));
-      const size_t ncap = std::max<size_t>(1, *std::max_element(hh.begin(), hh.end()));
+      // candidate capacity: the store size (stable across steps, so the
+      // buffers never regrow inside a dressing loop and no count is read back)
+      const size_t ncap = std::max<size_t>(1, s.M);
       // ping-pong candidate arrays: A0 = the bin, A_k = A_{k-1} matching
       // the prefix after k picks; 8-aligned so chunks load as 16-byte pairs
       const size_t ncap8 = (ncap + 7) & ~(size_t)7;
@@ -999,20 +998,25 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
       ull* ties = ai[cur];  // A_rounds: every bit fixed -> exactly the ties
-      SelState hs;
-      ull ntie = 0;
-      IQCC_CUDA(cudaMemcpyAsync(&hs, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaMemcpyAsync(&ntie, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaStreamSynchronize(st));
+      SelState* hsp = static_cast<SelState*>(host_pinned(sizeof(SelState) + sizeof(ull)));
+      ull* ntp = reinterpret_cast<ull*>(hsp + 1);
+      IQCC_CUDA(cudaMemcpyAsync(hsp, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaMemcpyAsync(ntp, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      host_sync(st);
+      SelState hs = *hsp;
+      const ull ntie = *ntp;
       if (hs.fail) throw std::runtime_error("compress: device select failed");
       hs.ntie = ntie;
       const ull vbits = hs.known_val;  // exact threshold value; hs.r ties at it are kept (globally)
       size_t r = hs.r;
       size_t local_above = hs.local_above;
       std::vector<ull> th(hs.ntie);
-      if (hs.ntie)
-        IQCC_CUDA(cudaMemcpyAsync(th.data(), ties, hs.ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaStreamSynchronize(st));
+      if (hs.ntie) {
+        ull* tp = static_cast<ull*>(host_pinned(hs.ntie * sizeof(ull)));
+        IQCC_CUDA(cudaMemcpyAsync(tp, ties, hs.ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
+        host_sync(st);
+        std::copy(tp, tp + hs.ntie, th.begin());
+      }
       if (getenv("IQCC_VERBOSE"))
         fprintf(stderr, "[compress] M=%zu ncap=%zu ntie=%llu r=%zu above=%llu\n", s.M, ncap,
                 (unsigned long long)hs.ntie, r, (unsigned long long)local_above);
@@ -1036,7 +1040,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
                                                                                    d_rows);
           count_launch("select");
           IQCC_CUDA(cudaMemcpyAsync(mine.data(), d_rows, mine.size() * sizeof(ull), cudaMemcpyDeviceToHost, st));
-          IQCC_CUDA(cudaStreamSynchronize(st));
+          host_sync(st);
         }
         size_t off = 0;
         std::vector<ull> all = red->gather_keys(mine, W, &off);
@@ -1080,7 +1084,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
     }
     std::vector<double> hp(grid);
     IQCC_CUDA(cudaMemcpyAsync(hp.data(), part, grid * sizeof(double), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
+    host_sync(st);
     double w = 0.0;
     for (double x : hp) w += x;
     res.dropped_weight = w;
