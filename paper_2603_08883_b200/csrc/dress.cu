@@ -54,8 +54,17 @@ struct Thr {
 };
 
 // ---------------------------------------------------------------- classify
+#ifndef IQCC_CLS_MINB
+#define IQCC_CLS_MINB 4
+#endif
+#ifndef IQCC_MERGE_MINB
+#define IQCC_MERGE_MINB 6
+#endif
+#ifndef IQCC_RANK_MINB
+#define IQCC_RANK_MINB 4
+#endif
 template <int B, int IT>
-__global__ void __launch_bounds__(256) k_classify(const ull* __restrict__ keys,
+__global__ void __launch_bounds__(256, IQCC_CLS_MINB) k_classify(const ull* __restrict__ keys,
                                                   const double* __restrict__ coef, Filter filt,
                                                   size_t M, Key<B> P, short* __restrict__ lcp,
                                                   unsigned* __restrict__ fmask,
@@ -279,6 +288,7 @@ __global__ void __launch_bounds__(GROUP) k_tile_carry(const int* __restrict__ ti
 #define IQCC_WI 8
 #endif
 constexpr int WI = IQCC_WI;  // terms per lane
+static_assert(WI % 8 == 0 && WI <= 32, "lcp rows load as int4 (8 shorts)");
 constexpr int WT = 32 * WI;
 
 struct WarpItems {
@@ -322,18 +332,28 @@ __global__ void __launch_bounds__(256) k_tile_agg_w(const short* __restrict__ lc
   const int cnt = __popc(it.bits);
   const int inc = warp_inclusive(cnt, OpAdd());
   const int cl = inc - cnt;
+  int lmax = INT_MIN;
+#pragma unroll
+  for (int k = 0; k < WI; ++k) lmax = max(lmax, it.l[k]);
+  lmax = __reduce_max_sync(0xffffffffu, lmax);
+  const int c_last = __shfl_sync(0xffffffffu, inc, 31) - (int)(__shfl_sync(0xffffffffu, it.bits, 31) >> (WI - 1));
 #pragma unroll
   for (int j = 0; j < NTHR; ++j) {
     const int T = thr.t[j];
     int fa = -1, ba = INT_MAX;
+    if (lmax <= T) {  // every term is a boundary (warp-uniform fast path)
+      fa = c_last;
+      ba = 0;
+    } else {
 #pragma unroll
-    for (int k = 0; k < WI; ++k)
-      if (it.l[k] <= T) fa = cl + __popc(it.bits & ((1u << k) - 1u));
+      for (int k = 0; k < WI; ++k)
+        if (it.l[k] <= T) fa = cl + __popc(it.bits & ((1u << k) - 1u));
 #pragma unroll
-    for (int k = WI - 1; k >= 0; --k)
-      if (it.l[k] <= T) ba = cl + __popc(it.bits & ((1u << k) - 1u));
-    fa = __reduce_max_sync(0xffffffffu, fa);
-    ba = __reduce_min_sync(0xffffffffu, ba);
+      for (int k = WI - 1; k >= 0; --k)
+        if (it.l[k] <= T) ba = cl + __popc(it.bits & ((1u << k) - 1u));
+      fa = __reduce_max_sync(0xffffffffu, fa);
+      ba = __reduce_min_sync(0xffffffffu, ba);
+    }
     if (lane == 0) {
       fwd_agg[wt * kThrPerChunk + j] = fa;
       bwd_agg[wt * kThrPerChunk + j] = ba == INT_MAX ? -1 : ba;
@@ -348,7 +368,7 @@ __global__ void __launch_bounds__(256) k_tile_agg_w(const short* __restrict__ lc
 // forward scan.  When the bit is 1 but the 0-child is empty both formulas
 // give 0, so  delta_l = D > 0 ? -D : (bwd[lt] - bwd[le]).
 template <int NTHR, bool FINAL>
-__global__ void __launch_bounds__(256) k_rank_w(const short* __restrict__ lcp,
+__global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __restrict__ lcp,
                                                 const unsigned* __restrict__ fmask, size_t M,
                                                 size_t ntiles, Thr thr,
                                                 const int* __restrict__ tile_pfx,
@@ -822,7 +842,7 @@ __device__ __forceinline__ void merge_flush(const MergeArgs& g, unsigned* shist,
 /// One tile per CTA (single input stage): the default; enough CTAs stay
 /// resident that load latency of one hides behind the merge of others.
 template <int B, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_merge1(MergeArgs g, Key<B> P) {
+__global__ void __launch_bounds__(NT, IQCC_MERGE_MINB) k_merge1(MergeArgs g, Key<B> P) {
   using Cfg = MergeCfg<B, NT, IPT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST - Cfg::STAGE);
@@ -959,7 +979,11 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
     lcp = ws.lcp.as<short>(M);
     {
       KernelScope ks("classify");
-      constexpr int IT = B >= 4 ? 2 : 4;
+#ifdef IQCC_CLS_IT
+      constexpr int IT = B >= 4 ? 2 : IQCC_CLS_IT;
+#else
+      constexpr int IT = 2;  // 56 registers: 4 CTAs / SM
+#endif
       k_classify<B, IT><<<(unsigned)((M + 256 * IT - 1) / (256 * IT)), 256, 0, st>>>(
           s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pl.pmask);
     }
@@ -1129,6 +1153,8 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     if (!attr1) {
       IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::bytes(true, 1)));
+      IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared));
       attr1 = true;
     }
     KernelScope ks("merge");

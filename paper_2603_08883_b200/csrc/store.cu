@@ -452,14 +452,19 @@ __global__ void k_digit_scatter(const ull* __restrict__ keys, const unsigned* __
   }
 }
 
-__global__ void k_scan_digits(unsigned* __restrict__ hist, size_t n) {
-  // single thread exclusive scan over 256 * nblocks counters (small)
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  unsigned s = 0;
-  for (size_t i = 0; i < n; ++i) {
-    unsigned v = hist[i];
-    hist[i] = s;
-    s += v;
+__global__ void __launch_bounds__(1024) k_scan_digits(unsigned* __restrict__ hist, size_t n) {
+  // exclusive scan of the 256 x nblocks digit counters: one block, each
+  // thread a contiguous run
+  __shared__ unsigned sm[1024 / 32 + 2];
+  const size_t per = (n + 1023) / 1024;
+  const size_t lo = threadIdx.x * per, hi = min(n, lo + per);
+  unsigned c = 0;
+  for (size_t i = lo; i < hi; ++i) c += hist[i];
+  unsigned run = block_exclusive<1024>(c, 0u, OpAdd(), sm, (unsigned*)nullptr);
+  for (size_t i = lo; i < hi; ++i) {
+    const unsigned v = hist[i];
+    hist[i] = run;
+    run += v;
   }
 }
 
@@ -543,7 +548,7 @@ static void gen_impl(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
     for (int shift = 0; shift < 64; shift += 8) {
       KernelScope ks("generate");
       k_digit_hist<<<(unsigned)nb, 256, 0, st>>>(tk, perm, N, W, word, shift, hist, per_block);
-      k_scan_digits<<<1, 1, 0, st>>>(hist, 256 * nb);
+      k_scan_digits<<<1, 1024, 0, st>>>(hist, 256 * nb);
       k_digit_scatter<<<(unsigned)nb, 32, 0, st>>>(tk, perm, N, W, word, shift, hist, perm2, per_block);
       std::swap(perm, perm2);
     }

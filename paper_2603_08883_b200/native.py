@@ -12,7 +12,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libiqcc_b200.so")
+LIB_PATH = os.environ.get("IQCC_LIB") or os.path.join(HERE, "libiqcc_b200.so")  # IQCC_LIB: tuning builds
 CSRC = os.path.join(HERE, "csrc")
 
 IQCC_OK, IQCC_EINVAL, IQCC_ERUNTIME, IQCC_ECUDA, IQCC_ENOMEM = 0, 1, 2, 3, 4
