@@ -515,13 +515,17 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       if (row_is_identity(gens + k * 2 * Bref, Bref))
         throw std::invalid_argument("dress_single: identity generator");
     if (terms_in_total) *terms_in_total = 0;
+    const bool fuse = getenv("IQCC_NO_META") == nullptr;  // A/B switch for the fused classify
     for (size_t k = 0; k < K; ++k) {
       auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
+      std::vector<uint64_t> next;
+      if (fuse && k + 1 < K) next = widen_row(gens + (k + 1) * 2 * Bref, Bref, h->s.B);
       if (terms_in_total) *terms_in_total += h->s.logical;
       const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
       const auto t0 = std::chrono::steady_clock::now();
       KernelScope* outer = new KernelScope("span_dress");
-      DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps);
+      DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps,
+                                  next.empty() ? nullptr : next.data());
       delete outer;
       host_ms("host_dress", t0);
       if (eps > 0.0 || h->s.logical > max_terms) {

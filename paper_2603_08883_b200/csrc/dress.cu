@@ -313,22 +313,72 @@ __device__ __forceinline__ WarpItems load_witems(const short* __restrict__ lcp,
 #pragma unroll
     for (int k = 0; k < WI; ++k) it.l[k] = first + k < M ? (int)lcp[first + k] : INT_MAX;
   }
-  it.bits = first < M ? (fmask[first >> 5] >> (first & 31)) & ((1u << WI) - 1u) : 0u;
+  it.bits = fmask && first < M ? (fmask[first >> 5] >> (first & 31)) & ((1u << WI) - 1u) : 0u;
   return it;
 }
 
-template <int NTHR>
+/// Present / anticommuting bits from the merge's next-step metadata (the
+/// classify pass of a dress_sequence step): present = filter_keep (dead
+/// slots and the pending compress filter are absent), anticommuting from
+/// the merge's bits.
+struct MaskArgs {
+  const double* coef;
+  const unsigned* amask;
+  const ull* keys;
+  int W;  // key words (identity check of slot 0)
+  Filter filt;
+  unsigned* fmask;  // out
+  unsigned* pmask;  // out
+};
+
+__device__ __forceinline__ unsigned lane_masks(const MaskArgs& ma, size_t M, size_t first, int lane) {
+  unsigned pb = 0, fb = 0;
+  if (first < M) {
+    const unsigned aw = (ma.amask[first >> 5] >> (first & 31)) & ((1u << WI) - 1u);
+    bool id0 = false;
+    if (first == 0) {
+      id0 = true;
+      for (int w = 0; w < ma.W; ++w) id0 = id0 && ma.keys[w] == 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < WI; ++k) {
+      const size_t i = first + k;
+      if (i < M) {
+        const bool pr = filter_keep(ma.filt, i, __ldg(ma.coef + i), k == 0 && id0);
+        pb |= (unsigned)pr << k;
+        fb |= (unsigned)(pr && ((aw >> k) & 1u)) << k;
+      }
+    }
+  }
+  // lanes 4j..4j+3 (WI = 8) share one 32-bit mask word
+  constexpr int LPW = 32 / WI;
+  const int sh = WI * (lane % LPW);
+  unsigned xp = pb << sh, xf = fb << sh;
+#pragma unroll
+  for (int o = 1; o < LPW; o <<= 1) {
+    xp |= __shfl_xor_sync(0xffffffffu, xp, o);
+    xf |= __shfl_xor_sync(0xffffffffu, xf, o);
+  }
+  if (lane % LPW == 0 && first < M) {
+    ma.pmask[first >> 5] = xp;
+    ma.fmask[first >> 5] = xf;
+  }
+  return fb;
+}
+
+template <int NTHR, bool MASKS>
 __global__ void __launch_bounds__(256) k_tile_agg_w(const short* __restrict__ lcp,
                                                     const unsigned* __restrict__ fmask, size_t M,
                                                     size_t ntiles, Thr thr,
                                                     int* __restrict__ tile_cnt,
                                                     int* __restrict__ fwd_agg,
-                                                    int* __restrict__ bwd_agg) {
+                                                    int* __restrict__ bwd_agg, MaskArgs ma) {
   const size_t wt = blockIdx.x * (size_t)8 + (threadIdx.x >> 5);
   if (wt >= ntiles) return;
   const int lane = threadIdx.x & 31;
   const size_t first = wt * WT + (size_t)lane * WI;
-  const WarpItems it = load_witems(lcp, fmask, M, first);
+  WarpItems it = load_witems(lcp, MASKS ? nullptr : fmask, M, first);
+  if (MASKS) it.bits = lane_masks(ma, M, first, lane);
   const int cnt = __popc(it.bits);
   const int inc = warp_inclusive(cnt, OpAdd());
   const int cl = inc - cnt;
@@ -624,6 +674,11 @@ struct MergeArgs {
   unsigned* hist;
   int want_hist;
   ull* dbg;
+  // next-step metadata (nullptr: none): LCP with the predecessor slot and
+  // anticommute bits against the next entangler pn
+  short* out_lcp;
+  unsigned* out_amask;
+  ull pn[8];
 };
 
 /// Issue the loads of one tile into one stage: survivors by the TMA bulk
@@ -803,21 +858,60 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
     }
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < nslots; q += NT) {
-    const int e = oute[q];
-    const double v = outv[q];
-    const Key<B> k = e < nS ? sm_key16<B>(sk, e) : qkey(e - nS);
-    store_key<B>(g.out_keys, o0 + q, k);
-    g.out_coef[o0 + q] = v;
-    if (is_dead(v)) {
-      ++n_dead;
-    } else if (g.want_hist) {
-      const double a = fabs(v);
-      const bool id = o0 + q == 0 && key_is_identity<B>(k);
-      if (id || a >= g.eps) ++n_eps;
-      if (!id && a >= g.eps) atomicAdd(shist + hist_bin(a), 1u);
+  const bool meta = g.out_lcp != nullptr;
+  Key<B> PN;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) PN.w[w] = g.pn[w];
+  for (int q0 = 0; q0 < nslots; q0 += NT) {  // block-uniform trip count
+    const int q = q0 + (int)threadIdx.x;
+    bool anti = false;
+    if (q < nslots) {
+      const int e = oute[q];
+      const double v = outv[q];
+      const Key<B> k = e < nS ? sm_key16<B>(sk, e) : qkey(e - nS);
+      store_key<B>(g.out_keys, o0 + q, k);
+      g.out_coef[o0 + q] = v;
+      if (is_dead(v)) {
+        ++n_dead;
+      } else if (g.want_hist) {
+        const double a = fabs(v);
+        const bool id = o0 + q == 0 && key_is_identity<B>(k);
+        if (id || a >= g.eps) ++n_eps;
+        if (!id && a >= g.eps) atomicAdd(shist + hist_bin(a), 1u);
+      }
+      if (meta) {
+        short l = -1;  // tile-first slot: fixed up by k_meta_fix
+        if (q > 0) {
+          const int ep = oute[q - 1];
+          l = (short)key_lcp<B>(ep < nS ? sm_key16<B>(sk, ep) : qkey(ep - nS), k);
+        }
+        g.out_lcp[o0 + q] = l;
+        anti = anticommutes<B>(k, PN);
+      }
+    }
+    if (meta) {
+      const unsigned bal = __ballot_sync(0xffffffffu, anti);
+      if ((threadIdx.x & 31) == 0 && bal) {
+        const size_t ob = o0 + q0 + (threadIdx.x & ~31u);
+        const unsigned sh = (unsigned)(ob & 31);
+        atomicOr(g.out_amask + (ob >> 5), bal << sh);
+        if (sh) atomicOr(g.out_amask + (ob >> 5) + 1, bal >> (32 - sh));
+      }
     }
   }
+}
+
+/// LCP of every tile's first output slot with its predecessor (the merge
+/// only sees predecessors inside its own tile).
+template <int B>
+__global__ void k_meta_fix(const ull* __restrict__ keys, const ull* __restrict__ part_o, size_t ntiles,
+                           short* __restrict__ lcp) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const size_t Mout = part_o[ntiles];
+  const size_t o = part_o[t];
+  if (o == 0 || o >= Mout) return;
+  lcp[o] = (short)key_lcp<B>(load_key<B>(keys, o - 1), load_key<B>(keys, o));
 }
 
 template <int B, int NT>
@@ -975,7 +1069,29 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
   pl.ptotal = bsum + (W + PW - 1) / PW + 4;
   IQCC_CUDA(cudaMemsetAsync(pl.ptotal, 0, sizeof(unsigned), st));
   short* lcp = nullptr;
-  if (M > 0) {
+  // the previous merge of a dress_sequence already classified the store
+  const bool use_meta = products && M > 0 && s.meta_valid &&
+                        std::equal(P.w, P.w + 2 * B, s.meta_P);
+  const size_t nb = (W + PW - 1) / PW;
+  auto run_present = [&]() {
+    KernelScope ks("present");
+    k_popc_blocks<<<(unsigned)nb, 256, 0, st>>>(pl.pmask, W, bsum);
+    k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, pl.ptotal);
+    k_popc_prefix<<<(unsigned)nb, 256, 0, st>>>(pl.pmask, W, bsum, pl.ppre);
+    count_launch("present");
+    count_launch("present");
+  };
+  MaskArgs ma{};
+  if (use_meta) {
+    lcp = s.meta_lcp.as<short>(M);
+    ma.coef = s.coef();
+    ma.amask = s.meta_amask.as<unsigned>(W + 2);
+    ma.keys = s.keys();
+    ma.W = 2 * B;
+    ma.filt = s.filt;
+    ma.fmask = fmask;
+    ma.pmask = pl.pmask;
+  } else if (M > 0) {
     lcp = ws.lcp.as<short>(M);
     {
       KernelScope ks("classify");
@@ -988,15 +1104,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
           s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pl.pmask);
     }
     if (getenv("IQCC_DEBUG")) debug_check("classify");
-    const size_t nb = (W + PW - 1) / PW;
-    {
-      KernelScope ks("present");
-      k_popc_blocks<<<(unsigned)nb, 256, 0, st>>>(pl.pmask, W, bsum);
-      k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, pl.ptotal);
-      k_popc_prefix<<<(unsigned)nb, 256, 0, st>>>(pl.pmask, W, bsum, pl.ppre);
-      count_launch("present");
-      count_launch("present");
-    }
+    run_present();
   }
   if (getenv("IQCC_DEBUG") && M > 0) debug_check("present");
   if (products && M > 0) {
@@ -1033,13 +1141,25 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
       const bool last = c == nch - 1;
       {
         KernelScope ks("tile_agg");
-        switch (nthr4) {
-          case 4: k_tile_agg_w<4><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
-          case 8: k_tile_agg_w<8><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
-          case 12: k_tile_agg_w<12><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
-          default: k_tile_agg_w<16><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg); break;
+#define IQCC_AGG(NT_, MK_) k_tile_agg_w<NT_, MK_><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_cnt, fwd_agg, bwd_agg, ma)
+        if (use_meta && c == 0) {
+          switch (nthr4) {
+            case 4: IQCC_AGG(4, true); break;
+            case 8: IQCC_AGG(8, true); break;
+            case 12: IQCC_AGG(12, true); break;
+            default: IQCC_AGG(16, true); break;
+          }
+        } else {
+          switch (nthr4) {
+            case 4: IQCC_AGG(4, false); break;
+            case 8: IQCC_AGG(8, false); break;
+            case 12: IQCC_AGG(12, false); break;
+            default: IQCC_AGG(16, false); break;
+          }
         }
+#undef IQCC_AGG
       }
+      if (use_meta && c == 0) run_present();
       {
         KernelScope ks("carry");
         k_group_agg<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
@@ -1089,7 +1209,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
 
 template <int B, int NT, int IPT>
 void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys, const double* q_vals,
-                    double cs, double sn, double drop, bool want_hist, double eps) {
+                    double cs, double sn, double drop, bool want_hist, double eps, const Key<B>* PN) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   const PlanState& pl = g_plan;
@@ -1134,6 +1254,16 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   g.hist = hist;
   g.want_hist = want_hist ? 1 : 0;
   g.dbg = debug_buffer();
+  g.out_lcp = nullptr;
+  g.out_amask = nullptr;
+  for (int w = 0; w < 8; ++w) g.pn[w] = 0;
+  if (PN) {
+    g.out_lcp = s.meta_lcp.as<short>(std::max<size_t>(total, 1));
+    const size_t wn = total / 32 + 2;
+    g.out_amask = s.meta_amask.as<unsigned>(wn);
+    IQCC_CUDA(cudaMemsetAsync(g.out_amask, 0, wn * sizeof(unsigned), st));
+    for (int w = 0; w < 2 * B; ++w) g.pn[w] = PN->w[w];
+  }
   static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
   if (persistent) {
     static int ctas_per_sm = 0, n_sm = 0;
@@ -1160,6 +1290,10 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     KernelScope ks("merge");
     k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
   }
+  if (PN) {
+    KernelScope ks("merge");
+    k_meta_fix<B><<<(unsigned)((ntm + 255) / 256), 256, 0, st>>>(out_keys, po, ntm, g.out_lcp);
+  }
   IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
   if (getenv("IQCC_DEBUG")) debug_check("merge");
 }
@@ -1167,14 +1301,14 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
 template <int B>
 DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys,
                         const double* q_vals, double cs, double sn, double drop, bool want_hist,
-                        double eps) {
+                        double eps, const Key<B>* PN = nullptr) {
   static int shape = -1;
   if (shape < 0) {
     const char* env = getenv("IQCC_MERGE_CFG");
     shape = env ? atoi(env) : 3;
     if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 3;
   }
-#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps)
+#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps, PN)
   switch (shape) {
     case 0: IQCC_MERGE(256, 4); break;
     case 1: IQCC_MERGE(128, 4); break;
@@ -1197,6 +1331,9 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
   s.M = hc[3];                // physical slots (live + dead)
   s.filt = Filter{};
   s.logical = hc[3] - hc[2];  // minus dead slots
+  s.meta_valid = PN != nullptr;
+  if (PN)
+    for (int w = 0; w < 2 * B; ++w) s.meta_P[w] = PN->w[w];
   add_alg_bytes("merge", (double)(logical_in + s.logical) * (16.0 * B + 8.0));
   DressOutcome out;
   out.count_eps = hc[1];
@@ -1206,10 +1343,13 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
 
 template <int B>
 DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps) {
+                        bool want_hist, double eps, const uint64_t* next_row) {
   const Key<B> P = make_key<B>(gen_row);
   plan_impl<B>(s, P, sn != 0.0);
-  return merge_impl<B>(s, P, g_plan.A, nullptr, nullptr, cs, sn, drop, want_hist, eps);
+  Key<B> PN;
+  if (next_row) PN = make_key<B>(next_row);
+  return merge_impl<B>(s, P, g_plan.A, nullptr, nullptr, cs, sn, drop, want_hist, eps,
+                       next_row ? &PN : nullptr);
 }
 
 // Sorted products as a contiguous buffer (keys ^ P, +-fl(c*sin)) for a peer.
@@ -1262,11 +1402,11 @@ DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, 
 }
 
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps) {
+                        bool want_hist, double eps, const uint64_t* next_row) {
   switch (s.B) {
-    case 1: return dress_impl<1>(s, gen_row, cs, sn, drop, want_hist, eps);
-    case 2: return dress_impl<2>(s, gen_row, cs, sn, drop, want_hist, eps);
-    case 4: return dress_impl<4>(s, gen_row, cs, sn, drop, want_hist, eps);
+    case 1: return dress_impl<1>(s, gen_row, cs, sn, drop, want_hist, eps, next_row);
+    case 2: return dress_impl<2>(s, gen_row, cs, sn, drop, want_hist, eps, next_row);
+    case 4: return dress_impl<4>(s, gen_row, cs, sn, drop, want_hist, eps, next_row);
     default: throw std::runtime_error("dress: unsupported block count");
   }
 }

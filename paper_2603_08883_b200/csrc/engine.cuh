@@ -373,12 +373,22 @@ struct DeviceStore {
   Filter filt;         // lazy compress filter (see filter_keep)
   size_t logical = 0;  // terms that pass filt
   bool has_identity = false;
+  // Next-step metadata written by the previous merge of a dress_sequence:
+  // LCP of every slot with its predecessor and the anticommute bits against
+  // the next entangler meta_P (device key words); replaces that step's
+  // classify pass.  Any other change of the slots clears meta_valid.
+  bool meta_valid = false;
+  ull meta_P[8] = {};
+  DevBuf meta_lcp, meta_amask;
   ull* keys() const { return static_cast<ull*>(kbuf.p); }
   double* coef() const { return static_cast<double*>(cbuf.p); }
   void ensure(size_t n);  // capacity >= n terms, contents NOT kept
   void free_all() {
     kbuf.release();
     cbuf.release();
+    meta_lcp.release();
+    meta_amask.release();
+    meta_valid = false;
   }
 };
 
@@ -401,8 +411,11 @@ struct DressOutcome {
 };
 /// One dressing step in place; if want_hist, also accumulates the |c|
 /// histogram of emitted terms for a following compress(eps).
+/// next_row (optional, device-width row): the entangler of the following
+/// step; the merge then also writes that step's classify metadata.
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cos_tau, double sin_tau,
-                        double drop_thr, bool want_hist, double eps);
+                        double drop_thr, bool want_hist, double eps,
+                        const uint64_t* next_row = nullptr);
 /// Phases of a step for the partitioned path: plan (classify, present
 /// prefix, product order; returns the product count A), materialize the
 /// sorted products (keys ^ P, values) into a buffer, and merge the store's

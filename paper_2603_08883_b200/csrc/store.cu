@@ -45,6 +45,7 @@ void DeviceStore::ensure(size_t n) {
   n = std::max<size_t>(n, 1);
   kbuf.get(n * 2 * B * sizeof(ull));
   cbuf.get(n * sizeof(double));
+  meta_valid = false;
 }
 
 // ------------------------------------------------------------------ upload
@@ -79,6 +80,7 @@ void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const d
   if (s.B > (uint32_t)kMaxB) throw std::invalid_argument("more than 256 qubits are not supported");
   s.ensure(M);
   s.M = M;
+  s.meta_valid = false;
   s.filt = Filter{};
   s.logical = M;
   s.has_identity = false;
@@ -219,6 +221,7 @@ void store_materialize(DeviceStore& s) {
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
   s.M = n;
+  s.meta_valid = false;
   s.logical = n;
   s.filt = Filter{};
 }
@@ -382,6 +385,7 @@ void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* 
   // the identity lives in the all-zero-key shard (partition.hpp:364-366)
   s.has_identity = s.has_identity && owner[0] == (size_t)rank;
   s.M = n;
+  s.meta_valid = false;
   s.logical = n;
   s.filt = Filter{};
 }
@@ -573,6 +577,7 @@ static void gen_impl(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
   IQCC_CUDA(cudaMemcpyAsync(&m, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
   host_sync(st);
   s.M = m;
+  s.meta_valid = false;
   s.logical = m;
   s.filt = Filter{};
   s.has_identity = true;  // term 0 of G_mol is the identity
