@@ -936,7 +936,7 @@ __device__ __forceinline__ void merge_flush(const MergeArgs& g, unsigned* shist,
 /// One tile per CTA (single input stage): the default; enough CTAs stay
 /// resident that load latency of one hides behind the merge of others.
 template <int B, int NT, int IPT>
-__global__ void __launch_bounds__(NT, IQCC_MERGE_MINB) k_merge1(MergeArgs g, Key<B> P) {
+__global__ void __launch_bounds__(NT, IQCC_MERGE_MINB * 256 / NT) k_merge1(MergeArgs g, Key<B> P) {
   using Cfg = MergeCfg<B, NT, IPT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST - Cfg::STAGE);
@@ -966,8 +966,11 @@ __global__ void __launch_bounds__(NT, IQCC_MERGE_MINB) k_merge1(MergeArgs g, Key
 /// Persistent merge: each CTA walks tiles blockIdx.x, +gridDim.x, ... with a
 /// two-stage pipeline: the next tile's TMA bulk copy and cp.async gathers
 /// are in flight while the current tile is merged and stored.
+#ifndef IQCC_PMERGE_MINB
+#define IQCC_PMERGE_MINB 4
+#endif
 template <int B, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_merge(MergeArgs g, Key<B> P) {
+__global__ void __launch_bounds__(NT, IQCC_PMERGE_MINB * 256 / NT) k_merge(MergeArgs g, Key<B> P) {
   using Cfg = MergeCfg<B, NT, IPT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
