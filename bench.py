@@ -231,13 +231,9 @@ def run_gpu_arm(args, rank, world, local_rank):
 
     def dress_step(store, s):
         ents = step_entanglers(N_QUBITS, s, flip)
-        if part:
-            tin = 0
-            for row, tau in ents:
-                tin += part.total_size(store)
-                part.dress(store, iqcc.PauliWord(N_QUBITS, row), tau, EPS, n_terms)
-            return tin
         ans = iqcc.Ansatz([iqcc.PauliWord(N_QUBITS, r) for r, _ in ents], [t for _, t in ents])
+        if part:
+            return part.dress_sequence(store, ans, EPS, n_terms)
         return store.dress_sequence(ans, EPS, n_terms)
 
     for w in range(args.warmup):

@@ -168,6 +168,17 @@ int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const
                             const uint64_t* gen, double cos_tau, double sin_tau, double eps,
                             size_t max_terms, iqcc_exchange_stats* xstats,
                             iqcc_compress_stats* cstats);
+/* dress_sequence (iqcc/dressing.hpp:311-324) over parallel_dress steps
+ * (partition.hpp:398-452): K entanglers gens[K][2B] with cos/sin of their
+ * angles, compress_partitioned(eps, max_terms) after each.  Keeps the
+ * store's classify metadata across steps (no per-step classify pass).
+ * xstats: NULL or K records; terms_in_total: NULL or the logical input
+ * size summed over the K steps and all ranks. */
+int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bits,
+                                     const size_t* owner, size_t K, const uint64_t* gens,
+                                     const double* cos_tau, const double* sin_tau, double eps,
+                                     size_t max_terms, iqcc_exchange_stats* xstats,
+                                     iqcc_compress_stats* cstats, size_t* terms_in_total);
 /* Partitioned energy: local expect + allreduce (parallel_expect, :241-254). */
 int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* energy);
 /* Total logical terms over all ranks. */

@@ -659,6 +659,31 @@ int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const
   });
 }
 
+int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bits,
+                                     const size_t* owner, size_t K, const uint64_t* gens,
+                                     const double* cos_tau, const double* sin_tau, double eps,
+                                     size_t max_terms, iqcc_exchange_stats* xs,
+                                     iqcc_compress_stats* cs, size_t* terms_in_total) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    if (max_terms < 1) throw std::invalid_argument("compress_partitioned: max_terms < 1");
+    for (size_t k = 0; k < K; ++k)
+      if (row_is_identity(gens + k * 2 * Bref, Bref))
+        throw std::invalid_argument("parallel_dress: identity generator");
+    size_t local_in = 0;
+    for (size_t k = 0; k < K; ++k) {
+      auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
+      std::vector<uint64_t> next;
+      if (k + 1 < K) next = widen_row(gens + (k + 1) * 2 * Bref, Bref, h->s.B);
+      local_in += h->s.logical;
+      parallel_dress_step(h->s, m, bits, owner, row.data(), cos_tau[k], sin_tau[k], eps, max_terms,
+                          xs ? xs + k : nullptr, cs, next.empty() ? nullptr : next.data());
+    }
+    if (terms_in_total) *terms_in_total = parallel_sum(local_in);
+  });
+}
+
 int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* energy) {
   return guarded([&] {
     need(h);

@@ -1050,11 +1050,12 @@ struct PlanState {
   unsigned* pmask = nullptr;
   unsigned* ppre = nullptr;
   unsigned* ptotal = nullptr;
+  const long long* a_dev = nullptr;  // device product count (nullptr: none)
 };
 PlanState g_plan;
 
 template <int B>
-void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
+void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = true) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   PlanState pl;
@@ -1196,6 +1197,11 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products) {
       }
     }
     if (getenv("IQCC_DEBUG")) debug_check("rank");
+    pl.a_dev = a_total;
+    if (!read_A) {  // the caller reads the count (with its own round trip)
+      g_plan = pl;
+      return;
+    }
     long long* a_host = static_cast<long long*>(host_pinned(sizeof(long long)));
     IQCC_CUDA(cudaMemcpyAsync(a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     host_sync(st);
@@ -1231,7 +1237,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   }
   ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
   double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   unsigned* hist = ws.hist.as<unsigned>(kHistBins);
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
   if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
@@ -1323,7 +1329,7 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
 #undef IQCC_MERGE
   Workspace& ws = workspace();
   cudaStream_t st = stream();
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   ull* hc = static_cast<ull*>(host_pinned(4 * sizeof(ull)));
   IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 4 * sizeof(ull), cudaMemcpyDeviceToHost, st));
   host_sync(st);
@@ -1371,6 +1377,17 @@ __global__ void k_materialize(const ull* __restrict__ keys, const double* __rest
 
 }  // namespace
 
+const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row) {
+  switch (s.B) {
+    case 1: plan_impl<1>(s, make_key<1>(gen_row), true, false); break;
+    case 2: plan_impl<2>(s, make_key<2>(gen_row), true, false); break;
+    default: plan_impl<4>(s, make_key<4>(gen_row), true, false); break;
+  }
+  return g_plan.a_dev;
+}
+
+void plan_set_products(size_t A) { g_plan.A = A; }
+
 size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products) {
   switch (s.B) {
     case 1: plan_impl<1>(s, make_key<1>(gen_row), products); break;
@@ -1394,13 +1411,23 @@ void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ul
   }
 }
 
+template <int B>
+DressOutcome merge_products_t(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
+                              double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
+                              const double* q_vals, const uint64_t* next_row) {
+  Key<B> PN;
+  if (next_row) PN = make_key<B>(next_row);
+  return merge_impl<B>(s, make_key<B>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps,
+                       next_row ? &PN : nullptr);
+}
+
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                            const double* q_vals) {
+                            const double* q_vals, const uint64_t* next_row) {
   switch (s.B) {
-    case 1: return merge_impl<1>(s, make_key<1>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps);
-    case 2: return merge_impl<2>(s, make_key<2>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps);
-    default: return merge_impl<4>(s, make_key<4>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps);
+    case 1: return merge_products_t<1>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row);
+    case 2: return merge_products_t<2>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row);
+    default: return merge_products_t<4>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row);
   }
 }
 
@@ -1438,7 +1465,7 @@ __global__ void k_growth(const ull* __restrict__ keys, size_t M, Filter filt,
 void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* na) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(ull), st));
   const unsigned grid = (unsigned)std::max<size_t>(1, (s.M + 255) / 256);
   {

@@ -422,11 +422,16 @@ DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cos_tau,
 /// survivors with products given as a buffer (q_keys != nullptr) or the
 /// planned local products.
 size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products);
+/// plan_products without reading the count back: returns its device
+/// address (nullptr: empty store); the caller then sets it with
+/// plan_set_products before materialize/merge.
+const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row);
+void plan_set_products(size_t A);
 void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
                           double* ovals);
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                            const double* q_vals);
+                            const double* q_vals, const uint64_t* next_row = nullptr);
 /// Selects the compress filter on a store without a filter.  If hist_ready,
 /// the histogram/count_eps of the last dress_step are used.
 /// Cross-rank hooks for compress_partitioned (iqcc/partition.hpp:325-396);

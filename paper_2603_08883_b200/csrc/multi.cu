@@ -58,10 +58,13 @@ struct NcclReducer : Reducer {
     Comm& c = comm();
     cudaStream_t st = stream();
     ull* d = workspace().partials.as<ull>(n);
-    IQCC_CUDA(cudaMemcpyAsync(d, vals, n * sizeof(ull), cudaMemcpyHostToDevice, st));
+    ull* hp = static_cast<ull*>(host_pinned(n * sizeof(ull)));
+    std::memcpy(hp, vals, n * sizeof(ull));
+    IQCC_CUDA(cudaMemcpyAsync(d, hp, n * sizeof(ull), cudaMemcpyHostToDevice, st));
     IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, c.comm, st));
-    IQCC_CUDA(cudaMemcpyAsync(vals, d, n * sizeof(ull), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
+    IQCC_CUDA(cudaMemcpyAsync(hp, d, n * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    host_sync(st);
+    std::memcpy(vals, hp, n * sizeof(ull));
   }
   void sum_device(ull* d, size_t n) override {
     IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, comm().comm, stream()));
@@ -88,7 +91,7 @@ struct NcclReducer : Reducer {
     IQCC_NCCL(ncclAllGather(dm, d, mx * W, ncclUint64, c.comm, st));
     std::vector<ull> padded((size_t)mx * W * c.world);
     IQCC_CUDA(cudaMemcpyAsync(padded.data(), d, padded.size() * sizeof(ull), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
+    host_sync(st);
     for (int r = 0; r < c.world; ++r)
       all.insert(all.end(), padded.begin() + (size_t)r * mx * W,
                  padded.begin() + (size_t)r * mx * W + counts[r] * W);
@@ -124,6 +127,23 @@ void multi_init(const void* uid128, int rank, int world) {
   IQCC_NCCL(ncclCommInitRank(&g_comm.comm, world, id, rank));
   g_comm.rank = rank;
   g_comm.world = world;
+  // NCCL connects point-to-point peers lazily on first use; touch every
+  // pair now so no connection setup lands inside a dressing sequence
+  if (world > 1) {
+    cudaStream_t st = stream();
+    ull* d = scratch(2 * (size_t)world);
+    IQCC_CUDA(cudaMemsetAsync(d, 0, 2 * (size_t)world * sizeof(ull), st));
+    IQCC_NCCL(ncclGroupStart());
+    for (int p = 0; p < world; ++p) {
+      if (p == rank) continue;
+      IQCC_NCCL(ncclSend(d + p, 1, ncclUint64, p, g_comm.comm, st));
+      IQCC_NCCL(ncclRecv(d + world + p, 1, ncclUint64, p, g_comm.comm, st));
+    }
+    IQCC_NCCL(ncclGroupEnd());
+    IQCC_NCCL(ncclAllReduce(d, d, 1, ncclUint64, ncclSum, g_comm.comm, st));
+    IQCC_NCCL(ncclAllGather(d + rank, d + world, 1, ncclUint64, g_comm.comm, st));
+    host_sync(st);
+  }
 }
 
 void multi_shutdown() {
@@ -135,7 +155,8 @@ void multi_shutdown() {
 
 void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner,
                          const uint64_t* gen_row, double cs, double sn, double eps,
-                         size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out) {
+                         size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out,
+                         const uint64_t* next_row) {
   Comm& c = comm();
   if (((size_t)1 << m) != (size_t)c.world)
     throw std::invalid_argument("parallel_dress: one partition per rank (2^m == world) required");
@@ -156,18 +177,19 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
   DressOutcome o;
   iqcc_exchange_stats x{mask, 0, 0, 0, 0};
   if (mask == 0 || sn == 0.0) {
-    o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps);
+    o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps, next_row);
   } else {
     cudaStream_t st = stream();
     Workspace& ws = workspace();
-    const size_t A = plan_products(s, gen_row, true);
-    const size_t W = 2 * s.B;
-    ull* sk = ws.xbuf_keys.as<ull>(std::max<size_t>(A, 1) * W);
-    double* sv = ws.xbuf_coef.as<double>(std::max<size_t>(A, 1));
-    materialize_products(s, gen_row, sn, sk, sv);
+    // plan, then swap the product counts with the partner straight from
+    // device memory: one round trip gives both A and the receive count
+    const long long* a_dev = plan_products_async(s, gen_row);
     const int peer = (int)owner[mine ^ mask];
     ull* cnt = scratch(4);
-    IQCC_CUDA(cudaMemcpyAsync(cnt, &A, sizeof(ull), cudaMemcpyHostToDevice, st));
+    if (a_dev)
+      IQCC_CUDA(cudaMemcpyAsync(cnt, a_dev, sizeof(ull), cudaMemcpyDeviceToDevice, st));
+    else
+      IQCC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(ull), st));
     {
       KernelScope ks("exchange");
       IQCC_NCCL(ncclGroupStart());
@@ -175,11 +197,21 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
       IQCC_NCCL(ncclRecv(cnt + 1, 1, ncclUint64, peer, c.comm, st));
       IQCC_NCCL(ncclGroupEnd());
     }
-    ull nrecv = 0;
-    IQCC_CUDA(cudaMemcpyAsync(&nrecv, cnt + 1, sizeof(ull), cudaMemcpyDeviceToHost, st));
-    IQCC_CUDA(cudaStreamSynchronize(st));
-    ull* rk = ws.rbuf_keys.as<ull>(std::max<size_t>(nrecv, 1) * W);
-    double* rv = ws.rbuf_coef.as<double>(std::max<size_t>(nrecv, 1));
+    ull* hp = static_cast<ull*>(host_pinned(2 * sizeof(ull)));
+    IQCC_CUDA(cudaMemcpyAsync(hp, cnt, 2 * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    host_sync(st);
+    const size_t A = hp[0];
+    const ull nrecv = hp[1];
+    plan_set_products(A);
+    const size_t W = 2 * s.B;
+    // exchange buffers sized by the shard (products <= terms), so they do
+    // not regrow from step to step
+    const size_t xcap = std::max<size_t>({A, nrecv, s.M, 1});
+    ull* sk = ws.xbuf_keys.as<ull>(xcap * W);
+    double* sv = ws.xbuf_coef.as<double>(xcap);
+    materialize_products(s, gen_row, sn, sk, sv);
+    ull* rk = ws.rbuf_keys.as<ull>(xcap * W);
+    double* rv = ws.rbuf_coef.as<double>(xcap);
     {
       KernelScope ks("exchange");
       IQCC_NCCL(ncclGroupStart());
@@ -197,13 +229,17 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     x.recv_terms = nrecv;
     x.bytes_wire = A * (W * 8 + 8);
     x.bytes_reference = A * (16 + Bref * 16);  // MessageLog formula, partition.hpp:420-422
-    o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv);
+    o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row);
   }
   if (xs) *xs = x;
-  ull tot[1] = {(ull)s.logical};
   NcclReducer red;
-  red.sum(tot, 1);
-  if (eps > 0.0 || tot[0] > max_terms) {
+  bool run = eps > 0.0;  // compress_partitioned always runs with a cut
+  if (!run) {
+    ull tot[1] = {(ull)s.logical};
+    red.sum(tot, 1);
+    run = tot[0] > max_terms;
+  }
+  if (run) {
     CompressResult r = compress_store(s, eps, max_terms, want_hist, o.count_eps, cs_out != nullptr, &red);
     if (cs_out) {
       cs_out->dropped_terms += r.dropped_terms;
@@ -221,10 +257,17 @@ double parallel_expect_store(DeviceStore& s, const double* factors) {
   IQCC_NCCL(ncclAllGather(d + c.world, d, 1, ncclFloat64, c.comm, st));
   std::vector<double> parts(c.world);
   IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, c.world * sizeof(double), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaStreamSynchronize(st));
+  host_sync(st);
   double e = 0.0;
   for (double v : parts) e += v;  // worker order (reduce_scalar)
   return e;
+}
+
+size_t parallel_sum(size_t v) {
+  ull a[1] = {(ull)v};
+  NcclReducer red;
+  red.sum(a, 1);
+  return (size_t)a[0];
 }
 
 size_t parallel_size(DeviceStore& s) {

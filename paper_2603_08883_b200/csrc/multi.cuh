@@ -9,7 +9,10 @@ void multi_init(const void* uid128, int rank, int world);
 void multi_shutdown();
 void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner,
                          const uint64_t* gen_row, double cs, double sn, double eps,
-                         size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out);
+                         size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out,
+                         const uint64_t* next_row = nullptr);
+/// Sum of a host value over the ranks (one allreduce).
+size_t parallel_sum(size_t v);
 double parallel_expect_store(DeviceStore& s, const double* factors);
 size_t parallel_size(DeviceStore& s);
 }  // namespace iqcc_b200

@@ -100,7 +100,7 @@ void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const d
                                 2 * Bref * sizeof(ull), Bref * sizeof(ull), M, kind, st));
   }
   IQCC_CUDA(cudaMemcpyAsync(d_coef, coeff, 2 * M * sizeof(double), kind, st));
-  ull* err = ws.counters.as<ull>(8);
+  ull* err = ws.counters.as<ull>(16);
   ull init[2] = {ULLONG_MAX, ULLONG_MAX};
   IQCC_CUDA(cudaMemcpyAsync(err, init, sizeof(init), cudaMemcpyHostToDevice, st));
   const unsigned grid = (unsigned)((M + 255) / 256);
@@ -194,7 +194,7 @@ static size_t run_compact(DeviceStore& s, int mode, uint32_t Bout, ull* okeys, d
   cudaStream_t st = stream();
   const size_t ntiles = std::max<size_t>(1, (s.M + CTILE - 1) / CTILE);
   ull* tstat = ws.tile_status.as<ull>(ntiles + 1);
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntiles + 1) * sizeof(ull), st));
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
   unsigned* tc = reinterpret_cast<unsigned*>(ctr + 4);
@@ -365,7 +365,7 @@ void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* 
   double* oc = ws.out_coef.as<double>(std::max<size_t>(s.M, 1));
   const size_t ntiles = std::max<size_t>(1, (s.M + CTILE - 1) / CTILE);
   ull* tstat = ws.tile_status.as<ull>(ntiles + 1);
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntiles + 1) * sizeof(ull), st));
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
   unsigned* tc = reinterpret_cast<unsigned*>(ctr + 4);
@@ -565,7 +565,7 @@ static void gen_impl(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
   s.ensure(N);
   const size_t ntiles = (N + CTILE - 1) / CTILE;
   ull* tstat = ws.tile_status.as<ull>(ntiles + 1);
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   IQCC_CUDA(cudaMemsetAsync(tstat, 0, (ntiles + 1) * sizeof(ull), st));
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
   {
@@ -921,7 +921,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
   CompressResult res;
   const size_t logical_before = s.logical;
   unsigned* hist = ws.hist.as<unsigned>(kHistBins);
-  ull* ctr = ws.counters.as<ull>(8);
+  ull* ctr = ws.counters.as<ull>(16);
   if (!hist_ready) {
     IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
     IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
@@ -1008,20 +1008,34 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
       ull* ties = ai[cur];  // A_rounds: every bit fixed -> exactly the ties
-      SelState* hsp = static_cast<SelState*>(host_pinned(sizeof(SelState) + sizeof(ull)));
+      // local and global tie counts come back with the select state
+      ull* gtie = ctr + 12;
+      if (red) {
+        IQCC_CUDA(cudaMemcpyAsync(gtie, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToDevice, st));
+        red->sum_device(gtie, 1);
+      }
+      // the first kTieSpec tied indices travel speculatively in the same copy
+      constexpr size_t kTieSpec = 64;
+      const size_t spec = std::min(kTieSpec, ncap8);
+      SelState* hsp = static_cast<SelState*>(host_pinned(sizeof(SelState) + (2 + kTieSpec) * sizeof(ull)));
       ull* ntp = reinterpret_cast<ull*>(hsp + 1);
       IQCC_CUDA(cudaMemcpyAsync(hsp, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
       IQCC_CUDA(cudaMemcpyAsync(ntp, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      if (red) IQCC_CUDA(cudaMemcpyAsync(ntp + 1, gtie, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaMemcpyAsync(ntp + 2, ties, spec * sizeof(ull), cudaMemcpyDeviceToHost, st));
       host_sync(st);
       SelState hs = *hsp;
-      const ull ntie = *ntp;
+      const ull ntie = ntp[0];
+      const ull ntie_global = red ? ntp[1] : ntie;
       if (hs.fail) throw std::runtime_error("compress: device select failed");
       hs.ntie = ntie;
       const ull vbits = hs.known_val;  // exact threshold value; hs.r ties at it are kept (globally)
       size_t r = hs.r;
       size_t local_above = hs.local_above;
       std::vector<ull> th(hs.ntie);
-      if (hs.ntie) {
+      if (hs.ntie <= spec) {
+        std::copy(ntp + 2, ntp + 2 + hs.ntie, th.begin());
+      } else {
         ull* tp = static_cast<ull*>(host_pinned(hs.ntie * sizeof(ull)));
         IQCC_CUDA(cudaMemcpyAsync(tp, ties, hs.ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
         host_sync(st);
@@ -1031,7 +1045,10 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         fprintf(stderr, "[compress] M=%zu ncap=%zu ntie=%llu r=%zu above=%llu\n", s.M, ncap,
                 (unsigned long long)hs.ntie, r, (unsigned long long)local_above);
       size_t keep_ties = r;
-      if (red) {
+      if (red && ntie_global == r) {
+        keep_ties = th.size();  // every tied word is kept: no canonical order needed
+        std::sort(th.begin(), th.end());
+      } else if (red) {
         // canonical tie-break across shards (partition.hpp:350-361): the
         // globally first r tied words are kept; local index order is
         // canonical order

@@ -566,6 +566,33 @@ class Partition:
             stats.dropped_weight += cs.dropped_weight
         return xs
 
+    def dress_sequence(self, d: DeviceSum, ansatz: Ansatz, eps: float, max_terms: int = U64_MAX,
+                       stats: CompressStats | None = None, exchange: list | None = None) -> int:
+        """dress_sequence over parallel_dress steps; returns the logical input
+        size summed over the steps and all ranks.  `exchange` (optional list)
+        receives one ExchangeStats per entangler."""
+        K = ansatz.size()
+        b = np.array(self.bits or [0], np.uintp)
+        o = np.array(self.owner, np.uintp)
+        W = 2 * blocks_for(self.n_qubits)
+        gens = np.zeros((max(K, 1), W), np.uint64)
+        for k, p in enumerate(ansatz.entanglers):
+            gens[k] = p.row
+        cs_ = np.array([math.cos(t) for t in ansatz.tau] or [1.0])
+        sn_ = np.array([math.sin(t) for t in ansatz.tau] or [0.0])
+        xs = (native.ExchangeStats * max(K, 1))()
+        cst = native.CompressStatsC()
+        tin = C.c_size_t(0)
+        check(lib.iqcc_gpu_parallel_dress_sequence(d.handle, self.m, _addr(b), _addr(o), K, _addr(gens),
+                                                   _addr(cs_), _addr(sn_), eps, max_terms, xs, C.byref(cst),
+                                                   C.byref(tin)))
+        if stats is not None:
+            stats.dropped_terms += cst.dropped_terms
+            stats.dropped_weight += cst.dropped_weight
+        if exchange is not None:
+            exchange.extend(xs[k] for k in range(K))
+        return tin.value
+
     def total_size(self, d: DeviceSum) -> int:
         n = C.c_size_t()
         check(lib.iqcc_gpu_parallel_size(d.handle, C.byref(n)))

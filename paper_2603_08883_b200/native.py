@@ -81,6 +81,9 @@ _SIGS = {
     "iqcc_gpu_parallel_dress": (C.c_int, [_vp, C.c_size_t, _szp, _szp, _u64p, C.c_double, C.c_double,
                                           C.c_double, C.c_size_t, C.POINTER(ExchangeStats),
                                           C.POINTER(CompressStatsC)]),
+    "iqcc_gpu_parallel_dress_sequence": (C.c_int, [_vp, C.c_size_t, _szp, _szp, C.c_size_t, _u64p, _f64p,
+                                                   _f64p, C.c_double, C.c_size_t, C.POINTER(ExchangeStats),
+                                                   C.POINTER(CompressStatsC), C.POINTER(C.c_size_t)]),
     "iqcc_gpu_parallel_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
     "iqcc_gpu_parallel_size": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),
 }

@@ -20,6 +20,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 def main():
     n, N, steps = int(sys.argv[1]), int(float(sys.argv[2])), int(sys.argv[3])
     eps, cap = float(sys.argv[4]), int(float(sys.argv[5]))
+    seq = len(sys.argv) > 6 and sys.argv[6] == "seq"  # one parallel dress_sequence call
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -51,10 +52,17 @@ def main():
             if y:
                 p.row[B + q // 64] |= np.uint64(1 << (q % 64))
         tau = float(rs.uniform(-0.2, 0.2))
-        xs = part.dress(d, p, tau, eps, cap)
-        exch += xs.sent_terms
+        if not seq:
+            xs = part.dress(d, p, tau, eps, cap)
+            exch += xs.sent_terms
         gens.append(p.row.copy())
         taus.append(tau)
+    if seq:
+        xl = []
+        ans = iqcc.Ansatz([iqcc.PauliWord(n, g) for g in gens], taus)
+        tin = part.dress_sequence(d, ans, eps, cap, exchange=xl)
+        exch = sum(x.sent_terms for x in xl)
+        assert tin > 0
     shard = d.download()
     th = np.where(np.arange(n) < n // 3, np.pi, 0.0)
     ph = np.zeros(n)

@@ -18,7 +18,8 @@ def n_gpus():
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("args", [("124", "2e5", "6", "1e-10", "2e5"), ("64", "1e5", "5", "0", "1e18")])
+@pytest.mark.parametrize("args", [("124", "2e5", "6", "1e-10", "2e5"), ("64", "1e5", "5", "0", "1e18"),
+                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq")])
 def test_partitioned_dressing_matches_serial(world, args):
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
