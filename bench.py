@@ -149,11 +149,12 @@ def measured_peaks():
 
 
 def profile_traffic():
-    """Per-launch DRAM bytes of the merge kernel from the committed ncu capture."""
+    """DRAM bytes (read + write) per merge launch from the committed
+    `ncu --set full` capture at this workload (profiles/merge_traffic.json)."""
     path = os.path.join(ROOT, "profiles", "merge_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            return float(json.load(f)["dram_bytes_per_launch"])
     except Exception:
         return None
 

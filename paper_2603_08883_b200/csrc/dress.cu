@@ -1300,7 +1300,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
   }
   if (PN) {
-    KernelScope ks("merge");
+    KernelScope ks("meta_fix");
     k_meta_fix<B><<<(unsigned)((ntm + 255) / 256), 256, 0, st>>>(out_keys, po, ntm, g.out_lcp);
   }
   IQCC_CUDA(cudaMemcpyAsync(ctr + 3, po + ntm, sizeof(ull), cudaMemcpyDeviceToDevice, st));
