@@ -264,7 +264,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     merge_ms, merge_n = native.profile_get("merge")
     fam = {f: native.profile_get(f)[0] for f in
            ["classify", "present", "tile_agg", "carry", "rank", "partition", "merge",
-            "select_gather", "select_digits", "exchange", "host_wait", "host_dress", "host_compress", "span_dress", "span_compress", "host_alloc", "host_compress_inner"]}
+            "select_gather", "select_digits", "exchange", "host_wait", "host_dress", "host_compress", "span_dress", "span_compress", "host_alloc", "host_compress_inner", "spec_redo"]}
     native.profile(False)
     if dist:
         t = torch.tensor([ms], device="cuda")

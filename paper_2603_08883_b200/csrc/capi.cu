@@ -516,6 +516,20 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
         throw std::invalid_argument("dress_single: identity generator");
     if (terms_in_total) *terms_in_total = 0;
     const bool fuse = getenv("IQCC_NO_META") == nullptr;  // A/B switch for the fused classify
+    // Output slots only for terms the following compress can keep (SlotRule,
+    // dress.cu): theta = eps is exact; theta = a power of two at least one
+    // binade under the previous cut is speculated and verified after the
+    // merge (more than max_terms terms at or above it), else the step is
+    // undone and redone with theta = eps.  Off when drop statistics are
+    // requested (they count every dropped term).
+    const bool slots = stats == nullptr && getenv("IQCC_NO_SPEC") == nullptr;
+    auto spec_theta = [&](const Filter& f) {
+      if (!slots || !f.active || !f.has_v || !(f.v > 0.0) || !std::isfinite(f.v)) return 0.0;
+      return f.v;  // scaled by the next step's |cos| below
+    };
+    const char* sc_env = getenv("IQCC_SPEC_SCALE");  // test hook: force bad guesses
+    const double spec_scale = sc_env ? std::atof(sc_env) : 1.0;
+    double spec = slots ? h->s.spec_cut : 0.0;
     for (size_t k = 0; k < K; ++k) {
       auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
       std::vector<uint64_t> next;
@@ -524,8 +538,32 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
       const auto t0 = std::chrono::steady_clock::now();
       KernelScope* outer = new KernelScope("span_dress");
+      const double exact = slots && eps > 0.0 ? eps : 0.0;
+      // the previous cut, shrunk by what an anticommuting survivor loses (|cos|)
+      const double guess = spec * std::min(1.0, std::fabs(cos_tau[k])) * 0.999 * spec_scale;
+      const double theta = maybe && guess > eps && max_terms != SIZE_MAX ? guess : exact;
+      const size_t M0 = h->s.M, L0 = h->s.logical;
+      const Filter F0 = h->s.filt;
       DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps,
-                                  next.empty() ? nullptr : next.data());
+                                  next.empty() ? nullptr : next.data(), theta);
+      if (getenv("IQCC_VERBOSE"))
+        fprintf(stderr, "[dress] k=%zu theta=%.3e exact=%.3e n_ge=%zu slots=%zu\n", k, theta, exact,
+                o.n_ge_theta, h->s.M);
+      // the slotted sum compresses like the full one iff the top `budget`
+      // terms are all >= theta and either the compress cuts or nothing below
+      // theta holds a slot
+      const size_t idc = h->s.has_identity ? 1 : 0;
+      const size_t budget = max_terms - idc;
+      const bool spec_ok = o.n_ge_theta >= budget &&
+                           (o.count_eps > max_terms || o.count_eps == o.n_ge_theta + idc);
+      if (theta > exact && !spec_ok) {  // speculation failed: redo exactly
+        dress_undo(h->s, M0, L0, F0);
+        host_ms("spec_redo", std::chrono::steady_clock::now());
+        o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps,
+                       next.empty() ? nullptr : next.data(), exact);
+        spec = 0.0;  // relearn from the next cut
+        h->s.spec_cut = 0.0;
+      }
       delete outer;
       host_ms("host_dress", t0);
       if (eps > 0.0 || h->s.logical > max_terms) {
@@ -533,6 +571,10 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
         KernelScope* outer2 = new KernelScope("span_compress");
         CompressResult r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr);
         delete outer2;
+        // a compress that cut sets the next guess; one that did not (every
+        // slotted term kept) leaves the last verified guess in place
+        const double sv = spec_theta(h->s.filt);
+        if (sv > 0.0) spec = h->s.spec_cut = sv;
         host_ms("host_compress", t1);
         if (stats) {
           stats->dropped_terms += r.dropped_terms;

@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <climits>
+#include <cstring>
 #include <stdexcept>
 
 #include "engine.cuh"
@@ -63,12 +64,45 @@ struct Thr {
 #ifndef IQCC_RANK_MINB
 #define IQCC_RANK_MINB 4
 #endif
+// Output slots.  Every present survivor and every product owns an output
+// slot ("pmask" / "qmask" bits) unless a compress whose cut is at least theta
+// follows the step (theta = eps: known; theta just under the previous cut:
+// speculated, verified after the merge by counting the slotted terms with
+// |c| >= theta) and its value cannot reach theta:
+//  * a commuting survivor keeps its value c and never meets a product (the
+//    partner of a product T^P anticommutes with P like T): slot iff |c| >= thc;
+//  * an anticommuting survivor always keeps its slot (ths = 0), so a partner
+//    pair's sum always has a slot;
+//  * a product without a partner keeps fl(c*sin): slot iff |c*sin| >= thq.
+// With thc = thq = theta every term of the dressed sum with |c| >= theta has a
+// slot; terms without one are below theta.  theta = 0: every term has a slot.
+struct SlotRule {
+  double cs, sn;
+  double thc, ths, thq;  // commuting survivor / anticommuting survivor / product
+};
+
+__host__ __device__ inline SlotRule make_slot_rule(double cs, double sn, double theta) {
+  return SlotRule{cs, sn, theta, 0.0, theta};
+}
+
+__device__ __forceinline__ bool survivor_slot(const SlotRule& r, bool present, bool id, bool anti,
+                                              double c) {
+  if (!present) return false;
+  if (id) return true;
+  return anti ? (r.ths == 0.0 || fabs(__dmul_rn(c, r.cs)) >= r.ths) : fabs(c) >= r.thc;
+}
+__device__ __forceinline__ bool product_slot(const SlotRule& r, bool anti_present, double c) {
+  if (!anti_present) return false;
+  return r.thq == 0.0 || fabs(__dmul_rn(c, r.sn)) >= r.thq;
+}
+
 template <int B, int IT>
 __global__ void __launch_bounds__(256, IQCC_CLS_MINB) k_classify(const ull* __restrict__ keys,
                                                   const double* __restrict__ coef, Filter filt,
                                                   size_t M, Key<B> P, short* __restrict__ lcp,
                                                   unsigned* __restrict__ fmask,
-                                                  unsigned* __restrict__ pmask) {
+                                                  unsigned* __restrict__ pmask, SlotRule rule,
+                                                  unsigned* __restrict__ qmask) {
   const int lane = threadIdx.x & 31;
   const size_t base = blockIdx.x * (size_t)(256 * IT);
   Key<B> k[IT], pk[IT];
@@ -90,20 +124,25 @@ __global__ void __launch_bounds__(256, IQCC_CLS_MINB) k_classify(const ull* __re
       const ull up = __shfl_up_sync(0xffffffffu, k[j].w[w], 1);
       if (lane > 0) pk[j].w[w] = up;
     }
-    int f = 0, pr = 0;
+    bool f = false, sl = false, qs = false;
     if (i < M) {
       lcp[i] = (short)(i > 0 ? key_lcp<B>(pk[j], k[j]) : -1);
       // dead slots and terms dropped by a pending compress filter are absent:
       // they emit nothing and generate no product
-      pr = filter_keep(filt, i, c[j], i == 0 && key_is_identity<B>(k[j]));
+      const bool id = i == 0 && key_is_identity<B>(k[j]);
+      const bool pr = filter_keep(filt, i, c[j], id);
       f = pr && anticommutes<B>(k[j], P);
+      sl = survivor_slot(rule, pr, id, f, c[j]);
+      qs = product_slot(rule, f, c[j]);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, f);
-    const unsigned pal = __ballot_sync(0xffffffffu, pr);
+    const unsigned pal = __ballot_sync(0xffffffffu, sl);
+    const unsigned qal = __ballot_sync(0xffffffffu, qs);
     const size_t i0 = i - lane;
     if (lane == 0 && i0 < M) {
       fmask[i0 >> 5] = bal;
       pmask[i0 >> 5] = pal;
+      qmask[i0 >> 5] = qal;
     }
   }
 }
@@ -327,12 +366,14 @@ struct MaskArgs {
   const ull* keys;
   int W;  // key words (identity check of slot 0)
   Filter filt;
-  unsigned* fmask;  // out
-  unsigned* pmask;  // out
+  SlotRule rule;
+  unsigned* fmask;  // out: present and anticommuting
+  unsigned* pmask;  // out: survivor owns an output slot
+  unsigned* qmask;  // out: its product owns an output slot
 };
 
 __device__ __forceinline__ unsigned lane_masks(const MaskArgs& ma, size_t M, size_t first, int lane) {
-  unsigned pb = 0, fb = 0;
+  unsigned pb = 0, fb = 0, qb = 0;
   if (first < M) {
     const unsigned aw = (ma.amask[first >> 5] >> (first & 31)) & ((1u << WI) - 1u);
     bool id0 = false;
@@ -344,24 +385,30 @@ __device__ __forceinline__ unsigned lane_masks(const MaskArgs& ma, size_t M, siz
     for (int k = 0; k < WI; ++k) {
       const size_t i = first + k;
       if (i < M) {
-        const bool pr = filter_keep(ma.filt, i, __ldg(ma.coef + i), k == 0 && id0);
-        pb |= (unsigned)pr << k;
-        fb |= (unsigned)(pr && ((aw >> k) & 1u)) << k;
+        const double c = __ldg(ma.coef + i);
+        const bool id = k == 0 && id0;
+        const bool pr = filter_keep(ma.filt, i, c, id);
+        const bool an = pr && ((aw >> k) & 1u);
+        pb |= (unsigned)survivor_slot(ma.rule, pr, id, an, c) << k;
+        fb |= (unsigned)an << k;
+        qb |= (unsigned)product_slot(ma.rule, an, c) << k;
       }
     }
   }
   // lanes 4j..4j+3 (WI = 8) share one 32-bit mask word
   constexpr int LPW = 32 / WI;
   const int sh = WI * (lane % LPW);
-  unsigned xp = pb << sh, xf = fb << sh;
+  unsigned xp = pb << sh, xf = fb << sh, xq = qb << sh;
 #pragma unroll
   for (int o = 1; o < LPW; o <<= 1) {
     xp |= __shfl_xor_sync(0xffffffffu, xp, o);
     xf |= __shfl_xor_sync(0xffffffffu, xf, o);
+    xq |= __shfl_xor_sync(0xffffffffu, xq, o);
   }
   if (lane % LPW == 0 && first < M) {
     ma.pmask[first >> 5] = xp;
     ma.fmask[first >> 5] = xf;
+    ma.qmask[first >> 5] = xq;
   }
   return fb;
 }
@@ -427,7 +474,9 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
                                                 int* __restrict__ rdelta, int has_rdelta,
                                                 unsigned* __restrict__ inv_perm,
                                                 const long long* __restrict__ a_total,
-                                                ull* __restrict__ dbg) {
+                                                ull* __restrict__ dbg,
+                                                const unsigned* __restrict__ qmask,
+                                                unsigned char* __restrict__ qflag) {
   const size_t wt = blockIdx.x * (size_t)8 + (threadIdx.x >> 5);
   if (wt >= ntiles) return;
   const int lane = threadIdx.x & 31;
@@ -497,16 +546,31 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
       if (it.l[k] <= thr.t[j]) st[j] = C[k];
   }
 #pragma unroll
+  const unsigned qm = FINAL && qflag && first < M ? (qmask[first >> 5] >> (first & 31)) : 0u;
   for (int k = 0; k < WI; ++k) {
     if (!((it.bits >> k) & 1u)) continue;
     const size_t g = first + k;
     const int d = delta[k] + (has_rdelta ? rdelta[g] : 0);
     if (FINAL) {
-      if (dbg_ok(dbg, 1, (ull)(long long)(C[k] + d), (ull)*a_total)) inv_perm[C[k] + d] = (unsigned)g;
+      if (dbg_ok(dbg, 1, (ull)(long long)(C[k] + d), (ull)*a_total)) {
+        inv_perm[C[k] + d] = (unsigned)g;
+        if (qflag) qflag[C[k] + d] = (unsigned char)((qm >> k) & 1u);
+      }
     } else {
       rdelta[g] = d;
     }
   }
+}
+
+/// Product slot flags (one byte per product, rank order) -> bit words.
+__global__ void k_pack_flags(const unsigned char* __restrict__ flag, size_t A,
+                             unsigned* __restrict__ bits) {
+  const size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (w * 32 >= A) return;
+  unsigned x = 0;
+  const size_t n = min((size_t)32, A - w * 32);
+  for (size_t k = 0; k < n; ++k) x |= (unsigned)(flag[w * 32 + k] & 1u) << k;
+  bits[w] = x;
 }
 
 // Debug: inv_perm must be a bijection onto the present anticommuting terms.
@@ -542,7 +606,9 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
                             ull* __restrict__ part_a, ull* __restrict__ part_b,
                             ull* __restrict__ part_o, const unsigned* __restrict__ pmask,
                             const unsigned* __restrict__ ppre, size_t W,
-                            const unsigned* __restrict__ ptotal) {
+                            const unsigned* __restrict__ ptotal, const unsigned* __restrict__ qbits,
+                            const unsigned* __restrict__ qpre, size_t Wq,
+                            const unsigned* __restrict__ qtotal) {
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t > ntiles) return;
   const size_t d = min(t * tile_items, nS + nQ);
@@ -562,9 +628,10 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
   }
   part_a[t] = a;
   part_b[t] = b;
-  // output slots before this tile: every present survivor and every product
-  // owns exactly one slot (live or dead)
-  part_o[t] = present_before(pmask, ppre, W, *ptotal, a) + b;
+  // output slots before this tile: survivors and products that own a slot
+  // (see SlotRule; with theta = 0 every present survivor and every product)
+  part_o[t] = present_before(pmask, ppre, W, *ptotal, a) +
+              (qbits ? present_before(qbits, qpre, Wq, *qtotal, b) : b);
 }
 
 template <int B>
@@ -635,8 +702,11 @@ struct MergeCfg {
   static constexpr size_t OFF_TA = (OFF_OUTE + (size_t)CAP * 2 + 15) & ~(size_t)15;
   static constexpr size_t OFF_PM = OFF_TA + (size_t)2 * NT * 4;  // present bits of S
   static constexpr int PMW = (CAP + 31) / 32;
-  static constexpr size_t OFF_PP = OFF_PM + (size_t)PMW * 4;     // their prefix
-  static constexpr size_t OFF_HIST = (OFF_PP + (size_t)PMW * 4 + 15) & ~(size_t)15;
+  static constexpr size_t OFF_SM = OFF_PM + (size_t)PMW * 4;     // slot bits of S
+  static constexpr size_t OFF_PP = OFF_SM + (size_t)PMW * 4;     // their prefix
+  static constexpr size_t OFF_QM = OFF_PP + (size_t)PMW * 4;     // slot bits of Q
+  static constexpr size_t OFF_QP = OFF_QM + (size_t)PMW * 4;     // their prefix
+  static constexpr size_t OFF_HIST = (OFF_QP + (size_t)PMW * 4 + 15) & ~(size_t)15;
   static constexpr int HBINS = kHistBins;  // |c| histogram (u32, per CTA) for compress
   static constexpr size_t bytes(bool hist, int stages) {
     return OFF_HIST - (2 - stages) * STAGE + (hist ? HBINS * 4 : 0);
@@ -679,6 +749,9 @@ struct MergeArgs {
   short* out_lcp;
   unsigned* out_amask;
   ull pn[8];
+  SlotRule rule;
+  const unsigned* qbits;  // product slot bits in product order (nullptr: all)
+  double theta;           // count emitted non-identity |c| >= theta (0: off)
 };
 
 /// Issue the loads of one tile into one stage: survivors by the TMA bulk
@@ -728,14 +801,17 @@ __device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull
 template <int B, int NT, int IPT>
 __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, const Key<B>& P,
                                               ull* sk, double* sc, unsigned char* smem_raw,
-                                              int& n_eps, int& n_dead) {
+                                              int& n_eps, int& n_dead, int& n_coll, int& n_ge) {
   using Cfg = MergeCfg<B, NT, IPT>;
   double* outv = reinterpret_cast<double*>(smem_raw + Cfg::OFF_OUTV);
   unsigned short* oute = reinterpret_cast<unsigned short*>(smem_raw + Cfg::OFF_OUTE);
   int* s_ta = reinterpret_cast<int*>(smem_raw + Cfg::OFF_TA);
   int* s_tb = s_ta + NT;
   unsigned* spm = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PM);
+  unsigned* ssm = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_SM);
   unsigned* spp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PP);
+  unsigned* sqm = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_QM);
+  unsigned* sqp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_QP);
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
   const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
   const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
@@ -745,18 +821,37 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   const int coff = (int)(a0 & 1);
   const int qc0 = nS + 4;
 
-  // present bits of the survivors (dead slots / compress-filtered are absent)
+  // present bits of the survivors (dead slots / compress-filtered are
+  // absent) and their slot bits (SlotRule); slot bits of the products
   {
     const int lane = threadIdx.x & 31;
     for (int e0 = (threadIdx.x & ~31); e0 < nS; e0 += NT) {
       const int e = e0 + lane;
-      bool pr = false;
-      if (e < nS)
-        pr = filter_keep(g.filt, a0 + e, sc[coff + e],
-                         a0 + e == 0 && key_is_identity<B>(sm_key16<B>(sk, e)));
+      bool pr = false, sl = false;
+      if (e < nS) {
+        const Key<B> ks = sm_key16<B>(sk, e);
+        const double c = sc[coff + e];
+        const bool id = a0 + e == 0 && key_is_identity<B>(ks);
+        pr = filter_keep(g.filt, a0 + e, c, id);
+        sl = survivor_slot(g.rule, pr, id, pr && g.rule.thc != 0.0 && anticommutes<B>(ks, P), c);
+      }
       const unsigned word = __ballot_sync(0xffffffffu, pr);
-      if (lane == 0) spm[e0 >> 5] = word;
+      const unsigned sword = __ballot_sync(0xffffffffu, sl);
+      if (lane == 0) {
+        spm[e0 >> 5] = word;
+        ssm[e0 >> 5] = sword;
+      }
     }
+    if (g.qbits)
+      for (int w = threadIdx.x; w < (nQ + 31) >> 5; w += NT) {
+        const size_t gb = b0 + (size_t)w * 32;
+        const unsigned sh = (unsigned)(gb & 31);
+        unsigned x = g.qbits[gb >> 5] >> sh;
+        if (sh) x |= g.qbits[(gb >> 5) + 1] << (32 - sh);
+        const int rem = nQ - w * 32;
+        if (rem < 32) x &= (1u << rem) - 1u;
+        sqm[w] = x;
+      }
   }
   // local products stay raw in shared memory (key = row ^ P on the fly);
   // received products arrive as final keys and values
@@ -788,15 +883,21 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
     s_tb[threadIdx.x] = b;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive prefix of the present-bit words
-    const int nw = (nS + 31) >> 5;
-    unsigned carry = 0;
-    for (int w0 = 0; w0 < nw; w0 += 32) {
-      const int w = w0 + threadIdx.x;
-      const unsigned c = w < nw ? __popc(spm[w]) : 0u;
-      const unsigned inc = warp_inclusive(c, OpAdd());
-      if (w < nw) spp[w] = carry + inc - c;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
+  if (threadIdx.x < 64) {  // exclusive prefixes of the slot-bit words (warp 0: S, warp 1: Q)
+    const bool isq = threadIdx.x >= 32;
+    if (!isq || g.qbits) {
+      const unsigned* m = isq ? sqm : ssm;
+      unsigned* pf = isq ? sqp : spp;
+      const int nw = ((isq ? nQ : nS) + 31) >> 5;
+      const int lane = threadIdx.x & 31;
+      unsigned carry = 0;
+      for (int w0 = 0; w0 < nw; w0 += 32) {
+        const int w = w0 + lane;
+        const unsigned c = w < nw ? __popc(m[w]) : 0u;
+        const unsigned inc = warp_inclusive(c, OpAdd());
+        if (w < nw) pf[w] = carry + inc - c;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
     }
   }
   __syncthreads();
@@ -804,14 +905,16 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   const int ia1 = threadIdx.x + 1 < NT ? s_ta[threadIdx.x + 1] : nS;
   const int ib1 = threadIdx.x + 1 < NT ? s_tb[threadIdx.x + 1] : nQ;
   auto present = [&](int e) { return (spm[e >> 5] >> (e & 31)) & 1u; };
-  int slot = 0;
-  if (nS > 0) {
-    const int x = min(ia0, nS);
-    const int w = min(x, nS - 1) >> 5;
-    const unsigned m = x >= nS ? (0xffffffffu >> (31 - ((nS - 1) & 31))) : ((1u << (x & 31)) - 1u);
-    slot = (int)(spp[w] + __popc(spm[w] & m));
-  }
-  slot += ib0;
+  auto sslot = [&](int e) { return (ssm[e >> 5] >> (e & 31)) & 1u; };
+  auto qslot = [&](int j) { return g.qbits ? (sqm[j >> 5] >> (j & 31)) & 1u : 1u; };
+  // slots before a position in a (prefixed) bit list of n entries
+  auto before = [&](const unsigned* m, const unsigned* pf, int n, int x) -> int {
+    if (n <= 0) return 0;
+    const int w = min(x, n - 1) >> 5;
+    const unsigned msk = x >= n ? (0xffffffffu >> (31 - ((n - 1) & 31))) : ((1u << (x & 31)) - 1u);
+    return (int)(pf[w] + __popc(m[w] & msk));
+  };
+  int slot = before(ssm, spp, nS, ia0) + (g.qbits ? before(sqm, sqp, nQ, ib0) : ib0);
 
   // single walk; every slot value goes straight to the staging list
   {
@@ -831,6 +934,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
       const int c = j >= ib1 ? -1 : (i >= ia1 ? 1 : key_cmp<B>(ks, kq));
       if (c <= 0) {
         const bool pres = present(i);
+        const bool sl = sslot(i);
         const bool id = a0 + i == 0 && key_is_identity<B>(ks);
         double v = 0.0;
         if (pres) {
@@ -839,17 +943,25 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
         }
         if (c == 0) {
           const double qv = qval(j, kq);
+          const bool qs = qslot(j);
           if (pres) {
+            ++n_coll;
+            // the sum goes to the survivor's slot, else to the product's;
+            // without either slot |sum| < theta (SlotRule)
             const double sum = __dadd_rn(v, qv);
-            put(keep_term(sum, id, g.drop) ? sum : dead_value(), i);
-            put(dead_value(), nS + j);  // the product's slot
-          } else {
+            if (sl) {
+              put(keep_term(sum, id, g.drop) ? sum : dead_value(), i);
+              if (qs) put(dead_value(), nS + j);  // the product's slot
+            } else if (qs) {
+              put(keep_term(sum, id, g.drop) ? sum : dead_value(), nS + j);
+            }
+          } else if (qs) {
             put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
           }
-        } else if (pres) {
+        } else if (sl) {
           put(keep_term(v, id, g.drop) ? v : dead_value(), i);
         }
-      } else {
+      } else if (qslot(j)) {
         const double qv = qval(j, kq);
         put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
       }
@@ -878,6 +990,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
         const bool id = o0 + q == 0 && key_is_identity<B>(k);
         if (id || a >= g.eps) ++n_eps;
         if (!id && a >= g.eps) atomicAdd(shist + hist_bin(a), 1u);
+        if (!id && g.theta != 0.0 && a >= g.theta) ++n_ge;
       }
       if (meta) {
         short l = -1;  // tile-first slot: fixed up by k_meta_fix
@@ -916,17 +1029,23 @@ __global__ void k_meta_fix(const ull* __restrict__ keys, const ull* __restrict__
 
 template <int B, int NT>
 __device__ __forceinline__ void merge_flush(const MergeArgs& g, unsigned* shist, int n_eps,
-                                            int n_dead, int* s_cnt) {
+                                            int n_dead, int n_coll, int n_ge, int* s_cnt) {
   n_dead = __reduce_add_sync(0xffffffffu, n_dead);
   n_eps = __reduce_add_sync(0xffffffffu, n_eps);
+  n_coll = __reduce_add_sync(0xffffffffu, n_coll);
+  n_ge = __reduce_add_sync(0xffffffffu, n_ge);
   if ((threadIdx.x & 31) == 0) {
     if (n_dead) atomicAdd(&s_cnt[0], n_dead);
     if (n_eps) atomicAdd(&s_cnt[1], n_eps);
+    if (n_coll) atomicAdd(&s_cnt[2], n_coll);
+    if (n_ge) atomicAdd(&s_cnt[3], n_ge);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_cnt[0]) atomicAdd(g.counters + 2, (ull)s_cnt[0]);
     if (s_cnt[1]) atomicAdd(g.counters + 1, (ull)s_cnt[1]);
+    if (s_cnt[2]) atomicAdd(g.counters + 5, (ull)s_cnt[2]);
+    if (s_cnt[3]) atomicAdd(g.counters + 6, (ull)s_cnt[3]);
   }
   if (g.want_hist)
     for (int b = threadIdx.x; b < kHistBins; b += NT)
@@ -941,11 +1060,11 @@ __global__ void __launch_bounds__(NT, IQCC_MERGE_MINB * 256 / NT) k_merge1(Merge
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST - Cfg::STAGE);
   __shared__ __align__(8) unsigned long long mbar;
-  __shared__ int s_cnt[2];
+  __shared__ int s_cnt[4];
   const size_t tile = blockIdx.x;
   if (threadIdx.x == 0) {
     mbar_init(&mbar, 1);
-    s_cnt[0] = s_cnt[1] = 0;
+    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
   }
   if (g.want_hist)
     for (int b = threadIdx.x; b < Cfg::HBINS; b += NT) shist[b] = 0;
@@ -957,10 +1076,10 @@ __global__ void __launch_bounds__(NT, IQCC_MERGE_MINB * 256 / NT) k_merge1(Merge
   if (g.part_a[tile + 1] > g.part_a[tile]) mbar_wait(&mbar, 0);
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar)) : "memory");
-  int n_eps = 0, n_dead = 0;
+  int n_eps = 0, n_dead = 0, n_coll = 0, n_ge = 0;
   // shared layout past the single stage is shifted down by one STAGE
-  merge_compute<B, NT, IPT>(g, tile, P, sk, sc, smem_raw - Cfg::STAGE, n_eps, n_dead);
-  merge_flush<B, NT>(g, shist, n_eps, n_dead, s_cnt);
+  merge_compute<B, NT, IPT>(g, tile, P, sk, sc, smem_raw - Cfg::STAGE, n_eps, n_dead, n_coll, n_ge);
+  merge_flush<B, NT>(g, shist, n_eps, n_dead, n_coll, n_ge, s_cnt);
 }
 
 /// Persistent merge: each CTA walks tiles blockIdx.x, +gridDim.x, ... with a
@@ -975,11 +1094,11 @@ __global__ void __launch_bounds__(NT, IQCC_PMERGE_MINB * 256 / NT) k_merge(Merge
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
   __shared__ __align__(8) unsigned long long mbar[2];
-  __shared__ int s_cnt[2];
+  __shared__ int s_cnt[4];
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
-    s_cnt[0] = s_cnt[1] = 0;
+    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
   }
   if (g.want_hist)
     for (int b = threadIdx.x; b < Cfg::HBINS; b += NT) shist[b] = 0;
@@ -991,7 +1110,7 @@ __global__ void __launch_bounds__(NT, IQCC_PMERGE_MINB * 256 / NT) k_merge(Merge
   size_t tile = blockIdx.x;
   if (tile < g.ntiles) merge_issue<B, NT>(g, tile, stage_k(0), stage_c(0), &mbar[0]);
   unsigned phase[2] = {0u, 0u};
-  int n_eps = 0, n_dead = 0;
+  int n_eps = 0, n_dead = 0, n_coll = 0, n_ge = 0;
   for (int it = 0; tile < g.ntiles; ++it, tile += gridDim.x) {
     const int cur = it & 1;
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -1002,10 +1121,10 @@ __global__ void __launch_bounds__(NT, IQCC_PMERGE_MINB * 256 / NT) k_merge(Merge
     __syncthreads();
     const size_t next = tile + gridDim.x;
     if (next < g.ntiles) merge_issue<B, NT>(g, next, stage_k(cur ^ 1), stage_c(cur ^ 1), &mbar[cur ^ 1]);
-    merge_compute<B, NT, IPT>(g, tile, P, stage_k(cur), stage_c(cur), smem_raw, n_eps, n_dead);
+    merge_compute<B, NT, IPT>(g, tile, P, stage_k(cur), stage_c(cur), smem_raw, n_eps, n_dead, n_coll, n_ge);
     __syncthreads();  // stage `cur` and the staging list are free again
   }
-  merge_flush<B, NT>(g, shist, n_eps, n_dead, s_cnt);
+  merge_flush<B, NT>(g, shist, n_eps, n_dead, n_coll, n_ge, s_cnt);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[0])) : "memory");
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[1])) : "memory");
@@ -1051,14 +1170,21 @@ struct PlanState {
   unsigned* ppre = nullptr;
   unsigned* ptotal = nullptr;
   const long long* a_dev = nullptr;  // device product count (nullptr: none)
+  SlotRule rule{1.0, 0.0, 0.0, 0.0, 0.0};
+  const unsigned* qbits = nullptr;   // product slot bits in rank order (nullptr: all)
+  const unsigned* qpre = nullptr;
+  const unsigned* qtotal = nullptr;
+  size_t Wq = 0;
 };
 PlanState g_plan;
 
 template <int B>
-void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = true) {
+void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = true,
+               SlotRule rule = SlotRule{1.0, 0.0, 0.0, 0.0, 0.0}) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   PlanState pl;
+  pl.rule = rule;
   const size_t M = s.M;
   pl.M = M;
   const std::vector<int> pos = level_positions<B>(P);
@@ -1066,8 +1192,9 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   const int nch = (m + kLevelsPerChunk - 1) / kLevelsPerChunk;
   const size_t W = (M + 31) / 32;
   pl.W = W;
-  unsigned* fmask = ws.fmask.as<unsigned>(2 * std::max<size_t>(W, 1) + 64);
+  unsigned* fmask = ws.fmask.as<unsigned>(3 * std::max<size_t>(W, 1) + 64);
   pl.pmask = fmask + std::max<size_t>(W, 1);
+  unsigned* qmask = pl.pmask + std::max<size_t>(W, 1);
   pl.ppre = ws.tables.as<unsigned>(std::max<size_t>(W, 1) + (W + PW - 1) / PW + 8);
   unsigned* bsum = pl.ppre + std::max<size_t>(W, 1);
   pl.ptotal = bsum + (W + PW - 1) / PW + 4;
@@ -1095,6 +1222,8 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
     ma.filt = s.filt;
     ma.fmask = fmask;
     ma.pmask = pl.pmask;
+    ma.qmask = qmask;
+    ma.rule = rule;
   } else if (M > 0) {
     lcp = ws.lcp.as<short>(M);
     {
@@ -1105,7 +1234,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
       constexpr int IT = 2;  // 56 registers: 4 CTAs / SM
 #endif
       k_classify<B, IT><<<(unsigned)((M + 256 * IT - 1) / (256 * IT)), 256, 0, st>>>(
-          s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pl.pmask);
+          s.keys(), s.coef(), s.filt, M, P, lcp, fmask, pl.pmask, rule, qmask);
     }
     if (getenv("IQCC_DEBUG")) debug_check("classify");
     run_present();
@@ -1128,6 +1257,8 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
     long long* a_total = g_bwd + ngroups * kThrPerChunk;
     int* rdelta = nch > 1 ? ws.rdelta.as<int>(M) : nullptr;
     pl.inv_perm = ws.inv_perm.as<unsigned>(M);
+    // product slot flags in rank order (only when some products lose their slot)
+    unsigned char* qflag = rule.thq != 0.0 ? ws.qflag.as<unsigned char>(M + 64) : nullptr;
     ull* dbg = debug_buffer();
     const unsigned wblocks = (unsigned)((ntiles + 7) / 8);
     for (int c = 0; c < nch; ++c) {
@@ -1177,7 +1308,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
       }
       {
         KernelScope ks("rank");
-#define IQCC_RANK(NT_, F_) k_rank_w<NT_, F_><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_pfx, fwd_carry, bwd_carry, rdelta, c > 0, pl.inv_perm, a_total, dbg)
+#define IQCC_RANK(NT_, F_) k_rank_w<NT_, F_><<<wblocks, 256, 0, st>>>(lcp, fmask, M, ntiles, thr, tile_pfx, fwd_carry, bwd_carry, rdelta, c > 0, pl.inv_perm, a_total, dbg, qmask, qflag)
         if (last) {
           switch (nthr4) {
             case 4: IQCC_RANK(4, true); break;
@@ -1206,6 +1337,29 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
     IQCC_CUDA(cudaMemcpyAsync(a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     host_sync(st);
     pl.A = (size_t)*a_host;
+    if (qflag) {  // flags -> bits + popcount prefix (like the survivor slot bits)
+      const size_t A = pl.A, Wq = (A + 31) / 32, nbq = (Wq + PW - 1) / PW;
+      unsigned* qb = ws.qbits.as<unsigned>(2 * std::max<size_t>(Wq, 1) + nbq + 64);
+      unsigned* qpre = qb + std::max<size_t>(Wq, 1) + 2;
+      unsigned* qbs = qpre + std::max<size_t>(Wq, 1);
+      unsigned* qtot = qbs + nbq + 4;
+      IQCC_CUDA(cudaMemsetAsync(qb, 0, (std::max<size_t>(Wq, 1) + 2) * sizeof(unsigned), st));
+      IQCC_CUDA(cudaMemsetAsync(qtot, 0, sizeof(unsigned), st));
+      if (A > 0) {
+        KernelScope ks("present");
+        k_pack_flags<<<(unsigned)((Wq + 255) / 256), 256, 0, st>>>(qflag, A, qb);
+        k_popc_blocks<<<(unsigned)nbq, 256, 0, st>>>(qb, Wq, qbs);
+        k_scan_blocks<<<1, 1024, 0, st>>>(qbs, nbq, qtot);
+        k_popc_prefix<<<(unsigned)nbq, 256, 0, st>>>(qb, Wq, qbs, qpre);
+        count_launch("present");
+        count_launch("present");
+        count_launch("present");
+      }
+      pl.qbits = qb;
+      pl.qpre = qpre;
+      pl.qtotal = qtot;
+      pl.Wq = Wq;
+    }
     if (getenv("IQCC_DEBUG") && pl.A > 0) {
       unsigned* seen = ws.misc2.as<unsigned>(M);
       IQCC_CUDA(cudaMemsetAsync(seen, 0, M * sizeof(unsigned), st));
@@ -1218,7 +1372,8 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
 
 template <int B, int NT, int IPT>
 void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys, const double* q_vals,
-                    double cs, double sn, double drop, bool want_hist, double eps, const Key<B>* PN) {
+                    double cs, double sn, double drop, bool want_hist, double eps, const Key<B>* PN,
+                    double theta) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   const PlanState& pl = g_plan;
@@ -1233,7 +1388,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     KernelScope ks("partition");
     k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
         s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
-        pl.ptotal);
+        pl.ptotal, q_keys ? nullptr : pl.qbits, pl.qpre, pl.Wq, pl.qtotal);
   }
   ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
   double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
@@ -1263,6 +1418,9 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   g.hist = hist;
   g.want_hist = want_hist ? 1 : 0;
   g.dbg = debug_buffer();
+  g.rule = pl.rule;
+  g.theta = want_hist ? theta : 0.0;
+  g.qbits = q_keys ? nullptr : pl.qbits;
   g.out_lcp = nullptr;
   g.out_amask = nullptr;
   for (int w = 0; w < 8; ++w) g.pn[w] = 0;
@@ -1310,14 +1468,14 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
 template <int B>
 DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys,
                         const double* q_vals, double cs, double sn, double drop, bool want_hist,
-                        double eps, const Key<B>* PN = nullptr) {
+                        double eps, const Key<B>* PN = nullptr, double theta = 0.0) {
   static int shape = -1;
   if (shape < 0) {
     const char* env = getenv("IQCC_MERGE_CFG");
     shape = env ? atoi(env) : 3;
     if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 3;
   }
-#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps, PN)
+#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps, PN, theta)
   switch (shape) {
     case 0: IQCC_MERGE(256, 4); break;
     case 1: IQCC_MERGE(128, 4); break;
@@ -1330,35 +1488,39 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   ull* ctr = ws.counters.as<ull>(16);
-  ull* hc = static_cast<ull*>(host_pinned(4 * sizeof(ull)));
-  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 4 * sizeof(ull), cudaMemcpyDeviceToHost, st));
+  ull* hc = static_cast<ull*>(host_pinned(8 * sizeof(ull)));
+  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 8 * sizeof(ull), cudaMemcpyDeviceToHost, st));
   host_sync(st);
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
-  // algorithmic bytes of the step: (M_in + M_out) * (16B + 8)
+  // algorithmic bytes of the step: (M_in + M_out) * (16B + 8),
+  // M_out = the dressed sum's size (present survivors + products - partner
+  // pairs) whether or not every term got an output slot
   const size_t logical_in = s.logical;
+  const size_t m_out = logical_in + nQ - hc[5];
   s.M = hc[3];                // physical slots (live + dead)
   s.filt = Filter{};
   s.logical = hc[3] - hc[2];  // minus dead slots
   s.meta_valid = PN != nullptr;
   if (PN)
     for (int w = 0; w < 2 * B; ++w) s.meta_P[w] = PN->w[w];
-  add_alg_bytes("merge", (double)(logical_in + s.logical) * (16.0 * B + 8.0));
+  add_alg_bytes("merge", (double)(logical_in + m_out) * (16.0 * B + 8.0));
   DressOutcome out;
   out.count_eps = hc[1];
   out.n_anticommuting = g_plan.A;
+  out.n_ge_theta = hc[6];
   return out;
 }
 
 template <int B>
 DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps, const uint64_t* next_row) {
+                        bool want_hist, double eps, const uint64_t* next_row, double theta) {
   const Key<B> P = make_key<B>(gen_row);
-  plan_impl<B>(s, P, sn != 0.0);
+  plan_impl<B>(s, P, sn != 0.0, true, make_slot_rule(cs, sn, theta));
   Key<B> PN;
   if (next_row) PN = make_key<B>(next_row);
   return merge_impl<B>(s, P, g_plan.A, nullptr, nullptr, cs, sn, drop, want_hist, eps,
-                       next_row ? &PN : nullptr);
+                       next_row ? &PN : nullptr, theta);
 }
 
 // Sorted products as a contiguous buffer (keys ^ P, +-fl(c*sin)) for a peer.
@@ -1431,12 +1593,22 @@ DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, 
   }
 }
 
+void dress_undo(DeviceStore& s, size_t M, size_t logical, const Filter& filt) {
+  Workspace& ws = workspace();
+  std::swap(s.kbuf, ws.out_keys);
+  std::swap(s.cbuf, ws.out_coef);
+  s.M = M;
+  s.logical = logical;
+  s.filt = filt;
+  s.meta_valid = false;  // the failed merge overwrote the metadata
+}
+
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps, const uint64_t* next_row) {
+                        bool want_hist, double eps, const uint64_t* next_row, double theta) {
   switch (s.B) {
-    case 1: return dress_impl<1>(s, gen_row, cs, sn, drop, want_hist, eps, next_row);
-    case 2: return dress_impl<2>(s, gen_row, cs, sn, drop, want_hist, eps, next_row);
-    case 4: return dress_impl<4>(s, gen_row, cs, sn, drop, want_hist, eps, next_row);
+    case 1: return dress_impl<1>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta);
+    case 2: return dress_impl<2>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta);
+    case 4: return dress_impl<4>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta);
     default: throw std::runtime_error("dress: unsupported block count");
   }
 }

@@ -355,7 +355,7 @@ struct DevBuf {
 
 struct Workspace {
   DevBuf lcp, mbits, fmask, tile_cnt, tile_pfx, fwd_agg, bwd_agg, fwd_carry, bwd_carry;
-  DevBuf inv_perm, rdelta, part_a, part_b, tile_status, counters, hist, cand_v, cand_i, cand_v2, cand_i2;
+  DevBuf inv_perm, rdelta, part_a, part_b, tile_status, counters, hist, cand_v, cand_i, cand_v2, cand_i2, qflag, qbits;
   DevBuf levels, stage_rows, stage_coef, partials, grad_part, tables, misc, misc2, misc3;
   DevBuf xbuf_keys, xbuf_coef, rbuf_keys, rbuf_coef;
   DevBuf out_keys, out_coef;  // double buffer swapped with the store after a step
@@ -379,6 +379,7 @@ struct DeviceStore {
   // classify pass.  Any other change of the slots clears meta_valid.
   bool meta_valid = false;
   ull meta_P[8] = {};
+  double spec_cut = 0.0;  // last compress cut: dress_sequence's slot speculation guess
   DevBuf meta_lcp, meta_amask;
   ull* keys() const { return static_cast<ull*>(kbuf.p); }
   double* coef() const { return static_cast<double*>(cbuf.p); }
@@ -408,14 +409,21 @@ void store_clone(const DeviceStore& src, DeviceStore& dst);
 struct DressOutcome {
   size_t n_anticommuting = 0;
   size_t count_eps = 0;  // emitted terms passing (identity || |c| >= eps)
+  size_t n_ge_theta = 0;  // emitted non-identity terms with |c| >= theta (theta > 0 only)
 };
 /// One dressing step in place; if want_hist, also accumulates the |c|
 /// histogram of emitted terms for a following compress(eps).
 /// next_row (optional, device-width row): the entangler of the following
 /// step; the merge then also writes that step's classify metadata.
+/// theta > 0: a compress whose cut is >= theta follows (theta <= eps: known;
+/// a power of two above eps: speculated, the caller verifies n_ge_theta);
+/// terms below theta/2 get no output slot (SlotRule in dress.cu).
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cos_tau, double sin_tau,
                         double drop_thr, bool want_hist, double eps,
-                        const uint64_t* next_row = nullptr);
+                        const uint64_t* next_row = nullptr, double theta = 0.0);
+/// Undo the last dress_step (the merge's input buffers are still the
+/// workspace's output pair): restores the store as it was before the step.
+void dress_undo(DeviceStore& s, size_t M, size_t logical, const Filter& filt);
 /// Phases of a step for the partitioned path: plan (classify, present
 /// prefix, product order; returns the product count A), materialize the
 /// sorted products (keys ^ P, values) into a buffer, and merge the store's

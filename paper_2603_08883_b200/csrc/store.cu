@@ -46,6 +46,7 @@ void DeviceStore::ensure(size_t n) {
   kbuf.get(n * 2 * B * sizeof(ull));
   cbuf.get(n * sizeof(double));
   meta_valid = false;
+  spec_cut = 0.0;
 }
 
 // ------------------------------------------------------------------ upload

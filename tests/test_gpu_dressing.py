@@ -271,3 +271,64 @@ def test_cpp_shim_against_reference():
     r = subprocess.run(args, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL OK" in r.stdout
+
+
+def _entanglers(n, steps, seed, zero_at=()):
+    rs = np.random.default_rng(seed)
+    B = (n + 63) // 64
+    gens, taus = [], []
+    for k in range(steps):
+        w = int(rs.integers(2, 5))
+        qs = rs.choice(n, w, replace=False)
+        ys = rs.integers(0, 2, w)
+        if ys.sum() % 2 == 0:
+            ys[-1] ^= 1
+        row = np.zeros(2 * B, np.uint64)
+        for q, y in zip(qs, ys):
+            row[q // 64] |= np.uint64(1 << int(q % 64))
+            if y:
+                row[B + q // 64] |= np.uint64(1 << int(q % 64))
+        gens.append(row)
+        taus.append(0.0 if k in zero_at else float(rs.uniform(-0.2, 0.2)))
+    return gens, taus
+
+
+@pytest.mark.parametrize("n,terms,steps,eps,cap,zero_at", [
+    (124, 200_000, 8, 1e-10, 200_000, (4,)),   # speculative slots; tau = 0 forces a redo
+    (124, 150_000, 6, 1e-6, 170_000, ()),      # eps slots + cap
+    (64, 100_000, 6, 1e-4, 2**64 - 1, ()),     # eps slots only (exact, no speculation)
+    (200, 50_000, 5, 1e-9, 55_000, (2,)),      # 4 device blocks
+])
+def test_sequence_output_slots(eng, port, n, terms, steps, eps, cap, zero_at):
+    """dress_sequence without drop statistics allocates output slots only for
+    terms the following compress can keep (speculated cut verified after each
+    merge, redone exactly when the check fails): the result must equal the
+    reference pipeline bit for bit, over one call and over per-step calls."""
+    from paper_2603_08883_b200 import native
+    gens, taus = _entanglers(n, steps, 31 + n, zero_at)
+    h = port.gen_mol(n, terms, 2)
+    ref, _ = port.dress_sequence(h, np.stack(gens), taus, eps, cap)
+    ans = eng.Ansatz([eng.PauliWord(n, g) for g in gens], taus)
+    native.profile(True)
+    native.profile_reset()
+    d = eng.DeviceSum.generate_mol(n, terms, 2)
+    d.dress_sequence(ans, eps, cap)
+    check_same(d.download(), ref)
+    d2 = eng.DeviceSum.generate_mol(n, terms, 2)
+    for g, t in zip(gens, taus):
+        d2.dress_sequence(eng.Ansatz([eng.PauliWord(n, g)], [t]), eps, cap)
+    check_same(d2.download(), ref)
+    # wrong guesses (the test hook scales every guess above the true cut) are
+    # detected after the merge and the step is redone exactly
+    os.environ["IQCC_SPEC_SCALE"] = "64"
+    try:
+        native.profile_reset()
+        d3 = eng.DeviceSum.generate_mol(n, terms, 2)
+        d3.dress_sequence(ans, eps, cap)
+        redo = native.profile_get("spec_redo")[1]
+    finally:
+        del os.environ["IQCC_SPEC_SCALE"]
+        native.profile(False)
+    check_same(d3.download(), ref)
+    if cap < 2**63:
+        assert redo > 0
