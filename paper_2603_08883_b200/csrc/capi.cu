@@ -547,8 +547,8 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps,
                                   next.empty() ? nullptr : next.data(), theta);
       if (getenv("IQCC_VERBOSE"))
-        fprintf(stderr, "[dress] k=%zu theta=%.3e exact=%.3e n_ge=%zu slots=%zu\n", k, theta, exact,
-                o.n_ge_theta, h->s.M);
+        fprintf(stderr, "[dress] k=%zu theta=%.3e exact=%.3e n_ge=%zu slots=%zu products=%zu pairs=%zu\n", k,
+                theta, exact, o.n_ge_theta, h->s.M, o.n_anticommuting, o.n_pairs);
       // the slotted sum compresses like the full one iff the top `budget`
       // terms are all >= theta and either the compress cuts or nothing below
       // theta holds a slot

@@ -1509,6 +1509,7 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
   out.count_eps = hc[1];
   out.n_anticommuting = g_plan.A;
   out.n_ge_theta = hc[6];
+  out.n_pairs = hc[5];
   return out;
 }
 

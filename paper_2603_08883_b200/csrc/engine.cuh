@@ -410,6 +410,7 @@ struct DressOutcome {
   size_t n_anticommuting = 0;
   size_t count_eps = 0;  // emitted terms passing (identity || |c| >= eps)
   size_t n_ge_theta = 0;  // emitted non-identity terms with |c| >= theta (theta > 0 only)
+  size_t n_pairs = 0;     // survivor/product partner pairs (same word)
 };
 /// One dressing step in place; if want_hist, also accumulates the |c|
 /// histogram of emitted terms for a following compress(eps).
