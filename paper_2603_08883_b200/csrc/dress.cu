@@ -599,6 +599,8 @@ __device__ __forceinline__ Key<B> q_key(const ull* __restrict__ keys,
   return key_xor<B>(load_key<B>(keys, inv_perm[j]), P);
 }
 
+constexpr int kPartShift = 5;  // coarse merge-path splits every 32 output tiles
+
 template <int B>
 __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __restrict__ inv_perm,
                             const ull* __restrict__ q_keys,
@@ -608,11 +610,20 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
                             const unsigned* __restrict__ ppre, size_t W,
                             const unsigned* __restrict__ ptotal, const unsigned* __restrict__ qbits,
                             const unsigned* __restrict__ qpre, size_t Wq,
-                            const unsigned* __restrict__ qtotal) {
-  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+                            const unsigned* __restrict__ qtotal, int coarse_shift,
+                            ull* __restrict__ raw_a) {
+  // two passes: coarse_shift > 0 searches every 2^shift-th boundary over the
+  // whole range and records the raw split; coarse_shift == 0 searches every
+  // boundary inside the window between its two coarse neighbours
+  const size_t t = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) << coarse_shift;
   if (t > ntiles) return;
   const size_t d = min(t * tile_items, nS + nQ);
   size_t lo = d > nQ ? d - nQ : 0, hi = min(d, nS);
+  if (coarse_shift == 0 && raw_a) {  // the raw split is monotone in the diagonal
+    const size_t c0 = t >> kPartShift;
+    lo = max(lo, (size_t)raw_a[c0]);
+    if (((c0 + 1) << kPartShift) <= ntiles) hi = min(hi, (size_t)raw_a[c0 + 1]);
+  }
   while (lo < hi) {
     size_t mid = (lo + hi) >> 1;
     if (key_cmp<B>(load_key<B>(keys, mid), q_key<B>(keys, inv_perm, q_keys, d - 1 - mid, P)) <= 0)
@@ -621,6 +632,10 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
       hi = mid;
   }
   size_t a = lo, b = d - lo;
+  if (coarse_shift) {
+    raw_a[t >> coarse_shift] = a;
+    return;
+  }
   // never split a run of equal survivors (live + dead slot) from its product
   if (b < nQ) {
     const Key<B> q = q_key<B>(keys, inv_perm, q_keys, b, P);
@@ -1381,14 +1396,21 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   const size_t M = s.M;
   const size_t total = M + nQ;
   const size_t ntm = std::max<size_t>(1, (total + TILEM - 1) / TILEM);
-  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1));
+  const size_t nco = (ntm >> kPartShift) + 1;  // coarse boundaries 0, 32, 64, ... <= ntm
+  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1) + nco + 8);
   ull* pb = pa + (ntm + 1);
   ull* po = pb + (ntm + 1);
   {
     KernelScope ks("partition");
+    ull* raw = po + (ntm + 1);
+    const unsigned* qb = q_keys ? nullptr : pl.qbits;
+    k_partition<B><<<(unsigned)((nco + 255) / 256), 256, 0, st>>>(
+        s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
+        pl.ptotal, qb, pl.qpre, pl.Wq, pl.qtotal, kPartShift, raw);
     k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
         s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
-        pl.ptotal, q_keys ? nullptr : pl.qbits, pl.qpre, pl.Wq, pl.qtotal);
+        pl.ptotal, qb, pl.qpre, pl.Wq, pl.qtotal, 0, raw);
+    count_launch("partition");
   }
   ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
   double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
