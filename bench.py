@@ -234,9 +234,13 @@ def run_gpu_arm(args, rank, world, local_rank):
         ents = step_entanglers(N_QUBITS, s, flip)
         ans = iqcc.Ansatz([iqcc.PauliWord(N_QUBITS, r) for r, _ in ents], [t for _, t in ents])
         if part:
-            return part.dress_sequence(store, ans, EPS, n_terms)
+            xl = []
+            tin = part.dress_sequence(store, ans, EPS, n_terms, exchange=xl)
+            sent[0] += sum(x.sent_terms for x in xl)
+            return tin
         return store.dress_sequence(ans, EPS, n_terms)
 
+    sent = [0]
     for w in range(args.warmup):
         dress_step(d, w)
     torch.cuda.synchronize()
@@ -249,6 +253,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     launches0 = native.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tin_total = 0
+    sent[0] = 0
     with ClockSampler(local_rank) as clk:
         time.sleep(0.6)  # let nvidia-smi start sampling before the timed region
         torch.cuda.synchronize()
@@ -265,8 +270,12 @@ def run_gpu_arm(args, rank, world, local_rank):
     fam = {f: native.profile_get(f)[0] for f in
            ["classify", "present", "tile_agg", "carry", "rank", "partition", "merge",
             "select_gather", "select_digits", "exchange", "host_wait", "host_dress", "host_compress", "span_dress", "span_compress", "host_alloc", "host_compress_inner", "spec_redo"]}
+    for f in ["materialize", "exch_count", "exch_signal"]:
+        fam[f] = native.profile_get(f)[0]
     native.profile(False)
     if dist:
+        print(f"[bench] rank {rank}: shard {d.size()} terms, sent {sent[0]} products, ms {ms:.2f}, kernel_ms "
+              + json.dumps({k: round(v, 2) for k, v in fam.items() if v}), file=sys.stderr)
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())

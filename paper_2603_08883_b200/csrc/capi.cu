@@ -697,6 +697,7 @@ int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const
     if (row_is_identity(gen, Bref)) throw std::invalid_argument("parallel_dress: identity generator");
     if (max_terms < 1) throw std::invalid_argument("compress_partitioned: max_terms < 1");
     auto row = widen_row(gen, Bref, h->s.B);
+    multi_prepare(h->s);
     parallel_dress_step(h->s, m, bits, owner, row.data(), cos_tau, sin_tau, eps, max_terms, xs, cs);
   });
 }
@@ -714,13 +715,30 @@ int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bi
       if (row_is_identity(gens + k * 2 * Bref, Bref))
         throw std::invalid_argument("parallel_dress: identity generator");
     size_t local_in = 0;
+    multi_prepare(h->s);
+    // output-slot speculation as in iqcc_gpu_dress_sequence; the cut is
+    // global (compress_partitioned), so every rank guesses the same theta
+    // and the verification runs on allreduced counts
+    const bool slots = cs == nullptr && getenv("IQCC_NO_SPEC") == nullptr;
+    const char* sc_env = getenv("IQCC_SPEC_SCALE");  // test hook: force bad guesses
+    const double spec_scale = sc_env ? std::atof(sc_env) : 1.0;
+    double spec = slots ? h->s.spec_cut : 0.0;
+    const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
     for (size_t k = 0; k < K; ++k) {
       auto row = widen_row(gens + k * 2 * Bref, Bref, h->s.B);
       std::vector<uint64_t> next;
       if (k + 1 < K) next = widen_row(gens + (k + 1) * 2 * Bref, Bref, h->s.B);
       local_in += h->s.logical;
+      const double exact = slots && eps > 0.0 ? eps : 0.0;
+      const double guess = spec * std::min(1.0, std::fabs(cos_tau[k])) * 0.999 * spec_scale;
+      const double theta = maybe && guess > eps && max_terms != SIZE_MAX ? guess : exact;
+      bool failed = false;
       parallel_dress_step(h->s, m, bits, owner, row.data(), cos_tau[k], sin_tau[k], eps, max_terms,
-                          xs ? xs + k : nullptr, cs, next.empty() ? nullptr : next.data());
+                          xs ? xs + k : nullptr, cs, next.empty() ? nullptr : next.data(), theta,
+                          exact, &failed);
+      if (failed) spec = h->s.spec_cut = 0.0;
+      const Filter& f = h->s.filt;
+      if (slots && f.active && f.has_v && f.v > 0.0 && std::isfinite(f.v)) spec = h->s.spec_cut = f.v;
     }
     if (terms_in_total) *terms_in_total = parallel_sum(local_in);
   });

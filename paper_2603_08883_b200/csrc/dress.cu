@@ -1403,7 +1403,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   {
     KernelScope ks("partition");
     ull* raw = po + (ntm + 1);
-    const unsigned* qb = q_keys ? nullptr : pl.qbits;
+    const unsigned* qb = pl.qbits;
     k_partition<B><<<(unsigned)((nco + 255) / 256), 256, 0, st>>>(
         s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
         pl.ptotal, qb, pl.qpre, pl.Wq, pl.qtotal, kPartShift, raw);
@@ -1442,7 +1442,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   g.dbg = debug_buffer();
   g.rule = pl.rule;
   g.theta = want_hist ? theta : 0.0;
-  g.qbits = q_keys ? nullptr : pl.qbits;
+  g.qbits = pl.qbits;
   g.out_lcp = nullptr;
   g.out_amask = nullptr;
   for (int w = 0; w < 8; ++w) g.pn[w] = 0;
@@ -1549,9 +1549,9 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
 // Sorted products as a contiguous buffer (keys ^ P, +-fl(c*sin)) for a peer.
 template <int B>
 __global__ void k_materialize(const ull* __restrict__ keys, const double* __restrict__ coef,
-                              const unsigned* __restrict__ inv_perm, size_t A, Key<B> P, double sn,
-                              ull* __restrict__ okeys, double* __restrict__ ovals) {
-  const size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+                              const unsigned* __restrict__ inv_perm, size_t r0, size_t A, Key<B> P,
+                              double sn, ull* __restrict__ okeys, double* __restrict__ ovals) {
+  const size_t r = r0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (r >= A) return;
   const unsigned src = inv_perm[r];
   const Key<B> k = load_key<B>(keys, src);
@@ -1560,15 +1560,117 @@ __global__ void k_materialize(const ull* __restrict__ keys, const double* __rest
   ovals[r] = product_phase<B>(k, P) == 1 ? pr : -pr;
 }
 
+/// Products pushed straight into a peer's receive buffer over NVLink (CUDA
+/// IPC mapping): each CTA gathers a tile of 256 products into shared memory,
+/// then writes it with fully coalesced 16-byte stores, so the remote writes
+/// leave as full lines (per-thread scattered row stores halve NVLink
+/// throughput).  Grid-stride over tiles; one CTA per SM slot.
+template <int B>
+__global__ void __launch_bounds__(256) k_push(const ull* __restrict__ keys, const double* __restrict__ coef,
+                                              const unsigned* __restrict__ inv_perm, size_t A, Key<B> P,
+                                              double sn, ull* __restrict__ okeys, double* __restrict__ ovals) {
+  __shared__ __align__(16) ull sk[256 * 2 * B];
+  __shared__ __align__(16) double sv[256];
+  for (size_t t = blockIdx.x; t * 256 < A; t += gridDim.x) {
+    const size_t r0 = t * 256;
+    const int n = (int)min((size_t)256, A - r0);
+    if ((int)threadIdx.x < n) {
+      const unsigned src = inv_perm[r0 + threadIdx.x];
+      const Key<B> k = load_key<B>(keys, src);
+      const double pr = __dmul_rn(coef[src], sn);
+      const Key<B> q = key_xor<B>(k, P);
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) sk[threadIdx.x * 2 * B + w] = q.w[w];
+      sv[threadIdx.x] = product_phase<B>(k, P) == 1 ? pr : -pr;
+    }
+    __syncthreads();
+    ulonglong2* dk = reinterpret_cast<ulonglong2*>(okeys + r0 * 2 * B);
+    const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(sk);
+    for (int j = threadIdx.x; j < n * B; j += 256) dk[j] = s2[j];
+    if (n == 256 && (r0 & 1) == 0) {
+      if (threadIdx.x < 128)
+        reinterpret_cast<double2*>(ovals + r0)[threadIdx.x] = reinterpret_cast<const double2*>(sv)[threadIdx.x];
+    } else if ((int)threadIdx.x < n) {
+      ovals[r0 + threadIdx.x] = sv[threadIdx.x];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
-const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row) {
+void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals) {
+  const size_t A = g_plan.A;
+  if (A == 0) return;
+  cudaStream_t st = stream();
+  KernelScope ks("exchange");
+  const unsigned grid = (unsigned)std::min<size_t>((A + 255) / 256, 148 * 8);
   switch (s.B) {
-    case 1: plan_impl<1>(s, make_key<1>(gen_row), true, false); break;
-    case 2: plan_impl<2>(s, make_key<2>(gen_row), true, false); break;
-    default: plan_impl<4>(s, make_key<4>(gen_row), true, false); break;
+    case 1: k_push<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<1>(gen_row), sn, okeys, ovals); break;
+    case 2: k_push<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<2>(gen_row), sn, okeys, ovals); break;
+    default: k_push<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<4>(gen_row), sn, okeys, ovals); break;
+  }
+}
+
+const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row, double cs,
+                                     double sn, double theta) {
+  // survivor slots by the rule; the products leave for the peer, whose
+  // slot bits the receiver derives from the values (recv_slot_bits)
+  const SlotRule r{cs, sn, theta, 0.0, 0.0};
+  switch (s.B) {
+    case 1: plan_impl<1>(s, make_key<1>(gen_row), true, false, r); break;
+    case 2: plan_impl<2>(s, make_key<2>(gen_row), true, false, r); break;
+    default: plan_impl<4>(s, make_key<4>(gen_row), true, false, r); break;
   }
   return g_plan.a_dev;
+}
+
+void plan_survivors(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double theta) {
+  const SlotRule r{cs, sn, theta, 0.0, 0.0};
+  switch (s.B) {
+    case 1: plan_impl<1>(s, make_key<1>(gen_row), false, true, r); break;
+    case 2: plan_impl<2>(s, make_key<2>(gen_row), false, true, r); break;
+    default: plan_impl<4>(s, make_key<4>(gen_row), false, true, r); break;
+  }
+}
+
+/// Slot bits of received products (final values, rank order): a product
+/// without a partner keeps its value, so slot iff |v| >= thq (SlotRule).
+__global__ void k_value_slots(const double* __restrict__ v, size_t n, double thq,
+                              unsigned* __restrict__ bits) {
+  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const bool f = j < n && fabs(v[j]) >= thq;
+  const unsigned b = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && j < n) bits[j >> 5] = b;
+}
+
+void recv_slot_bits(const double* rv, size_t n, double thq) {
+  g_plan.qbits = g_plan.qpre = g_plan.qtotal = nullptr;
+  g_plan.Wq = 0;
+  if (thq == 0.0) return;  // every received product owns a slot
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const size_t Wq = (n + 31) / 32, nbq = (Wq + PW - 1) / PW;
+  unsigned* qb = ws.qbits.as<unsigned>(2 * std::max<size_t>(Wq, 1) + nbq + 64);
+  unsigned* qpre = qb + std::max<size_t>(Wq, 1) + 2;
+  unsigned* qbs = qpre + std::max<size_t>(Wq, 1);
+  unsigned* qtot = qbs + nbq + 4;
+  IQCC_CUDA(cudaMemsetAsync(qb, 0, (std::max<size_t>(Wq, 1) + 2) * sizeof(unsigned), st));
+  IQCC_CUDA(cudaMemsetAsync(qtot, 0, sizeof(unsigned), st));
+  if (n > 0) {
+    KernelScope ks("present");
+    k_value_slots<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rv, n, thq, qb);
+    k_popc_blocks<<<(unsigned)nbq, 256, 0, st>>>(qb, Wq, qbs);
+    k_scan_blocks<<<1, 1024, 0, st>>>(qbs, nbq, qtot);
+    k_popc_prefix<<<(unsigned)nbq, 256, 0, st>>>(qb, Wq, qbs, qpre);
+    count_launch("present");
+    count_launch("present");
+    count_launch("present");
+  }
+  g_plan.qbits = qb;
+  g_plan.qpre = qpre;
+  g_plan.qtotal = qtot;
+  g_plan.Wq = Wq;
 }
 
 void plan_set_products(size_t A) { g_plan.A = A; }
@@ -1583,36 +1685,36 @@ size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products) {
 }
 
 void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
-                          double* ovals) {
-  const size_t A = g_plan.A;
-  if (A == 0) return;
+                          double* ovals, size_t r0, size_t r1, const char* family) {
+  r1 = std::min(r1, g_plan.A);
+  if (r1 <= r0) return;
   cudaStream_t st = stream();
-  KernelScope ks("materialize");
-  const unsigned grid = (unsigned)((A + 255) / 256);
+  KernelScope ks(family);
+  const unsigned grid = (unsigned)((r1 - r0 + 255) / 256);
   switch (s.B) {
-    case 1: k_materialize<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<1>(gen_row), sn, okeys, ovals); break;
-    case 2: k_materialize<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<2>(gen_row), sn, okeys, ovals); break;
-    default: k_materialize<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<4>(gen_row), sn, okeys, ovals); break;
+    case 1: k_materialize<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<1>(gen_row), sn, okeys, ovals); break;
+    case 2: k_materialize<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<2>(gen_row), sn, okeys, ovals); break;
+    default: k_materialize<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<4>(gen_row), sn, okeys, ovals); break;
   }
 }
 
 template <int B>
 DressOutcome merge_products_t(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                               double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                              const double* q_vals, const uint64_t* next_row) {
+                              const double* q_vals, const uint64_t* next_row, double theta) {
   Key<B> PN;
   if (next_row) PN = make_key<B>(next_row);
   return merge_impl<B>(s, make_key<B>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps,
-                       next_row ? &PN : nullptr);
+                       next_row ? &PN : nullptr, theta);
 }
 
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                            const double* q_vals, const uint64_t* next_row) {
+                            const double* q_vals, const uint64_t* next_row, double theta) {
   switch (s.B) {
-    case 1: return merge_products_t<1>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row);
-    case 2: return merge_products_t<2>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row);
-    default: return merge_products_t<4>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row);
+    case 1: return merge_products_t<1>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
+    case 2: return merge_products_t<2>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
+    default: return merge_products_t<4>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
   }
 }
 

@@ -434,13 +434,26 @@ size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products);
 /// plan_products without reading the count back: returns its device
 /// address (nullptr: empty store); the caller then sets it with
 /// plan_set_products before materialize/merge.
-const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row);
+/// (survivor slots by SlotRule theta; products always planned in full)
+const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row, double cs = 1.0,
+                                     double sn = 0.0, double theta = 0.0);
+/// Survivor classification and slot bits only (redo of a failed speculation
+/// in the partitioned step: the received products are kept).
+void plan_survivors(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double theta);
+/// Slot bits of n received products (values rv): |v| >= thq; thq = 0: all.
+void recv_slot_bits(const double* rv, size_t n, double thq);
 void plan_set_products(size_t A);
+/// All planned products written straight into a peer's receive buffer
+/// (okeys/ovals: CUDA IPC mapping over NVLink), staged per 256-product tile.
+void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals);
+/// Products [r0, r1) of the planned order (clamped to the product count).
 void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
-                          double* ovals);
+                          double* ovals, size_t r0 = 0, size_t r1 = SIZE_MAX,
+                          const char* family = "materialize");
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                            const double* q_vals, const uint64_t* next_row = nullptr);
+                            const double* q_vals, const uint64_t* next_row = nullptr,
+                            double theta = 0.0);
 /// Selects the compress filter on a store without a filter.  If hist_ready,
 /// the histogram/count_eps of the last dress_step are used.
 /// Cross-rank hooks for compress_partitioned (iqcc/partition.hpp:325-396);
@@ -454,8 +467,11 @@ struct Reducer {
   virtual std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t words_per_key,
                                        size_t* mine_offset) = 0;
 };
+/// glob_known (partitioned, optional): {global count_eps, global identity
+/// count} already reduced by the caller, saving the first reduction.
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
-                              size_t count_eps, bool want_stats, Reducer* red = nullptr);
+                              size_t count_eps, bool want_stats, Reducer* red = nullptr,
+                              const ull* glob_known = nullptr);
 void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* na);
 
 double expect_store(DeviceStore& s, const double* factors);

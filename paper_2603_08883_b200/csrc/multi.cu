@@ -99,6 +99,110 @@ struct NcclReducer : Reducer {
   }
 };
 
+/// Receive buffers in peer-visible memory (CUDA IPC over NVLink).  Every
+/// rank owns one buffer of the same agreed capacity `cap` (terms): keys
+/// [cap][W] then values [cap].  A sender pushes its sorted products straight
+/// into the partner's buffer (no staging copy, no NCCL data transfer), then
+/// signals with a one-word NCCL send/recv, which orders the push before the
+/// partner's merge.  Reuse is safe: a rank pushes only after the count swap
+/// of that step, which the partner posts after its previous merge.
+struct P2P {
+  bool tried = false, ok = false;
+  size_t cap = 0, W = 0;
+  char* mine = nullptr;
+  std::vector<char*> peer;  // mapping of every rank's buffer (own rank: mine)
+};
+P2P g_p2p;
+
+ull allreduce_host(ull v, ncclRedOp_t op) {
+  Comm& c = comm();
+  cudaStream_t st = stream();
+  ull* d = scratch(2);
+  ull* hp = static_cast<ull*>(host_pinned(sizeof(ull)));
+  *hp = v;
+  IQCC_CUDA(cudaMemcpyAsync(d, hp, sizeof(ull), cudaMemcpyHostToDevice, st));
+  IQCC_NCCL(ncclAllReduce(d, d, 1, ncclUint64, op, c.comm, st));
+  IQCC_CUDA(cudaMemcpyAsync(hp, d, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  host_sync(st);
+  return *hp;
+}
+
+void p2p_close() {
+  for (size_t r = 0; r < g_p2p.peer.size(); ++r)
+    if (g_p2p.peer[r] && g_p2p.peer[r] != g_p2p.mine) cudaIpcCloseMemHandle(g_p2p.peer[r]);
+  g_p2p.peer.clear();
+}
+
+void p2p_free() {
+  if (g_p2p.mine) cudaFree(g_p2p.mine);
+  g_p2p.mine = nullptr;
+  g_p2p.cap = 0;
+  g_p2p.ok = false;
+}
+
+/// Collective (every rank, same call sequence): make every receive buffer
+/// hold at least `need` terms of W words (max over ranks).  Any failure on
+/// any rank turns the P2P path off everywhere (NCCL transfers instead).
+void p2p_prepare(size_t need, size_t W) {
+  Comm& c = comm();
+  if (c.world < 2) return;
+  static const bool off = getenv("IQCC_NO_P2P") != nullptr;
+  if (off || (g_p2p.tried && !g_p2p.ok && g_p2p.cap == 0 && g_p2p.W == (size_t)-1)) return;
+  const ull need_g = allreduce_host((ull)need, ncclMax);
+  if (g_p2p.ok && need_g <= g_p2p.cap && W == g_p2p.W) return;
+  cudaStream_t st = stream();
+  IQCC_CUDA(cudaStreamSynchronize(st));
+  p2p_close();
+  allreduce_host(0, ncclSum);  // every mapping of the old buffers is closed
+  p2p_free();
+  g_p2p.tried = true;
+  const size_t cap = (size_t)need_g + need_g / 4 + 1024;
+  bool ok = cudaMalloc(&g_p2p.mine, cap * (W * 8 + 8)) == cudaSuccess;
+  cudaIpcMemHandle_t h;
+  std::memset(&h, 0, sizeof(h));
+  if (ok) ok = cudaIpcGetMemHandle(&h, g_p2p.mine) == cudaSuccess;
+  cudaGetLastError();
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::vector<ull> all(8 * (size_t)c.world);
+  {
+    ull* d = workspace().misc3.as<ull>(8 * ((size_t)c.world + 1));
+    ull* hp = static_cast<ull*>(host_pinned(8 * ((size_t)c.world + 1) * sizeof(ull)));
+    std::memcpy(hp, &h, 64);
+    IQCC_CUDA(cudaMemcpyAsync(d + 8 * c.world, hp, 64, cudaMemcpyHostToDevice, st));
+    IQCC_NCCL(ncclAllGather(d + 8 * c.world, d, 8, ncclUint64, c.comm, st));
+    IQCC_CUDA(cudaMemcpyAsync(hp, d, 64 * c.world, cudaMemcpyDeviceToHost, st));
+    host_sync(st);
+    std::memcpy(all.data(), hp, 64 * c.world);
+  }
+  if (allreduce_host(ok ? 1 : 0, ncclMin) == 1) {
+    g_p2p.peer.assign(c.world, nullptr);
+    for (int r = 0; r < c.world && ok; ++r) {
+      if (r == c.rank) {
+        g_p2p.peer[r] = g_p2p.mine;
+        continue;
+      }
+      cudaIpcMemHandle_t hr;
+      std::memcpy(&hr, all.data() + 8 * r, 64);
+      void* p = nullptr;
+      ok = cudaIpcOpenMemHandle(&p, hr, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      g_p2p.peer[r] = static_cast<char*>(p);
+    }
+    cudaGetLastError();
+  } else {
+    ok = false;
+  }
+  if (allreduce_host(ok ? 1 : 0, ncclMin) == 1) {
+    g_p2p.ok = true;
+    g_p2p.cap = cap;
+    g_p2p.W = W;
+    return;
+  }
+  if (getenv("IQCC_VERBOSE")) fprintf(stderr, "[p2p] CUDA IPC unavailable: NCCL transfers\n");
+  p2p_close();
+  p2p_free();
+  g_p2p.W = (size_t)-1;  // permanently off
+}
+
 size_t key_of_row(const uint64_t* row, uint32_t B, size_t n, size_t m, const size_t* bits) {
   size_t key = 0;
   for (size_t b = 0; b < m; ++b) {
@@ -146,8 +250,14 @@ void multi_init(const void* uid128, int rank, int world) {
   }
 }
 
+void multi_prepare(DeviceStore& s) { p2p_prepare(s.M, 2 * (size_t)s.B); }
+
 void multi_shutdown() {
   if (g_comm.comm) {
+    cudaDeviceSynchronize();
+    p2p_close();
+    p2p_free();
+    g_p2p = P2P{};
     ncclCommDestroy(g_comm.comm);
     g_comm = Comm{};
   }
@@ -156,7 +266,7 @@ void multi_shutdown() {
 void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner,
                          const uint64_t* gen_row, double cs, double sn, double eps,
                          size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out,
-                         const uint64_t* next_row) {
+                         const uint64_t* next_row, double theta, double exact, bool* spec_failed) {
   Comm& c = comm();
   if (((size_t)1 << m) != (size_t)c.world)
     throw std::invalid_argument("parallel_dress: one partition per rank (2^m == world) required");
@@ -174,16 +284,23 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
   }
   const size_t mask = key_of_row(ref_row.data(), Bref, s.n_qubits, m, bits);
   const bool want_hist = eps > 0.0 || max_terms != SIZE_MAX;
+  if (!want_hist) theta = exact = 0.0;  // no compress follows: every term keeps a slot
+  const bool exch = !(mask == 0 || sn == 0.0);
+  const size_t M0 = s.M, L0 = s.logical;
+  const Filter F0 = s.filt;
   DressOutcome o;
   iqcc_exchange_stats x{mask, 0, 0, 0, 0};
-  if (mask == 0 || sn == 0.0) {
-    o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps, next_row);
+  size_t nrecv = 0;
+  ull* rk = nullptr;
+  double* rv = nullptr;
+  if (!exch) {
+    o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps, next_row, theta);
   } else {
     cudaStream_t st = stream();
     Workspace& ws = workspace();
     // plan, then swap the product counts with the partner straight from
     // device memory: one round trip gives both A and the receive count
-    const long long* a_dev = plan_products_async(s, gen_row);
+    const long long* a_dev = plan_products_async(s, gen_row, cs, sn, theta);
     const int peer = (int)owner[mine ^ mask];
     ull* cnt = scratch(4);
     if (a_dev)
@@ -191,7 +308,7 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     else
       IQCC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(ull), st));
     {
-      KernelScope ks("exchange");
+      KernelScope ks("exch_count");
       IQCC_NCCL(ncclGroupStart());
       IQCC_NCCL(ncclSend(cnt, 1, ncclUint64, peer, c.comm, st));
       IQCC_NCCL(ncclRecv(cnt + 1, 1, ncclUint64, peer, c.comm, st));
@@ -201,18 +318,36 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     IQCC_CUDA(cudaMemcpyAsync(hp, cnt, 2 * sizeof(ull), cudaMemcpyDeviceToHost, st));
     host_sync(st);
     const size_t A = hp[0];
-    const ull nrecv = hp[1];
+    nrecv = hp[1];
     plan_set_products(A);
     const size_t W = 2 * s.B;
+    // both ends see the same (A, nrecv) and the same agreed capacity
+    const bool p2p = g_p2p.ok && g_p2p.W == W && A <= g_p2p.cap && nrecv <= g_p2p.cap;
     // exchange buffers sized by the shard (products <= terms), so they do
     // not regrow from step to step
     const size_t xcap = std::max<size_t>({A, nrecv, s.M, 1});
-    ull* sk = ws.xbuf_keys.as<ull>(xcap * W);
-    double* sv = ws.xbuf_coef.as<double>(xcap);
-    materialize_products(s, gen_row, sn, sk, sv);
-    ull* rk = ws.rbuf_keys.as<ull>(xcap * W);
-    double* rv = ws.rbuf_coef.as<double>(xcap);
-    {
+    ull* sk = p2p ? nullptr : ws.xbuf_keys.as<ull>(xcap * W);
+    double* sv = p2p ? nullptr : ws.xbuf_coef.as<double>(xcap);
+    if (p2p) {
+      // the SMs gather the sorted products and write them, tile by tile,
+      // straight into the partner's receive buffer over NVLink
+      char* dst = g_p2p.peer[peer];
+      push_products(s, gen_row, sn, reinterpret_cast<ull*>(dst),
+                    reinterpret_cast<double*>(dst + g_p2p.cap * W * 8));
+      KernelScope ks2("exch_signal");
+      rk = reinterpret_cast<ull*>(g_p2p.mine);
+      rv = reinterpret_cast<double*>(g_p2p.mine + g_p2p.cap * W * 8);
+      // push done -> the partner may merge (and my own products arrived)
+      IQCC_NCCL(ncclGroupStart());
+      IQCC_NCCL(ncclSend(cnt, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclRecv(cnt + 2, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclGroupEnd());
+    } else {
+      materialize_products(s, gen_row, sn, sk, sv);
+      rk = ws.rbuf_keys.as<ull>(xcap * W);
+      rv = ws.rbuf_coef.as<double>(xcap);
+    }
+    if (!p2p) {
       KernelScope ks("exchange");
       IQCC_NCCL(ncclGroupStart());
       if (A) {
@@ -229,18 +364,42 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     x.recv_terms = nrecv;
     x.bytes_wire = A * (W * 8 + 8);
     x.bytes_reference = A * (16 + Bref * 16);  // MessageLog formula, partition.hpp:420-422
-    o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row);
+    recv_slot_bits(rv, nrecv, theta);
+    o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, theta);
   }
   if (xs) *xs = x;
   NcclReducer red;
-  bool run = eps > 0.0;  // compress_partitioned always runs with a cut
-  if (!run) {
-    ull tot[1] = {(ull)s.logical};
-    red.sum(tot, 1);
-    run = tot[0] > max_terms;
+  if (!want_hist) return;  // eps == 0 and no cap: compress_partitioned is a no-op
+  // global counts of the step: count_eps, |c| >= theta, identity
+  ull glob[3] = {(ull)o.count_eps, (ull)o.n_ge_theta, (ull)(s.has_identity ? 1 : 0)};
+  red.sum(glob, 3);
+  if (theta > exact) {
+    // the slotted shards compress like the full ones iff the global top
+    // `budget` terms are all >= theta and either the compress cuts or no
+    // term below theta held a slot (as in the single-device sequence)
+    const ull idc = glob[2] ? 1 : 0;
+    const ull budget = max_terms - idc;
+    const bool ok = glob[1] >= budget && (glob[0] > max_terms || glob[0] == glob[1] + idc);
+    if (!ok) {  // every rank sees the same sums and redoes the step exactly
+      dress_undo(s, M0, L0, F0);
+      if (!exch) {
+        o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps, next_row, exact);
+      } else {  // the received products stay; only the slot bits change
+        plan_survivors(s, gen_row, cs, sn, exact);
+        recv_slot_bits(rv, nrecv, exact);
+        o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, exact);
+      }
+      glob[0] = o.count_eps;
+      glob[1] = o.n_ge_theta;
+      glob[2] = s.has_identity ? 1 : 0;
+      red.sum(glob, 3);
+      if (spec_failed) *spec_failed = true;
+    }
   }
-  if (run) {
-    CompressResult r = compress_store(s, eps, max_terms, want_hist, o.count_eps, cs_out != nullptr, &red);
+  if (eps > 0.0 || glob[0] > max_terms) {  // compress_partitioned always runs with a cut
+    const ull gk[2] = {glob[0], glob[2]};
+    CompressResult r =
+        compress_store(s, eps, max_terms, true, o.count_eps, cs_out != nullptr, &red, gk);
     if (cs_out) {
       cs_out->dropped_terms += r.dropped_terms;
       cs_out->dropped_weight += r.dropped_weight;

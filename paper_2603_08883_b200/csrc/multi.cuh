@@ -7,10 +7,14 @@ namespace iqcc_b200 {
 void multi_unique_id(void* out128);
 void multi_init(const void* uid128, int rank, int world);
 void multi_shutdown();
+/// Collective at the start of every partitioned call: (re)size the CUDA IPC
+/// receive buffers of the NVLink product push to the largest shard.
+void multi_prepare(DeviceStore& s);
 void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner,
                          const uint64_t* gen_row, double cs, double sn, double eps,
                          size_t max_terms, iqcc_exchange_stats* xs, iqcc_compress_stats* cs_out,
-                         const uint64_t* next_row = nullptr);
+                         const uint64_t* next_row = nullptr, double theta = 0.0,
+                         double exact = 0.0, bool* spec_failed = nullptr);
 /// Sum of a host value over the ranks (one allreduce).
 size_t parallel_sum(size_t v);
 double parallel_expect_store(DeviceStore& s, const double* factors);

@@ -909,7 +909,8 @@ __global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __r
 }
 
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
-                              size_t count_eps, bool want_stats, Reducer* red) {
+                              size_t count_eps, bool want_stats, Reducer* red,
+                              const ull* glob_known) {
   HostScope hscope("host_compress_inner");
   if (eps < 0) throw std::invalid_argument("compress: epsilon < 0");
   if (max_terms < 1) throw std::invalid_argument("compress: max_terms < 1");
@@ -942,7 +943,13 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
   }
   // global view (compress_partitioned: per-shard eps cut, one global budget)
   ull glob[2] = {(ull)count_eps, (ull)(s.has_identity ? 1 : 0)};
-  if (red) red->sum(glob, 2);
+  if (red && glob_known && !hist_ready) throw std::logic_error("compress: stale global counts");
+  if (red && glob_known) {
+    glob[0] = glob_known[0];
+    glob[1] = glob_known[1];
+  } else if (red) {
+    red->sum(glob, 2);
+  }
   Filter f;
   f.active = 1;
   f.eps = eps;

@@ -584,7 +584,8 @@ class Partition:
         cst = native.CompressStatsC()
         tin = C.c_size_t(0)
         check(lib.iqcc_gpu_parallel_dress_sequence(d.handle, self.m, _addr(b), _addr(o), K, _addr(gens),
-                                                   _addr(cs_), _addr(sn_), eps, max_terms, xs, C.byref(cst),
+                                                   _addr(cs_), _addr(sn_), eps, max_terms, xs,
+                                                   C.byref(cst) if stats is not None else None,
                                                    C.byref(tin)))
         if stats is not None:
             stats.dropped_terms += cst.dropped_terms

@@ -19,13 +19,22 @@ def n_gpus():
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("args", [("124", "2e5", "6", "1e-10", "2e5"), ("64", "1e5", "5", "0", "1e18"),
-                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq")])
+                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq"),
+                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "badspec"),
+                                  ("200", "1e5", "6", "1e-10", "1.2e5", "seq")])
 def test_partitioned_dressing_matches_serial(world, args):
+    """The sequence cases exercise the output-slot speculation on the
+    exchange and the local steps; "badspec" forces every guess too high
+    (IQCC_SPEC_SCALE), so every step is undone and redone exactly."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ)
+    if args[-1] == "badspec":
+        env["IQCC_SPEC_SCALE"] = "64"
+        args = args[:-1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "multi_worker.py"),
            *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "bitexact=True" in r.stdout and "energy_ok=True" in r.stdout
