@@ -1487,6 +1487,16 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   if (getenv("IQCC_DEBUG")) debug_check("merge");
 }
 
+Reducer* g_merge_red = nullptr;
+
+__global__ void k_pack_glob(ull* ctr, ull identity) {
+  if (threadIdx.x == 0) {
+    ctr[8] = ctr[1];
+    ctr[9] = ctr[6];
+    ctr[10] = identity;
+  }
+}
+
 template <int B>
 DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys,
                         const double* q_vals, double cs, double sn, double drop, bool want_hist,
@@ -1510,8 +1520,12 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   ull* ctr = ws.counters.as<ull>(16);
-  ull* hc = static_cast<ull*>(host_pinned(8 * sizeof(ull)));
-  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, 8 * sizeof(ull), cudaMemcpyDeviceToHost, st));
+  ull* hc = static_cast<ull*>(host_pinned(16 * sizeof(ull)));
+  if (g_merge_red) {
+    k_pack_glob<<<1, 32, 0, st>>>(ctr, s.has_identity ? 1ull : 0ull);
+    g_merge_red->sum_device(ctr + 8, 3);
+  }
+  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, (g_merge_red ? 11 : 8) * sizeof(ull), cudaMemcpyDeviceToHost, st));
   host_sync(st);
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
@@ -1532,6 +1546,10 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
   out.n_anticommuting = g_plan.A;
   out.n_ge_theta = hc[6];
   out.n_pairs = hc[5];
+  if (g_merge_red) {
+    out.has_glob = true;
+    for (int k = 0; k < 3; ++k) out.glob[k] = hc[8 + k];
+  }
   return out;
 }
 
@@ -1674,6 +1692,8 @@ void recv_slot_bits(const double* rv, size_t n, double thq) {
 }
 
 void plan_set_products(size_t A) { g_plan.A = A; }
+
+void set_merge_reducer(Reducer* red) { g_merge_red = red; }
 
 size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products) {
   switch (s.B) {

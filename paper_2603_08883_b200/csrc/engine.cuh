@@ -411,7 +411,15 @@ struct DressOutcome {
   size_t count_eps = 0;  // emitted terms passing (identity || |c| >= eps)
   size_t n_ge_theta = 0;  // emitted non-identity terms with |c| >= theta (theta > 0 only)
   size_t n_pairs = 0;     // survivor/product partner pairs (same word)
+  // partitioned steps (merge_reducer set): {count_eps, n_ge_theta, identity}
+  // summed over the ranks, fetched with the merge counters (one round trip)
+  bool has_glob = false;
+  unsigned long long glob[3] = {0, 0, 0};
 };
+struct Reducer;
+/// While set, every merge also allreduces its (count_eps, n_ge_theta,
+/// identity) on the device before the counter read-back.
+void set_merge_reducer(Reducer* red);
 /// One dressing step in place; if want_hist, also accumulates the |c|
 /// histogram of emitted terms for a following compress(eps).
 /// next_row (optional, device-width row): the entangler of the following

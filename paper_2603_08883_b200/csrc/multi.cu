@@ -293,6 +293,11 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
   size_t nrecv = 0;
   ull* rk = nullptr;
   double* rv = nullptr;
+  NcclReducer red;
+  struct Hook {  // merges of this step allreduce their counts on the device
+    explicit Hook(Reducer* r) { set_merge_reducer(r); }
+    ~Hook() { set_merge_reducer(nullptr); }
+  } hook(want_hist ? &red : nullptr);
   if (!exch) {
     o = dress_step(s, gen_row, cs, sn, 1e-12, want_hist, eps, next_row, theta);
   } else {
@@ -368,11 +373,13 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, theta);
   }
   if (xs) *xs = x;
-  NcclReducer red;
   if (!want_hist) return;  // eps == 0 and no cap: compress_partitioned is a no-op
   // global counts of the step: count_eps, |c| >= theta, identity
   ull glob[3] = {(ull)o.count_eps, (ull)o.n_ge_theta, (ull)(s.has_identity ? 1 : 0)};
-  red.sum(glob, 3);
+  if (o.has_glob)
+    std::copy(o.glob, o.glob + 3, glob);
+  else
+    red.sum(glob, 3);
   if (theta > exact) {
     // the slotted shards compress like the full ones iff the global top
     // `budget` terms are all >= theta and either the compress cuts or no
@@ -392,7 +399,10 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
       glob[0] = o.count_eps;
       glob[1] = o.n_ge_theta;
       glob[2] = s.has_identity ? 1 : 0;
-      red.sum(glob, 3);
+      if (o.has_glob)
+        std::copy(o.glob, o.glob + 3, glob);
+      else
+        red.sum(glob, 3);
       if (spec_failed) *spec_failed = true;
     }
   }
