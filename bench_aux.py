@@ -1,0 +1,256 @@
+#!/usr/bin/env python3
+"""bench_aux.py — the SURVEY.md §8(d) configs other than the headline C3 line.
+
+bench.py carries the driver's one-line contract (C3 dressing throughput);
+this script measures the remaining §8(d) rows on one B200 and prints one
+JSON object per row (profiles/r1_aux_*.json keeps the committed copy):
+
+  C2      G_uniform(64, 1e6, seed 1): one 4-qubit entangler (tau 0.37, drop
+          1e-12) + compress(1e-3), and the max_terms = 1.2e6 variant
+          (latency-dominated; roofline (M_in + M_out) * 24 B)
+  energy  expect_sum / qmf_energy_gradient on G_mol(124, 1e8, seed 2) at a
+          generic Omega (HBM: M * 40 B per call)
+  C4      DIS gradient sweep on G_mol(100, 1e7, seed 3): odd-Y candidates
+          (seed 4) at a generic Omega (compute-bound, pairs/s) and at HF
+          poles with the flip-group restriction (group_gradient)
+  C5      200-qubit slice: G_mol(200, 5e7, seed 5) dressed without a cap
+          until > 1.25e8 terms (the per-GPU share of 1e9 over 8 B200), then
+          compress(max_terms = 1.25e8) (truncation time)
+
+Times are device-synchronous wall clock around the public API calls (each
+call ends with a stream synchronize), after a warm-up call.  Synthetic data
+only; nothing here reads /root/reference or oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+HBM_GBS = 6551.0
+
+
+def peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return HBM_GBS
+
+
+def brev64(a: np.ndarray) -> np.ndarray:
+    a = a.astype(np.uint64)
+    out = np.zeros_like(a)
+    for b in range(64):
+        out |= ((a >> np.uint64(b)) & np.uint64(1)) << np.uint64(63 - b)
+    return out
+
+
+def g_uniform(n: int, m: int, seed: int):
+    """iid letters over {I,X,Y,Z}, U(-1,1) coefficients, canonical order
+    (iqcc/pauli.hpp:146-161: lowest bit most significant, x plane first),
+    duplicates dropped (tests/helpers.hpp:74-99 semantics)."""
+    from paper_2603_08883_b200 import iqcc
+    assert n == 64
+    rs = np.random.default_rng(seed)
+    x = rs.integers(0, 2**63, m, dtype=np.uint64) | (rs.integers(0, 2, m, dtype=np.uint64) << np.uint64(63))
+    z = rs.integers(0, 2**63, m, dtype=np.uint64) | (rs.integers(0, 2, m, dtype=np.uint64) << np.uint64(63))
+    kx, kz = brev64(x), brev64(z)
+    order = np.lexsort((kz, kx))
+    x, z, kx, kz = x[order], z[order], kx[order], kz[order]
+    keep = np.ones(m, bool)
+    keep[1:] = (kx[1:] != kx[:-1]) | (kz[1:] != kz[:-1])
+    rows = np.stack([x[keep], z[keep]], axis=1)
+    c = rs.uniform(-1.0, 1.0, int(keep.sum())).astype(np.complex128)
+    return iqcc.PauliSum(n, rows, c)
+
+
+def word(n, qs, ys):
+    from paper_2603_08883_b200 import iqcc
+    p = iqcc.PauliWord(n)
+    B = iqcc.blocks_for(n)
+    for q, y in zip(qs, ys):
+        p.row[q // 64] |= np.uint64(1 << (q % 64))
+        if y:
+            p.row[B + q // 64] |= np.uint64(1 << (q % 64))
+    return p
+
+
+def odd_y_candidates(n, k, seed):
+    """DIS candidates as dis_candidates makes them (iqcc/dis.hpp:89-116):
+    random flip sets of 4 qubits, each with its 2^3 odd-#Y assignments (one
+    support per group of 8 candidates)."""
+    from paper_2603_08883_b200 import iqcc
+    rs = np.random.default_rng(seed)
+    B = iqcc.blocks_for(n)
+    out = np.zeros((k, 2 * B), np.uint64)
+    i = 0
+    while i < k:
+        qs = sorted(int(q) for q in rs.choice(n, 4, replace=False))
+        for m in range(16):
+            if bin(m).count("1") % 2 == 1 and i < k:
+                out[i] = word(n, qs, [(m >> b) & 1 for b in range(4)]).row
+                i += 1
+    return out
+
+
+def timed(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return best, r
+
+
+def row(name, **kv):
+    d = {"config": name, **kv}
+    print(json.dumps(d), flush=True)
+    return d
+
+
+def run_c2(args):
+    from paper_2603_08883_b200 import iqcc
+    h = g_uniform(64, 1_000_000, 1)
+    base = iqcc.DeviceSum.upload(h)
+    p = word(64, [3, 17, 40, 59], [1, 0, 0, 0])
+    out = []
+    for cap in (None, 1_200_000):
+        def once():
+            d = base.clone()
+            t0 = time.perf_counter()
+            st = d.dress(p, 0.37, 1e-12)
+            d.compress(1e-3, cap if cap else iqcc.U64_MAX)
+            import torch
+            torch.cuda.synchronize()
+            return time.perf_counter() - t0, st.n_in, st.n_out, len(d)
+        once()
+        best = min(once() for _ in range(5))
+        secs, nin, nout, kept = best
+        S = 24
+        out.append(row("C2", variant="max_terms=1.2e6" if cap else "eps=1e-3", n_in=nin, n_out=nout,
+                       kept=kept, ms=1e3 * secs, terms_per_s=nin / secs,
+                       hbm_frac=(nin + nout) * S / secs / 1e9 / peak(),
+                       note="dress + compress, host-synchronous; latency-dominated at 1e6 terms"))
+    return out
+
+
+def run_energy(args):
+    from paper_2603_08883_b200 import iqcc
+    n, m = 124, int(args.energy_terms)
+    d = iqcc.DeviceSum.generate_mol(n, m, 2)
+    rs = np.random.default_rng(7)
+    om = iqcc.QmfState(rs.uniform(-3, 3, n), rs.uniform(-3, 3, n))
+    S = 40
+    t, e = timed(lambda: d.expect(om))
+    r1 = row("energy", op="expect_sum", n_qubits=n, terms=m, ms=1e3 * t, terms_per_s=m / t,
+             gbs=m * S / t / 1e9, hbm_frac=m * S / t / 1e9 / peak(), energy=e)
+    t2, _ = timed(lambda: d.qmf_energy_gradient(om))
+    r2 = row("energy", op="qmf_energy_gradient", n_qubits=n, terms=m, ms=1e3 * t2, terms_per_s=m / t2,
+             gbs=m * S / t2 / 1e9, hbm_frac=m * S / t2 / 1e9 / peak())
+    return [r1, r2]
+
+
+def run_c4(args):
+    from paper_2603_08883_b200 import iqcc
+    n, m = 100, int(args.dis_terms)
+    d = iqcc.DeviceSum.generate_mol(n, m, 3)
+    rs = np.random.default_rng(9)
+    generic = iqcc.QmfState(rs.uniform(-3, 3, n), rs.uniform(-3, 3, n))
+    hf = iqcc.hf_reference([q < n // 4 for q in range(n)])
+    out = []
+    kg = int(args.dis_generic)
+    cands = odd_y_candidates(n, max(kg, int(args.dis_poles)), 4)
+    mg = int(args.dis_generic_terms)
+    dg = iqcc.DeviceSum.generate_mol(n, mg, 3) if mg != m else d
+    t, g = timed(lambda: dg.gradients(generic, cands[:kg]), reps=1)
+    out.append(row("C4", omega="generic", n_qubits=n, terms=mg, candidates=kg, s=t,
+                   pairs_per_s=kg * mg / t,
+                   note="bit-exact per candidate (sequential canonical-order sum); compute-bound: "
+                        "one fp64 multiply per qubit of supp(T) | supp(P) per anticommuting pair"))
+    del dg
+    kp = int(args.dis_poles)
+    t, g = timed(lambda: d.gradients(hf, cands[:kp], True), reps=1)
+    out.append(row("C4", omega="HF poles, flip-group restricted", n_qubits=n, terms=m, candidates=kp, s=t,
+                   candidates_per_s=kp / t, nonzero=int(np.count_nonzero(g))))
+    return out
+
+
+def run_c5(args):
+    from paper_2603_08883_b200 import iqcc
+    import torch
+    n = 200
+    d = iqcc.DeviceSum.generate_mol(n, int(args.c5_terms), 5)
+    target = int(args.c5_target)
+    steps, tin, secs = 0, 0, 0.0
+    k = 0
+    while len(d) <= target and steps < 12:
+        rs = np.random.default_rng([5, k])
+        w = int(rs.integers(2, 5))
+        qs = [int(q) for q in rs.choice(n, w, replace=False)]
+        ys = [int(y) for y in rs.integers(0, 2, w)]
+        if sum(ys) % 2 == 0:
+            ys[-1] ^= 1
+        p = word(n, qs, ys)
+        tau = float(rs.uniform(-0.2, 0.2))
+        k += 1
+        nin = len(d)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = d.dress(p, tau, 1e-12)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if st.n_anticommuting == 0:
+            continue
+        steps += 1
+        tin += nin
+        secs += dt
+    grown = len(d)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d.compress(1e-10, target)
+    torch.cuda.synchronize()
+    tc = time.perf_counter() - t0
+    return [row("C5", n_qubits=n, start_terms=int(args.c5_terms), steps=steps, grown_to=grown,
+                dress_terms_per_s=tin / secs if secs else None, compress_to=len(d), compress_ms=1e3 * tc,
+                compress_gbs=grown * 72 / tc / 1e9,
+                note="1-GPU slice of C5: per-GPU share of 1e9 terms over 8 B200 (no exchange)")]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="c2,energy,c4,c5")
+    ap.add_argument("--energy-terms", type=float, default=1e8)
+    ap.add_argument("--dis-terms", type=float, default=1e7)
+    ap.add_argument("--dis-generic", type=float, default=1e5)
+    ap.add_argument("--dis-generic-terms", type=float, default=1e6)
+    ap.add_argument("--dis-poles", type=float, default=1e5)
+    ap.add_argument("--c5-terms", type=float, default=5e7)
+    ap.add_argument("--c5-target", type=float, default=1.25e8)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+    torch.cuda.set_device(0)
+    from paper_2603_08883_b200 import native
+    native.init(0)
+    rows = []
+    for part in args.only.split(","):
+        rows += {"c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5}[part](args)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(rows, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

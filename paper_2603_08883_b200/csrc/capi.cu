@@ -207,6 +207,61 @@ static void profile_flush() {
   }
 }
 
+// Large buffers (stores, merge outputs, scratch of the hot path) come from
+// cudaMalloc: on B200 mapping fresh memory through the stream-ordered pool
+// costs ~15-50 ms per call (measured: 16 GB cudaMallocAsync 51 ms vs
+// cudaMalloc 1.8 ms), which dominated uncapped growth (C5).  cudaFree
+// synchronizes the device, so a large buffer is never freed under a running
+// kernel.  Small buffers stay stream-ordered.
+constexpr size_t kBigAlloc = (size_t)32 << 20;
+
+// Freed large blocks are cached for reuse (the engine runs on one stream, so
+// a block handed out again is only touched by later work in stream order);
+// a cached block serves requests between half its size and its size.
+struct BigCache {
+  std::vector<std::pair<void*, size_t>> blocks;
+  size_t bytes = 0;
+};
+static BigCache g_big;
+
+static void big_release_all() {
+  if (g_big.blocks.empty()) return;
+  cudaDeviceSynchronize();
+  for (auto& b : g_big.blocks) cudaFree(b.first);
+  g_big.blocks.clear();
+  g_big.bytes = 0;
+}
+
+static void* big_take(size_t want, size_t* got) {
+  size_t best = SIZE_MAX;
+  for (size_t i = 0; i < g_big.blocks.size(); ++i) {
+    const size_t b = g_big.blocks[i].second;
+    if (b >= want && b / 2 <= want && (best == SIZE_MAX || b < g_big.blocks[best].second)) best = i;
+  }
+  if (best == SIZE_MAX) return nullptr;
+  void* p = g_big.blocks[best].first;
+  *got = g_big.blocks[best].second;
+  g_big.bytes -= *got;
+  g_big.blocks.erase(g_big.blocks.begin() + best);
+  return p;
+}
+
+static void devbuf_free(void* p, bool big, size_t bytes) {
+  if (!p) return;
+  if (big) {
+    g_big.blocks.emplace_back(p, bytes);
+    g_big.bytes += bytes;
+    // bound the cache (largest blocks leave last): at most 64 blocks
+    while (g_big.blocks.size() > 64) {
+      IQCC_CUDA(cudaFree(g_big.blocks.front().first));
+      g_big.bytes -= g_big.blocks.front().second;
+      g_big.blocks.erase(g_big.blocks.begin());
+    }
+  } else {
+    IQCC_CUDA(cudaFreeAsync(p, stream()));
+  }
+}
+
 void* DevBuf::get(size_t n) {
   if (n <= bytes && p) return p;
   HostScope hs("host_alloc");
@@ -217,19 +272,31 @@ void* DevBuf::get(size_t n) {
     fprintf(stderr, "[alloc] buf@ws+%td n=%zu had=%zu\n",
             (const char*)this - (const char*)&w, n, bytes);
   }
-  if (p) IQCC_CUDA(cudaFreeAsync(p, st));
+  devbuf_free(p, big, bytes);
   p = nullptr;
+  bytes = 0;
   size_t want = std::max<size_t>(n + n / 2, 256);  // generous slack: stores grow ~1.5x per step
-  cudaError_t e = cudaMallocAsync(&p, want, st);
+  big = want >= kBigAlloc;
+  if (big) {
+    size_t got = 0;
+    if ((p = big_take(n, &got)) != nullptr) {
+      bytes = got;
+      return p;
+    }
+  }
+  cudaError_t e = big ? cudaMalloc(&p, want) : cudaMallocAsync(&p, want, st);
   if (e != cudaSuccess) {
-    // retry without slack once the pool has released cached blocks
+    // retry without slack once the caches have released their blocks
     cudaGetLastError();
+    if (verbose) fprintf(stderr, "[alloc] %zu bytes failed: release the caches and retry\n", want);
     IQCC_CUDA(cudaStreamSynchronize(st));
+    big_release_all();
     cudaMemPool_t pool;
     IQCC_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx().device));
     cudaMemPoolTrimTo(pool, 0);
     want = std::max<size_t>(n, 256);
-    e = cudaMallocAsync(&p, want, st);
+    big = want >= kBigAlloc;
+    e = big ? cudaMalloc(&p, want) : cudaMallocAsync(&p, want, st);
     if (e != cudaSuccess) {
       cudaGetLastError();
       p = nullptr;
@@ -242,9 +309,15 @@ void* DevBuf::get(size_t n) {
 }
 
 void DevBuf::release() {
-  if (p && g_ctx) cudaFreeAsync(p, g_ctx->cur);
+  if (p && g_ctx) {
+    if (big)
+      devbuf_free(p, true, bytes);
+    else
+      cudaFreeAsync(p, g_ctx->cur);
+  }
   p = nullptr;
   bytes = 0;
+  big = false;
 }
 
 void Workspace::release_all() {
@@ -348,6 +421,7 @@ int iqcc_gpu_finalize(void) {
     multi_shutdown();
     g_ctx->ws.release_all();
     cudaStreamSynchronize(g_ctx->cur);
+    big_release_all();
     if (g_ctx->pinned) cudaFreeHost(g_ctx->pinned);
     cudaStreamDestroy(g_ctx->own);
     delete g_ctx;

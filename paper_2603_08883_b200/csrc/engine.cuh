@@ -347,6 +347,7 @@ struct KernelScope {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool big = false;  // cudaMalloc (large) vs stream-ordered pool (small)
   void* get(size_t n);
   template <class T>
   T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }

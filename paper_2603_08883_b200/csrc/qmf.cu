@@ -64,14 +64,44 @@ struct TwoSum {  // Neumaier compensated accumulator
   }
 };
 
+// Factor rows F4[q][code], code = x | z << 1 (0: I -> 1.0, 1: X, 2: Z, 3: Y),
+// 64*B rows (padding qubits are identities).  Every lane of a warp walks the
+// qubits in the same ascending order, so the table reads of a warp hit one
+// 32-byte row (one shared-memory wavefront) and there is no divergence;
+// identity positions multiply by 1.0, which is exact, so the product is
+// bit-identical to expect_word's product over the support only
+// (iqcc/qmf.hpp:67-80).
+template <int B, class Fn>
+__device__ __forceinline__ void for_each_qubit_code(const Key<B>& k, Fn&& fn) {
+#pragma unroll
+  for (int w = 0; w < B; ++w) {
+#pragma unroll
+    for (int h = 1; h >= 0; --h) {  // device bits 63..32 hold qubits 64w + 0..31
+      const unsigned xh = (unsigned)(k.w[w] >> (32 * h)), zh = (unsigned)(k.w[B + w] >> (32 * h));
+#pragma unroll
+      for (int b = 31; b >= 0; --b) {
+        const int q = 64 * w + (1 - h) * 32 + (31 - b);
+        fn(q, ((xh >> b) & 1u) | (((zh >> b) & 1u) << 1));
+      }
+    }
+  }
+}
+
+template <int B>
+__device__ __forceinline__ double lockstep_expect(const Key<B>& k, const double* __restrict__ f4) {
+  double val = 1.0;
+  for_each_qubit_code<B>(k, [&](int q, unsigned code) { val = __dmul_rn(val, f4[4 * q + code]); });
+  return val;
+}
+
 template <int B>
 __global__ void __launch_bounds__(256) k_expect(const ull* __restrict__ keys,
                                                 const double* __restrict__ coef, size_t M,
-                                                Filter filt, const double* __restrict__ tab_g,
-                                                int nq, double* __restrict__ partial) {
-  extern __shared__ double tab[];
+                                                Filter filt, const double* __restrict__ f4_g,
+                                                double* __restrict__ partial) {
+  __shared__ double f4[4 * 64 * B];
   __shared__ double rs[256], rc[256];
-  for (int i = threadIdx.x; i < 3 * nq; i += blockDim.x) tab[i] = tab_g[i];
+  for (int i = threadIdx.x; i < 4 * 64 * B; i += blockDim.x) f4[i] = f4_g[i];
   __syncthreads();
   TwoSum acc;
   const size_t per = (M + gridDim.x - 1) / gridDim.x;
@@ -80,7 +110,7 @@ __global__ void __launch_bounds__(256) k_expect(const ull* __restrict__ keys,
     const Key<B> k = load_key<B>(keys, i);
     const double c = coef[i];
     if (!filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k))) continue;
-    acc.add(__dmul_rn(c, word_expect<B>(k, tab)));
+    acc.add(__dmul_rn(c, lockstep_expect<B>(k, f4)));
   }
   rs[threadIdx.x] = acc.s;
   rc[threadIdx.x] = acc.c;
@@ -98,6 +128,17 @@ __global__ void __launch_bounds__(256) k_expect(const ull* __restrict__ keys,
     partial[2 * blockIdx.x] = rs[0];
     partial[2 * blockIdx.x + 1] = rc[0];
   }
+}
+
+/// F4 rows from the host factor table [nq][3] = (X, Z, Y).
+static std::vector<double> factor_rows(const double* factors, int nq, uint32_t B) {
+  std::vector<double> f4((size_t)4 * 64 * B, 1.0);
+  for (int q = 0; q < nq; ++q) {
+    f4[4 * q + 1] = factors[3 * q + 0];
+    f4[4 * q + 2] = factors[3 * q + 1];
+    f4[4 * q + 3] = factors[3 * q + 2];
+  }
+  return f4;
 }
 
 static std::vector<double> fetch(const double* d, size_t n) {
@@ -124,115 +165,153 @@ double expect_store(DeviceStore& s, const double* factors) {
   cudaStream_t st = stream();
   if (s.logical == 0) return 0.0;
   const int nq = (int)s.n_qubits;
-  double* tab = ws.tables.as<double>(3 * (size_t)std::max(nq, 1));
-  IQCC_CUDA(cudaMemcpyAsync(tab, factors, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, st));
-  const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (s.M + 1023) / 1024));
+  const std::vector<double> f4 = factor_rows(factors, nq, s.B);
+  double* tab = ws.tables.as<double>(f4.size());
+  IQCC_CUDA(cudaMemcpyAsync(tab, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  const unsigned grid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (s.M + 1023) / 1024));
   double* part = ws.partials.as<double>(2 * grid);
-  const size_t smem = 3 * (size_t)std::max(nq, 1) * sizeof(double);
   {
     KernelScope ks("expect");
     switch (s.B) {
-      case 1: k_expect<1><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, nq, part); break;
-      case 2: k_expect<2><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, nq, part); break;
-      default: k_expect<4><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, nq, part); break;
+      case 1: k_expect<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, part); break;
+      case 2: k_expect<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, part); break;
+      default: k_expect<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, part); break;
     }
   }
   return host_sum_pairs(fetch(part, 2 * grid));
 }
 
 // -------------------------------------------------------- QMF gradient
-// One term per warp.  Lane L owns qubits [QPL*L, QPL*L+QPL).  Factors of
-// identity positions are 1.0 (exact), so the products equal the support-only
-// products up to association; rest_k = prefix_k * suffix_k.
-template <int B>
-__global__ void __launch_bounds__(256) k_qmf_grad(const ull* __restrict__ keys,
+// d/d angle_k of c * prod_j f_j is c * rest_k * f'_k with rest_k the product
+// of the other factors.  For a term without a zero factor rest_k * f'_k =
+// P * (f'_k / f_k), so the gradient is a weighted histogram:
+//   g[k] = sum_code R[k][code] * H[k][code],  H[k][code] = sum of c*P over
+//   the terms with letter `code` at qubit k,   R = f' / f  (host, per Omega).
+// A term with exactly one zero factor (at k0) contributes only to k0:
+// c * P_nz * f'_k0 (P_nz = product of its nonzero factors); two or more
+// zeros contribute nothing (iqcc/qmf.hpp:94-148, prefix/suffix products).
+// Phase 1 (thread per term): the product in lockstep (as expect), staged in
+// shared memory with the term's key.  Phase 2 (thread per qubit): every
+// qubit's thread walks the staged batch and adds each weight to the bin of
+// the term's letter at that qubit (two-level sums: per batch, then running).
+// Deterministic: fixed batches per block, blocks summed on the host in order.
+constexpr int kQB = 256;  // terms per batch = threads per block
+
+template <int B, bool ZEROS>
+__global__ void __launch_bounds__(kQB) k_qmf_grad(const ull* __restrict__ keys,
                                                   const double* __restrict__ coef, size_t M,
-                                                  Filter filt, const double* __restrict__ tab_g,
-                                                  const double* __restrict__ der_g, int nq,
+                                                  Filter filt, const double* __restrict__ f4_g,
+                                                  const unsigned char* __restrict__ zm_g, int nq,
                                                   double* __restrict__ partial) {
-  constexpr int QPL = 2 * B;  // qubits per lane: 64*B / 32
-  extern __shared__ double sm[];
-  double* tab = sm;                  // [nq][3]
-  double* der = tab + 3 * nq;        // [nq][6]
-  double* wgrad = der + 6 * nq;      // [8 warps][2 nq]
-  __shared__ double es[8], ec[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 3 * nq; i += blockDim.x) tab[i] = tab_g[i];
-  for (int i = threadIdx.x; i < 6 * nq; i += blockDim.x) der[i] = der_g[i];
-  for (int i = threadIdx.x; i < 16 * nq; i += blockDim.x) wgrad[i] = 0.0;
+  __shared__ double f4[4 * 64 * B];
+  __shared__ unsigned char zm[64 * B];  // bit `code`: that factor is zero
+  __shared__ ull skx[kQB * B], skz[kQB * B];  // staged keys (x / z planes)
+  __shared__ double wa[kQB], wb[kQB];
+  __shared__ int k0s[kQB];
+  __shared__ double rs[kQB], rc[kQB];
+  for (int i = threadIdx.x; i < 4 * 64 * B; i += kQB) f4[i] = f4_g[i];
+  for (int i = threadIdx.x; i < 64 * B; i += kQB) zm[i] = ZEROS ? zm_g[i] : 0;
   __syncthreads();
-  double* mg = wgrad + (size_t)warp * 2 * nq;
+  // phase 2: TPQ threads per qubit slot, each summing every TPQ-th staged term
+  constexpr int TPQ = 4 / B;
+  const int k = threadIdx.x % (64 * B), part = threadIdx.x / (64 * B);
+  // 32-bit half of the staged word holding the qubit, and the bit in it
+  const int kw = k >> 6, khalf = (k & 63) < 32 ? 1 : 0, kb = 31 - (k & 31);
+  double h[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
   TwoSum e;
-  const size_t nw = (size_t)gridDim.x * 8;
-  for (size_t i = blockIdx.x * (size_t)8 + warp; i < M; i += nw) {
-    const Key<B> k = load_key<B>(keys, i);
-    const double c = coef[i];
-    if (!filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k))) continue;
-    double f[QPL];
-    int li[QPL];
-    double lp = 1.0;
+  for (size_t base = (size_t)blockIdx.x * kQB; base < M; base += (size_t)gridDim.x * kQB) {
+    const size_t i = base + threadIdx.x;
+    double a = 0.0, b1 = 0.0;
+    int k0 = -1;
+    Key<B> key;
 #pragma unroll
-    for (int t = 0; t < QPL; ++t) {
-      const int q = QPL * lane + t;
-      const int w = q >> 6, bit = 63 - (q & 63);
-      ull xw = 0, zw = 0;
-#pragma unroll
-      for (int j = 0; j < B; ++j) {
-        xw = (j == w) ? k.w[j] : xw;
-        zw = (j == w) ? k.w[B + j] : zw;
+    for (int w = 0; w < 2 * B; ++w) key.w[w] = 0;
+    if (i < M) {
+      key = load_key<B>(keys, i);
+      const double c = coef[i];
+      if (filter_keep(filt, i, c, i == 0 && key_is_identity<B>(key))) {
+        double p = 1.0;
+        int nz = 0;
+        for_each_qubit_code<B>(key, [&](int q, unsigned code) {
+          if (ZEROS && ((zm[q] >> code) & 1u)) {
+            ++nz;
+            k0 = q;
+          } else {
+            p = __dmul_rn(p, f4[4 * q + code]);
+          }
+        });
+        const double w = __dmul_rn(c, p);
+        if (nz == 0) {
+          a = w;
+          e.add(w);
+        } else if (nz == 1) {
+          b1 = w;
+        }
       }
-      const unsigned x = (unsigned)(xw >> bit) & 1u, z = (unsigned)(zw >> bit) & 1u;
-      li[t] = (x | z) && q < nq ? letter_index(x, z) : -1;
-      f[t] = li[t] >= 0 ? tab[3 * q + li[t]] : 1.0;
-      lp = __dmul_rn(lp, f[t]);
     }
-    // exclusive prefix / suffix of the lane products across the warp
-    double pre = lp, suf = lp;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double a = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre = __dmul_rn(a, pre);
-      const double b = __shfl_down_sync(0xffffffffu, suf, o);
-      if (lane + o < 32) suf = __dmul_rn(suf, b);
+    for (int w = 0; w < B; ++w) {
+      skx[threadIdx.x * B + w] = key.w[w];
+      skz[threadIdx.x * B + w] = key.w[B + w];
     }
-    const double total = __shfl_sync(0xffffffffu, pre, 31);
-    double pex = __shfl_up_sync(0xffffffffu, pre, 1);
-    double sex = __shfl_down_sync(0xffffffffu, suf, 1);
-    if (lane == 0) pex = 1.0;
-    if (lane == 31) sex = 1.0;
-    if (lane == 0) e.add(__dmul_rn(c, total));
-    double run = pex;  // product of factors before position t
+    wa[threadIdx.x] = a;
+    wb[threadIdx.x] = b1;
+    k0s[threadIdx.x] = k0;
+    __syncthreads();
+    if (k < nq) {
+      // four interleaved accumulator sets keep four independent add chains
+      double ba[4][3] = {};
+      const int n = (int)min((size_t)kQB, M - base);
+      const unsigned* sx32 = reinterpret_cast<const unsigned*>(skx) + 2 * kw + khalf;
+      const unsigned* sz32 = reinterpret_cast<const unsigned*>(skz) + 2 * kw + khalf;
+      for (int t0 = part; t0 < n; t0 += 4 * TPQ) {
 #pragma unroll
-    for (int t = 0; t < QPL; ++t) {
-      double after = sex;  // product of factors after position t
-#pragma unroll
-      for (int u = QPL - 1; u > t; --u) after = __dmul_rn(f[u], after);
-      if (li[t] >= 0) {
-        const int q = QPL * lane + t;
-        const double rest = __dmul_rn(run, after);
-        const double cr = __dmul_rn(c, rest);
-        mg[q] = __dadd_rn(mg[q], __dmul_rn(cr, der[6 * q + 2 * li[t]]));
-        mg[nq + q] = __dadd_rn(mg[nq + q], __dmul_rn(cr, der[6 * q + 2 * li[t] + 1]));
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * TPQ;
+          if (t < n) {
+            const unsigned code = ((sx32[2 * B * t] >> kb) & 1u) | (((sz32[2 * B * t] >> kb) & 1u) << 1);
+            const double v = wa[t];
+            if (code == 1) ba[u][0] = __dadd_rn(ba[u][0], v);
+            if (code == 2) ba[u][1] = __dadd_rn(ba[u][1], v);
+            if (code == 3) ba[u][2] = __dadd_rn(ba[u][2], v);
+            if (ZEROS && k0s[t] == k) {
+              const double w1 = wb[t];
+              if (code == 1) h1[0] = __dadd_rn(h1[0], w1);
+              if (code == 2) h1[1] = __dadd_rn(h1[1], w1);
+              if (code == 3) h1[2] = __dadd_rn(h1[2], w1);
+            }
+          }
+        }
       }
-      run = __dmul_rn(run, f[t]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        h[c] = __dadd_rn(h[c], __dadd_rn(__dadd_rn(ba[0][c], ba[1][c]), __dadd_rn(ba[2][c], ba[3][c])));
+    }
+    __syncthreads();
+  }
+  double* out = partial + (size_t)blockIdx.x * (6 * (size_t)nq * TPQ + 2);
+  if (k < nq) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      out[6 * ((size_t)nq * part + k) + c] = h[c];
+      out[6 * ((size_t)nq * part + k) + 3 + c] = h1[c];
     }
   }
-  if (lane == 0) {
-    es[warp] = e.s;
-    ec[warp] = e.c;
-  }
+  rs[threadIdx.x] = e.s;
+  rc[threadIdx.x] = e.c;
   __syncthreads();
-  double* out = partial + (size_t)blockIdx.x * (2 * nq + 2);
-  for (int j = threadIdx.x; j < 2 * nq; j += blockDim.x) {
-    double acc = 0.0;
-    for (int w = 0; w < 8; ++w) acc = __dadd_rn(acc, wgrad[(size_t)w * 2 * nq + j]);
-    out[j] = acc;
+  for (int o = kQB / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      TwoSum x{rs[threadIdx.x], rc[threadIdx.x]}, y{rs[threadIdx.x + o], rc[threadIdx.x + o]};
+      x.merge(y);
+      rs[threadIdx.x] = x.s;
+      rc[threadIdx.x] = x.c;
+    }
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
-    TwoSum t;
-    for (int w = 0; w < 8; ++w) t.merge(TwoSum{es[w], ec[w]});
-    out[2 * nq] = t.s;
-    out[2 * nq + 1] = t.c;
+    out[6 * (size_t)nq * TPQ] = rs[0];
+    out[6 * (size_t)nq * TPQ + 1] = rc[0];
   }
 }
 
@@ -242,39 +321,63 @@ double qmf_grad_store(DeviceStore& s, const double* factors, const double* deriv
   const int nq = (int)s.n_qubits;
   std::fill(grad, grad + 2 * nq, 0.0);
   if (s.logical == 0) return 0.0;
-  double* tab = ws.tables.as<double>(9 * (size_t)nq);
-  IQCC_CUDA(cudaMemcpyAsync(tab, factors, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, st));
-  IQCC_CUDA(cudaMemcpyAsync(tab + 3 * nq, derivs, 6 * nq * sizeof(double), cudaMemcpyHostToDevice, st));
-  const unsigned grid = (unsigned)std::min<size_t>(592, std::max<size_t>(1, (s.M + 63) / 64));
-  double* part = ws.grad_part.as<double>((size_t)grid * (2 * nq + 2));
-  const size_t smem = (size_t)(3 + 6 + 16) * nq * sizeof(double);
+  std::vector<double> f4 = factor_rows(factors, nq, s.B);
+  std::vector<unsigned char> zm((size_t)64 * s.B, 0);
+  bool zeros = false;
+  for (int q = 0; q < nq; ++q)
+    for (int c = 1; c < 4; ++c)
+      if (f4[4 * q + c] == 0.0) {
+        zm[q] |= (unsigned char)(1u << c);
+        zeros = true;
+      }
+  double* tab = ws.tables.as<double>(f4.size() + zm.size() / 8 + 8);
+  unsigned char* zmd = reinterpret_cast<unsigned char*>(tab + f4.size());
+  IQCC_CUDA(cudaMemcpyAsync(tab, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  IQCC_CUDA(cudaMemcpyAsync(zmd, zm.data(), zm.size(), cudaMemcpyHostToDevice, st));
+  const unsigned grid = (unsigned)std::min<size_t>(148 * 6, std::max<size_t>(1, (s.M + kQB - 1) / kQB));
+  const size_t tpq = 4 / s.B;  // threads per qubit slot in the kernel's phase 2
+  const size_t stride = 6 * (size_t)nq * tpq + 2;
+  double* part = ws.grad_part.as<double>((size_t)grid * stride);
   {
     KernelScope ks("qmf_grad");
+#define IQCC_QG(B_)                                                                                     \
+  if (zeros)                                                                                            \
+    k_qmf_grad<B_, true><<<grid, kQB, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, zmd, nq, part);  \
+  else                                                                                                  \
+    k_qmf_grad<B_, false><<<grid, kQB, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, zmd, nq, part)
     switch (s.B) {
-      case 1:
-        IQCC_CUDA(cudaFuncSetAttribute(k_qmf_grad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_qmf_grad<1><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, tab + 3 * nq, nq, part);
-        break;
-      case 2:
-        IQCC_CUDA(cudaFuncSetAttribute(k_qmf_grad<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_qmf_grad<2><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, tab + 3 * nq, nq, part);
-        break;
-      default:
-        IQCC_CUDA(cudaFuncSetAttribute(k_qmf_grad<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_qmf_grad<4><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, tab + 3 * nq, nq, part);
-        break;
+      case 1: IQCC_QG(1); break;
+      case 2: IQCC_QG(2); break;
+      default: IQCC_QG(4); break;
     }
+#undef IQCC_QG
   }
-  std::vector<double> h = fetch(part, (size_t)grid * (2 * nq + 2));
+  std::vector<double> h = fetch(part, (size_t)grid * stride);
+  std::vector<double> H(6 * (size_t)nq, 0.0);
   double es = 0.0, ec = 0.0;
   for (unsigned b = 0; b < grid; ++b) {
-    const double* p = h.data() + (size_t)b * (2 * nq + 2);
-    for (int j = 0; j < 2 * nq; ++j) grad[j] += p[j];
-    const double x = p[2 * nq];
+    const double* p = h.data() + (size_t)b * stride;
+    for (size_t r = 0; r < tpq; ++r)
+      for (size_t j = 0; j < 6 * (size_t)nq; ++j) H[j] += p[6 * nq * r + j];
+    const double x = p[stride - 2];
     const double t = es + x;
     ec += std::fabs(es) >= std::fabs(x) ? (es - t) + x : (x - t) + es;
     es = t;
-    ec += p[2 * nq + 1];
+    ec += p[stride - 1];
+  }
+  // derivs [q][6] = (dth, dph) for X, Z, Y; bins [q][code-1] with code 1 X, 2 Z, 3 Y
+  for (int q = 0; q < nq; ++q) {
+    for (int c = 0; c < 3; ++c) {
+      const double f = f4[4 * q + 1 + c];
+      const double dth = derivs[6 * q + 2 * c], dph = derivs[6 * q + 2 * c + 1];
+      const double hn = H[6 * q + c], h1 = H[6 * q + 3 + c];
+      if (f != 0.0) {
+        grad[q] += hn * (dth / f);
+        grad[nq + q] += hn * (dph / f);
+      }
+      grad[q] += h1 * dth;
+      grad[nq + q] += h1 * dph;
+    }
   }
   return es + ec;
 }
@@ -284,21 +387,37 @@ double qmf_grad_store(DeviceStore& s, const double* factors, const double* deriv
 // c_k, Im(c i^t) = c (t=1), -c (t=3), 0 otherwise (even t: commuting).
 // One candidate per thread; the term range [lo, hi) is streamed through
 // shared memory tiles shared by the whole block.
+// All lanes of a warp read the same staged term; each lane's product T^P is
+// taken over U = supp(T) | (union of the warp's candidate supports) in
+// ascending qubit order, identity positions multiplying by 1.0 (exact), so
+// the loop is warp-uniform, the factor reads of a warp hit one row, and the
+// value is bit-identical to expect_word over supp(T^P).  Candidates of one
+// flip group share their support (dis_candidates), so U is supp(T) plus a
+// few qubits.
 template <int B>
 __global__ void __launch_bounds__(128) k_dis_full(const ull* __restrict__ keys,
                                                   const double* __restrict__ coef, size_t M,
-                                                  Filter filt, const double* __restrict__ tab_g,
-                                                  int nq, const ull* __restrict__ cands, size_t K,
+                                                  Filter filt, const double* __restrict__ f4_g,
+                                                  const ull* __restrict__ cands, size_t K,
                                                   double* __restrict__ g_out) {
   constexpr int TT = 128;
-  extern __shared__ double dsm[];
-  double* tab = dsm;
-  ull* tk = reinterpret_cast<ull*>(tab + 3 * nq);
-  double* tc = reinterpret_cast<double*>(tk + (size_t)TT * 2 * B);
-  for (int i = threadIdx.x; i < 3 * nq; i += blockDim.x) tab[i] = tab_g[i];
+  __shared__ double f4[4 * 64 * B];
+  __shared__ ull tk[TT * 2 * B];
+  __shared__ double tc[TT];
+  for (int i = threadIdx.x; i < 4 * 64 * B; i += blockDim.x) f4[i] = f4_g[i];
   const size_t cid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   Key<B> P;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) P.w[w] = 0;
   if (cid < K) P = load_key<B>(cands, cid);
+  ull up[B];
+#pragma unroll
+  for (int w = 0; w < B; ++w) {
+    const ull s = P.w[w] | P.w[B + w];
+    const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)s);
+    const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(s >> 32));
+    up[w] = ((ull)hi << 32) | lo;
+  }
   double g = 0.0;
   for (size_t base = 0; base < M; base += TT) {
     __syncthreads();
@@ -312,16 +431,32 @@ __global__ void __launch_bounds__(128) k_dis_full(const ull* __restrict__ keys,
       tc[threadIdx.x] = c;
     }
     __syncthreads();
-    if (cid >= K) continue;
     const int n = (int)min((size_t)TT, M - base);
     for (int j = 0; j < n; ++j) {
       Key<B> k;
 #pragma unroll
       for (int w = 0; w < 2 * B; ++w) k.w[w] = tk[(size_t)j * 2 * B + w];
       const double c = tc[j];
-      if (c == 0.0 || !anticommutes<B>(k, P)) continue;
-      const double im = product_phase<B>(k, P) == 1 ? c : -c;
-      g = __dadd_rn(g, __dmul_rn(im, word_expect<B>(key_xor<B>(k, P), tab)));
+      const bool anti = cid < K && c != 0.0 && anticommutes<B>(k, P);
+      if (!__any_sync(0xffffffffu, anti)) continue;  // warp-uniform
+      const Key<B> kp = key_xor<B>(k, P);
+      double val = 1.0;
+#pragma unroll
+      for (int w = 0; w < B; ++w) {
+        ull s = k.w[w] | k.w[B + w] | up[w];
+        while (s) {
+          const int lz = __clzll((long long)s);
+          const int bit = 63 - lz;
+          const unsigned code =
+              (unsigned)((kp.w[w] >> bit) & 1ull) | ((unsigned)((kp.w[B + w] >> bit) & 1ull) << 1);
+          val = __dmul_rn(val, f4[4 * (64 * w + lz) + code]);
+          s &= ~(1ull << bit);
+        }
+      }
+      if (anti) {
+        const double im = product_phase<B>(k, P) == 1 ? c : -c;
+        g = __dadd_rn(g, __dmul_rn(im, val));
+      }
     }
   }
   if (cid < K) g_out[cid] = g;
@@ -405,10 +540,12 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
         s.keys(), s.coef(), s.filt, tab, nq, dc, rng, K, dg);
     count_launch("dis_gradient");
   } else {
+    const std::vector<double> f4 = factor_rows(factors, nq, B);
+    double* f4d = ws.grad_part.as<double>(f4.size());
+    IQCC_CUDA(cudaMemcpyAsync(f4d, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
     KernelScope ks("dis_gradient");
-    const size_t smem = 3 * nq * sizeof(double) + 128 * (16 * B + 8);
-    k_dis_full<B><<<(unsigned)((K + 127) / 128), 128, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, tab,
-                                                                    nq, dc, K, dg);
+    k_dis_full<B><<<(unsigned)((K + 127) / 128), 128, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, f4d, dc,
+                                                                K, dg);
   }
   IQCC_CUDA(cudaMemcpyAsync(g, dg, K * sizeof(double), cudaMemcpyDeviceToHost, st));
   IQCC_CUDA(cudaStreamSynchronize(st));
