@@ -565,12 +565,21 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
 /// Product slot flags (one byte per product, rank order) -> bit words.
 __global__ void k_pack_flags(const unsigned char* __restrict__ flag, size_t A,
                              unsigned* __restrict__ bits) {
+  // one word per thread from two 16-byte loads (flag bytes are 0 or 1; the
+  // buffer is padded past A, bits past A are masked off)
   const size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (w * 32 >= A) return;
+  const uint4* p = reinterpret_cast<const uint4*>(flag + w * 32);
+  const uint4 a = __ldg(p), b = __ldg(p + 1);
+  const unsigned q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
   unsigned x = 0;
-  const size_t n = min((size_t)32, A - w * 32);
-  for (size_t k = 0; k < n; ++k) x |= (unsigned)(flag[w * 32 + k] & 1u) << k;
-  bits[w] = x;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const unsigned v = q[k] & 0x01010101u;  // bytes -> bits 0, 8, 16, 24
+    x |= ((v | (v >> 7) | (v >> 14) | (v >> 21)) & 0xFu) << (4 * k);
+  }
+  const size_t n = A - w * 32;
+  bits[w] = n >= 32 ? x : x & ((1u << n) - 1u);
 }
 
 // Debug: inv_perm must be a bijection onto the present anticommuting terms.

@@ -774,7 +774,7 @@ __device__ __forceinline__ void chunk_emit(const ull (&v)[8], unsigned hit, size
         oi[slot] = ci ? ci[first + k] : first + k;
         ++slot;
       }
-      if (do_hist) {
+      if (do_hist && __any_sync(0xFFFFFFFFu, h)) {
         const unsigned d = h ? (unsigned)((v[k] >> shift) & dmask) : 0xFFFFFFFFu;
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
         if (h && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(sh + d, (unsigned)__popc(peers));
