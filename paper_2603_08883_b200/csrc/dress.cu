@@ -433,6 +433,10 @@ __global__ void __launch_bounds__(256) k_tile_agg_w(const short* __restrict__ lc
 #pragma unroll
   for (int k = 0; k < WI; ++k) lmax = max(lmax, it.l[k]);
   lmax = __reduce_max_sync(0xffffffffu, lmax);
+  int lmin = INT_MAX;
+#pragma unroll
+  for (int k = 0; k < WI; ++k) lmin = min(lmin, it.l[k]);
+  lmin = __reduce_min_sync(0xffffffffu, lmin);
   const int c_last = __shfl_sync(0xffffffffu, inc, 31) - (int)(__shfl_sync(0xffffffffu, it.bits, 31) >> (WI - 1));
 #pragma unroll
   for (int j = 0; j < NTHR; ++j) {
@@ -441,6 +445,7 @@ __global__ void __launch_bounds__(256) k_tile_agg_w(const short* __restrict__ lc
     if (lmax <= T) {  // every term is a boundary (warp-uniform fast path)
       fa = c_last;
       ba = 0;
+    } else if (T < lmin) {  // no boundary in the tile: fa = -1, ba = none
     } else {
 #pragma unroll
       for (int k = 0; k < WI; ++k)
@@ -494,9 +499,21 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
     used[k] = 0;
   }
   int st[NTHR];
+  // a threshold below every LCP of the warp tile has no boundary in it: its
+  // scans reduce to the carries (warp-uniform skip; common for shallow
+  // levels inside runs of equal x planes)
+  int lmin = INT_MAX;
+#pragma unroll
+  for (int k = 0; k < WI; ++k) lmin = min(lmin, it.l[k]);
+  lmin = __reduce_min_sync(0xffffffffu, lmin);
   // forward: last boundary at or before the term
 #pragma unroll
   for (int j = 0; j < NTHR; ++j) {
+    const int fc = fwd_carry[wt * kThrPerChunk + j];
+    if (thr.t[j] < lmin) {
+      st[j] = fc;
+      continue;
+    }
     int a = -1;
 #pragma unroll
     for (int k = 0; k < WI; ++k)
@@ -504,7 +521,7 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
     a = warp_inclusive(a, OpMax());
     int ex = __shfl_up_sync(0xffffffffu, a, 1);
     if (lane == 0) ex = -1;
-    st[j] = max(ex, fwd_carry[wt * kThrPerChunk + j]);
+    st[j] = max(ex, fc);
   }
 #pragma unroll
   for (int k = 0; k < WI; ++k) {
@@ -525,6 +542,11 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
   // backward: first boundary strictly after the term
 #pragma unroll
   for (int j = 0; j < NTHR; ++j) {
+    const int bc = bwd_carry[wt * kThrPerChunk + j];
+    if (thr.t[j] < lmin) {
+      st[j] = bc;
+      continue;
+    }
     int b = INT_MAX;
 #pragma unroll
     for (int k = WI - 1; k >= 0; --k)
@@ -532,7 +554,7 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
     b = warp_inclusive_rev(b, OpMin());
     int ex = __shfl_down_sync(0xffffffffu, b, 1);
     if (lane == 31) ex = INT_MAX;
-    st[j] = min(ex, bwd_carry[wt * kThrPerChunk + j]);
+    st[j] = min(ex, bc);
   }
 #pragma unroll
   for (int k = WI - 1; k >= 0; --k) {
