@@ -208,114 +208,177 @@ __device__ __forceinline__ size_t present_before(const unsigned* __restrict__ pm
 }
 
 // ---------------------------------------------------------- carry scans
-// Group level: values relative to the group start.
-__global__ void __launch_bounds__(GROUP) k_group_agg(const int* __restrict__ tile_cnt,
-                                                     const int* __restrict__ fwd_agg,
-                                                     const int* __restrict__ bwd_agg, size_t ntiles,
-                                                     int nthr, long long* __restrict__ g_cnt,
-                                                     long long* __restrict__ g_fwd,
-                                                     long long* __restrict__ g_bwd) {
-  __shared__ long long sm[GROUP / 32 + 2];
-  const size_t tile = blockIdx.x * (size_t)GROUP + threadIdx.x;
-  const bool in = tile < ntiles;
-  long long cnt = in ? tile_cnt[tile] : 0;
-  long long total;
-  long long pfx = block_exclusive<GROUP>(cnt, 0LL, OpAdd(), sm, &total);
-  if (threadIdx.x == 0) g_cnt[blockIdx.x] = total;
-  for (int j = 0; j < nthr; ++j) {
-    long long f = -1, b = LLONG_MAX;
-    if (in) {
-      int fv = fwd_agg[tile * kThrPerChunk + j], bv = bwd_agg[tile * kThrPerChunk + j];
-      if (fv >= 0) f = fv + pfx;
-      if (bv >= 0) b = bv + pfx;
+// One warp per threshold (blockDim = 32 * nthr): the thresholds' scans run
+// side by side instead of one after another behind block barriers, so the
+// carry phase costs a few microseconds of latency per launch at any shard
+// size.  Tile counts and their prefix are computed once per block into
+// shared memory.  Values are relative to the group start (group level) or
+// global (carry level), as the rank kernels expect.
+constexpr int TPL = GROUP / 32;  // tiles per lane in a group
+
+// tile-count exclusive prefix of the block's group (relative), by warp 0
+__device__ __forceinline__ int group_tile_prefix(const int* __restrict__ tile_cnt, size_t g0,
+                                                 size_t nt, int* s_pfx) {
+  __shared__ int s_total;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int run = 0;
+#pragma unroll 8
+    for (int i = 0; i < TPL; ++i) {
+      const int t = i * 32 + lane;
+      const int c = t < (int)nt ? tile_cnt[g0 + t] : 0;
+      const int inc = warp_inclusive(c, OpAdd());
+      s_pfx[t] = run + inc - c;
+      run += __shfl_sync(0xffffffffu, inc, 31);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      f = max(f, __shfl_xor_sync(0xffffffffu, f, o));
-      b = min(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (lane == 0) s_total = run;
+  }
+  __syncthreads();
+  return s_total;
+}
+
+__global__ void __launch_bounds__(512) k_group_agg(const int* __restrict__ tile_cnt,
+                                                   const int* __restrict__ fwd_agg,
+                                                   const int* __restrict__ bwd_agg, size_t ntiles,
+                                                   int nthr, long long* __restrict__ g_cnt,
+                                                   long long* __restrict__ g_fwd,
+                                                   long long* __restrict__ g_bwd) {
+  __shared__ int s_pfx[GROUP];
+  const size_t g0 = blockIdx.x * (size_t)GROUP;
+  const size_t nt = min((size_t)GROUP, ntiles - g0);
+  const int total = group_tile_prefix(tile_cnt, g0, nt, s_pfx);
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j >= nthr) return;
+  int f = -1, b = INT_MAX;
+#pragma unroll 8
+  for (int i = 0; i < TPL; ++i) {
+    const int t = i * 32 + lane;
+    if (t < (int)nt) {
+      const int fv = fwd_agg[(g0 + t) * kThrPerChunk + j], bv = bwd_agg[(g0 + t) * kThrPerChunk + j];
+      if (fv >= 0) f = max(f, fv + s_pfx[t]);
+      if (bv >= 0) b = min(b, bv + s_pfx[t]);
     }
-    __shared__ long long rf[GROUP / 32], rb[GROUP / 32];
-    if ((threadIdx.x & 31) == 0) {
-      rf[threadIdx.x >> 5] = f;
-      rb[threadIdx.x >> 5] = b;
+  }
+  f = __reduce_max_sync(0xffffffffu, f);
+  b = __reduce_min_sync(0xffffffffu, b);
+  if (lane == 0) {
+    g_fwd[blockIdx.x * kThrPerChunk + j] = f;
+    g_bwd[blockIdx.x * kThrPerChunk + j] = b == INT_MAX ? LLONG_MAX : (long long)b;
+    if (j == 0) g_cnt[blockIdx.x] = total;
+  }
+}
+
+// Single block over groups (<= 1024 groups = 2^28 terms).
+__global__ void __launch_bounds__(512) k_group_scan(size_t ngroups, int nthr,
+                                                    long long* __restrict__ g_cnt,
+                                                    long long* __restrict__ g_fwd,
+                                                    long long* __restrict__ g_bwd,
+                                                    long long* __restrict__ a_total) {
+  __shared__ long long s_pfx[1024];
+  __shared__ long long s_total;
+  const int ng = (int)ngroups;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    long long run = 0;
+    for (int i = 0; i * 32 < ng; ++i) {
+      const int g = i * 32 + lane;
+      const long long c = g < ng ? g_cnt[g] : 0;
+      const long long inc = warp_inclusive(c, OpAdd());
+      if (g < ng) s_pfx[g] = run + inc - c;
+      run += __shfl_sync(0xffffffffu, inc, 31);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long a = -1, c = LLONG_MAX;
-      for (int w = 0; w < GROUP / 32; ++w) {
-        a = max(a, rf[w]);
-        c = min(c, rb[w]);
+    if (lane == 0) s_total = run;
+  }
+  __syncthreads();
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j < nthr) {
+    // forward: exclusive max over the groups before (carry into the group)
+    long long run = -1;
+    for (int i = 0; i * 32 < ng; ++i) {
+      const int g = i * 32 + lane;
+      long long f = -1;
+      if (g < ng) {
+        const long long fv = g_fwd[g * kThrPerChunk + j];
+        if (fv >= 0) f = fv + s_pfx[g];
       }
-      g_fwd[blockIdx.x * kThrPerChunk + j] = a;
-      g_bwd[blockIdx.x * kThrPerChunk + j] = c;
+      const long long inc = warp_inclusive(f, OpMax());
+      long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) ex = -1;
+      if (g < ng) g_fwd[g * kThrPerChunk + j] = max(run, ex);
+      run = max(run, __shfl_sync(0xffffffffu, inc, 31));
     }
-    __syncthreads();
-  }
-}
-
-// Single block over groups (<= 1024 groups = 2^31 terms).
-__global__ void __launch_bounds__(1024) k_group_scan(size_t ngroups, int nthr,
-                                                     long long* __restrict__ g_cnt,
-                                                     long long* __restrict__ g_fwd,
-                                                     long long* __restrict__ g_bwd,
-                                                     long long* __restrict__ a_total) {
-  __shared__ long long sm[1024 / 32 + 2];
-  const int g = threadIdx.x;
-  const bool in = g < (int)ngroups;
-  long long cnt = in ? g_cnt[g] : 0;
-  long long total;
-  long long pfx = block_exclusive<1024>(cnt, 0LL, OpAdd(), sm, &total);
-  for (int j = 0; j < nthr; ++j) {
-    long long f = -1, b = LLONG_MAX;
-    if (in) {
-      long long fv = g_fwd[g * kThrPerChunk + j], bv = g_bwd[g * kThrPerChunk + j];
-      if (fv >= 0) f = fv + pfx;
-      if (bv != LLONG_MAX) b = bv + pfx;
-    }
-    long long fe = block_exclusive<1024>(f, -1LL, OpMax(), sm, (long long*)nullptr);
-    long long be = block_exclusive_rev<1024>(b, LLONG_MAX, OpMin(), sm);
-    if (in) {
-      g_fwd[g * kThrPerChunk + j] = fe;  // carry INTO the group (global C)
-      g_bwd[g * kThrPerChunk + j] = be;
+    // backward: exclusive min over the groups after
+    run = LLONG_MAX;
+    const int nchunk = (ng + 31) / 32;
+    for (int i = nchunk - 1; i >= 0; --i) {
+      const int g = i * 32 + lane;
+      long long b = LLONG_MAX;
+      if (g < ng) {
+        const long long bv = g_bwd[g * kThrPerChunk + j];
+        if (bv != LLONG_MAX) b = bv + s_pfx[g];
+      }
+      const long long inc = warp_inclusive_rev(b, OpMin());
+      long long ex = __shfl_down_sync(0xffffffffu, inc, 1);
+      if (lane == 31) ex = LLONG_MAX;
+      if (g < ng) g_bwd[g * kThrPerChunk + j] = min(run, ex);
+      run = min(run, __shfl_sync(0xffffffffu, inc, 0));
     }
   }
-  if (in) g_cnt[g] = pfx;  // group exclusive prefix
-  if (g == 0) *a_total = total;
+  __syncthreads();
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) g_cnt[g] = s_pfx[g];  // group exclusive prefix
+  if (threadIdx.x == 0) *a_total = s_total;
 }
 
-__global__ void __launch_bounds__(GROUP) k_tile_carry(const int* __restrict__ tile_cnt,
-                                                      const int* __restrict__ fwd_agg,
-                                                      const int* __restrict__ bwd_agg,
-                                                      size_t ntiles, int nthr,
-                                                      const long long* __restrict__ g_pfx,
-                                                      const long long* __restrict__ g_fwd,
-                                                      const long long* __restrict__ g_bwd,
-                                                      const long long* __restrict__ a_total,
-                                                      int* __restrict__ tile_pfx,
-                                                      int* __restrict__ fwd_carry,
-                                                      int* __restrict__ bwd_carry) {
-  __shared__ long long sm[GROUP / 32 + 2];
-  const size_t tile = blockIdx.x * (size_t)GROUP + threadIdx.x;
-  const bool in = tile < ntiles;
-  long long cnt = in ? tile_cnt[tile] : 0;
-  long long pfx = block_exclusive<GROUP>(cnt, 0LL, OpAdd(), sm, (long long*)nullptr) + g_pfx[blockIdx.x];
+__global__ void __launch_bounds__(512) k_tile_carry(const int* __restrict__ tile_cnt,
+                                                    const int* __restrict__ fwd_agg,
+                                                    const int* __restrict__ bwd_agg,
+                                                    size_t ntiles, int nthr,
+                                                    const long long* __restrict__ g_pfx,
+                                                    const long long* __restrict__ g_fwd,
+                                                    const long long* __restrict__ g_bwd,
+                                                    const long long* __restrict__ a_total,
+                                                    int* __restrict__ tile_pfx,
+                                                    int* __restrict__ fwd_carry,
+                                                    int* __restrict__ bwd_carry) {
+  __shared__ int s_pfx[GROUP];
+  const size_t g0 = blockIdx.x * (size_t)GROUP;
+  const size_t nt = min((size_t)GROUP, ntiles - g0);
+  group_tile_prefix(tile_cnt, g0, nt, s_pfx);
+  const long long gp = g_pfx[blockIdx.x];
+  for (int t = threadIdx.x; t < (int)nt; t += blockDim.x) tile_pfx[g0 + t] = (int)(gp + s_pfx[t]);
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j >= nthr) return;
   const long long A = *a_total;
-  if (in) tile_pfx[tile] = (int)pfx;
-  for (int j = 0; j < nthr; ++j) {
-    long long f = -1, b = LLONG_MAX;
-    if (in) {
-      int fv = fwd_agg[tile * kThrPerChunk + j], bv = bwd_agg[tile * kThrPerChunk + j];
-      if (fv >= 0) f = fv + pfx;
-      if (bv >= 0) b = bv + pfx;
+  long long run = g_fwd[blockIdx.x * kThrPerChunk + j];  // carry into the group
+#pragma unroll 8
+  for (int i = 0; i < TPL; ++i) {
+    const int t = i * 32 + lane;
+    long long f = -1;
+    if (t < (int)nt) {
+      const int fv = fwd_agg[(g0 + t) * kThrPerChunk + j];
+      if (fv >= 0) f = gp + s_pfx[t] + fv;
     }
-    long long fe = block_exclusive<GROUP>(f, -1LL, OpMax(), sm, (long long*)nullptr);
-    long long be = block_exclusive_rev<GROUP>(b, LLONG_MAX, OpMin(), sm);
-    fe = max(fe, g_fwd[blockIdx.x * kThrPerChunk + j]);
-    be = min(be, g_bwd[blockIdx.x * kThrPerChunk + j]);
-    if (in) {
-      fwd_carry[tile * kThrPerChunk + j] = (int)fe;
-      bwd_carry[tile * kThrPerChunk + j] = (int)(be == LLONG_MAX ? A : be);
+    const long long inc = warp_inclusive(f, OpMax());
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = -1;
+    if (t < (int)nt) fwd_carry[(g0 + t) * kThrPerChunk + j] = (int)max(run, ex);
+    run = max(run, __shfl_sync(0xffffffffu, inc, 31));
+  }
+  run = g_bwd[blockIdx.x * kThrPerChunk + j];  // first boundary after the group
+#pragma unroll 8
+  for (int i = TPL - 1; i >= 0; --i) {
+    const int t = i * 32 + lane;
+    long long b = LLONG_MAX;
+    if (t < (int)nt) {
+      const int bv = bwd_agg[(g0 + t) * kThrPerChunk + j];
+      if (bv >= 0) b = gp + s_pfx[t] + bv;
     }
+    const long long inc = warp_inclusive_rev(b, OpMin());
+    long long ex = __shfl_down_sync(0xffffffffu, inc, 1);
+    if (lane == 31) ex = LLONG_MAX;
+    const long long be = min(run, ex);
+    if (t < (int)nt) bwd_carry[(g0 + t) * kThrPerChunk + j] = (int)(be == LLONG_MAX ? A : be);
+    run = min(run, __shfl_sync(0xffffffffu, inc, 0));
   }
 }
 
@@ -1343,10 +1406,11 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
       if (use_meta && c == 0) run_present();
       {
         KernelScope ks("carry");
-        k_group_agg<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
-                                                         g_cnt, g_fwd, g_bwd);
-        k_group_scan<<<1, 1024, 0, st>>>(ngroups, thr.n, g_cnt, g_fwd, g_bwd, a_total);
-        k_tile_carry<<<(unsigned)ngroups, GROUP, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
+        const unsigned cthreads = 32u * (unsigned)thr.n;  // one warp per threshold
+        k_group_agg<<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
+                                                            g_cnt, g_fwd, g_bwd);
+        k_group_scan<<<1, cthreads, 0, st>>>(ngroups, thr.n, g_cnt, g_fwd, g_bwd, a_total);
+        k_tile_carry<<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
                                                           g_cnt, g_fwd, g_bwd, a_total, tile_pfx,
                                                           fwd_carry, bwd_carry);
         count_launch("carry");
