@@ -46,7 +46,8 @@ namespace iqcc_b200 {
 constexpr int TT = 256;  // threads per scan tile
 constexpr int TI = 8;    // terms per thread
 constexpr int TILE = TT * TI;
-constexpr int GROUP = 1024;  // tiles per carry group
+constexpr int GROUP = 256;  // tiles per carry group (one 8-tile batch per lane)
+constexpr int kMaxGroups = 4096;  // k_group_scan capacity: 2^28 terms per device shard
 
 struct Thr {
   int t[kThrPerChunk];
@@ -268,13 +269,13 @@ __global__ void __launch_bounds__(512) k_group_agg(const int* __restrict__ tile_
   }
 }
 
-// Single block over groups (<= 1024 groups = 2^28 terms).
+// Single block over groups (<= kMaxGroups groups = 2^28 terms).
 __global__ void __launch_bounds__(512) k_group_scan(size_t ngroups, int nthr,
                                                     long long* __restrict__ g_cnt,
                                                     long long* __restrict__ g_fwd,
                                                     long long* __restrict__ g_bwd,
                                                     long long* __restrict__ a_total) {
-  __shared__ long long s_pfx[1024];
+  __shared__ long long s_pfx[kMaxGroups];
   __shared__ long long s_total;
   const int ng = (int)ngroups;
   if (threadIdx.x < 32) {
@@ -741,6 +742,42 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
   // (see SlotRule; with theta = 0 every present survivor and every product)
   part_o[t] = present_before(pmask, ppre, W, *ptotal, a) +
               (qbits ? present_before(qbits, qpre, Wq, *qtotal, b) : b);
+}
+
+/// Coarse merge-path splits (every 2^kPartShift-th tile boundary), one warp
+/// per boundary with a 32-ary search: each round the lanes probe 32
+/// positions at once, so a search over 1e8 survivors takes 6 dependent
+/// probe rounds instead of 27 (the coarse pass is pure latency).
+template <int B>
+__global__ void k_partition_coarse(const ull* __restrict__ keys, const unsigned* __restrict__ inv_perm,
+                                   const ull* __restrict__ q_keys, size_t nS, size_t nQ, Key<B> P,
+                                   size_t tile_items, size_t ntiles, ull* __restrict__ raw_a) {
+  const size_t c = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const size_t t = c << kPartShift;
+  if (t > ntiles) return;  // warp-uniform
+  const size_t d = min(t * tile_items, nS + nQ);
+  size_t lo = d > nQ ? d - nQ : 0, hi = min(d, nS);
+  // invariant: the split a is in [lo, hi]; pred(m) = key(m) <= qkey(d-1-m) holds below a
+  while (hi > lo) {
+    const size_t span = hi - lo;
+    const size_t step = (span + 31) / 32;  // probe lo + step*(lane+1) - 1
+    const size_t m = lo + step * (lane + 1) - 1;
+    bool pr = true;
+    if (m < hi) pr = key_cmp<B>(load_key<B>(keys, m), q_key<B>(keys, inv_perm, q_keys, d - 1 - m, P)) <= 0;
+    const unsigned fails = __ballot_sync(0xffffffffu, !pr);
+    if (fails == 0) {
+      // every probe below hi held: the split lies past the last of them
+      // (a tail shorter than `step` may remain unprobed)
+      lo += step * min((size_t)32, span / step);
+    } else {
+      const int f = __ffs(fails) - 1;  // first probe where the predicate fails
+      const size_t mf = lo + step * (f + 1) - 1;
+      lo += step * f;  // probes < f held: the split is past them
+      hi = mf;         // and at or before the failing probe
+    }
+  }
+  if (lane == 0) raw_a[c] = lo;
 }
 
 template <int B>
@@ -1352,7 +1389,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   if (products && M > 0) {
     const size_t ntiles = (M + WT - 1) / WT;
     const size_t ngroups = (ntiles + GROUP - 1) / GROUP;
-    if (ngroups > 1024) throw std::runtime_error("dress: more than 2^28 terms per device shard");
+    if (ngroups > (size_t)kMaxGroups) throw std::runtime_error("dress: more than 2^28 terms per device shard");
     int* tile_cnt = ws.tile_cnt.as<int>(ntiles);
     int* fwd_agg = ws.fwd_agg.as<int>(ntiles * kThrPerChunk);
     int* bwd_agg = ws.bwd_agg.as<int>(ntiles * kThrPerChunk);
@@ -1499,9 +1536,8 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     KernelScope ks("partition");
     ull* raw = po + (ntm + 1);
     const unsigned* qb = pl.qbits;
-    k_partition<B><<<(unsigned)((nco + 255) / 256), 256, 0, st>>>(
-        s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
-        pl.ptotal, qb, pl.qpre, pl.Wq, pl.qtotal, kPartShift, raw);
+    k_partition_coarse<B><<<(unsigned)((nco * 32 + 255) / 256), 256, 0, st>>>(
+        s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, raw);
     k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
         s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
         pl.ptotal, qb, pl.qpre, pl.Wq, pl.qtotal, 0, raw);

@@ -641,7 +641,8 @@ __device__ __forceinline__ void next_digit(const SelState* st, int& shift, unsig
 // Parallel pick over a histogram, largest values first: find the bin x
 // (scanning from the top) where the running global count reaches r.
 // 256 threads, each owning a contiguous run of bins from the top.
-__device__ __forceinline__ bool block_pick(const ull* __restrict__ hg, const unsigned* __restrict__ hl,
+template <class HG>
+__device__ __forceinline__ bool block_pick(const HG* __restrict__ hg, const unsigned* __restrict__ hl,
                                            int nbins, ull r, int* x_out, ull* before_g,
                                            ull* before_l) {
   __shared__ ull sg[256], sl[256];
@@ -694,7 +695,8 @@ __device__ __forceinline__ bool block_pick(const ull* __restrict__ hg, const uns
 
 // hist_g[256] (global counts, u64) / hist_l[256] (local, u32): pick the
 // coarse bin holding the budget-th largest |c|.
-__global__ void __launch_bounds__(256) k_pick_bin(const ull* __restrict__ hist_g,
+template <class HG>
+__global__ void __launch_bounds__(256) k_pick_bin(const HG* __restrict__ hist_g,
                                                   const unsigned* __restrict__ hist_l, ull budget,
                                                   SelState* __restrict__ st) {
   int b;
@@ -717,7 +719,8 @@ __global__ void __launch_bounds__(256) k_pick_bin(const ull* __restrict__ hist_g
   st->ntie = 0;
 }
 
-__global__ void __launch_bounds__(256) k_pick_digit(const ull* __restrict__ dh_g,
+template <class HG>
+__global__ void __launch_bounds__(256) k_pick_digit(const HG* __restrict__ dh_g,
                                                     const unsigned* __restrict__ dh_l,
                                                     SelState* __restrict__ st) {
   if (st->fail || st->top < 0) return;  // uniform across the block
@@ -968,10 +971,16 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       ull* gbuf = ws.partials.as<ull>(kHistBins + (1 << kDigitBits));
       hist_g = gbuf;
       ull* dh_g = gbuf + kHistBins;
-      k_widen<<<1, 256, 0, st>>>(hist, hist_g, kHistBins);
-      if (red) red->sum_device(hist_g, kHistBins);
-      k_pick_bin<<<1, 256, 0, st>>>(hist_g, hist, (ull)budget, sel);
-      count_launch("select");
+      // a single store picks straight from its own (u32) histograms; ranks
+      // widen them to u64 for the allreduce
+      if (red) {
+        k_widen<<<1, 256, 0, st>>>(hist, hist_g, kHistBins);
+        red->sum_device(hist_g, kHistBins);
+        k_pick_bin<ull><<<1, 256, 0, st>>>(hist_g, hist, (ull)budget, sel);
+        count_launch("select");
+      } else {
+        k_pick_bin<unsigned><<<1, 256, 0, st>>>(hist, hist, (ull)budget, sel);
+      }
       count_launch("select");
       // candidate capacity: the store size (stable across steps, so the
       // buffers never regrow inside a dressing loop and no count is read back)
@@ -1004,13 +1013,20 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       for (int round = 0; round < rounds; ++round) {
         KernelScope ks("select_digits");
         unsigned* h = dh + hsz * round;
-        k_widen<<<4, 256, 0, st>>>(h, dh_g, (int)hsz);
-        if (red) red->sum_device(dh_g, hsz);
-        k_pick_digit<<<1, 256, 0, st>>>(dh_g, h, sel);
+        if (red) {
+          k_widen<<<4, 256, 0, st>>>(h, dh_g, (int)hsz);
+          red->sum_device(dh_g, hsz);
+          k_pick_digit<ull><<<1, 256, 0, st>>>(dh_g, h, sel);
+          count_launch("select_digits");
+        } else {
+          k_pick_digit<unsigned><<<1, 256, 0, st>>>(h, h, sel);
+        }
         const int nxt = cur ^ 1;
-        k_cand_filter<<<cgrid, 256, 0, st>>>(av[cur], ai[cur], cnt + round, sel, av[nxt], ai[nxt],
-                                             cnt + round + 1, round + 1 < rounds ? h + hsz : h);
-        count_launch("select_digits");
+        // the candidate set shrinks by ~2^12 per round: later rounds use a
+        // small grid-stride grid
+        const unsigned g = round == 0 ? cgrid : std::min<unsigned>(cgrid, 2 * 148);
+        k_cand_filter<<<g, 256, 0, st>>>(av[cur], ai[cur], cnt + round, sel, av[nxt], ai[nxt],
+                                         cnt + round + 1, round + 1 < rounds ? h + hsz : h);
         count_launch("select_digits");
         cur = nxt;
       }
