@@ -632,8 +632,13 @@ struct SelState {
   int top;                    // highest magnitude bit not fixed yet (-1: done)
 };
 
+// 12-bit digits: the 52 mantissa bits of an interior exponent bin take five
+// rounds (the host plans five and runs the sixth only for an edge bin);
+// 13-bit digits measured slower (larger per-block histogram flushes)
+constexpr int kDigitBitsDev = 12;
+
 __device__ __forceinline__ void next_digit(const SelState* st, int& shift, unsigned& dmask) {
-  const int width = min(12, st->top + 1);
+  const int width = min(kDigitBitsDev, st->top + 1);
   shift = st->top + 1 - width;
   dmask = (1u << width) - 1u;
 }
@@ -752,7 +757,7 @@ __global__ void k_gather_rows(const ull* __restrict__ keys, const ull* __restric
   if (t < n * W) out[t] = keys[idx[t / W] * W + t % W];
 }
 
-constexpr int kDigitBits = 12;  // digit histograms privatized in shared memory
+constexpr int kDigitBits = kDigitBitsDev;  // digit histograms privatized in shared memory
 
 // Append the hit lanes of one 2048-element chunk (8 per thread) to (ov, oi)
 // with one global atomic per block, and histogram their next digit in
@@ -991,13 +996,16 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       ull* av[3] = {ws.cand_v.as<ull>(ncap8), ws.cand_v2.as<ull>(ncap8), nullptr};
       ull* ai[3] = {ws.cand_i.as<ull>(ncap8), ws.cand_i2.as<ull>(ncap8), nullptr};
       // digit rounds: the device tracks the next unfixed bit (interior bins
-      // start below the exponent); spare rounds only re-compact the ties
-      const int rounds = (63 + kDigitBits - 1) / kDigitBits;
+      // start below the exponent); kPlanned rounds resolve an interior bin,
+      // an edge bin (63 free bits) is finished after the read-back shows it
+      constexpr int kPlanned = (52 + kDigitBits - 1) / kDigitBits;
+      constexpr int kMaxRounds = (63 + kDigitBits - 1) / kDigitBits;
       const size_t hsz = (size_t)1 << kDigitBits;
-      unsigned* dh = ws.misc2.as<unsigned>(hsz * rounds);
+      unsigned* dh = ws.misc2.as<unsigned>(hsz * (kMaxRounds + 1));
       ull* cnt = ctr + 2;  // cnt[k] = |A_k|
-      IQCC_CUDA(cudaMemsetAsync(dh, 0, hsz * rounds * sizeof(unsigned), st));
-      IQCC_CUDA(cudaMemsetAsync(cnt, 0, (rounds + 1) * sizeof(ull), st));
+      static_assert(2 + kMaxRounds + 1 <= 12, "candidate counts overlap the tie count");
+      IQCC_CUDA(cudaMemsetAsync(dh, 0, hsz * (kMaxRounds + 1) * sizeof(unsigned), st));
+      IQCC_CUDA(cudaMemsetAsync(cnt, 0, (kMaxRounds + 1) * sizeof(ull), st));
       {
         KernelScope ks("select_gather");
         const unsigned grid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (s.M + 2047) / 2048));
@@ -1010,48 +1018,61 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       if (getenv("IQCC_DEBUG")) debug_check("select gather");
       const unsigned cgrid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (ncap + 2047) / 2048));
       int cur = 0;
-      for (int round = 0; round < rounds; ++round) {
-        KernelScope ks("select_digits");
-        unsigned* h = dh + hsz * round;
-        if (red) {
-          k_widen<<<4, 256, 0, st>>>(h, dh_g, (int)hsz);
-          red->sum_device(dh_g, hsz);
-          k_pick_digit<ull><<<1, 256, 0, st>>>(dh_g, h, sel);
+      auto run_rounds = [&](int from, int to) {
+        for (int round = from; round < to; ++round) {
+          KernelScope ks("select_digits");
+          unsigned* h = dh + hsz * round;
+          if (red) {
+            k_widen<<<4, 256, 0, st>>>(h, dh_g, (int)hsz);
+            red->sum_device(dh_g, hsz);
+            k_pick_digit<ull><<<1, 256, 0, st>>>(dh_g, h, sel);
+            count_launch("select_digits");
+          } else {
+            k_pick_digit<unsigned><<<1, 256, 0, st>>>(h, h, sel);
+          }
+          const int nxt = cur ^ 1;
+          // the candidate set shrinks by ~2^12 per round: later rounds use a
+          // small grid-stride grid
+          const unsigned g = round == 0 ? cgrid : std::min<unsigned>(cgrid, 2 * 148);
+          k_cand_filter<<<g, 256, 0, st>>>(av[cur], ai[cur], cnt + round, sel, av[nxt], ai[nxt],
+                                           cnt + round + 1, h + hsz);
           count_launch("select_digits");
-        } else {
-          k_pick_digit<unsigned><<<1, 256, 0, st>>>(h, h, sel);
+          cur = nxt;
         }
-        const int nxt = cur ^ 1;
-        // the candidate set shrinks by ~2^12 per round: later rounds use a
-        // small grid-stride grid
-        const unsigned g = round == 0 ? cgrid : std::min<unsigned>(cgrid, 2 * 148);
-        k_cand_filter<<<g, 256, 0, st>>>(av[cur], ai[cur], cnt + round, sel, av[nxt], ai[nxt],
-                                         cnt + round + 1, round + 1 < rounds ? h + hsz : h);
-        count_launch("select_digits");
-        cur = nxt;
-      }
+      };
+      run_rounds(0, kPlanned);
+      int rounds = kPlanned;
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
-      ull* ties = ai[cur];  // A_rounds: every bit fixed -> exactly the ties
-      // local and global tie counts come back with the select state
-      ull* gtie = ctr + 12;
-      if (red) {
-        IQCC_CUDA(cudaMemcpyAsync(gtie, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToDevice, st));
-        red->sum_device(gtie, 1);
-      }
-      // the first kTieSpec tied indices travel speculatively in the same copy
+      // local and global tie counts come back with the select state; the
+      // first kTieSpec tied indices travel speculatively in the same copy
       constexpr size_t kTieSpec = 64;
       const size_t spec = std::min(kTieSpec, ncap8);
       SelState* hsp = static_cast<SelState*>(host_pinned(sizeof(SelState) + (2 + kTieSpec) * sizeof(ull)));
       ull* ntp = reinterpret_cast<ull*>(hsp + 1);
-      IQCC_CUDA(cudaMemcpyAsync(hsp, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaMemcpyAsync(ntp, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
-      if (red) IQCC_CUDA(cudaMemcpyAsync(ntp + 1, gtie, sizeof(ull), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaMemcpyAsync(ntp + 2, ties, spec * sizeof(ull), cudaMemcpyDeviceToHost, st));
-      host_sync(st);
+      ull* gtie = ctr + 12;
+      auto read_back = [&]() {
+        ull* ties = ai[cur];  // every bit fixed -> exactly the ties
+        if (red) {
+          IQCC_CUDA(cudaMemcpyAsync(gtie, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToDevice, st));
+          red->sum_device(gtie, 1);
+        }
+        IQCC_CUDA(cudaMemcpyAsync(hsp, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
+        IQCC_CUDA(cudaMemcpyAsync(ntp, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
+        if (red) IQCC_CUDA(cudaMemcpyAsync(ntp + 1, gtie, sizeof(ull), cudaMemcpyDeviceToHost, st));
+        IQCC_CUDA(cudaMemcpyAsync(ntp + 2, ties, spec * sizeof(ull), cudaMemcpyDeviceToHost, st));
+        host_sync(st);
+      };
+      read_back();
+      if (!hsp->fail && hsp->top >= 0) {  // edge bin: finish the remaining bits
+        run_rounds(kPlanned, kMaxRounds);
+        rounds = kMaxRounds;
+        read_back();
+      }
+      ull* ties = ai[cur];
       SelState hs = *hsp;
       const ull ntie = ntp[0];
       const ull ntie_global = red ? ntp[1] : ntie;
-      if (hs.fail) throw std::runtime_error("compress: device select failed");
+      if (hs.fail || hs.top >= 0) throw std::runtime_error("compress: device select failed");
       hs.ntie = ntie;
       const ull vbits = hs.known_val;  // exact threshold value; hs.r ties at it are kept (globally)
       size_t r = hs.r;
