@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(512) k_group_scan(size_t ngroups, int nthr,
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     long long run = 0;
+#pragma unroll 8
     for (int i = 0; i * 32 < ng; ++i) {
       const int g = i * 32 + lane;
       const long long c = g < ng ? g_cnt[g] : 0;
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(512) k_group_scan(size_t ngroups, int nthr,
   if (j < nthr) {
     // forward: exclusive max over the groups before (carry into the group)
     long long run = -1;
+#pragma unroll 8
     for (int i = 0; i * 32 < ng; ++i) {
       const int g = i * 32 + lane;
       long long f = -1;
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(512) k_group_scan(size_t ngroups, int nthr,
     // backward: exclusive min over the groups after
     run = LLONG_MAX;
     const int nchunk = (ng + 31) / 32;
+#pragma unroll 8
     for (int i = nchunk - 1; i >= 0; --i) {
       const int g = i * 32 + lane;
       long long b = LLONG_MAX;
