@@ -21,16 +21,22 @@ def n_gpus():
 @pytest.mark.parametrize("args", [("124", "2e5", "6", "1e-10", "2e5"), ("64", "1e5", "5", "0", "1e18"),
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq"),
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "badspec"),
+                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "nccl"),
                                   ("200", "1e5", "6", "1e-10", "1.2e5", "seq")])
 def test_partitioned_dressing_matches_serial(world, args):
     """The sequence cases exercise the output-slot speculation on the
     exchange and the local steps; "badspec" forces every guess too high
-    (IQCC_SPEC_SCALE), so every step is undone and redone exactly."""
+    (IQCC_SPEC_SCALE), so every step is undone and redone exactly; "nccl"
+    moves the products with NCCL send/recv (the fallback of the CUDA-IPC
+    NVLink push)."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ)
     if args[-1] == "badspec":
         env["IQCC_SPEC_SCALE"] = "64"
+        args = args[:-1]
+    elif args[-1] == "nccl":  # products over NCCL send/recv instead of the NVLink push
+        env["IQCC_NO_P2P"] = "1"
         args = args[:-1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "multi_worker.py"),
