@@ -590,19 +590,35 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
     if (lane == 0) ex = -1;
     st[j] = max(ex, fc);
   }
+  // per level (thresholds 2lv, 2lv+1) the item walk only needs that level's
+  // two running boundaries, so levels run one after another and a level
+  // without any boundary in the tile (both thresholds below lmin) costs no
+  // compares: its D is the constant carry difference
+  const int nlev = thr.nlev;
 #pragma unroll
-  for (int k = 0; k < WI; ++k) {
+  for (int lv = 0; lv < NTHR / 2; ++lv) {
+    if (lv >= nlev) break;  // padded levels: D == 0 everywhere
+    int a = st[2 * lv], b = st[2 * lv + 1];
+    if (thr.t[2 * lv + 1] < lmin) {
+      const int D = b - a;
+      if (D > 0) {
 #pragma unroll
-    for (int j = 0; j < NTHR; ++j)
-      if (it.l[k] <= thr.t[j]) st[j] = C[k];
-    if ((it.bits >> k) & 1u) {
+        for (int k = 0; k < WI; ++k)
+          if ((it.bits >> k) & 1u) {
+            delta[k] -= D;
+            used[k] |= 1u << lv;
+          }
+      }
+      continue;
+    }
 #pragma unroll
-      for (int lv = 0; lv < NTHR / 2; ++lv) {
-        const int D = st[2 * lv + 1] - st[2 * lv];
-        if (D > 0) {
-          delta[k] -= D;
-          used[k] |= 1u << lv;
-        }
+    for (int k = 0; k < WI; ++k) {
+      if (it.l[k] <= thr.t[2 * lv]) a = C[k];
+      if (it.l[k] <= thr.t[2 * lv + 1]) b = C[k];
+      const int D = b - a;
+      if (((it.bits >> k) & 1u) && D > 0) {
+        delta[k] -= D;
+        used[k] |= 1u << lv;
       }
     }
   }
@@ -624,15 +640,22 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
     st[j] = min(ex, bc);
   }
 #pragma unroll
-  for (int k = WI - 1; k >= 0; --k) {
-    if ((it.bits >> k) & 1u) {
+  for (int lv = 0; lv < NTHR / 2; ++lv) {
+    if (lv >= nlev) break;
+    int a = st[2 * lv], b = st[2 * lv + 1];
+    if (thr.t[2 * lv + 1] < lmin) {
+      const int E = a - b;
 #pragma unroll
-      for (int lv = 0; lv < NTHR / 2; ++lv)
-        if (!((used[k] >> lv) & 1u)) delta[k] += st[2 * lv] - st[2 * lv + 1];
+      for (int k = 0; k < WI; ++k)
+        if (((it.bits >> k) & 1u) && !((used[k] >> lv) & 1u)) delta[k] += E;
+      continue;
     }
 #pragma unroll
-    for (int j = 0; j < NTHR; ++j)
-      if (it.l[k] <= thr.t[j]) st[j] = C[k];
+    for (int k = WI - 1; k >= 0; --k) {
+      if (((it.bits >> k) & 1u) && !((used[k] >> lv) & 1u)) delta[k] += a - b;
+      if (it.l[k] <= thr.t[2 * lv]) a = C[k];
+      if (it.l[k] <= thr.t[2 * lv + 1]) b = C[k];
+    }
   }
 #pragma unroll
   const unsigned qm = FINAL && qflag && first < M ? (qmask[first >> 5] >> (first & 31)) : 0u;
