@@ -46,7 +46,9 @@ namespace iqcc_b200 {
 constexpr int TT = 256;  // threads per scan tile
 constexpr int TI = 8;    // terms per thread
 constexpr int TILE = TT * TI;
-constexpr int GROUP = 256;  // tiles per carry group (one 8-tile batch per lane)
+// tiles per carry group: 256 for small shards (latency), 1024 when that keeps
+// the single-block group scan short
+constexpr int kGroupSmall = 256, kGroupLarge = 1024;
 constexpr int kMaxGroups = 4096;  // k_group_scan capacity: 2^28 terms per device shard
 
 struct Thr {
@@ -215,12 +217,13 @@ __device__ __forceinline__ size_t present_before(const unsigned* __restrict__ pm
 // size.  Tile counts and their prefix are computed once per block into
 // shared memory.  Values are relative to the group start (group level) or
 // global (carry level), as the rank kernels expect.
-constexpr int TPL = GROUP / 32;  // tiles per lane in a group
 
 // tile-count exclusive prefix of the block's group (relative), by warp 0
+template <int GROUP>
 __device__ __forceinline__ int group_tile_prefix(const int* __restrict__ tile_cnt, size_t g0,
                                                  size_t nt, int* s_pfx) {
   __shared__ int s_total;
+  constexpr int TPL = GROUP / 32;  // tiles per lane in a group
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int run = 0;
@@ -238,6 +241,7 @@ __device__ __forceinline__ int group_tile_prefix(const int* __restrict__ tile_cn
   return s_total;
 }
 
+template <int GROUP>
 __global__ void __launch_bounds__(512) k_group_agg(const int* __restrict__ tile_cnt,
                                                    const int* __restrict__ fwd_agg,
                                                    const int* __restrict__ bwd_agg, size_t ntiles,
@@ -247,7 +251,8 @@ __global__ void __launch_bounds__(512) k_group_agg(const int* __restrict__ tile_
   __shared__ int s_pfx[GROUP];
   const size_t g0 = blockIdx.x * (size_t)GROUP;
   const size_t nt = min((size_t)GROUP, ntiles - g0);
-  const int total = group_tile_prefix(tile_cnt, g0, nt, s_pfx);
+  constexpr int TPL = GROUP / 32;
+  const int total = group_tile_prefix<GROUP>(tile_cnt, g0, nt, s_pfx);
   const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (j >= nthr) return;
   int f = -1, b = INT_MAX;
@@ -333,6 +338,7 @@ __global__ void __launch_bounds__(512) k_group_scan(size_t ngroups, int nthr,
   if (threadIdx.x == 0) *a_total = s_total;
 }
 
+template <int GROUP>
 __global__ void __launch_bounds__(512) k_tile_carry(const int* __restrict__ tile_cnt,
                                                     const int* __restrict__ fwd_agg,
                                                     const int* __restrict__ bwd_agg,
@@ -347,7 +353,8 @@ __global__ void __launch_bounds__(512) k_tile_carry(const int* __restrict__ tile
   __shared__ int s_pfx[GROUP];
   const size_t g0 = blockIdx.x * (size_t)GROUP;
   const size_t nt = min((size_t)GROUP, ntiles - g0);
-  group_tile_prefix(tile_cnt, g0, nt, s_pfx);
+  constexpr int TPL = GROUP / 32;
+  group_tile_prefix<GROUP>(tile_cnt, g0, nt, s_pfx);
   const long long gp = g_pfx[blockIdx.x];
   for (int t = threadIdx.x; t < (int)nt; t += blockDim.x) tile_pfx[g0 + t] = (int)(gp + s_pfx[t]);
   const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1414,7 +1421,8 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   if (getenv("IQCC_DEBUG") && M > 0) debug_check("present");
   if (products && M > 0) {
     const size_t ntiles = (M + WT - 1) / WT;
-    const size_t ngroups = (ntiles + GROUP - 1) / GROUP;
+    const int group = ntiles > (size_t)kGroupSmall * 1024 ? kGroupLarge : kGroupSmall;
+    const size_t ngroups = (ntiles + group - 1) / group;
     if (ngroups > (size_t)kMaxGroups) throw std::runtime_error("dress: more than 2^28 terms per device shard");
     int* tile_cnt = ws.tile_cnt.as<int>(ntiles);
     int* fwd_agg = ws.fwd_agg.as<int>(ntiles * kThrPerChunk);
@@ -1470,10 +1478,19 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
       {
         KernelScope ks("carry");
         const unsigned cthreads = 32u * (unsigned)thr.n;  // one warp per threshold
-        k_group_agg<<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
-                                                            g_cnt, g_fwd, g_bwd);
+        if (group == kGroupLarge)
+          k_group_agg<kGroupLarge><<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles,
+                                                                           thr.n, g_cnt, g_fwd, g_bwd);
+        else
+          k_group_agg<kGroupSmall><<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles,
+                                                                           thr.n, g_cnt, g_fwd, g_bwd);
         k_group_scan<<<1, cthreads, 0, st>>>(ngroups, thr.n, g_cnt, g_fwd, g_bwd, a_total);
-        k_tile_carry<<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
+        if (group == kGroupLarge)
+          k_tile_carry<kGroupLarge><<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
+                                                          g_cnt, g_fwd, g_bwd, a_total, tile_pfx,
+                                                          fwd_carry, bwd_carry);
+        else
+          k_tile_carry<kGroupSmall><<<(unsigned)ngroups, cthreads, 0, st>>>(tile_cnt, fwd_agg, bwd_agg, ntiles, thr.n,
                                                           g_cnt, g_fwd, g_bwd, a_total, tile_pfx,
                                                           fwd_carry, bwd_carry);
         count_launch("carry");
