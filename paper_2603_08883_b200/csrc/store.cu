@@ -830,9 +830,9 @@ __global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys
   hist_begin(sel, do_hist, shift, dmask, sh);
   const unsigned bin = (unsigned)sel->bin;
   const bool has_id = key_is_identity<B>(load_key<B>(keys, 0));
-  for (size_t base = blockIdx.x * (size_t)2048; base < M; base += (size_t)gridDim.x * 2048) {
-    const size_t first = base + (size_t)threadIdx.x * 8;
-    double c[8];
+  // the next chunk's coefficients are loaded before this chunk is compacted
+  // (the block scans and barriers of chunk_emit hide the load latency)
+  auto load8 = [&](size_t first, double (&c)[8]) {
     if (first + 8 <= M) {
       const double2* p = reinterpret_cast<const double2*>(coef + first);
 #pragma unroll
@@ -845,6 +845,16 @@ __global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys
 #pragma unroll
       for (int k = 0; k < 8; ++k) c[k] = first + k < M ? coef[first + k] : 0.0;
     }
+  };
+  const size_t stride = (size_t)gridDim.x * 2048;
+  double cn[8];
+  if (blockIdx.x * (size_t)2048 < M) load8(blockIdx.x * (size_t)2048 + (size_t)threadIdx.x * 8, cn);
+  for (size_t base = blockIdx.x * (size_t)2048; base < M; base += stride) {
+    const size_t first = base + (size_t)threadIdx.x * 8;
+    double c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = cn[k];
+    if (base + stride < M) load8(first + stride, cn);
     unsigned hit = 0;
     ull v[8];
 #pragma unroll
