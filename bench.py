@@ -83,10 +83,11 @@ def entangler(n_qubits: int, index: int, flip=None):
 
 
 def step_entanglers(n_qubits, step, flip=None):
-    """10 entanglers; #0, #3, #6 (and #9) flip the first partition bit."""
+    """10 entanglers; #0, #3 and #6 flip the first partition bit (SURVEY.md
+    §8(d) C3: at least 3 of the 10 exercise the exchange)."""
     out = []
     for k in range(ENTANGLERS_PER_STEP):
-        f = flip if (flip is not None and k % 3 == 0) else None
+        f = flip if (flip is not None and k in (0, 3, 6)) else None
         out.append(entangler(n_qubits, step * ENTANGLERS_PER_STEP + k, f))
     return out
 
