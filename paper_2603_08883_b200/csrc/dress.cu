@@ -885,7 +885,8 @@ struct MergeCfg {
   static constexpr size_t OFF_PP = OFF_SM + (size_t)PMW * 4;     // their prefix
   static constexpr size_t OFF_QM = OFF_PP + (size_t)PMW * 4;     // slot bits of Q
   static constexpr size_t OFF_QP = OFF_QM + (size_t)PMW * 4;     // their prefix
-  static constexpr size_t OFF_HIST = (OFF_QP + (size_t)PMW * 4 + 15) & ~(size_t)15;
+  static constexpr size_t OFF_AM = OFF_QP + (size_t)PMW * 4;     // anticommute bits of S
+  static constexpr size_t OFF_HIST = (OFF_AM + (size_t)PMW * 4 + 15) & ~(size_t)15;
   static constexpr int HBINS = kHistBins;  // |c| histogram (u32, per CTA) for compress
   static constexpr size_t bytes(bool hist, int stages) {
     return OFF_HIST - (2 - stages) * STAGE + (hist ? HBINS * 4 : 0);
@@ -930,6 +931,11 @@ struct MergeArgs {
   ull pn[8];
   SlotRule rule;
   const unsigned* qbits;  // product slot bits in product order (nullptr: all)
+  // the plan's per-slot bits of the store: survivor owns an output slot
+  // (pmask) and present & anticommuting (fmask); a present survivor without
+  // a slot commutes and is dropped by the compress, so it acts as absent
+  const unsigned* pmask;
+  const unsigned* fmask;
   double theta;           // count emitted non-identity |c| >= theta (0: off)
 };
 
@@ -991,6 +997,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   unsigned* spp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_PP);
   unsigned* sqm = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_QM);
   unsigned* sqp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_QP);
+  unsigned* sam = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_AM);
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
   const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
   const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
@@ -1000,26 +1007,22 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   const int coff = (int)(a0 & 1);
   const int qc0 = nS + 4;
 
-  // present bits of the survivors (dead slots / compress-filtered are
-  // absent) and their slot bits (SlotRule); slot bits of the products
+  // survivor bits from the plan: slot (pmask, also "present": see MergeArgs)
+  // and present & anticommuting (fmask); slot bits of the products
   {
-    const int lane = threadIdx.x & 31;
-    for (int e0 = (threadIdx.x & ~31); e0 < nS; e0 += NT) {
-      const int e = e0 + lane;
-      bool pr = false, sl = false;
-      if (e < nS) {
-        const Key<B> ks = sm_key16<B>(sk, e);
-        const double c = sc[coff + e];
-        const bool id = a0 + e == 0 && key_is_identity<B>(ks);
-        pr = filter_keep(g.filt, a0 + e, c, id);
-        sl = survivor_slot(g.rule, pr, id, pr && g.rule.thc != 0.0 && anticommutes<B>(ks, P), c);
-      }
-      const unsigned word = __ballot_sync(0xffffffffu, pr);
-      const unsigned sword = __ballot_sync(0xffffffffu, sl);
-      if (lane == 0) {
-        spm[e0 >> 5] = word;
-        ssm[e0 >> 5] = sword;
-      }
+    auto bits_at = [&](const unsigned* m, size_t gb, int rem) {
+      const unsigned sh = (unsigned)(gb & 31);
+      unsigned x = m[gb >> 5] >> sh;
+      if (sh) x |= m[(gb >> 5) + 1] << (32 - sh);
+      return rem < 32 ? x & ((1u << rem) - 1u) : x;
+    };
+    for (int w = threadIdx.x; w < (nS + 31) >> 5; w += NT) {
+      const size_t gb = a0 + (size_t)w * 32;
+      const int rem = nS - w * 32;
+      const unsigned sl = bits_at(g.pmask, gb, rem);
+      spm[w] = sl;
+      ssm[w] = sl;
+      sam[w] = bits_at(g.fmask, gb, rem);
     }
     if (g.qbits)
       for (int w = threadIdx.x; w < (nQ + 31) >> 5; w += NT) {
@@ -1118,7 +1121,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
         double v = 0.0;
         if (pres) {
           const double cv = sc[coff + i];
-          v = anticommutes<B>(ks, P) ? __dmul_rn(cv, g.cs) : cv;
+          v = ((sam[i >> 5] >> (i & 31)) & 1u) ? __dmul_rn(cv, g.cs) : cv;
         }
         if (c == 0) {
           const double qv = qval(j, kq);
@@ -1346,6 +1349,7 @@ struct PlanState {
   size_t M = 0, A = 0, W = 0;
   unsigned* inv_perm = nullptr;
   unsigned* pmask = nullptr;
+  unsigned* fmask = nullptr;
   unsigned* ppre = nullptr;
   unsigned* ptotal = nullptr;
   const long long* a_dev = nullptr;  // device product count (nullptr: none)
@@ -1372,6 +1376,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   const size_t W = (M + 31) / 32;
   pl.W = W;
   unsigned* fmask = ws.fmask.as<unsigned>(3 * std::max<size_t>(W, 1) + 64);
+  pl.fmask = fmask;
   pl.pmask = fmask + std::max<size_t>(W, 1);
   unsigned* qmask = pl.pmask + std::max<size_t>(W, 1);
   pl.ppre = ws.tables.as<unsigned>(std::max<size_t>(W, 1) + (W + PW - 1) / PW + 8);
@@ -1617,6 +1622,8 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   g.rule = pl.rule;
   g.theta = want_hist ? theta : 0.0;
   g.qbits = pl.qbits;
+  g.pmask = pl.pmask;
+  g.fmask = pl.fmask;
   g.out_lcp = nullptr;
   g.out_amask = nullptr;
   for (int w = 0; w < 8; ++w) g.pn[w] = 0;
