@@ -630,6 +630,7 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       const size_t budget = max_terms - idc;
       const bool spec_ok = o.n_ge_theta >= budget &&
                            (o.count_eps > max_terms || o.count_eps == o.n_ge_theta + idc);
+      double floor_cut = theta > exact && spec_ok ? theta : 0.0;  // verified: cut >= theta
       if (theta > exact && !spec_ok) {  // speculation failed: redo exactly
         dress_undo(h->s, M0, L0, F0);
         host_ms("spec_redo", std::chrono::steady_clock::now());
@@ -643,7 +644,8 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       if (eps > 0.0 || h->s.logical > max_terms) {
         const auto t1 = std::chrono::steady_clock::now();
         KernelScope* outer2 = new KernelScope("span_compress");
-        CompressResult r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr);
+        CompressResult r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr,
+                                          nullptr, nullptr, floor_cut);
         delete outer2;
         // a compress that cut sets the next guess; one that did not (every
         // slotted term kept) leaves the last verified guess in place

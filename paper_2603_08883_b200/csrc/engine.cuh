@@ -478,9 +478,12 @@ struct Reducer {
 };
 /// glob_known (partitioned, optional): {global count_eps, global identity
 /// count} already reduced by the caller, saving the first reduction.
+/// cand_floor: a verified lower bound of the cut value (a slot speculation
+/// that passed: at least `budget` terms are >= theta), so the select only
+/// gathers candidates >= it.
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
                               size_t count_eps, bool want_stats, Reducer* red = nullptr,
-                              const ull* glob_known = nullptr);
+                              const ull* glob_known = nullptr, double cand_floor = 0.0);
 void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* na);
 
 double expect_store(DeviceStore& s, const double* factors);

@@ -380,6 +380,7 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     std::copy(o.glob, o.glob + 3, glob);
   else
     red.sum(glob, 3);
+  double floor_cut = 0.0;  // verified lower bound of the cut (speculation passed)
   if (theta > exact) {
     // the slotted shards compress like the full ones iff the global top
     // `budget` terms are all >= theta and either the compress cuts or no
@@ -387,6 +388,7 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     const ull idc = glob[2] ? 1 : 0;
     const ull budget = max_terms - idc;
     const bool ok = glob[1] >= budget && (glob[0] > max_terms || glob[0] == glob[1] + idc);
+    if (ok) floor_cut = theta;
     if (!ok) {  // every rank sees the same sums and redoes the step exactly
       dress_undo(s, M0, L0, F0);
       if (!exch) {
@@ -409,7 +411,7 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
   if (eps > 0.0 || glob[0] > max_terms) {  // compress_partitioned always runs with a cut
     const ull gk[2] = {glob[0], glob[2]};
     CompressResult r =
-        compress_store(s, eps, max_terms, true, o.count_eps, cs_out != nullptr, &red, gk);
+        compress_store(s, eps, max_terms, true, o.count_eps, cs_out != nullptr, &red, gk, floor_cut);
     if (cs_out) {
       cs_out->dropped_terms += r.dropped_terms;
       cs_out->dropped_weight += r.dropped_weight;

@@ -928,7 +928,7 @@ __global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __r
 
 CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool hist_ready,
                               size_t count_eps, bool want_stats, Reducer* red,
-                              const ull* glob_known) {
+                              const ull* glob_known, double cand_floor) {
   HostScope hscope("host_compress_inner");
   if (eps < 0) throw std::invalid_argument("compress: epsilon < 0");
   if (max_terms < 1) throw std::invalid_argument("compress: max_terms < 1");
@@ -1018,11 +1018,14 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       IQCC_CUDA(cudaMemsetAsync(cnt, 0, (kMaxRounds + 1) * sizeof(ull), st));
       {
         KernelScope ks("select_gather");
+        // candidates below a verified floor of the cut can never be selected
+        // (every term at or above the cut is >= the floor)
+        const double lo = std::max(eps, cand_floor);
         const unsigned grid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (s.M + 2047) / 2048));
         switch (s.B) {
-          case 1: k_gather_bin<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, sel, av[0], ai[0], cnt, dh); break;
-          case 2: k_gather_bin<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, sel, av[0], ai[0], cnt, dh); break;
-          default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, eps, sel, av[0], ai[0], cnt, dh); break;
+          case 1: k_gather_bin<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, lo, sel, av[0], ai[0], cnt, dh); break;
+          case 2: k_gather_bin<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, lo, sel, av[0], ai[0], cnt, dh); break;
+          default: k_gather_bin<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, lo, sel, av[0], ai[0], cnt, dh); break;
         }
       }
       if (getenv("IQCC_DEBUG")) debug_check("select gather");
