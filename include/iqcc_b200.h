@@ -129,6 +129,15 @@ int iqcc_gpu_expect(iqcc_gpu_sum* h, const double* factors, double* energy);
  * grad receives 2n values (theta block then phi block). */
 int iqcc_gpu_qmf_energy_gradient(iqcc_gpu_sum* h, const double* factors, const double* derivs,
                                  double* energy, double* grad);
+/* qcc_energy (iqcc/optimizer.hpp:19-25): <omega| U^dag H U |omega> through
+ * the fully dressed Hamiltonian (no compression, merges drop exact zeros),
+ * for K entanglers gens [K][2B] with host cos/sin of the amplitudes. */
+int iqcc_gpu_qcc_energy(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
+                        const double* sin_tau, const double* factors, double* energy);
+/* qcc_gradient (iqcc/optimizer.hpp:54-77): dE/dtau_k for every k (grad [K]);
+ * step k's derivative (dress_derivative, :31-48) dressed through the rest. */
+int iqcc_gpu_qcc_gradient(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
+                          const double* sin_tau, const double* factors, double* grad);
 /* gradient (iqcc/dis.hpp:39-52) for K candidate generators [K][2B];
  * flip_group_only != 0 restricts each sum to the candidate's flip group
  * (group_gradient, iqcc/dis.hpp:121-132, exact at poles). */

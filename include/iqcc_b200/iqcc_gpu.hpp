@@ -175,10 +175,39 @@ class DeviceSum {
     detail::check(iqcc_gpu_expect(d_.get(), t.data(), &e));
     return e;
   }
+  /// qcc_energy / qcc_gradient (iqcc/optimizer.hpp:19-77) on device copies.
+  double qcc_energy(const QmfState& omega, const Ansatz& a) const {
+    std::vector<uint64_t> gens;
+    std::vector<double> c, s;
+    ansatz_arrays(a, gens, c, s);
+    const auto t = detail::factor_table(omega);
+    double e = 0.0;
+    detail::check(iqcc_gpu_qcc_energy(d_.get(), a.size(), gens.data(), c.data(), s.data(), t.data(), &e));
+    return e;
+  }
+  std::vector<double> qcc_gradient(const QmfState& omega, const Ansatz& a) const {
+    std::vector<uint64_t> gens;
+    std::vector<double> c, s;
+    ansatz_arrays(a, gens, c, s);
+    const auto t = detail::factor_table(omega);
+    std::vector<double> g(a.size(), 0.0);
+    detail::check(iqcc_gpu_qcc_gradient(d_.get(), a.size(), gens.data(), c.data(), s.data(), t.data(), g.data()));
+    return g;
+  }
   PauliSum download() const { return detail::download(d_, n_); }
   iqcc_gpu_sum* handle() const { return d_.get(); }
 
  private:
+  void ansatz_arrays(const Ansatz& a, std::vector<uint64_t>& gens, std::vector<double>& c,
+                     std::vector<double>& s) const {
+    for (std::size_t k = 0; k < a.size(); ++k) {
+      if (a.entanglers[k].n_qubits() != n_) throw std::invalid_argument("dress_single: mismatched qubit counts");
+      const auto row = detail::row_of(a.entanglers[k].view());
+      gens.insert(gens.end(), row.begin(), row.end());
+      c.push_back(std::cos(a.tau[k]));
+      s.push_back(std::sin(a.tau[k]));
+    }
+  }
   std::size_t n_;
   detail::Handle d_;
 };
@@ -246,6 +275,20 @@ inline double expect_sum(const QmfState& omega, const PauliSum& h) {
   if (h.empty()) return 0.0;
   DeviceSum d(h);
   return d.expect(omega);
+}
+
+/// iqcc::qcc_energy (iqcc/optimizer.hpp:19-25).
+inline double qcc_energy(const PauliSum& h, const QmfState& omega, const Ansatz& ansatz) {
+  if (h.empty()) return 0.0;
+  DeviceSum d(h);
+  return d.qcc_energy(omega, ansatz);
+}
+
+/// iqcc::qcc_gradient (iqcc/optimizer.hpp:54-77).
+inline std::vector<double> qcc_gradient(const PauliSum& h, const QmfState& omega, const Ansatz& ansatz) {
+  if (h.empty()) return std::vector<double>(ansatz.size(), 0.0);
+  DeviceSum d(h);
+  return d.qcc_gradient(omega, ansatz);
 }
 
 /// iqcc::qmf_energy_gradient (iqcc/qmf.hpp:94-148).

@@ -640,6 +640,54 @@ double orc_expect_word(size_t n, const double* th, const double* ph, const uint6
 double orc_expect_sum(const double* th, const double* ph, const orc_sum* h) {
   return expect_sum(th, ph, *h);
 }
+// qcc_energy, iqcc/optimizer.hpp:19-25: dress_sequence without compression
+// and MergeOptions{0.0, true}, then expect_sum.
+double orc_qcc_energy(const orc_sum* h, const double* th, const double* ph, size_t K,
+                      const uint64_t* gens, const double* taus) {
+  return guard([&]() -> double {
+    orc_sum cur = *h;
+    for (size_t k = 0; k < K; ++k) cur = dress(cur, gens + k * 2 * h->B, taus[k], 0.0, true, 1e-10);
+    return expect_sum(th, ph, cur);
+  }, 0.0);
+}
+
+// dress_derivative, iqcc/optimizer.hpp:31-48: the anticommuting part of a
+// maps to -sin(tau) c T + cos(tau) (phase) c (-i) (T*P); merged with drop 0.
+static orc_sum dress_derivative(const orc_sum& a, const u64* P, double tau) {
+  const std::size_t B = a.B;
+  const double cs = std::cos(tau), sn = std::sin(tau);
+  orc_sum surv, prod;
+  surv.n = prod.n = a.n;
+  surv.B = prod.B = B;
+  std::vector<u64> tmp(2 * B);
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    if (commute(a.row(i), P, B)) continue;
+    surv.push(a.row(i), -sn * a.c[i]);
+    int t = mult(a.row(i), P, tmp.data(), B);
+    prod.push(tmp.data(), a.c[i] * cs * cplx{0.0, -1.0} * phase(t));
+  }
+  orc_sum sorted = from_terms(a.n, prod.rows.data(), prod.c.data(), prod.size(), 0.0, false, 0.0);
+  return merge(surv, sorted, 0.0, false, 0.0);
+}
+
+// qcc_gradient, iqcc/optimizer.hpp:54-77: forward chain A_k (exact merges),
+// derivative of step k, dressed through the remaining entanglers.
+int orc_qcc_gradient(const orc_sum* h, const double* th, const double* ph, size_t K,
+                     const uint64_t* gens, const double* taus, double* g) {
+  return guard([&]() -> int {
+    const std::size_t B = h->B;
+    std::vector<orc_sum> chain{*h};
+    for (size_t k = 0; k + 1 < K; ++k)
+      chain.push_back(dress(chain.back(), gens + k * 2 * B, taus[k], 0.0, true, 1e-10));
+    for (size_t k = 0; k < K; ++k) {
+      orc_sum d = dress_derivative(chain[k], gens + k * 2 * B, taus[k]);
+      for (size_t j = k + 1; j < K; ++j) d = dress(d, gens + j * 2 * B, taus[j], 0.0, false, 0.0);
+      g[k] = expect_sum(th, ph, d);
+    }
+    return 0;
+  }, -1);
+}
+
 double orc_qmf_energy_gradient(const orc_sum* h, const double* th, const double* ph, double* g) {
   return energy_grad(*h, th, ph, g);
 }

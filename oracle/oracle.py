@@ -95,6 +95,8 @@ class Oracle:
             "orc_expect_word": (C.c_double, [C.c_size_t, _f64p, _f64p, _u64p]),
             "orc_expect_sum": (C.c_double, [_f64p, _f64p, _vp]),
             "orc_qmf_energy_gradient": (C.c_double, [_vp, _f64p, _f64p, _f64p]),
+            "orc_qcc_energy": (C.c_double, [_vp, _f64p, _f64p, C.c_size_t, _u64p, _f64p]),
+            "orc_qcc_gradient": (C.c_int, [_vp, _f64p, _f64p, C.c_size_t, _u64p, _f64p, _f64p]),
             "orc_gradient": (C.c_double, [_vp, _f64p, _f64p, _u64p]),
             "orc_dis_candidates": (C.c_size_t, [_vp, _f64p, _f64p, C.c_size_t, C.c_double, C.c_size_t,
                                                 C.c_int, C.c_uint64, _u64p, _f64p, C.c_size_t]),
@@ -216,6 +218,26 @@ class Oracle:
         g = np.zeros(2 * h.n_qubits, np.float64)
         e = self.lib.orc_qmf_energy_gradient(h.handle, _p(th, _f64p), _p(ph, _f64p), _p(g, _f64p))
         return e, g
+
+    def qcc_energy(self, h, theta, phi, gens, taus):
+        """qcc_energy (iqcc/optimizer.hpp:19-25)."""
+        th, ph = np.ascontiguousarray(theta, np.float64), np.ascontiguousarray(phi, np.float64)
+        g = np.ascontiguousarray(gens, np.uint64)
+        t = np.ascontiguousarray(taus, np.float64)
+        return self.lib.orc_qcc_energy(h.handle, _p(th, _f64p), _p(ph, _f64p), len(t), _p(g, _u64p),
+                                       _p(t, _f64p))
+
+    def qcc_gradient(self, h, theta, phi, gens, taus):
+        """qcc_gradient (iqcc/optimizer.hpp:54-77)."""
+        th, ph = np.ascontiguousarray(theta, np.float64), np.ascontiguousarray(phi, np.float64)
+        g = np.ascontiguousarray(gens, np.uint64)
+        t = np.ascontiguousarray(taus, np.float64)
+        out = np.zeros(max(1, len(t)), np.float64)
+        rc = self.lib.orc_qcc_gradient(h.handle, _p(th, _f64p), _p(ph, _f64p), len(t), _p(g, _u64p),
+                                       _p(t, _f64p), _p(out, _f64p))
+        if rc != 0:
+            raise RuntimeError(self.lib.orc_last_error().decode())
+        return out[: len(t)]
 
     def gradient(self, h, theta, phi, p):
         th, ph, p = np.ascontiguousarray(theta, np.float64), np.ascontiguousarray(phi, np.float64), self._row(p)

@@ -74,6 +74,12 @@ size_t orc_dis_candidates(const orc_sum* h, const double* theta, const double* p
                           size_t out_cap);
 size_t orc_flip_groups(const orc_sum* h, size_t* starts_out, size_t out_cap);
 
+/* variational energy and amplitude gradient (iqcc/optimizer.hpp:19-77) ---- */
+double orc_qcc_energy(const orc_sum* h, const double* theta, const double* phi, size_t K,
+                      const uint64_t* gens, const double* taus);
+int orc_qcc_gradient(const orc_sum* h, const double* theta, const double* phi, size_t K,
+                     const uint64_t* gens, const double* taus, double* grad_out);
+
 /* partitioning (iqcc/partition.hpp) --------------------------------------- */
 double orc_choose_partition_bits(const orc_sum* h, size_t m, size_t* bits_out);
 /* Runs distribute -> parallel_dress -> gather.  shard_sizes_out[2^m];

@@ -201,6 +201,26 @@ double orc_expect_word(size_t n, const double* th, const double* ph, const uint6
 double orc_expect_sum(const double* th, const double* ph, const orc_sum* h) {
   return iqcc::expect_sum(qmf_of(h->h.n_qubits(), th, ph), h->h);
 }
+double orc_qcc_energy(const orc_sum* h, const double* th, const double* ph, size_t K,
+                      const uint64_t* gens, const double* taus) {
+  return guard([&]() -> double {
+    iqcc::Ansatz a;
+    std::size_t n = h->h.n_qubits(), B = iqcc::blocks_for(n);
+    for (size_t k = 0; k < K; ++k) a.push(word_of(n, gens + k * 2 * B), taus[k]);
+    return iqcc::qcc_energy(h->h, qmf_of(n, th, ph), a);
+  }, 0.0);
+}
+int orc_qcc_gradient(const orc_sum* h, const double* th, const double* ph, size_t K,
+                     const uint64_t* gens, const double* taus, double* g) {
+  return guard([&]() -> int {
+    iqcc::Ansatz a;
+    std::size_t n = h->h.n_qubits(), B = iqcc::blocks_for(n);
+    for (size_t k = 0; k < K; ++k) a.push(word_of(n, gens + k * 2 * B), taus[k]);
+    auto v = iqcc::qcc_gradient(h->h, qmf_of(n, th, ph), a);
+    for (size_t k = 0; k < K; ++k) g[k] = v[k];
+    return 0;
+  }, -1);
+}
 double orc_qmf_energy_gradient(const orc_sum* h, const double* th, const double* ph, double* g) {
   std::size_t n = h->h.n_qubits();
   return iqcc::qmf_energy_gradient(h->h, qmf_of(n, th, ph), std::span<double>(g, 2 * n));

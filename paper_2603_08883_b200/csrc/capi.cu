@@ -669,6 +669,62 @@ int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* nc, size
   });
 }
 
+// qcc_energy / qcc_gradient (iqcc/optimizer.hpp:19-77): device-resident
+// dressing chains on working copies of the store; merges drop exact zeros
+// only (MergeOptions{0.0, ...}) and nothing is compressed.
+namespace {
+struct ScratchStore {
+  DeviceStore s;
+  ~ScratchStore() { s.free_all(); }
+};
+void check_gens(const uint64_t* gens, size_t K, uint32_t Bref) {
+  for (size_t k = 0; k < K; ++k)
+    if (row_is_identity(gens + k * 2 * Bref, Bref))
+      throw std::invalid_argument("dress_single: identity generator");
+}
+}  // namespace
+
+int iqcc_gpu_qcc_energy(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
+                        const double* sin_tau, const double* factors, double* energy) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    check_gens(gens, K, Bref);
+    ScratchStore d;
+    store_clone(h->s, d.s);
+    for (size_t k = 0; k < K; ++k) {
+      const auto row = widen_row(gens + k * 2 * Bref, Bref, d.s.B);
+      dress_step(d.s, row.data(), cos_tau[k], sin_tau[k], 0.0, false, 0.0);
+    }
+    *energy = expect_store(d.s, factors);
+  });
+}
+
+int iqcc_gpu_qcc_gradient(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
+                          const double* sin_tau, const double* factors, double* grad) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    check_gens(gens, K, Bref);
+    ScratchStore a;  // forward chain A_k = h dressed through entanglers [0, k)
+    store_clone(h->s, a.s);
+    for (size_t k = 0; k < K; ++k) {
+      const auto rk = widen_row(gens + k * 2 * Bref, Bref, a.s.B);
+      {
+        ScratchStore d;  // derivative of step k, dressed through the rest
+        store_clone(a.s, d.s);
+        dress_step(d.s, rk.data(), -sin_tau[k], cos_tau[k], 0.0, false, 0.0, nullptr, 0.0, true);
+        for (size_t j = k + 1; j < K; ++j) {
+          const auto rj = widen_row(gens + j * 2 * Bref, Bref, d.s.B);
+          dress_step(d.s, rj.data(), cos_tau[j], sin_tau[j], 0.0, false, 0.0);
+        }
+        grad[k] = expect_store(d.s, factors);
+      }
+      if (k + 1 < K) dress_step(a.s, rk.data(), cos_tau[k], sin_tau[k], 0.0, false, 0.0);
+    }
+  });
+}
+
 int iqcc_gpu_expect(iqcc_gpu_sum* h, const double* factors, double* energy) {
   return guarded([&] {
     need(h);

@@ -82,17 +82,21 @@ struct Thr {
 struct SlotRule {
   double cs, sn;
   double thc, ths, thq;  // commuting survivor / anticommuting survivor / product
+  // the derivative of a dressing (dress_derivative, iqcc/optimizer.hpp:31-48)
+  // keeps only the anticommuting part: commuting survivors and the identity
+  // get no slot
+  int anti_only;
 };
 
 __host__ __device__ inline SlotRule make_slot_rule(double cs, double sn, double theta) {
-  return SlotRule{cs, sn, theta, 0.0, theta};
+  return SlotRule{cs, sn, theta, 0.0, theta, 0};
 }
 
 __device__ __forceinline__ bool survivor_slot(const SlotRule& r, bool present, bool id, bool anti,
                                               double c) {
   if (!present) return false;
-  if (id) return true;
-  return anti ? (r.ths == 0.0 || fabs(__dmul_rn(c, r.cs)) >= r.ths) : fabs(c) >= r.thc;
+  if (id) return !r.anti_only;
+  return anti ? (r.ths == 0.0 || fabs(__dmul_rn(c, r.cs)) >= r.ths) : (!r.anti_only && fabs(c) >= r.thc);
 }
 __device__ __forceinline__ bool product_slot(const SlotRule& r, bool anti_present, double c) {
   if (!anti_present) return false;
@@ -1353,7 +1357,7 @@ struct PlanState {
   unsigned* ppre = nullptr;
   unsigned* ptotal = nullptr;
   const long long* a_dev = nullptr;  // device product count (nullptr: none)
-  SlotRule rule{1.0, 0.0, 0.0, 0.0, 0.0};
+  SlotRule rule{1.0, 0.0, 0.0, 0.0, 0.0, 0};
   const unsigned* qbits = nullptr;   // product slot bits in rank order (nullptr: all)
   const unsigned* qpre = nullptr;
   const unsigned* qtotal = nullptr;
@@ -1363,7 +1367,7 @@ PlanState g_plan;
 
 template <int B>
 void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = true,
-               SlotRule rule = SlotRule{1.0, 0.0, 0.0, 0.0, 0.0}) {
+               SlotRule rule = SlotRule{1.0, 0.0, 0.0, 0.0, 0.0, 0}) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   PlanState pl;
@@ -1736,9 +1740,12 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
 
 template <int B>
 DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps, const uint64_t* next_row, double theta) {
+                        bool want_hist, double eps, const uint64_t* next_row, double theta,
+                        bool anti_only) {
   const Key<B> P = make_key<B>(gen_row);
-  plan_impl<B>(s, P, sn != 0.0, true, make_slot_rule(cs, sn, theta));
+  SlotRule rule = make_slot_rule(cs, sn, theta);
+  rule.anti_only = anti_only ? 1 : 0;
+  plan_impl<B>(s, P, sn != 0.0, true, rule);
   Key<B> PN;
   if (next_row) PN = make_key<B>(next_row);
   return merge_impl<B>(s, P, g_plan.A, nullptr, nullptr, cs, sn, drop, want_hist, eps,
@@ -1815,7 +1822,7 @@ const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row, do
                                      double sn, double theta) {
   // survivor slots by the rule; the products leave for the peer, whose
   // slot bits the receiver derives from the values (recv_slot_bits)
-  const SlotRule r{cs, sn, theta, 0.0, 0.0};
+  const SlotRule r{cs, sn, theta, 0.0, 0.0, 0};
   switch (s.B) {
     case 1: plan_impl<1>(s, make_key<1>(gen_row), true, false, r); break;
     case 2: plan_impl<2>(s, make_key<2>(gen_row), true, false, r); break;
@@ -1825,7 +1832,7 @@ const long long* plan_products_async(DeviceStore& s, const uint64_t* gen_row, do
 }
 
 void plan_survivors(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double theta) {
-  const SlotRule r{cs, sn, theta, 0.0, 0.0};
+  const SlotRule r{cs, sn, theta, 0.0, 0.0, 0};
   switch (s.B) {
     case 1: plan_impl<1>(s, make_key<1>(gen_row), false, true, r); break;
     case 2: plan_impl<2>(s, make_key<2>(gen_row), false, true, r); break;
@@ -1930,11 +1937,12 @@ void dress_undo(DeviceStore& s, size_t M, size_t logical, const Filter& filt) {
 }
 
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cs, double sn, double drop,
-                        bool want_hist, double eps, const uint64_t* next_row, double theta) {
+                        bool want_hist, double eps, const uint64_t* next_row, double theta,
+                        bool anti_only) {
   switch (s.B) {
-    case 1: return dress_impl<1>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta);
-    case 2: return dress_impl<2>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta);
-    case 4: return dress_impl<4>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta);
+    case 1: return dress_impl<1>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta, anti_only);
+    case 2: return dress_impl<2>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta, anti_only);
+    case 4: return dress_impl<4>(s, gen_row, cs, sn, drop, want_hist, eps, next_row, theta, anti_only);
     default: throw std::runtime_error("dress: unsupported block count");
   }
 }

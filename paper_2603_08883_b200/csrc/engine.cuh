@@ -428,9 +428,13 @@ void set_merge_reducer(Reducer* red);
 /// theta > 0: a compress whose cut is >= theta follows (theta <= eps: known;
 /// a power of two above eps: speculated, the caller verifies n_ge_theta);
 /// terms below theta/2 get no output slot (SlotRule in dress.cu).
+/// anti_only: keep only the anticommuting part (commuting terms and the
+/// identity are dropped): with (cos, sin) = (-sin tau, cos tau) this is
+/// dress_derivative (iqcc/optimizer.hpp:31-48).
 DressOutcome dress_step(DeviceStore& s, const uint64_t* gen_row, double cos_tau, double sin_tau,
                         double drop_thr, bool want_hist, double eps,
-                        const uint64_t* next_row = nullptr, double theta = 0.0);
+                        const uint64_t* next_row = nullptr, double theta = 0.0,
+                        bool anti_only = false);
 /// Undo the last dress_step (the merge's input buffers are still the
 /// workspace's output pair): restores the store as it was before the step.
 void dress_undo(DeviceStore& s, size_t M, size_t logical, const Filter& filt);

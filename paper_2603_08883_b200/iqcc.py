@@ -341,6 +341,32 @@ class DeviceSum:
         check(lib.iqcc_gpu_qmf_energy_gradient(self.handle, _addr(t), _addr(d), C.byref(e), _addr(g)))
         return e.value, g
 
+    def _ansatz_arrays(self, ansatz: "Ansatz"):
+        K = ansatz.size()
+        W = 2 * blocks_for(self.n_qubits)
+        gens = np.zeros((max(K, 1), W), np.uint64)
+        for k, p in enumerate(ansatz.entanglers):
+            gens[k] = p.row
+        cs_ = np.array([math.cos(t) for t in ansatz.tau] or [1.0])
+        sn_ = np.array([math.sin(t) for t in ansatz.tau] or [0.0])
+        return K, gens, cs_, sn_
+
+    def qcc_energy(self, omega: QmfState, ansatz: "Ansatz") -> float:
+        """qcc_energy (iqcc/optimizer.hpp:19-25) on a device copy; the sum is unchanged."""
+        K, gens, cs_, sn_ = self._ansatz_arrays(ansatz)
+        t = qmf_factor_table(omega)
+        e = C.c_double()
+        check(lib.iqcc_gpu_qcc_energy(self.handle, K, _addr(gens), _addr(cs_), _addr(sn_), _addr(t), C.byref(e)))
+        return e.value
+
+    def qcc_gradient(self, omega: QmfState, ansatz: "Ansatz") -> np.ndarray:
+        """qcc_gradient (iqcc/optimizer.hpp:54-77): dE/dtau_k for every entangler."""
+        K, gens, cs_, sn_ = self._ansatz_arrays(ansatz)
+        t = qmf_factor_table(omega)
+        g = np.zeros(max(K, 1), np.float64)
+        check(lib.iqcc_gpu_qcc_gradient(self.handle, K, _addr(gens), _addr(cs_), _addr(sn_), _addr(t), _addr(g)))
+        return g[:K]
+
     def gradients(self, omega: QmfState, cands: np.ndarray, flip_group_only: bool = False) -> np.ndarray:
         t = qmf_factor_table(omega)
         c = np.ascontiguousarray(cands, np.uint64).reshape(-1, 2 * blocks_for(self.n_qubits))
@@ -459,6 +485,20 @@ def expect_sum(omega: QmfState, h: PauliSum) -> float:
 def qmf_energy_gradient(h: PauliSum, omega: QmfState):
     """iqcc/qmf.hpp:94-148; returns (energy, grad[2n])."""
     return DeviceSum.upload(h).qmf_energy_gradient(omega)
+
+
+def qcc_energy(h: PauliSum, omega: QmfState, ansatz: Ansatz) -> float:
+    """iqcc::qcc_energy (iqcc/optimizer.hpp:19-25)."""
+    if len(h) == 0:
+        return 0.0
+    return DeviceSum.upload(h).qcc_energy(omega, ansatz)
+
+
+def qcc_gradient(h: PauliSum, omega: QmfState, ansatz: Ansatz) -> np.ndarray:
+    """iqcc::qcc_gradient (iqcc/optimizer.hpp:54-77)."""
+    if len(h) == 0:
+        return np.zeros(ansatz.size())
+    return DeviceSum.upload(h).qcc_gradient(omega, ansatz)
 
 
 def gradient(h: PauliSum, omega: QmfState, p: PauliWord) -> float:

@@ -3,11 +3,14 @@
 // on the reference tests' seeds.  Built by tests/cpp/Makefile where
 // /root/reference exists; the binary (tests/cpp/_bin) runs on the GPU box.
 // Prints one "ok <name> <cases>" line per check; exits 1 on any mismatch.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <random>
 
 #include "iqcc/dressing.hpp"
 #include "iqcc/io.hpp"
+#include "iqcc/optimizer.hpp"
 #include "iqcc/pauli.hpp"
 #include "iqcc/qmf.hpp"
 #include "iqcc_b200/iqcc_gpu.hpp"
@@ -99,6 +102,32 @@ int main(int argc, char** argv) {
     for (int k = 0; k < 3; ++k) a.push(rand_word(rng, h.n_qubits(), false), amp(rng));
     expect(iqcc::gpu::dress_sequence(h, a, 0.0) == iqcc::dress_sequence(h, a, 0.0), "h2 sequence", 0);
     std::printf("ok fcidump_sequence 1\n");
+  }
+  // qcc_energy / qcc_gradient, iqcc/optimizer.hpp:19-77 (tests/test_optimizer.cpp shapes)
+  {
+    std::mt19937_64 rng(619);
+    std::uniform_real_distribution<double> amp(-1.0, 1.0), ang(-3.0, 3.0);
+    int cases = 0;
+    for (int t = 0; t < 12; ++t) {
+      std::size_t n = 3 + t % 5;
+      auto h = rand_sum(rng, n, 10 * n);
+      iqcc::QmfState om(n);
+      for (std::size_t j = 0; j < n; ++j) {
+        om.theta[j] = ang(rng);
+        om.phi[j] = ang(rng);
+      }
+      iqcc::Ansatz a;
+      for (int k = 0; k < 3; ++k) a.push(rand_word(rng, n, false), amp(rng));
+      const double e = iqcc::gpu::qcc_energy(h, om, a), er = iqcc::qcc_energy(h, om, a);
+      expect(std::fabs(e - er) <= 1e-10 * std::max(1.0, std::fabs(er)), "qcc_energy/619", t);
+      const auto g = iqcc::gpu::qcc_gradient(h, om, a), gr = iqcc::qcc_gradient(h, om, a);
+      double scale = 1.0;
+      for (double v : gr) scale = std::max(scale, std::fabs(v));
+      for (std::size_t k = 0; k < g.size(); ++k)
+        expect(std::fabs(g[k] - gr[k]) <= 1e-10 * scale, "qcc_gradient/619", t);
+      ++cases;
+    }
+    std::printf("ok qcc_energy_gradient %d\n", cases);
   }
   // identity generator rejected with std::invalid_argument
   {

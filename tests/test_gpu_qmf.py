@@ -154,3 +154,33 @@ def test_choose_partition_bits(eng, port):  # test_partition.cpp:79-134
         bits, imb = eng.choose_partition_bits(d, m)
         wb, wi = port.choose_partition_bits(hm, m)
         assert bits == list(wb) and imb == pytest.approx(wi, rel=1e-15)
+
+
+@pytest.mark.parametrize("n,terms,K", [(6, 60, 3), (20, 800, 4), (64, 3000, 5)])
+def test_qcc_energy_and_gradient(eng, port, n, terms, K):  # optimizer.hpp:19-77 (test_optimizer.cpp shapes)
+    rng = port.rng(613 + n)
+    h = rng.sum(n, terms)
+    th, ph = rng.qmf(n)
+    gens = np.stack([rng.word(n, False) for _ in range(K)])
+    taus = [0.31, -0.17, 0.09, 0.23, -0.41][:K]
+    ans = eng.Ansatz([eng.PauliWord(n, g) for g in gens], taus)
+    om = eng.QmfState(th, ph)
+    e = eng.qcc_energy(host(eng, h), om, ans)
+    assert close(e, port.qcc_energy(h, th, ph, gens, taus))
+    g = eng.qcc_gradient(host(eng, h), om, ans)
+    gr = port.qcc_gradient(h, th, ph, gens, taus)
+    assert np.abs(g - gr).max() <= REL * max(1.0, np.abs(gr).max())
+
+
+def test_qcc_gradient_at_zero_is_dis_gradient(eng):
+    # optimizer.hpp:50-53: at tau = 0 component k is the DIS screening
+    # gradient of generator k (test_optimizer.cpp)
+    g = load_golden("c1_h2_ccpvdz.npz")
+    n, ne = int(g["n_qubits"]), int(g["n_electrons"])
+    h = eng.PauliSum(n, g["rows0"], g["coeffs0"])
+    hf = eng.hf_reference([q < ne for q in range(n)])
+    picks = eng.dis_candidates(h, hf, 3)
+    ans = eng.Ansatz([p.word for p in picks], [0.0] * len(picks))
+    grad = eng.qcc_gradient(h, hf, ans)
+    for k, p in enumerate(picks):
+        assert close(grad[k], p.gradient, 1e-10) or abs(grad[k] - p.gradient) < 1e-12
