@@ -16,6 +16,8 @@ JSON object per row (profiles/r1_aux_*.json keeps the committed copy):
   C5      200-qubit slice: G_mol(200, 5e7, seed 5) dressed without a cap
           until > 1.25e8 terms (the per-GPU share of 1e9 over 8 B200), then
           compress(max_terms = 1.25e8) (truncation time)
+  qcc     qcc_energy / qcc_gradient (iqcc/optimizer.hpp:19-77) on
+          G_mol(124, 1e7) with 4 entanglers (uncompressed chains)
 
 Times are device-synchronous wall clock around the public API calls (each
 call ends with a stream synchronize), after a warm-up call.  Synthetic data
@@ -228,9 +230,33 @@ def run_c5(args):
                 note="1-GPU slice of C5: per-GPU share of 1e9 terms over 8 B200 (no exchange)")]
 
 
+def run_qcc(args):
+    """qcc_energy / qcc_gradient (iqcc/optimizer.hpp:19-77, SURVEY.md §8(f)
+    rank 1): uncompressed device-resident dressing chains."""
+    from paper_2603_08883_b200 import iqcc
+    n, m, K = 124, int(args.qcc_terms), 4
+    d = iqcc.DeviceSum.generate_mol(n, m, 2)
+    rs = np.random.default_rng(11)
+    om = iqcc.QmfState(rs.uniform(-3, 3, n), rs.uniform(-3, 3, n))
+    ents = []
+    for k in range(K):
+        r = np.random.default_rng([6, k])
+        qs = [int(q) for q in r.choice(n, 4, replace=False)]
+        ents.append(word(n, qs, [1, 0, 0, 0]))
+    ans = iqcc.Ansatz(ents, [0.1, -0.2, 0.15, 0.05][:K])
+    t, e = timed(lambda: d.qcc_energy(om, ans), reps=2)
+    r1 = row("qcc", op="qcc_energy", n_qubits=n, terms=m, entanglers=K, ms=1e3 * t, energy=e,
+             note="clone + K uncompressed dressings + expect_sum")
+    t2, _ = timed(lambda: d.qcc_gradient(om, ans), reps=1)
+    r2 = row("qcc", op="qcc_gradient", n_qubits=n, terms=m, entanglers=K, ms=1e3 * t2,
+             note="K derivative chains (K(K+1)/2 dressings + K-1 forward) + K expect_sum")
+    return [r1, r2]
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c2,energy,c4,c5")
+    ap.add_argument("--only", default="c2,energy,c4,c5,qcc")
+    ap.add_argument("--qcc-terms", type=float, default=1e7)
     ap.add_argument("--energy-terms", type=float, default=1e8)
     ap.add_argument("--dis-terms", type=float, default=1e7)
     ap.add_argument("--dis-generic", type=float, default=1e5)
@@ -246,7 +272,7 @@ def main():
     native.init(0)
     rows = []
     for part in args.only.split(","):
-        rows += {"c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5}[part](args)
+        rows += {"c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5, "qcc": run_qcc}[part](args)
     if args.out:
         with open(args.out, "w") as f:
             json.dump(rows, f, indent=1)
