@@ -891,7 +891,7 @@ struct MergeCfg {
   static constexpr size_t OFF_QP = OFF_QM + (size_t)PMW * 4;     // their prefix
   static constexpr size_t OFF_AM = OFF_QP + (size_t)PMW * 4;     // anticommute bits of S
   static constexpr size_t OFF_HIST = (OFF_AM + (size_t)PMW * 4 + 15) & ~(size_t)15;
-  static constexpr int HBINS = kHistBins;  // |c| histogram (u32, per CTA) for compress
+  static constexpr int HBINS = kHistBins + kSubBins;  // |c| histograms (u32, per CTA) for compress
   static constexpr size_t bytes(bool hist, int stages) {
     return OFF_HIST - (2 - stages) * STAGE + (hist ? HBINS * 4 : 0);
   }
@@ -941,6 +941,7 @@ struct MergeArgs {
   const unsigned* pmask;
   const unsigned* fmask;
   double theta;           // count emitted non-identity |c| >= theta (0: off)
+  int sub_b0;             // first exponent bin of the fine histogram (< 0: none)
 };
 
 /// Issue the loads of one tile into one stage: survivors by the TMA bulk
@@ -1175,7 +1176,15 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
         const double a = fabs(v);
         const bool id = o0 + q == 0 && key_is_identity<B>(k);
         if (id || a >= g.eps) ++n_eps;
-        if (!id && a >= g.eps) atomicAdd(shist + hist_bin(a), 1u);
+        if (!id && a >= g.eps) {
+          const unsigned hb = hist_bin(a);
+          atomicAdd(shist + hb, 1u);
+          const unsigned sb = hb - (unsigned)g.sub_b0;
+          if (sb < (unsigned)kSubWindow)
+            atomicAdd(shist + kHistBins + sb * kSubBinsPer +
+                          (unsigned)(((ull)__double_as_longlong(a) >> 46) & (kSubBinsPer - 1)),
+                      1u);
+        }
         if (!id && g.theta != 0.0 && a >= g.theta) ++n_ge;
       }
       if (meta) {
@@ -1234,7 +1243,7 @@ __device__ __forceinline__ void merge_flush(const MergeArgs& g, unsigned* shist,
     if (s_cnt[3]) atomicAdd(g.counters + 6, (ull)s_cnt[3]);
   }
   if (g.want_hist)
-    for (int b = threadIdx.x; b < kHistBins; b += NT)
+    for (int b = threadIdx.x; b < kHistBins + kSubBins; b += NT)
       if (shist[b]) atomicAdd(g.hist + b, shist[b]);
 }
 
@@ -1569,6 +1578,8 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   g_plan = pl;
 }
 
+int g_sub_b0 = -(1 << 20);  // fine-histogram window of the last merge (see kSubBins)
+
 template <int B, int NT, int IPT>
 void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys, const double* q_vals,
                     double cs, double sn, double drop, bool want_hist, double eps, const Key<B>* PN,
@@ -1598,9 +1609,9 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
   double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
   ull* ctr = ws.counters.as<ull>(16);
-  unsigned* hist = ws.hist.as<unsigned>(kHistBins);
+  unsigned* hist = ws.hist.as<unsigned>(kHistBins + kSubBins);
   IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
-  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
+  if (want_hist) IQCC_CUDA(cudaMemsetAsync(hist, 0, (kHistBins + kSubBins) * sizeof(unsigned), st));
   using Cfg = MergeCfg<B, NT, IPT>;
   MergeArgs g;
   g.keys = s.keys();
@@ -1625,6 +1636,10 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   g.dbg = debug_buffer();
   g.rule = pl.rule;
   g.theta = want_hist ? theta : 0.0;
+  // the cut lies at or above the (verified) floor theta: a fine histogram of
+  // the exponent bins from theta's up lets the select skip ~6 bits
+  g.sub_b0 = want_hist && theta > 0.0 ? hist_bin_of(theta) : -(1 << 20);
+  g_sub_b0 = g.sub_b0;
   g.qbits = pl.qbits;
   g.pmask = pl.pmask;
   g.fmask = pl.fmask;
@@ -1882,6 +1897,8 @@ void recv_slot_bits(const double* rv, size_t n, double thq) {
 void plan_set_products(size_t A) { g_plan.A = A; }
 
 void set_merge_reducer(Reducer* red) { g_merge_red = red; }
+
+int merge_sub_window() { return g_sub_b0; }
 
 size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products) {
   switch (s.B) {

@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -159,6 +160,20 @@ __device__ __forceinline__ unsigned hist_bin(double a) {
   const int e = (int)((ull)__double_as_longlong(a) >> 52) - (1023 - 192);
   return (unsigned)min(max(e, 0), kHistBins - 1);
 }
+
+/// Fine |c| histogram of the merge for the compress select: the 4 exponent
+/// bins from the speculated cut floor's bin up, 64 sub-bins each (the top 6
+/// mantissa bits), appended to the 256-bin histogram.  The select then
+/// starts with exponent + 6 mantissa bits fixed (64x fewer candidates).
+constexpr int kSubBinsPer = 64, kSubWindow = 4, kSubBins = kSubBinsPer * kSubWindow;
+__host__ __device__ inline int hist_bin_of(double a) {
+  unsigned long long b;
+  memcpy(&b, &a, 8);
+  const int e = (int)(b >> 52) - (1023 - 192);
+  return e < 0 ? 0 : (e > kHistBins - 1 ? kHistBins - 1 : e);
+}
+/// window start (exponent bin) of the last merge's fine histogram; < 0: none
+int merge_sub_window();
 
 /// keep_term (iqcc/pauli.hpp:180-184) for a real coefficient.
 __device__ __forceinline__ bool keep_term(double c, bool identity, double thr) {

@@ -698,15 +698,23 @@ __device__ __forceinline__ bool block_pick(const HG* __restrict__ hg, const unsi
   return s_x >= 0;
 }
 
-// hist_g[256] (global counts, u64) / hist_l[256] (local, u32): pick the
-// coarse bin holding the budget-th largest |c|.
+// hist_g (global counts) / hist_l (local, u32): pick the coarse bin holding
+// the budget-th largest |c|; if the bin lies in the merge's fine-histogram
+// window (kSubBins), also pick its sub-bin (top 6 mantissa bits).
 template <class HG>
 __global__ void __launch_bounds__(256) k_pick_bin(const HG* __restrict__ hist_g,
                                                   const unsigned* __restrict__ hist_l, ull budget,
-                                                  SelState* __restrict__ st) {
+                                                  SelState* __restrict__ st, int sub_b0) {
   int b;
   ull bg, bl;
   const bool ok = block_pick(hist_g, hist_l, kHistBins, budget, &b, &bg, &bl);
+  const int sb = b - sub_b0;  // uniform: b comes from shared memory
+  bool refine = ok && b > 0 && b < kHistBins - 1 && sb >= 0 && sb < kSubWindow;
+  int x = -1;
+  ull sg = 0, sl = 0;
+  if (refine)
+    refine = block_pick(hist_g + kHistBins + sb * kSubBinsPer, hist_l + kHistBins + sb * kSubBinsPer,
+                        kSubBinsPer, budget - bg, &x, &sg, &sl);
   if (threadIdx.x != 0) return;
   st->fail = ok ? 0 : 1;
   if (!ok) return;
@@ -720,6 +728,13 @@ __global__ void __launch_bounds__(256) k_pick_bin(const HG* __restrict__ hist_g,
     st->known_mask |= 0x7FFull << 52;
     st->known_val = (ull)(b + (1023 - 192)) << 52;
     st->top = 51;
+    if (refine) {  // and the top 6 mantissa bits
+      st->r -= sg;
+      st->local_above += sl;
+      st->known_mask |= (ull)(kSubBinsPer - 1) << 46;
+      st->known_val |= (ull)x << 46;
+      st->top = 45;
+    }
   }
   st->ntie = 0;
 }
@@ -829,6 +844,7 @@ __global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys
   unsigned dmask;
   hist_begin(sel, do_hist, shift, dmask, sh);
   const unsigned bin = (unsigned)sel->bin;
+  const ull km = sel->known_mask, kv = sel->known_val;  // includes a picked sub-bin
   const bool has_id = key_is_identity<B>(load_key<B>(keys, 0));
   // the next chunk's coefficients are loaded before this chunk is compacted
   // (the block scans and barriers of chunk_emit hide the load latency)
@@ -861,7 +877,8 @@ __global__ void __launch_bounds__(256) k_gather_bin(const ull* __restrict__ keys
     for (int k = 0; k < 8; ++k) {
       const double a = fabs(c[k]);
       v[k] = (ull)__double_as_longlong(a);
-      if (first + k < M && a >= eps && hist_bin(a) == bin && !(first + k == 0 && has_id)) hit |= 1u << k;
+      if (first + k < M && a >= eps && hist_bin(a) == bin && (v[k] & km) == kv && !(first + k == 0 && has_id))
+        hit |= 1u << k;
     }
     chunk_emit(v, hit, first, nullptr, cv, ci, n_out, do_hist, shift, dmask, sh, scratch, &s_base);
   }
@@ -940,10 +957,12 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
   }
   CompressResult res;
   const size_t logical_before = s.logical;
-  unsigned* hist = ws.hist.as<unsigned>(kHistBins);
+  unsigned* hist = ws.hist.as<unsigned>(kHistBins + kSubBins);
   ull* ctr = ws.counters.as<ull>(16);
+  // the fine histogram comes only with a merge's histogram
+  const int sub_b0 = hist_ready ? merge_sub_window() : -(1 << 20);
   if (!hist_ready) {
-    IQCC_CUDA(cudaMemsetAsync(hist, 0, kHistBins * sizeof(unsigned), st));
+    IQCC_CUDA(cudaMemsetAsync(hist, 0, (kHistBins + kSubBins) * sizeof(unsigned), st));
     IQCC_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(ull), st));
     const unsigned grid = (unsigned)std::min<size_t>(1184, std::max<size_t>(1, (s.M + 255) / 256));
     if (s.M) {
@@ -983,18 +1002,18 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
     } else {
       SelState* sel = reinterpret_cast<SelState*>(ws.misc.as<ull>(16));
       ull* hist_g = ws.misc.as<ull>(16) + 8;  // placeholder, resized below
-      ull* gbuf = ws.partials.as<ull>(kHistBins + (1 << kDigitBits));
+      ull* gbuf = ws.partials.as<ull>(kHistBins + kSubBins + (1 << kDigitBits));
       hist_g = gbuf;
-      ull* dh_g = gbuf + kHistBins;
+      ull* dh_g = gbuf + kHistBins + kSubBins;
       // a single store picks straight from its own (u32) histograms; ranks
       // widen them to u64 for the allreduce
       if (red) {
-        k_widen<<<1, 256, 0, st>>>(hist, hist_g, kHistBins);
-        red->sum_device(hist_g, kHistBins);
-        k_pick_bin<ull><<<1, 256, 0, st>>>(hist_g, hist, (ull)budget, sel);
+        k_widen<<<1, 256, 0, st>>>(hist, hist_g, kHistBins + kSubBins);
+        red->sum_device(hist_g, kHistBins + kSubBins);
+        k_pick_bin<ull><<<1, 256, 0, st>>>(hist_g, hist, (ull)budget, sel, sub_b0);
         count_launch("select");
       } else {
-        k_pick_bin<unsigned><<<1, 256, 0, st>>>(hist, hist, (ull)budget, sel);
+        k_pick_bin<unsigned><<<1, 256, 0, st>>>(hist, hist, (ull)budget, sel, sub_b0);
       }
       count_launch("select");
       // candidate capacity: the store size (stable across steps, so the
@@ -1008,7 +1027,8 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       // digit rounds: the device tracks the next unfixed bit (interior bins
       // start below the exponent); kPlanned rounds resolve an interior bin,
       // an edge bin (63 free bits) is finished after the read-back shows it
-      constexpr int kPlanned = (52 + kDigitBits - 1) / kDigitBits;
+      // with the fine window (expected to hold the cut) 46 bits remain
+      const int kPlanned = sub_b0 >= 0 ? (46 + kDigitBits - 1) / kDigitBits : (52 + kDigitBits - 1) / kDigitBits;
       constexpr int kMaxRounds = (63 + kDigitBits - 1) / kDigitBits;
       const size_t hsz = (size_t)1 << kDigitBits;
       unsigned* dh = ws.misc2.as<unsigned>(hsz * (kMaxRounds + 1));
