@@ -1182,7 +1182,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
           const unsigned sb = hb - (unsigned)g.sub_b0;
           if (sb < (unsigned)kSubWindow)
             atomicAdd(shist + kHistBins + sb * kSubBinsPer +
-                          (unsigned)(((ull)__double_as_longlong(a) >> 46) & (kSubBinsPer - 1)),
+                          (unsigned)(((ull)__double_as_longlong(a) >> (52 - kSubBits)) & (kSubBinsPer - 1)),
                       1u);
         }
         if (!id && g.theta != 0.0 && a >= g.theta) ++n_ge;

@@ -162,10 +162,11 @@ __device__ __forceinline__ unsigned hist_bin(double a) {
 }
 
 /// Fine |c| histogram of the merge for the compress select: the 4 exponent
-/// bins from the speculated cut floor's bin up, 64 sub-bins each (the top 6
+/// bins from the speculated cut floor's bin up, 16 sub-bins each (the top 4
 /// mantissa bits), appended to the 256-bin histogram.  The select then
-/// starts with exponent + 6 mantissa bits fixed (64x fewer candidates).
-constexpr int kSubBinsPer = 64, kSubWindow = 4, kSubBins = kSubBinsPer * kSubWindow;
+/// starts with exponent + 4 mantissa bits fixed (16x fewer candidates).
+constexpr int kSubBinsPer = 16, kSubWindow = 4, kSubBins = kSubBinsPer * kSubWindow;
+constexpr int kSubBits = 4;  // log2(kSubBinsPer)
 __host__ __device__ inline int hist_bin_of(double a) {
   unsigned long long b;
   memcpy(&b, &a, 8);

@@ -700,7 +700,7 @@ __device__ __forceinline__ bool block_pick(const HG* __restrict__ hg, const unsi
 
 // hist_g (global counts) / hist_l (local, u32): pick the coarse bin holding
 // the budget-th largest |c|; if the bin lies in the merge's fine-histogram
-// window (kSubBins), also pick its sub-bin (top 6 mantissa bits).
+// window (kSubBins), also pick its sub-bin (top kSubBits mantissa bits).
 template <class HG>
 __global__ void __launch_bounds__(256) k_pick_bin(const HG* __restrict__ hist_g,
                                                   const unsigned* __restrict__ hist_l, ull budget,
@@ -731,9 +731,9 @@ __global__ void __launch_bounds__(256) k_pick_bin(const HG* __restrict__ hist_g,
     if (refine) {  // and the top 6 mantissa bits
       st->r -= sg;
       st->local_above += sl;
-      st->known_mask |= (ull)(kSubBinsPer - 1) << 46;
-      st->known_val |= (ull)x << 46;
-      st->top = 45;
+      st->known_mask |= (ull)(kSubBinsPer - 1) << (52 - kSubBits);
+      st->known_val |= (ull)x << (52 - kSubBits);
+      st->top = 51 - kSubBits;
     }
   }
   st->ntie = 0;
@@ -1027,8 +1027,9 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       // digit rounds: the device tracks the next unfixed bit (interior bins
       // start below the exponent); kPlanned rounds resolve an interior bin,
       // an edge bin (63 free bits) is finished after the read-back shows it
-      // with the fine window (expected to hold the cut) 46 bits remain
-      const int kPlanned = sub_b0 >= 0 ? (46 + kDigitBits - 1) / kDigitBits : (52 + kDigitBits - 1) / kDigitBits;
+      // with the fine window (expected to hold the cut) 52 - kSubBits bits remain
+      const int kPlanned = sub_b0 >= 0 ? (52 - kSubBits + kDigitBits - 1) / kDigitBits
+                                       : (52 + kDigitBits - 1) / kDigitBits;
       constexpr int kMaxRounds = (63 + kDigitBits - 1) / kDigitBits;
       const size_t hsz = (size_t)1 << kDigitBits;
       unsigned* dh = ws.misc2.as<unsigned>(hsz * (kMaxRounds + 1));
