@@ -18,10 +18,14 @@ JSON object per row (profiles/r1_aux_*.json keeps the committed copy):
           compress(max_terms = 1.25e8) (truncation time)
   qcc     qcc_energy / qcc_gradient (iqcc/optimizer.hpp:19-77) on
           G_mol(124, 1e7) with 4 entanglers (uncompressed chains)
+  poly    build_poly_kernels (iqcc/optimizer.hpp:340-368) on G_mol(124, 1e7),
+          6 entanglers to order 2 (22 subsets, 253 sandwiches), generic omega;
+          its CPU arm times oracle/_ref (the reference) on a 2e4-term sample
 
 Times are device-synchronous wall clock around the public API calls (each
 call ends with a stream synchronize), after a warm-up call.  Synthetic data
-only; nothing here reads /root/reference or oracle/.
+only; nothing here reads /root/reference; oracle/ is used only as the poly
+row's CPU arm (the checker timed, never the measured GPU path).
 """
 from __future__ import annotations
 
@@ -253,9 +257,40 @@ def run_qcc(args):
     return [r1, r2]
 
 
+def run_poly(args):
+    """build_poly_kernels (iqcc/optimizer.hpp:340-368, SURVEY.md §8(f) rank
+    2): t(t+1)/2 sandwiches <omega|W_a H W_b|omega> over a G_mol sum at a
+    generic omega; the CPU arm is oracle/_ref (the reference) on a sample."""
+    from paper_2603_08883_b200 import iqcc
+    from oracle.oracle import Oracle
+    n, m, K, order = 124, int(args.poly_terms), 6, 2
+    d = iqcc.DeviceSum.generate_mol(n, m, 2)
+    rs = np.random.default_rng(13)
+    om = iqcc.QmfState(rs.uniform(-3, 3, n), rs.uniform(-3, 3, n))
+    ents = []
+    for k in range(K):
+        r = np.random.default_rng([8, k])
+        qs = [int(q) for q in r.choice(n, 4, replace=False)]
+        ents.append(word(n, qs, [1, 0, 0, 0]))
+    ex = iqcc.build_poly(ents, om, order)
+    t_sub = len(ex.subsets)
+    pairs = t_sub * (t_sub + 1) // 2
+    t, _ = timed(lambda: d.poly_kernels(om, ex), reps=2)
+    kind = "reference" if Oracle.available("reference") else "port"
+    orc = Oracle(kind)
+    ms_ = int(args.poly_cpu_terms)
+    hs = orc.gen_mol(n, ms_, 2)
+    t0 = time.perf_counter()
+    orc.poly_kernels(hs, om.theta, om.phi, np.stack([e.row for e in ents]), order)
+    tc = time.perf_counter() - t0
+    return [row("poly", op="build_poly_kernels", n_qubits=n, terms=m, entanglers=K, order=order, subsets=t_sub,
+                pairs=pairs, ms=1e3 * t, pair_terms_per_s=pairs * m / t,
+                cpu={"kind": kind, "cores": 1, "sample_terms": ms_, "s": tc, "pair_terms_per_s": pairs * ms_ / tc})]
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c2,energy,c4,c5,qcc")
+    ap.add_argument("--only", default="c2,energy,c4,c5,qcc,poly")
     ap.add_argument("--qcc-terms", type=float, default=1e7)
     ap.add_argument("--energy-terms", type=float, default=1e8)
     ap.add_argument("--dis-terms", type=float, default=1e7)
@@ -264,6 +299,8 @@ def main():
     ap.add_argument("--dis-poles", type=float, default=1e5)
     ap.add_argument("--c5-terms", type=float, default=5e7)
     ap.add_argument("--c5-target", type=float, default=1.25e8)
+    ap.add_argument("--poly-terms", type=float, default=1e7)
+    ap.add_argument("--poly-cpu-terms", type=float, default=2e4)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -272,7 +309,7 @@ def main():
     native.init(0)
     rows = []
     for part in args.only.split(","):
-        rows += {"c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5, "qcc": run_qcc}[part](args)
+        rows += {"c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5, "qcc": run_qcc, "poly": run_poly}[part](args)
     if args.out:
         with open(args.out, "w") as f:
             json.dump(rows, f, indent=1)

@@ -143,6 +143,13 @@ int iqcc_gpu_qcc_gradient(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const
  * (group_gradient, iqcc/dis.hpp:121-132, exact at poles). */
 int iqcc_gpu_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* cands, size_t K,
                        int flip_group_only, double* g);
+/* build_poly_kernels (iqcc/optimizer.hpp:340-368) for the t subset words
+ * [t][2B] of a build_poly expansion (optimizer.hpp:219-268, host side):
+ * h_kernel[a][b] = sum_k C_k <W_a P_k W_b> and n_kernel[a][b] = <W_a W_b>,
+ * both [t][t][2] (re, im).  at_poles != 0 (QmfState::at_poles) restricts
+ * each sum to the x run x_a ^ x_b as sandwich does (optimizer.hpp:288-333). */
+int iqcc_gpu_poly_kernels(iqcc_gpu_sum* h, const double* factors, int at_poles, const uint64_t* words,
+                          size_t t, double* h_kernel, double* n_kernel);
 /* dis_candidates (iqcc/dis.hpp:140-191).  Picks are ranked by (|g| desc,
  * canonical); when has_seed, runs of equal |g| are reshuffled with
  * std::mt19937_64(seed) + std::shuffle exactly as the reference does.

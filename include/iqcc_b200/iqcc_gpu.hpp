@@ -29,6 +29,7 @@
 
 #include "iqcc/dis.hpp"
 #include "iqcc/dressing.hpp"
+#include "iqcc/optimizer.hpp"
 #include "iqcc/pauli.hpp"
 #include "iqcc/qmf.hpp"
 #include "iqcc_b200.h"
@@ -338,6 +339,36 @@ inline std::vector<RankedGenerator> dis_candidates(const PauliSum& h, const QmfS
                                std::span<const Block>(rows.data() + i * 2 * B + B, B)),
                      g[i]});
   return picks;
+}
+
+/// iqcc::build_poly_kernels (iqcc/optimizer.hpp:340-368).  The expansion
+/// (build_poly, optimizer.hpp:219-268) is host data and used as given; the
+/// t(t+1)/2 sandwiches and the n_kernel run on the device, bit-identical to
+/// the reference whenever one chunk covers the sum (<= 4096 terms or enough
+/// pairs to fill the GPU), else equal up to fp64 reassociation of the chunks.
+inline PolyKernels build_poly_kernels(const PauliSum& h, const QmfState& omega, const PolyExpansion& ex) {
+  const std::size_t t = ex.subsets.size(), n = ex.n_qubits, B = blocks_for(n);
+  PauliSum zero(n);
+  if (h.empty()) zero.append(PauliWord(n).view(), Complex{});  // h_kernel stays 0
+  DeviceSum d(h.empty() ? zero : h);
+  const auto tab = detail::factor_table(omega);
+  std::vector<uint64_t> words(std::max<std::size_t>(t, 1) * 2 * B);
+  for (std::size_t s = 0; s < t; ++s) {
+    const auto row = detail::row_of(ex.subsets[s].word.view());
+    std::copy(row.begin(), row.end(), words.begin() + s * 2 * B);
+  }
+  std::vector<double> hk(std::max<std::size_t>(t * t, 1) * 2), nk(hk.size());
+  detail::check(iqcc_gpu_poly_kernels(d.handle(), tab.data(), omega.at_poles(), words.data(), t, hk.data(),
+                                      nk.data()));
+  PolyKernels ker;
+  ker.t = t;
+  ker.h_kernel.resize(t * t);
+  ker.n_kernel.resize(t * t);
+  for (std::size_t i = 0; i < t * t; ++i) {
+    ker.h_kernel[i] = Complex(hk[2 * i], hk[2 * i + 1]);
+    ker.n_kernel[i] = Complex(nk[2 * i], nk[2 * i + 1]);
+  }
+  return ker;
 }
 
 }  // namespace iqcc::gpu

@@ -688,6 +688,95 @@ int orc_qcc_gradient(const orc_sum* h, const double* th, const double* ph, size_
   }, -1);
 }
 
+// build_poly (iqcc/optimizer.hpp:219-268): subsets of size <= k in
+// lexicographic index order, each word the ordered product of its
+// entanglers extended on the right, phase exponents accumulated mod 4.
+// build_poly_kernels (optimizer.hpp:340-368) with sandwich (288-333): at the
+// poles only the run of terms whose x plane is x_a ^ x_b is summed.
+int orc_poly_kernels(const orc_sum* h, const double* th, const double* ph, size_t N,
+                     const uint64_t* ents, size_t k, size_t cap, size_t* t_out, uint64_t* words_out,
+                     int* phase_out, double* hk_out, double* nk_out) {
+  return guard([&]() -> int {
+    const std::size_t n = h->n, B = h->B;
+    if (k > N) throw invalid_arg("build_poly: order exceeds N");
+    for (size_t j = 0; j < N; ++j)
+      if (is_id(ents + j * 2 * B, B)) throw invalid_arg("build_poly: identity entangler");
+    double count = 0, binom = 1;
+    for (std::size_t j = 0; j <= k; ++j) {
+      count += binom;
+      binom = binom * double(N - j) / double(j + 1);
+      if (count > 200000.0) throw std::runtime_error("build_poly: subset budget exceeded");
+    }
+    std::vector<u64> words(2 * B, 0);
+    std::vector<int> phs{0}, last{-1};
+    std::size_t beg = 0, end = 1;
+    for (std::size_t sz = 1; sz <= k; ++sz) {
+      const std::size_t next = phs.size();
+      for (std::size_t s = beg; s < end; ++s)
+        for (std::size_t e = (std::size_t)(last[s] + 1); e < N; ++e) {
+          std::vector<u64> w(2 * B);
+          const int t = mult(&words[s * 2 * B], ents + e * 2 * B, w.data(), B);
+          words.insert(words.end(), w.begin(), w.end());
+          phs.push_back((phs[s] + t) & 3);
+          last.push_back((int)e);
+        }
+      beg = next;
+      end = phs.size();
+    }
+    const std::size_t t = phs.size();
+    *t_out = t;
+    if (t > cap) throw std::runtime_error("orc_poly_kernels: capacity");
+    bool poles = true;  // QmfState::at_poles, iqcc/qmf.hpp:26-30
+    for (std::size_t j = 0; j < n; ++j)
+      if (std::abs(std::sin(th[j])) > 1e-12) poles = false;
+    std::vector<u64> w1(2 * B), w2(2 * B);
+    for (std::size_t a = 0; a < t; ++a)
+      for (std::size_t b = a; b < t; ++b) {
+        const u64* wa = &words[a * 2 * B];
+        const u64* wb = &words[b * 2 * B];
+        const int tw = mult(wa, wb, w1.data(), B);
+        const cplx nv = phase(tw) * expect_word(th, ph, w1.data(), B);
+        std::size_t lo = 0, hi = h->size();
+        if (poles) {  // the x run x_a ^ x_b (canonical order is x-major)
+          std::vector<u64> tx(2 * B, 0);
+          for (std::size_t q = 0; q < B; ++q) tx[q] = wa[q] ^ wb[q];
+          auto x_cmp = [&](std::size_t i) {
+            for (std::size_t q = 0; q < B; ++q)
+              if (h->row(i)[q] != tx[q]) return rev64(h->row(i)[q]) < rev64(tx[q]) ? -1 : 1;
+            return 0;
+          };
+          std::size_t l = 0, r = h->size();
+          while (l < r) {
+            const std::size_t mid = (l + r) / 2;
+            if (x_cmp(mid) < 0) l = mid + 1; else r = mid;
+          }
+          lo = hi = l;
+          while (hi < h->size() && x_cmp(hi) == 0) ++hi;
+        }
+        cplx hv{};
+        for (std::size_t i = lo; i < hi; ++i) {
+          const int t1 = mult(wa, h->row(i), w1.data(), B);
+          const int t2 = mult(w1.data(), wb, w2.data(), B);
+          const double e = expect_word(th, ph, w2.data(), B);
+          if (e != 0.0) hv += h->c[i] * phase((t1 + t2) & 3) * e;
+        }
+        nk_out[2 * (a * t + b)] = nv.real();
+        nk_out[2 * (a * t + b) + 1] = nv.imag();
+        nk_out[2 * (b * t + a)] = std::conj(nv).real();
+        nk_out[2 * (b * t + a) + 1] = std::conj(nv).imag();
+        hk_out[2 * (a * t + b)] = hv.real();
+        hk_out[2 * (a * t + b) + 1] = hv.imag();
+        hk_out[2 * (b * t + a)] = std::conj(hv).real();
+        hk_out[2 * (b * t + a) + 1] = std::conj(hv).imag();
+      }
+    for (std::size_t s = 0; s < t; ++s) {
+      std::copy(&words[s * 2 * B], &words[s * 2 * B] + 2 * B, words_out + s * 2 * B);
+      phase_out[s] = phs[s];
+    }
+    return 0;
+  }, -1);
+}
+
 double orc_qmf_energy_gradient(const orc_sum* h, const double* th, const double* ph, double* g) {
   return energy_grad(*h, th, ph, g);
 }

@@ -97,6 +97,8 @@ class Oracle:
             "orc_qmf_energy_gradient": (C.c_double, [_vp, _f64p, _f64p, _f64p]),
             "orc_qcc_energy": (C.c_double, [_vp, _f64p, _f64p, C.c_size_t, _u64p, _f64p]),
             "orc_qcc_gradient": (C.c_int, [_vp, _f64p, _f64p, C.c_size_t, _u64p, _f64p, _f64p]),
+            "orc_poly_kernels": (C.c_int, [_vp, _f64p, _f64p, C.c_size_t, _u64p, C.c_size_t, C.c_size_t,
+                                            _szp, _u64p, C.POINTER(C.c_int), _f64p, _f64p]),
             "orc_gradient": (C.c_double, [_vp, _f64p, _f64p, _u64p]),
             "orc_dis_candidates": (C.c_size_t, [_vp, _f64p, _f64p, C.c_size_t, C.c_double, C.c_size_t,
                                                 C.c_int, C.c_uint64, _u64p, _f64p, C.c_size_t]),
@@ -226,6 +228,33 @@ class Oracle:
         t = np.ascontiguousarray(taus, np.float64)
         return self.lib.orc_qcc_energy(h.handle, _p(th, _f64p), _p(ph, _f64p), len(t), _p(g, _u64p),
                                        _p(t, _f64p))
+
+    def poly_kernels(self, h, theta, phi, ents, k):
+        """build_poly + build_poly_kernels (iqcc/optimizer.hpp:219-368).
+        Returns (words [t][2B], phases [t], h_kernel [t][t] complex, n_kernel)."""
+        th, ph = np.ascontiguousarray(theta, np.float64), np.ascontiguousarray(phi, np.float64)
+        B2 = 2 * ((h.n_qubits + 63) // 64 or 1)
+        e = np.ascontiguousarray(np.asarray(ents, np.uint64).reshape(-1, B2))
+        N = e.shape[0]
+        cap, binom = 0, 1
+        for j in range(min(k, N) + 1):
+            cap += binom
+            binom = binom * (N - j) // (j + 1)
+        cap = max(cap, 1)
+        words = np.zeros((cap, B2), np.uint64)
+        phs = np.zeros(cap, np.int32)
+        hk = np.zeros((cap * cap, 2), np.float64)
+        nk = np.zeros((cap * cap, 2), np.float64)
+        t = C.c_size_t(0)
+        rc = self.lib.orc_poly_kernels(h.handle, _p(th, _f64p), _p(ph, _f64p), N, _p(e, _u64p), k, cap,
+                                       C.byref(t), _p(words, _u64p), phs.ctypes.data_as(C.POINTER(C.c_int)),
+                                       _p(hk, _f64p), _p(nk, _f64p))
+        if rc != 0:
+            raise RuntimeError(self.lib.orc_last_error().decode())
+        t = t.value
+        hc = hk[: t * t].copy().view(np.complex128).reshape(t, t)  # signed zeros kept
+        nc = nk[: t * t].copy().view(np.complex128).reshape(t, t)
+        return words[:t], phs[:t], hc, nc, (hk[: t * t].copy(), nk[: t * t].copy())
 
     def qcc_gradient(self, h, theta, phi, gens, taus):
         """qcc_gradient (iqcc/optimizer.hpp:54-77)."""

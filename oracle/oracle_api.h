@@ -80,6 +80,15 @@ double orc_qcc_energy(const orc_sum* h, const double* theta, const double* phi, 
 int orc_qcc_gradient(const orc_sum* h, const double* theta, const double* phi, size_t K,
                      const uint64_t* gens, const double* taus, double* grad_out);
 
+/* build_poly + build_poly_kernels (iqcc/optimizer.hpp:219-368): expansion of
+ * the N entanglers ents [N][2B] to order k (subset budget 200000); t_out =
+ * subset count, words_out [cap][2B] and phase_out [cap] the subsets in
+ * build_poly order, hk_out / nk_out [cap*cap][2] the kernels (row stride
+ * t).  Returns 0, or -1 on error (orc_last_error). */
+int orc_poly_kernels(const orc_sum* h, const double* theta, const double* phi, size_t N,
+                     const uint64_t* ents, size_t k, size_t cap, size_t* t_out, uint64_t* words_out,
+                     int* phase_out, double* hk_out, double* nk_out);
+
 /* partitioning (iqcc/partition.hpp) --------------------------------------- */
 double orc_choose_partition_bits(const orc_sum* h, size_t m, size_t* bits_out);
 /* Runs distribute -> parallel_dress -> gather.  shard_sizes_out[2^m];

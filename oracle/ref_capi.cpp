@@ -221,6 +221,34 @@ int orc_qcc_gradient(const orc_sum* h, const double* th, const double* ph, size_
     return 0;
   }, -1);
 }
+int orc_poly_kernels(const orc_sum* h, const double* th, const double* ph, size_t N,
+                     const uint64_t* ents, size_t k, size_t cap, size_t* t_out, uint64_t* words_out,
+                     int* phase_out, double* hk_out, double* nk_out) {
+  return guard([&]() -> int {
+    std::size_t n = h->h.n_qubits(), B = iqcc::blocks_for(n);
+    std::vector<iqcc::PauliWord> e;
+    for (size_t j = 0; j < N; ++j) e.push_back(word_of(n, ents + j * 2 * B));
+    iqcc::QmfState om = qmf_of(n, th, ph);
+    iqcc::PolyExpansion ex = iqcc::build_poly(e, om, k);
+    const std::size_t t = ex.subsets.size();
+    *t_out = t;
+    if (t > cap) throw std::runtime_error("orc_poly_kernels: capacity");
+    iqcc::PolyKernels ker = iqcc::build_poly_kernels(h->h, om, ex);
+    for (std::size_t s = 0; s < t; ++s) {
+      auto v = ex.subsets[s].word.view();
+      std::copy(v.x.begin(), v.x.end(), words_out + s * 2 * B);
+      std::copy(v.z.begin(), v.z.end(), words_out + s * 2 * B + B);
+      phase_out[s] = ex.subsets[s].phase_exponent;
+    }
+    for (std::size_t i = 0; i < t * t; ++i) {
+      hk_out[2 * i] = ker.h_kernel[i].real();
+      hk_out[2 * i + 1] = ker.h_kernel[i].imag();
+      nk_out[2 * i] = ker.n_kernel[i].real();
+      nk_out[2 * i + 1] = ker.n_kernel[i].imag();
+    }
+    return 0;
+  }, -1);
+}
 double orc_qmf_energy_gradient(const orc_sum* h, const double* th, const double* ph, double* g) {
   std::size_t n = h->h.n_qubits();
   return iqcc::qmf_energy_gradient(h->h, qmf_of(n, th, ph), std::span<double>(g, 2 * n));

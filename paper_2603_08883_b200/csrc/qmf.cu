@@ -831,4 +831,243 @@ double choose_bits_store(DeviceStore& s, size_t m, size_t* bits_out) {
   return (double)*std::max_element(final_cnt.begin(), final_cnt.end()) / std::max(1.0, ideal);
 }
 
+
+// ------------------------------------------------ polynomial kernels
+// build_poly_kernels (iqcc/optimizer.hpp:340-368) over the device store:
+//   h_kernel[a][b] = sum_i c_i i^(t1+t2) <omega| W_a P_i W_b |omega>
+//   n_kernel[a][b] = i^tw <omega| W_a W_b |omega>
+// for the t subset words W of a build_poly expansion, a <= b (b > a is the
+// conjugate).  One (a, b) pair per thread; the block streams the store
+// through shared-memory tiles and every lane of a warp reads the same staged
+// term.  Per term the product W_a P W_b and its phase come from the same
+// popcount rule as multiply_into (pauli.hpp:202-215); its expectation runs
+// over U = supp(P) | (union of the warp's supp(W_a) | supp(W_b)) in ascending
+// qubit order with identity positions multiplying by 1.0 (exact), so each
+// per-term value is bit-identical to sandwich's (optimizer.hpp:288-333),
+// including its complex arithmetic: (c + 0i)(pr + pi i) = (c pr - 0 pi,
+// c pi + 0 pr), then times e, skipped when e == 0.  A pair's terms are summed
+// in canonical order inside one chunk of the store; chunks (only when the
+// pair count alone cannot fill the GPU) are summed on the host in order, so
+// the result is bit-identical to the reference whenever one chunk covers the
+// store.  At the poles only the run of terms whose x plane is x_a ^ x_b
+// contributes (sandwich's binary search): one thread per pair walks that
+// run, bit-identical always.
+struct PolyPair {
+  unsigned a, b;
+};
+
+template <int B>
+__device__ __forceinline__ void sandwich_term(const Key<B>& wa, const Key<B>& wb, const Key<B>& k,
+                                              Key<B>& w, int& t) {
+  const Key<B> w1 = key_xor<B>(wa, k);
+  t = (product_phase<B>(wa, k) + product_phase<B>(w1, wb)) & 3;
+  w = key_xor<B>(w1, wb);
+}
+
+__device__ __forceinline__ void sandwich_add(double c, int t, double e, double& re, double& im) {
+  const double pr = t == 0 ? 1.0 : (t == 2 ? -1.0 : 0.0);
+  const double pi = t == 1 ? 1.0 : (t == 3 ? -1.0 : 0.0);
+  const double vr = __dsub_rn(__dmul_rn(c, pr), __dmul_rn(0.0, pi));
+  const double vi = __dadd_rn(__dmul_rn(c, pi), __dmul_rn(0.0, pr));
+  re = __dadd_rn(re, __dmul_rn(vr, e));
+  im = __dadd_rn(im, __dmul_rn(vi, e));
+}
+
+template <int B>
+__global__ void __launch_bounds__(128) k_poly_h(const ull* __restrict__ keys,
+                                                const double* __restrict__ coef, size_t M,
+                                                Filter filt, const double* __restrict__ f4_g,
+                                                const ull* __restrict__ words,
+                                                const PolyPair* __restrict__ pairs, size_t np,
+                                                size_t chunk, double* __restrict__ out) {
+  constexpr int TT = 128;
+  __shared__ double f4[4 * 64 * B];
+  __shared__ ull tk[TT * 2 * B];
+  __shared__ double tc[TT];
+  for (int i = threadIdx.x; i < 4 * 64 * B; i += blockDim.x) f4[i] = f4_g[i];
+  const size_t pid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  Key<B> wa, wb;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) wa.w[w] = wb.w[w] = 0;
+  if (pid < np) {
+    wa = load_key<B>(words, pairs[pid].a);
+    wb = load_key<B>(words, pairs[pid].b);
+  }
+  ull up[B];
+#pragma unroll
+  for (int w = 0; w < B; ++w) {
+    const ull s = wa.w[w] | wa.w[B + w] | wb.w[w] | wb.w[B + w];
+    const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)s);
+    const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(s >> 32));
+    up[w] = ((ull)hi << 32) | lo;
+  }
+  const size_t lo = blockIdx.y * chunk, hi = min(M, lo + chunk);
+  double re = 0.0, im = 0.0;
+  for (size_t base = lo; base < hi; base += TT) {
+    __syncthreads();
+    const size_t i = base + threadIdx.x;
+    if (i < hi) {
+      const Key<B> k = load_key<B>(keys, i);
+      const double c = coef[i];
+      const bool keep = filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k));
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) tk[(size_t)threadIdx.x * 2 * B + w] = k.w[w];
+      tc[threadIdx.x] = keep ? c : dead_value();
+    }
+    __syncthreads();
+    const int n = (int)min((size_t)TT, hi - base);
+    for (int j = 0; j < n; ++j) {
+      const double c = tc[j];
+      if (is_dead(c)) continue;  // block-uniform
+      Key<B> k;
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) k.w[w] = tk[(size_t)j * 2 * B + w];
+      Key<B> prod;
+      int t;
+      sandwich_term<B>(wa, wb, k, prod, t);
+      double e = 1.0;
+#pragma unroll
+      for (int w = 0; w < B; ++w) {
+        ull s = k.w[w] | k.w[B + w] | up[w];
+        while (s) {  // warp-uniform: U is the same for every lane
+          const int lz = __clzll((long long)s);
+          const int bit = 63 - lz;
+          const unsigned code = (unsigned)((prod.w[w] >> bit) & 1ull) |
+                                ((unsigned)((prod.w[B + w] >> bit) & 1ull) << 1);
+          e = __dmul_rn(e, f4[4 * (64 * w + lz) + code]);
+          s &= ~(1ull << bit);
+        }
+      }
+      if (e != 0.0) sandwich_add(c, t, e, re, im);
+    }
+  }
+  if (pid < np) {
+    out[2 * (blockIdx.y * np + pid)] = re;
+    out[2 * (blockIdx.y * np + pid) + 1] = im;
+  }
+}
+
+// Poles: the x run [lower_bound(x_a ^ x_b), upper_bound) of the store.
+template <int B>
+__global__ void k_poly_h_poles(const ull* __restrict__ keys, const double* __restrict__ coef,
+                               size_t M, Filter filt, const double* __restrict__ tab, int nq,
+                               const ull* __restrict__ words, const PolyPair* __restrict__ pairs,
+                               size_t np, double* __restrict__ out) {
+  const size_t pid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (pid >= np) return;
+  const Key<B> wa = load_key<B>(words, pairs[pid].a), wb = load_key<B>(words, pairs[pid].b);
+  Key<B> tgt;
+#pragma unroll
+  for (int w = 0; w < B; ++w) {
+    tgt.w[w] = wa.w[w] ^ wb.w[w];
+    tgt.w[B + w] = 0;
+  }
+  size_t lo = 0, hi = M;
+  while (lo < hi) {
+    const size_t mid = (lo + hi) >> 1;
+    if (cmp_x<B>(load_key<B>(keys, mid), tgt) < 0) lo = mid + 1; else hi = mid;
+  }
+  double re = 0.0, im = 0.0;
+  for (size_t i = lo; i < M; ++i) {
+    const Key<B> k = load_key<B>(keys, i);
+    if (cmp_x<B>(k, tgt) != 0) break;
+    const double c = coef[i];
+    if (!filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k))) continue;
+    Key<B> prod;
+    int t;
+    sandwich_term<B>(wa, wb, k, prod, t);
+    const double e = word_expect<B>(prod, tab);
+    if (e != 0.0) sandwich_add(c, t, e, re, im);
+  }
+  out[2 * pid] = re;
+  out[2 * pid + 1] = im;
+}
+
+// n_kernel: i^tw <W_a W_b> (complex times real: (pr e, pi e)).
+template <int B>
+__global__ void k_poly_n(const double* __restrict__ tab, const ull* __restrict__ words,
+                         const PolyPair* __restrict__ pairs, size_t np, double* __restrict__ out) {
+  const size_t pid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (pid >= np) return;
+  const Key<B> wa = load_key<B>(words, pairs[pid].a), wb = load_key<B>(words, pairs[pid].b);
+  const int t = product_phase<B>(wa, wb);
+  const double e = word_expect<B>(key_xor<B>(wa, wb), tab);
+  const double pr = t == 0 ? 1.0 : (t == 2 ? -1.0 : 0.0);
+  const double pi = t == 1 ? 1.0 : (t == 3 ? -1.0 : 0.0);
+  out[2 * pid] = __dmul_rn(pr, e);
+  out[2 * pid + 1] = __dmul_rn(pi, e);
+}
+
+template <int B>
+static void poly_impl(DeviceStore& s, const double* factors, bool poles, const uint64_t* words_rows,
+                      size_t t, double* hk, double* nk) {
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const int nq = (int)s.n_qubits;
+  std::vector<ull> wk(t * 2 * B);
+  for (size_t k = 0; k < t; ++k) row_to_device_key(words_rows + k * 2 * B, B, wk.data() + k * 2 * B);
+  std::vector<PolyPair> pr;
+  pr.reserve(t * (t + 1) / 2);
+  for (unsigned a = 0; a < t; ++a)
+    for (unsigned b = a; b < t; ++b) pr.push_back({a, b});
+  const size_t np = pr.size();
+  const unsigned pblocks = (unsigned)((np + 127) / 128);
+  // chunks of >= 4096 terms, only as many as needed to fill 4 blocks per SM
+  size_t chunks = 1;
+  if (!poles && s.M > 4096)
+    chunks = std::min<size_t>((s.M + 4095) / 4096, std::max<size_t>(1, (148 * 4 + pblocks - 1) / pblocks));
+  chunks = std::min<size_t>(chunks, 65535);
+  const size_t chunk = chunks == 1 ? std::max<size_t>(s.M, 1) : (s.M + chunks - 1) / chunks;
+  ull* dw = ws.misc3.as<ull>(std::max<size_t>(t, 1) * 2 * B);
+  PolyPair* dp = ws.misc2.as<PolyPair>(std::max<size_t>(np, 1));
+  double* tab = ws.tables.as<double>(3 * (size_t)std::max(nq, 1));
+  double* part = ws.partials.as<double>(2 * np * chunks + 2 * np);
+  double* dn = part + 2 * np * chunks;
+  IQCC_CUDA(cudaMemcpyAsync(dw, wk.data(), wk.size() * sizeof(ull), cudaMemcpyHostToDevice, st));
+  IQCC_CUDA(cudaMemcpyAsync(dp, pr.data(), np * sizeof(PolyPair), cudaMemcpyHostToDevice, st));
+  IQCC_CUDA(cudaMemcpyAsync(tab, factors, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, st));
+  {
+    KernelScope ks("poly_kernels");
+    if (poles) {
+      k_poly_h_poles<B><<<pblocks, 128, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, nq, dw, dp, np, part);
+    } else {
+      const std::vector<double> f4 = factor_rows(factors, nq, B);
+      double* f4d = ws.grad_part.as<double>(f4.size());
+      IQCC_CUDA(cudaMemcpyAsync(f4d, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      k_poly_h<B><<<dim3(pblocks, (unsigned)chunks), 128, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, f4d, dw,
+                                                                   dp, np, chunk, part);
+    }
+    k_poly_n<B><<<pblocks, 128, 0, st>>>(tab, dw, dp, np, dn);
+    count_launch("poly_kernels");
+  }
+  const std::vector<double> h = fetch(part, 2 * np * chunks + 2 * np);
+  const double* hn = h.data() + 2 * np * chunks;
+  for (size_t p = 0; p < np; ++p) {
+    double re = h[2 * p], im = h[2 * p + 1];  // chunk 0 as is (no +0 added)
+    for (size_t c = 1; c < chunks; ++c) {
+      re += h[2 * (c * np + p)];
+      im += h[2 * (c * np + p) + 1];
+    }
+    const size_t a = pr[p].a, b = pr[p].b;
+    hk[2 * (a * t + b)] = re;
+    hk[2 * (a * t + b) + 1] = im;
+    hk[2 * (b * t + a)] = re;  // std::conj
+    hk[2 * (b * t + a) + 1] = -im;
+    nk[2 * (a * t + b)] = hn[2 * p];
+    nk[2 * (a * t + b) + 1] = hn[2 * p + 1];
+    nk[2 * (b * t + a)] = hn[2 * p];
+    nk[2 * (b * t + a) + 1] = -hn[2 * p + 1];
+  }
+}
+
+void poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const uint64_t* words,
+                        size_t t, double* hk, double* nk) {
+  if (t == 0) return;
+  switch (s.B) {
+    case 1: poly_impl<1>(s, factors, poles, words, t, hk, nk); break;
+    case 2: poly_impl<2>(s, factors, poles, words, t, hk, nk); break;
+    default: poly_impl<4>(s, factors, poles, words, t, hk, nk); break;
+  }
+}
+
 }  // namespace iqcc_b200

@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -81,6 +81,21 @@ class PauliWord:
     def __repr__(self) -> str:
         return f"PauliWord('{self.to_string()}')"
 
+
+def multiply(p: PauliWord, q: PauliWord):
+    """multiply_into (iqcc/pauli.hpp:202-215): returns (p xor q, t) with
+    p*q = i^t (p xor q), t reduced mod 4."""
+    B = blocks_for(p.n_qubits)
+    t = 0
+    for b in range(B):
+        px, pz, qx, qz = (int(v) for v in (p.row[b], p.row[B + b], q.row[b], q.row[B + b]))
+        rx, rz = px ^ qx, pz ^ qz
+        t += (px & pz).bit_count() + (qx & qz).bit_count() - (rx & rz).bit_count() + 2 * (pz & qx).bit_count()
+    return PauliWord(p.n_qubits, p.row ^ q.row), t % 4
+
+def _complex_of(pairs: np.ndarray) -> np.ndarray:
+    """(re, im) rows -> complex128 with both parts' bits (signed zeros) kept."""
+    return np.ascontiguousarray(pairs, np.float64).reshape(-1, 2).view(np.complex128).reshape(-1).copy()
 
 # ------------------------------------------------------------ containers
 class PauliSum:
@@ -375,6 +390,18 @@ class DeviceSum:
         return g[: c.shape[0]]
 
 
+    def poly_kernels(self, omega: QmfState, ex: "PolyExpansion") -> "PolyKernels":
+        """build_poly_kernels (iqcc/optimizer.hpp:340-368) against this sum."""
+        t = len(ex.subsets)
+        words = np.ascontiguousarray(np.stack([s.word.row for s in ex.subsets]) if t else
+                                     np.zeros((1, 2 * blocks_for(self.n_qubits)), np.uint64))
+        hk = np.zeros((max(t, 1) ** 2, 2), np.float64)
+        nk = np.zeros((max(t, 1) ** 2, 2), np.float64)
+        tab = qmf_factor_table(omega)  # kept alive across the call
+        check(lib.iqcc_gpu_poly_kernels(self.handle, _addr(tab), int(omega.at_poles()),
+                                        _addr(words), t, _addr(hk), _addr(nk)))
+        return PolyKernels(t, _complex_of(hk[: t * t]).reshape(t, t), _complex_of(nk[: t * t]).reshape(t, t))
+
 def pinned_buffers(n_qubits: int, n_terms: int):
     """Page-locked host arrays (rows uint64[n, 2B], coeffs complex128[n])."""
     import torch
@@ -655,3 +682,98 @@ def partition_key(row, n_qubits: int, bits) -> int:
         w = int(row[(0 if p < n_qubits else B) + q // 64])
         key |= ((w >> (q % 64)) & 1) << i
     return key
+
+
+# ------------------------------------------- polynomial expansion kernels
+@dataclass
+class PolySubset:
+    """iqcc/optimizer.hpp:150-157: entangler indices (ascending), the ordered
+    product word and its phase exponent (W_S = i^phase * word)."""
+    indices: List[int]
+    word: PauliWord
+    phase_exponent: int
+
+
+@dataclass
+class PolyExpansion:
+    """iqcc/optimizer.hpp:159-217 (subsets of size <= order_k)."""
+    order_k: int
+    n_entanglers: int
+    n_qubits: int
+    subsets: List[PolySubset]
+
+
+@dataclass
+class PolyKernels:
+    """iqcc/optimizer.hpp:271-281: t x t complex kernels."""
+    t: int
+    h_kernel: np.ndarray
+    n_kernel: np.ndarray
+
+
+def build_poly(entanglers: Sequence[PauliWord], omega: QmfState, k: int,
+               subset_budget: int = 200000) -> PolyExpansion:
+    """build_poly (iqcc/optimizer.hpp:219-268): every subset of size <= k in
+    lexicographic index order, words extended on the right by multiply."""
+    n = len(entanglers)
+    if k > n:
+        raise ValueError("build_poly: order exceeds N")
+    nq = omega.n_qubits()
+    for p in entanglers:
+        if p.n_qubits != nq:
+            raise ValueError("build_poly: mismatched qubit counts")
+        if not p.row.any():
+            raise ValueError("build_poly: identity entangler")
+    count, binom = 0.0, 1.0
+    for j in range(k + 1):
+        count += binom
+        binom = binom * float(n - j) / float(j + 1)
+        if count > float(subset_budget):
+            raise RuntimeError("build_poly: subset budget exceeded")
+    subs = [PolySubset([], PauliWord(nq), 0)]
+    beg, end = 0, 1
+    for _ in range(1, k + 1):
+        nxt = len(subs)
+        for s in range(beg, end):
+            lo = subs[s].indices[-1] + 1 if subs[s].indices else 0
+            for e in range(lo, n):
+                w, t = multiply(subs[s].word, entanglers[e])
+                subs.append(PolySubset(subs[s].indices + [e], w, (subs[s].phase_exponent + t) & 3))
+        beg, end = nxt, len(subs)
+    return PolyExpansion(k, n, nq, subs)
+
+
+def build_poly_kernels(h: PauliSum, omega: QmfState, ex: PolyExpansion) -> PolyKernels:
+    """iqcc::build_poly_kernels (iqcc/optimizer.hpp:340-368) on the B200: the
+    t(t+1)/2 sandwiches <omega|W_a H W_b|omega> in one pass over the sum."""
+    if len(h) == 0:  # zero Hamiltonian: h_kernel is 0, n_kernel still needed
+        z = PauliSum(h.n_qubits)
+        z.append(PauliWord(h.n_qubits), 0.0)
+        return DeviceSum.upload(z).poly_kernels(omega, ex)
+    return DeviceSum.upload(h).poly_kernels(omega, ex)
+
+
+def poly_weights(ex: PolyExpansion, tau: Sequence[float]) -> np.ndarray:
+    """PolyExpansion::weights (iqcc/optimizer.hpp:166-190):
+    q_S = i^(phase_S + 3|S|) prod_{k in S} sin(tau_k/2) prod_{k not in S} cos(tau_k/2)."""
+    ch = [math.cos(t / 2.0) for t in tau]
+    sh = [math.sin(t / 2.0) for t in tau]
+    q = np.zeros(len(ex.subsets), np.complex128)
+    for s, sub in enumerate(ex.subsets):
+        mag = 1.0
+        idx = set(sub.indices)
+        for k in range(ex.n_entanglers):
+            mag *= sh[k] if k in idx else ch[k]
+        q[s] = mag * (1, 1j, -1, -1j)[(sub.phase_exponent + 3 * len(sub.indices)) & 3]
+    return q
+
+
+def poly_energy_from_kernels(ex: PolyExpansion, ker: PolyKernels, tau: Sequence[float]):
+    """poly_energy_from_kernels (iqcc/optimizer.hpp:452-466): the Rayleigh
+    quotient q^H H q / q^H N q; returns (energy, norm)."""
+    q = poly_weights(ex, tau)
+    num = float(np.vdot(q, ker.h_kernel @ q).real)
+    nrm = float(np.vdot(q, ker.n_kernel @ q).real)
+    if nrm < 1e-14:
+        raise RuntimeError("poly_energy: vanishing norm (over-truncation)")
+    return num / nrm, nrm

@@ -3,6 +3,8 @@
 // on the reference tests' seeds.  Built by tests/cpp/Makefile where
 // /root/reference exists; the binary (tests/cpp/_bin) runs on the GPU box.
 // Prints one "ok <name> <cases>" line per check; exits 1 on any mismatch.
+#include <cstring>
+#include <numbers>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -128,6 +130,33 @@ int main(int argc, char** argv) {
       ++cases;
     }
     std::printf("ok qcc_energy_gradient %d\n", cases);
+  }
+  // build_poly_kernels, iqcc/optimizer.hpp:340-368 (tests/test_optimizer.cpp:185-230 shapes):
+  // bit-identical kernels (each sum fits one chunk)
+  {
+    std::mt19937_64 rng(757);
+    std::uniform_real_distribution<double> ang(-3.0, 3.0);
+    int cases = 0;
+    for (int t = 0; t < 8; ++t) {
+      std::size_t n = 3 + 9 * (t % 4);
+      auto h = rand_sum(rng, n, 12 * n);
+      iqcc::QmfState om(n);
+      for (std::size_t j = 0; j < n; ++j) {
+        om.theta[j] = t % 2 ? (j % 3 ? 0.0 : std::numbers::pi) : ang(rng);
+        om.phi[j] = t % 2 ? 0.0 : ang(rng);
+      }
+      std::vector<iqcc::PauliWord> ents;
+      for (int k = 0; k < 4; ++k) ents.push_back(rand_word(rng, n, false));
+      iqcc::PolyExpansion ex = iqcc::build_poly(ents, om, 2 + t % 3);
+      auto a = iqcc::gpu::build_poly_kernels(h, om, ex), b = iqcc::build_poly_kernels(h, om, ex);
+      bool same = a.t == b.t;
+      for (std::size_t i = 0; same && i < b.t * b.t; ++i)
+        same = std::memcmp(&a.h_kernel[i], &b.h_kernel[i], sizeof(iqcc::Complex)) == 0 &&
+               std::memcmp(&a.n_kernel[i], &b.n_kernel[i], sizeof(iqcc::Complex)) == 0;
+      expect(same, "build_poly_kernels/757", t);
+      ++cases;
+    }
+    std::printf("ok build_poly_kernels %d\n", cases);
   }
   // identity generator rejected with std::invalid_argument
   {

@@ -184,3 +184,89 @@ def test_qcc_gradient_at_zero_is_dis_gradient(eng):
     grad = eng.qcc_gradient(h, hf, ans)
     for k, p in enumerate(picks):
         assert close(grad[k], p.gradient, 1e-10) or abs(grad[k] - p.gradient) < 1e-12
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def _kernels_equal(ker, ref_tuple):
+    hk = np.stack([ker.h_kernel.real.ravel(), ker.h_kernel.imag.ravel()], 1)
+    nk = np.stack([ker.n_kernel.real.ravel(), ker.n_kernel.imag.ravel()], 1)
+    return (np.array_equal(_bits(hk), _bits(ref_tuple[4][0])) and
+            np.array_equal(_bits(nk), _bits(ref_tuple[4][1])))
+
+
+@pytest.mark.parametrize("seed,n,terms,N,k", [(757, 4, 25, 4, 4), (761, 3, 30, 4, 4), (701, 20, 400, 4, 2),
+                                              (703, 64, 1500, 5, 2), (705, 124, 800, 3, 3),
+                                              (707, 200, 3000, 6, 2)])
+def test_poly_kernels_bit_exact(eng, port, seed, n, terms, N, k):
+    # build_poly_kernels (iqcc/optimizer.hpp:340-368): one chunk covers the
+    # sum (<= 4096 terms), so every kernel element is bit-identical
+    rng = port.rng(seed)
+    h = rng.sum(n, terms)
+    th, ph = rng.qmf(n)
+    ents = np.stack([rng.word(n, False) for _ in range(N)])
+    om = eng.QmfState(th, ph)
+    ex = eng.build_poly([eng.PauliWord(n, e) for e in ents], om, k)
+    ker = eng.build_poly_kernels(host(eng, h), om, ex)
+    assert _kernels_equal(ker, port.poly_kernels(h, th, ph, ents, k))
+
+
+def test_poly_kernels_at_poles_bit_exact(eng, port):
+    # sandwich's pole path (optimizer.hpp:295-326) on H2 cc-pVDZ at HF
+    g = load_golden("c1_h2_ccpvdz.npz")
+    n, ne = int(g["n_qubits"]), int(g["n_electrons"])
+    h = port.sum(n, g["rows0"], g["coeffs0"])
+    th = np.array([math.pi if j < ne else 0.0 for j in range(n)])
+    ph = np.zeros(n)
+    rows, _ = port.dis_candidates(h, th, ph, 6)
+    om = eng.QmfState(th, ph)
+    ex = eng.build_poly([eng.PauliWord(n, r) for r in rows], om, 3)
+    ker = eng.build_poly_kernels(host(eng, h), om, ex)
+    assert _kernels_equal(ker, port.poly_kernels(h, th, ph, rows, 3))
+    e0, nrm = eng.poly_energy_from_kernels(ex, ker, [0.0] * len(rows))
+    assert close(e0, port.expect_sum(th, ph, h), 1e-12) and nrm == pytest.approx(1.0, abs=1e-12)
+
+
+def test_poly_kernels_chunked_large(eng, port):
+    # 124 qubits, 60000 G_mol terms: the store is split into chunks summed in
+    # order, so elements agree to fp64 reassociation (1e-12 of the row scale)
+    n = 124
+    hm = port.gen_mol(n, 60000, 3)
+    d = eng.DeviceSum.generate_mol(n, 60000, 3)
+    rng = port.rng(709)
+    th, ph = rng.qmf(n)
+    rs = np.random.default_rng(709)  # weight-4 odd-#Y entanglers (dis.hpp:89-116 shape)
+    rows = []
+    for _ in range(4):
+        w = ["I"] * n
+        for j, q in enumerate(rs.choice(n, 4, replace=False)):
+            w[q] = "Y" if j == 0 else "X"
+        rows.append(eng.PauliWord.from_string("".join(w)).row)
+    rows = np.stack(rows)
+    om = eng.QmfState(th, ph)
+    ex = eng.build_poly([eng.PauliWord(n, r) for r in rows], om, 2)
+    ker = d.poly_kernels(om, ex)
+    _, _, hc, nc, raw = port.poly_kernels(hm, th, ph, rows, 2)
+    scale = max(1e-300, np.abs(hc).max())
+    assert np.abs(ker.h_kernel - hc).max() <= 1e-12 * scale
+    assert np.array_equal(_bits(np.stack([ker.n_kernel.real.ravel(), ker.n_kernel.imag.ravel()], 1)), _bits(raw[1]))
+
+
+def test_poly_energy_full_order_is_qcc_energy(eng, port):
+    # tests/test_optimizer.cpp:203-216: the untruncated expansion reproduces
+    # qcc_energy (both computed on the device)
+    rng = port.rng(761)
+    for trial in range(6):
+        n = 3 + trial % 2
+        h = rng.sum(n, 30)
+        th, ph = rng.qmf(n)
+        ents = [eng.PauliWord(n, rng.word(n, False)) for _ in range(4)]
+        taus = [0.3 * (trial + 1), -0.2, 0.45, 0.1]
+        om = eng.QmfState(th, ph)
+        ex = eng.build_poly(ents, om, 4)
+        ker = eng.build_poly_kernels(host(eng, h), om, ex)
+        e, _ = eng.poly_energy_from_kernels(ex, ker, taus)
+        exact = eng.qcc_energy(host(eng, h), om, eng.Ansatz(ents, taus))
+        assert abs(e - exact) <= 1e-12 * max(1.0, abs(exact))
