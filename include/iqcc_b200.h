@@ -197,6 +197,11 @@ int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bi
                                      iqcc_compress_stats* cstats, size_t* terms_in_total);
 /* Partitioned energy: local expect + allreduce (parallel_expect, :241-254). */
 int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* energy);
+/* Partitioned build_poly_kernels (iqcc/optimizer.hpp:371-422): local
+ * sandwiches over this rank's shard, allgathered over NCCL and summed in
+ * worker order; same arguments as iqcc_gpu_poly_kernels, collective. */
+int iqcc_gpu_parallel_poly_kernels(iqcc_gpu_sum* h, const double* factors, int at_poles, const uint64_t* words,
+                                   size_t t, double* h_kernel, double* n_kernel);
 /* Total logical terms over all ranks. */
 int iqcc_gpu_parallel_size(iqcc_gpu_sum* h, size_t* total);
 

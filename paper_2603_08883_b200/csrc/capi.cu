@@ -899,6 +899,22 @@ int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* ene
   });
 }
 
+int iqcc_gpu_parallel_poly_kernels(iqcc_gpu_sum* h, const double* factors, int at_poles, const uint64_t* words,
+                                   size_t t, double* h_kernel, double* n_kernel) {
+  return guarded([&] {
+    need(h);
+    if (t > 0 && (!words || !h_kernel || !n_kernel))
+      throw std::invalid_argument("build_poly_kernels: null buffer");
+    const uint32_t Bref = ref_blocks(h->s);
+    std::vector<uint64_t> wide(t * 2 * h->s.B);
+    for (size_t k = 0; k < t; ++k) {
+      auto r = widen_row(words + k * 2 * Bref, Bref, h->s.B);
+      std::copy(r.begin(), r.end(), wide.begin() + k * 2 * h->s.B);
+    }
+    parallel_poly_kernels_store(h->s, factors, at_poles != 0, wide.data(), t, h_kernel, n_kernel);
+  });
+}
+
 int iqcc_gpu_parallel_size(iqcc_gpu_sum* h, size_t* total) {
   return guarded([&] {
     need(h);

@@ -514,9 +514,12 @@ size_t dis_store(DeviceStore& s, const double* factors, bool poles, size_t top_k
                  size_t cap_per_group, std::vector<uint64_t>& rows_out, std::vector<double>& g_out);
 double choose_bits_store(DeviceStore& s, size_t m, size_t* bits_out);
 /// build_poly_kernels (iqcc/optimizer.hpp:340-368): words [t][2B] (device B,
-/// reference row layout), hk / nk [t][t][2] on the host.
+/// reference row layout), hk / nk [t][t][2] on the host.  worker_local:
+/// the per-worker h_kernel of the partitioned form (diagonal not conjugated).
 void poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const uint64_t* words,
-                        size_t t, double* hk, double* nk);
+                        size_t t, double* hk, double* nk, bool worker_local = false);
+void parallel_poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const uint64_t* words,
+                                 size_t t, double* hk, double* nk);
 void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner, int rank);
 
 /// Partition bits as (device word, bit) pairs (iqcc/partition.hpp:40-42).

@@ -448,4 +448,29 @@ size_t parallel_size(DeviceStore& s) {
   return (size_t)v[0];
 }
 
+/// Partitioned build_poly_kernels (iqcc/optimizer.hpp:371-422): each rank's
+/// h_kernel over its shard, allgathered and combined element by element in
+/// worker order from 0.0 (reduce_scalar, partition.hpp:233-237); the
+/// tau-independent n_kernel comes from the expansion alone.
+void parallel_poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const uint64_t* words,
+                                 size_t t, double* hk, double* nk) {
+  Comm& c = comm();
+  const size_t n = 2 * t * t;
+  if (n == 0) return;
+  std::vector<double> local(n);
+  poly_kernels_store(s, factors, poles, words, t, local.data(), nk, true);
+  cudaStream_t st = stream();
+  double* d = workspace().partials.as<double>((c.world + 1) * n);
+  IQCC_CUDA(cudaMemcpyAsync(d + c.world * n, local.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  IQCC_NCCL(ncclAllGather(d + c.world * n, d, n, ncclFloat64, c.comm, st));
+  std::vector<double> parts(c.world * n);
+  IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  host_sync(st);
+  for (size_t i = 0; i < n; ++i) {
+    double v = 0.0;
+    for (int w = 0; w < c.world; ++w) v += parts[w * n + i];
+    hk[i] = v;
+  }
+}
+
 }  // namespace iqcc_b200

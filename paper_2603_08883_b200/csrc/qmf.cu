@@ -1000,7 +1000,8 @@ __global__ void k_poly_n(const double* __restrict__ tab, const ull* __restrict__
 
 template <int B>
 static void poly_impl(DeviceStore& s, const double* factors, bool poles, const uint64_t* words_rows,
-                      size_t t, double* hk, double* nk) {
+                      size_t t, double* hk, double* nk, bool worker_local) {
+  if (poles) store_materialize(s);  // the x-run search wants live keys only
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   const int nq = (int)s.n_qubits;
@@ -1049,10 +1050,19 @@ static void poly_impl(DeviceStore& s, const double* factors, bool poles, const u
       im += h[2 * (c * np + p) + 1];
     }
     const size_t a = pr[p].a, b = pr[p].b;
-    hk[2 * (a * t + b)] = re;
-    hk[2 * (a * t + b) + 1] = im;
-    hk[2 * (b * t + a)] = re;  // std::conj
-    hk[2 * (b * t + a) + 1] = -im;
+    if (worker_local) {  // partitioned form (optimizer.hpp:386-394): zeroed local += hv, += conj(hv) off the diagonal
+      hk[2 * (a * t + b)] = 0.0 + re;
+      hk[2 * (a * t + b) + 1] = 0.0 + im;
+      if (b != a) {
+        hk[2 * (b * t + a)] = 0.0 + re;
+        hk[2 * (b * t + a) + 1] = 0.0 + -im;
+      }
+    } else {
+      hk[2 * (a * t + b)] = re;
+      hk[2 * (a * t + b) + 1] = im;
+      hk[2 * (b * t + a)] = re;  // std::conj
+      hk[2 * (b * t + a) + 1] = -im;
+    }
     nk[2 * (a * t + b)] = hn[2 * p];
     nk[2 * (a * t + b) + 1] = hn[2 * p + 1];
     nk[2 * (b * t + a)] = hn[2 * p];
@@ -1061,12 +1071,12 @@ static void poly_impl(DeviceStore& s, const double* factors, bool poles, const u
 }
 
 void poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const uint64_t* words,
-                        size_t t, double* hk, double* nk) {
+                        size_t t, double* hk, double* nk, bool worker_local) {
   if (t == 0) return;
   switch (s.B) {
-    case 1: poly_impl<1>(s, factors, poles, words, t, hk, nk); break;
-    case 2: poly_impl<2>(s, factors, poles, words, t, hk, nk); break;
-    default: poly_impl<4>(s, factors, poles, words, t, hk, nk); break;
+    case 1: poly_impl<1>(s, factors, poles, words, t, hk, nk, worker_local); break;
+    case 2: poly_impl<2>(s, factors, poles, words, t, hk, nk, worker_local); break;
+    default: poly_impl<4>(s, factors, poles, words, t, hk, nk, worker_local); break;
   }
 }
 

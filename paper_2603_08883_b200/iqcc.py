@@ -390,16 +390,17 @@ class DeviceSum:
         return g[: c.shape[0]]
 
 
-    def poly_kernels(self, omega: QmfState, ex: "PolyExpansion") -> "PolyKernels":
-        """build_poly_kernels (iqcc/optimizer.hpp:340-368) against this sum."""
+    def poly_kernels(self, omega: QmfState, ex: "PolyExpansion", partitioned: bool = False) -> "PolyKernels":
+        """build_poly_kernels (iqcc/optimizer.hpp:340-368) against this sum
+        (partitioned: the PartitionedSum overload, :371-422, a collective)."""
         t = len(ex.subsets)
         words = np.ascontiguousarray(np.stack([s.word.row for s in ex.subsets]) if t else
                                      np.zeros((1, 2 * blocks_for(self.n_qubits)), np.uint64))
         hk = np.zeros((max(t, 1) ** 2, 2), np.float64)
         nk = np.zeros((max(t, 1) ** 2, 2), np.float64)
         tab = qmf_factor_table(omega)  # kept alive across the call
-        check(lib.iqcc_gpu_poly_kernels(self.handle, _addr(tab), int(omega.at_poles()),
-                                        _addr(words), t, _addr(hk), _addr(nk)))
+        fn = lib.iqcc_gpu_parallel_poly_kernels if partitioned else lib.iqcc_gpu_poly_kernels
+        check(fn(self.handle, _addr(tab), int(omega.at_poles()), _addr(words), t, _addr(hk), _addr(nk)))
         return PolyKernels(t, _complex_of(hk[: t * t]).reshape(t, t), _complex_of(nk[: t * t]).reshape(t, t))
 
 def pinned_buffers(n_qubits: int, n_terms: int):
@@ -671,6 +672,11 @@ class Partition:
         e = C.c_double()
         check(lib.iqcc_gpu_parallel_expect(d.handle, _addr(t), C.byref(e)))
         return e.value
+
+    def poly_kernels(self, d: DeviceSum, omega: QmfState, ex: "PolyExpansion") -> "PolyKernels":
+        """Partitioned build_poly_kernels (iqcc/optimizer.hpp:371-422): local
+        sandwiches, allgathered over NCCL, summed in worker order.  Collective."""
+        return d.poly_kernels(omega, ex, partitioned=True)
 
 
 def partition_key(row, n_qubits: int, bits) -> int:

@@ -74,6 +74,7 @@ _SIGS = {
     "iqcc_gpu_qcc_gradient": (C.c_int, [_vp, C.c_size_t, _u64p, _f64p, _f64p, _f64p, _f64p]),
     "iqcc_gpu_gradients": (C.c_int, [_vp, _f64p, _u64p, C.c_size_t, C.c_int, _f64p]),
     "iqcc_gpu_poly_kernels": (C.c_int, [_vp, _f64p, C.c_int, _u64p, C.c_size_t, _f64p, _f64p]),
+    "iqcc_gpu_parallel_poly_kernels": (C.c_int, [_vp, _f64p, C.c_int, _u64p, C.c_size_t, _f64p, _f64p]),
     "iqcc_gpu_dis_candidates": (C.c_int, [_vp, _f64p, C.c_int, C.c_size_t, C.c_double, C.c_size_t, C.c_int,
                                           C.c_uint64, _u64p, _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_choose_partition_bits": (C.c_int, [_vp, C.c_size_t, _szp, C.POINTER(C.c_double)]),

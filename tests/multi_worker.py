@@ -67,6 +67,14 @@ def main():
     th = np.where(np.arange(n) < n // 3, np.pi, 0.0)
     ph = np.zeros(n)
     e_par = part.expect(d, iqcc.QmfState(th, ph))
+    # partitioned build_poly_kernels (optimizer.hpp:371-422) at the poles
+    # (x-run path) and at a generic omega, 3 of the entanglers to order 2
+    ents = [iqcc.PauliWord(n, g) for g in gens[:3]]
+    th2 = np.random.default_rng(5).uniform(-3, 3, n)
+    kers = []
+    for tt, pp in ((th, ph), (th2, ph)):
+        om = iqcc.QmfState(tt, pp)
+        kers.append(part.poly_kernels(d, om, iqcc.build_poly(ents, om, 2)))
     objs = [None] * world
     dist.all_gather_object(objs, (shard.rows, shard.coeffs, exch))
     if rank == 0:
@@ -82,6 +90,10 @@ def main():
         ok = rows.shape == r.shape and np.array_equal(rows, r) and np.array_equal(coeffs, c)
         e_ref = port.expect_sum(th, ph, h)
         e_ok = abs(e_par - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
+        for ker, tt in zip(kers, (th, th2)):
+            _, _, hc, nc, _ = port.poly_kernels(h, tt, ph, np.stack(gens[:3]), 2)
+            scale = max(1e-300, np.abs(hc).max())
+            e_ok = e_ok and np.abs(ker.h_kernel - hc).max() <= 1e-12 * scale and np.array_equal(ker.n_kernel, nc)
         print(f"MULTI world={world} terms={len(r)} exchanged={sum(o[2] for o in objs)} "
               f"bitexact={ok} energy_ok={e_ok}", flush=True)
         if not (ok and e_ok):
