@@ -1013,10 +1013,12 @@ static void poly_impl(DeviceStore& s, const double* factors, bool poles, const u
     for (unsigned b = a; b < t; ++b) pr.push_back({a, b});
   const size_t np = pr.size();
   const unsigned pblocks = (unsigned)((np + 127) / 128);
-  // chunks of >= 4096 terms, only as many as needed to fill 4 blocks per SM
+  // chunks of >= 4096 terms, only as many as needed to fill 8 blocks (32
+  // warps) per SM: the per-lane product is a dependent dmul chain, so the
+  // kernel needs warps to hide its latency
   size_t chunks = 1;
   if (!poles && s.M > 4096)
-    chunks = std::min<size_t>((s.M + 4095) / 4096, std::max<size_t>(1, (148 * 4 + pblocks - 1) / pblocks));
+    chunks = std::min<size_t>((s.M + 4095) / 4096, std::max<size_t>(1, (148 * 8 + pblocks - 1) / pblocks));
   chunks = std::min<size_t>(chunks, 65535);
   const size_t chunk = chunks == 1 ? std::max<size_t>(s.M, 1) : (s.M + chunks - 1) / chunks;
   ull* dw = ws.misc3.as<ull>(std::max<size_t>(t, 1) * 2 * B);
