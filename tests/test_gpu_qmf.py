@@ -270,3 +270,36 @@ def test_poly_energy_full_order_is_qcc_energy(eng, port):
         e, _ = eng.poly_energy_from_kernels(ex, ker, taus)
         exact = eng.qcc_energy(host(eng, h), om, eng.Ansatz(ents, taus))
         assert abs(e - exact) <= 1e-12 * max(1.0, abs(exact))
+
+
+def test_poly_kernels_edge_cases(eng, port):
+    # order 0 (t = 1: h_kernel = <H>, n_kernel = 1), an empty sum (h_kernel 0),
+    # and the pole path at 200 qubits (B = 4 blocks)
+    rng = port.rng(719)
+    n = 12
+    h = rng.sum(n, 80)
+    th, ph = rng.qmf(n)
+    ents = np.stack([rng.word(n, False) for _ in range(3)])
+    om = eng.QmfState(th, ph)
+    ex0 = eng.build_poly([eng.PauliWord(n, e) for e in ents], om, 0)
+    ker = eng.build_poly_kernels(host(eng, h), om, ex0)
+    assert ker.t == 1 and _kernels_equal(ker, port.poly_kernels(h, th, ph, ents, 0))
+    ex = eng.build_poly([eng.PauliWord(n, e) for e in ents], om, 2)
+    kz = eng.build_poly_kernels(eng.PauliSum(n), om, ex)
+    assert not np.any(kz.h_kernel) and np.array_equal(kz.n_kernel, ker_n(eng, port, n, th, ph, ents))
+    with pytest.raises(ValueError):
+        eng.build_poly([eng.PauliWord(n)], om, 1)  # identity entangler
+    n = 200
+    hm = port.gen_mol(n, 3000, 4)
+    d = eng.DeviceSum.generate_mol(n, 3000, 4)
+    th = np.array([math.pi if q % 4 == 0 else 0.0 for q in range(n)])
+    ph = np.zeros(n)
+    rows, _ = port.dis_candidates(hm, th, ph, 4)
+    om = eng.QmfState(th, ph)
+    ex = eng.build_poly([eng.PauliWord(n, r) for r in rows], om, 2)
+    assert _kernels_equal(d.poly_kernels(om, ex), port.poly_kernels(hm, th, ph, rows, 2))
+
+
+def ker_n(eng, port, n, th, ph, ents):
+    z = port.sum(n, np.zeros((0, 2 * eng.blocks_for(n)), np.uint64), np.zeros(0, np.complex128))
+    return port.poly_kernels(z, th, ph, ents, 2)[3]
