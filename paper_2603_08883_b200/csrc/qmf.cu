@@ -916,29 +916,42 @@ __global__ void __launch_bounds__(128) k_poly_h(const ull* __restrict__ keys,
     }
     __syncthreads();
     const int n = (int)min((size_t)TT, hi - base);
-    for (int j = 0; j < n; ++j) {
-      const double c = tc[j];
-      if (is_dead(c)) continue;  // block-uniform
-      Key<B> k;
+    // two staged terms per iteration: independent dmul chains (ILP); the
+    // positions walked are the union of both supports and U, a term's
+    // identity positions multiply by 1.0 (exact), and the two values are
+    // added in canonical order
+    for (int j = 0; j < n; j += 2) {
+      const double c0 = tc[j];
+      const double c1 = j + 1 < n ? tc[j + 1] : dead_value();
+      const bool d0 = is_dead(c0), d1 = is_dead(c1);  // block-uniform
+      if (d0 && d1) continue;
+      Key<B> k0, k1;
 #pragma unroll
-      for (int w = 0; w < 2 * B; ++w) k.w[w] = tk[(size_t)j * 2 * B + w];
-      Key<B> prod;
-      int t;
-      sandwich_term<B>(wa, wb, k, prod, t);
-      double e = 1.0;
+      for (int w = 0; w < 2 * B; ++w) {
+        k0.w[w] = d0 ? 0ull : tk[(size_t)j * 2 * B + w];
+        k1.w[w] = d1 ? 0ull : tk[(size_t)(j + 1) * 2 * B + w];
+      }
+      Key<B> p0, p1;
+      int t0, t1;
+      sandwich_term<B>(wa, wb, k0, p0, t0);
+      sandwich_term<B>(wa, wb, k1, p1, t1);
+      double e0 = 1.0, e1 = 1.0;
 #pragma unroll
       for (int w = 0; w < B; ++w) {
-        ull s = k.w[w] | k.w[B + w] | up[w];
-        while (s) {  // warp-uniform: U is the same for every lane
+        ull s = k0.w[w] | k0.w[B + w] | k1.w[w] | k1.w[B + w] | up[w];
+        while (s) {  // warp-uniform
           const int lz = __clzll((long long)s);
           const int bit = 63 - lz;
-          const unsigned code = (unsigned)((prod.w[w] >> bit) & 1ull) |
-                                ((unsigned)((prod.w[B + w] >> bit) & 1ull) << 1);
-          e = __dmul_rn(e, f4[4 * (64 * w + lz) + code]);
+          const double* row = f4 + 4 * (64 * w + lz);
+          const unsigned q0 = (unsigned)((p0.w[w] >> bit) & 1ull) | ((unsigned)((p0.w[B + w] >> bit) & 1ull) << 1);
+          const unsigned q1 = (unsigned)((p1.w[w] >> bit) & 1ull) | ((unsigned)((p1.w[B + w] >> bit) & 1ull) << 1);
+          e0 = __dmul_rn(e0, row[q0]);
+          e1 = __dmul_rn(e1, row[q1]);
           s &= ~(1ull << bit);
         }
       }
-      if (e != 0.0) sandwich_add(c, t, e, re, im);
+      if (!d0 && e0 != 0.0) sandwich_add(c0, t0, e0, re, im);
+      if (!d1 && e1 != 0.0) sandwich_add(c1, t1, e1, re, im);
     }
   }
   if (pid < np) {
