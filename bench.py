@@ -161,9 +161,11 @@ def profile_traffic():
 
 
 # ----------------------------------------------------------------- CPU arm
-def cpu_reference(n_terms=SAMPLE_TERMS, steps=1):
+def cpu_reference(n_terms=SAMPLE_TERMS, steps=1, want_digest=False):
     """UNMODIFIED reference on a bounded sample: parallel_dress (kThreaded) over
-    2^ceil(log2 nproc) partitions, 10 entanglers per step, compress each."""
+    2^ceil(log2 nproc) partitions, 10 entanglers per step, compress each.
+    want_digest: also return the SHA-256 of the reference's final sum (one
+    step), which the GPU arm reproduces on the same sample."""
     from oracle.oracle import Oracle
     kind = "reference" if Oracle.available("reference") else "port"
     orc = Oracle(kind)
@@ -171,18 +173,47 @@ def cpu_reference(n_terms=SAMPLE_TERMS, steps=1):
     nproc = os.cpu_count() or 1
     m = max(0, math.ceil(math.log2(nproc))) if kind == "reference" else 0
     total_terms, total_s = 0, 0.0
+    dig = None
     for s in range(steps):
         ents = step_entanglers(N_QUBITS, s)
         gens = np.stack([e[0] for e in ents])
         taus = np.array([e[1] for e in ents])
-        secs, tin, _ = orc.time_dress_sequence(h, gens, taus, EPS, n_terms, m_bits=m, threads=nproc)
+        r = orc.time_dress_sequence(h, gens, taus, EPS, n_terms, m_bits=m, threads=nproc,
+                                    want_out=want_digest and s == 0)
+        secs, tin = r[0], r[1]
+        if want_digest and s == 0:
+            dig = sum_digest(*r[3].export())
         total_terms += tin
         total_s += secs
-    return {"value": total_terms / total_s, "unit": "terms/s", "cores": min(nproc, 1 << m) if m else 1,
+    out = {"value": total_terms / total_s, "unit": "terms/s", "cores": min(nproc, 1 << m) if m else 1,
             "kind": kind,
             "sample": f"G_mol({N_QUBITS}q, {n_terms:.0e} terms, seed {SEED_H}), {steps}x10 DIS-like "
                       f"entanglers, eps={EPS}, max_terms={n_terms}, parallel_dress kThreaded m={m}",
             "seconds": total_s}
+    if want_digest:
+        out["_digest"] = dig
+    return out
+
+
+def sum_digest(rows, coeffs):
+    """SHA-256 of a sum's canonical bytes (reference row layout, complex
+    coefficients by value: -0.0 == +0.0, as PauliSum == compares)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(rows, np.uint64).tobytes())
+    h.update((np.ascontiguousarray(coeffs, np.complex128).view(np.float64) + 0.0).tobytes())
+    return h.hexdigest()
+
+
+def gpu_sample_digest(iqcc):
+    """The reference arm's exact sample dressed by the engine (one bench step
+    of 10 entanglers with compress), for the in-bench parity check."""
+    d = iqcc.DeviceSum.generate_mol(N_QUBITS, SAMPLE_TERMS, SEED_H)
+    ents = step_entanglers(N_QUBITS, 0)
+    ans = iqcc.Ansatz([iqcc.PauliWord(N_QUBITS, r) for r, _ in ents], [t for _, t in ents])
+    d.dress_sequence(ans, EPS, SAMPLE_TERMS)
+    out = d.download()
+    return sum_digest(out.rows, out.coeffs)
 
 
 def run_reference_arm(args, rank):
@@ -254,6 +285,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     # of the same length below gives the per-kernel breakdown and the merge
     # roofline
     native.profile(False)
+    native.profile_reset()
     launches0 = native.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tin_total = 0
@@ -270,6 +302,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1)
     print(f"[bench] wall {1e3 * (time.perf_counter() - w0):.1f} ms for {args.steps} steps", file=sys.stderr)
     launches = native.launch_count() - launches0
+    step_bytes = native.profile_bytes("merge")  # (M_in + M_out) * S of every dressing step, timed pass
     native.profile(True)
     native.profile_reset()
     for s in range(args.steps):
@@ -288,9 +321,11 @@ def run_gpu_arm(args, rank, world, local_rank):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        tt = torch.tensor([float(tin_total)], device="cuda")
-        dist.all_reduce(tt)  # shards: each rank counted the global size; keep rank 0's view
-        tin_total = tin_total
+        # every rank reports the global input size of each step (the
+        # partitioned call sums the shards); check they agree
+        tt = torch.tensor([float(tin_total), -float(tin_total)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        assert float(tt[0]) == -float(tt[1]) == float(tin_total), "ranks disagree on the global term count"
     value = tin_total / (ms / 1e3)
 
     # ---- roofline of the merge kernel (algorithmic bytes per launch)
@@ -300,6 +335,9 @@ def run_gpu_arm(args, rank, world, local_rank):
     alg_bytes = native.profile_bytes("merge")
     achieved = alg_bytes / (merge_ms / 1e3) / 1e9 if merge_ms > 0 else 0.0
     traffic = profile_traffic()
+    # whole dressing step (plan + merge + compress) against the same peak:
+    # the timed pass's algorithmic bytes over its device time (per rank)
+    step_achieved = step_bytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -324,7 +362,12 @@ def run_gpu_arm(args, rank, world, local_rank):
                "ms_per_step": 1e3 * secs / e2e_steps}
 
     if rank == 0:
-        cpu = None if args.no_cpu else cpu_reference(SAMPLE_TERMS, 1)
+        cpu = None if args.no_cpu else cpu_reference(SAMPLE_TERMS, 1, want_digest=True)
+        parity = None
+        if cpu is not None:
+            # in-bench parity: the engine on the reference arm's exact sample
+            # must reproduce the reference's final sum bit for bit
+            parity = gpu_sample_digest(iqcc) == cpu.pop("_digest")
         line = {
             "metric": "pauli_terms_dressed_merged_per_s", "value": value, "unit": "terms/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -341,10 +384,18 @@ def run_gpu_arm(args, rank, world, local_rank):
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "launches": merge_n,
                          "algorithmic_bytes": alg_bytes, "bytes_per_term": S},
+            "step_roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
+                              "frac": step_achieved / peak,
+                              "note": "sum over dressing steps of (M_in + M_out) * S bytes / whole timed "
+                                      "region (plan, merge, compress, host gaps) on rank 0"},
+            "spec_redos": native.profile_get("spec_redo")[1],
             "kernel_ms": fam,
             "kernel_ms_note": "CUDA events per kernel family over a second, profiled pass of the same K steps (the timed pass runs with profiling off)",
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
+            "parity_note": "SHA-256 of the engine's result on the cpu_baseline sample (G_mol 124q 2e6, "
+                           "10 entanglers, compress) == the unmodified reference's (null: --no-cpu)",
         }
         print(json.dumps(line), flush=True)
 

@@ -111,10 +111,14 @@ int iqcc_gpu_dress(iqcc_gpu_sum* h, const uint64_t* gen, double cos_tau, double 
 int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compress_stats* stats);
 /* In place dress_sequence (iqcc/dressing.hpp:311-324): K entanglers in
  * order, compress(eps, max_terms) after each step when eps > 0 or the size
- * exceeds max_terms.  gens [K][2B].  *terms_in_total (optional) receives
- * the sum of the logical input sizes of the K steps. */
+ * exceeds max_terms.  gens [K][2B].  drop_thr = MergeOptions::drop_threshold
+ * (iqcc/pauli.hpp:236-240), forwarded to every step's merge as the reference
+ * does (dressing.hpp:319); check_hermitian is moot for real sums.
+ * *terms_in_total (optional) receives the sum of the logical input sizes of
+ * the K steps.  On failure the handle's contents are unspecified (partly
+ * dressed); destroy or re-upload it. */
 int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
-                            const double* sin_tau, double eps, size_t max_terms,
+                            const double* sin_tau, double eps, size_t max_terms, double drop_thr,
                             iqcc_compress_stats* stats, size_t* terms_in_total /* nullable */);
 /* growth_split (iqcc/dressing.hpp:41-50). */
 int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* n_commuting,

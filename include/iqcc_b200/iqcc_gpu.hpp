@@ -152,7 +152,7 @@ class DeviceSum {
   }
   void dress_sequence(const Ansatz& a, double epsilon,
                       std::size_t max_terms = std::numeric_limits<std::size_t>::max(),
-                      CompressStats* stats = nullptr) {
+                      CompressStats* stats = nullptr, const MergeOptions& opts = {}) {
     std::vector<uint64_t> gens;
     std::vector<double> c, s;
     for (std::size_t k = 0; k < a.size(); ++k) {
@@ -164,7 +164,7 @@ class DeviceSum {
     }
     iqcc_compress_stats st{0, 0.0};
     detail::check(iqcc_gpu_dress_sequence(d_.get(), a.size(), gens.data(), c.data(), s.data(), epsilon,
-                                          max_terms, &st, nullptr));
+                                          max_terms, opts.drop_threshold, stats ? &st : nullptr, nullptr));
     if (stats) {
       stats->dropped_terms += st.dropped_terms;
       stats->dropped_weight += st.dropped_weight;
@@ -242,10 +242,9 @@ inline PauliSum sortless_dress(const PauliSum& h, const DressOp& op, const Merge
 inline PauliSum dress_sequence(const PauliSum& h, const Ansatz& ansatz, double epsilon,
                                std::size_t max_terms = std::numeric_limits<std::size_t>::max(),
                                CompressStats* stats = nullptr, const MergeOptions& opts = {}) {
-  (void)opts;
   if (max_terms < 1) throw std::invalid_argument("dress_sequence: max_terms < 1");
   DeviceSum d(h);
-  d.dress_sequence(ansatz, epsilon, max_terms, stats);
+  d.dress_sequence(ansatz, epsilon, max_terms, stats, opts);
   return d.download();
 }
 

@@ -269,12 +269,14 @@ orc_sum compress(const orc_sum& h, double eps, std::size_t max_terms, std::size_
 }
 
 // dress_sequence, iqcc/dressing.hpp:311-324
+// dress_sequence, iqcc/dressing.hpp:311-324: opts (drop threshold) forwarded
+// to every step's merge (:319)
 orc_sum dress_seq(const orc_sum& h, std::size_t K, const u64* gens, const double* taus,
-                  double eps, std::size_t max_terms, std::size_t* dt, double* dw) {
+                  double eps, std::size_t max_terms, double drop, std::size_t* dt, double* dw) {
   if (max_terms < 1) throw invalid_arg("dress_sequence: max_terms < 1");
   orc_sum out = h;
   for (std::size_t k = 0; k < K; ++k) {
-    out = dress(out, gens + k * 2 * h.B, taus[k], 1e-12, true, 1e-10);
+    out = dress(out, gens + k * 2 * h.B, taus[k], drop, true, 1e-10);
     if (eps > 0.0 || out.size() > max_terms) out = compress(out, eps, max_terms, dt, dw);
   }
   return out;
@@ -624,8 +626,8 @@ orc_sum* orc_sortless_dress(const orc_sum* h, const uint64_t* gen, double tau, d
 }
 
 orc_sum* orc_dress_sequence(const orc_sum* h, size_t K, const uint64_t* gens, const double* taus,
-                            double eps, size_t max_terms, size_t* dt, double* dw) {
-  return guard([&]() -> orc_sum* { return box(dress_seq(*h, K, gens, taus, eps, max_terms, dt, dw)); },
+                            double eps, size_t max_terms, double drop_thr, size_t* dt, double* dw) {
+  return guard([&]() -> orc_sum* { return box(dress_seq(*h, K, gens, taus, eps, max_terms, drop_thr, dt, dw)); },
                nullptr);
 }
 
@@ -946,7 +948,7 @@ orc_sum* orc_gen_mol(size_t n, size_t count, uint64_t seed) {
 
 double orc_time_dress_sequence(const orc_sum* h, size_t K, const uint64_t* gens, const double* taus,
                                double eps, size_t max_terms, size_t m_bits, int threads,
-                               size_t* terms_in_total, size_t* final_size) {
+                               size_t* terms_in_total, size_t* final_size, orc_sum** out) {
   (void)m_bits;
   (void)threads;
   auto t0 = std::chrono::steady_clock::now();
@@ -960,6 +962,7 @@ double orc_time_dress_sequence(const orc_sum* h, size_t K, const uint64_t* gens,
   auto t1 = std::chrono::steady_clock::now();
   *terms_in_total = tin;
   *final_size = cur.size();
+  if (out) *out = box(std::move(cur));
   return std::chrono::duration<double>(t1 - t0).count();
 }
 

@@ -90,7 +90,8 @@ class Oracle:
             "orc_compress": (_vp, [_vp, C.c_double, C.c_size_t, _szp, _f64p]),
             "orc_dress_single": (_vp, [_vp, _u64p, C.c_double, C.c_double, C.c_int, C.c_double]),
             "orc_sortless_dress": (_vp, [_vp, _u64p, C.c_double, C.c_double, _szp, _szp]),
-            "orc_dress_sequence": (_vp, [_vp, C.c_size_t, _u64p, _f64p, C.c_double, C.c_size_t, _szp, _f64p]),
+            "orc_dress_sequence": (_vp, [_vp, C.c_size_t, _u64p, _f64p, C.c_double, C.c_size_t, C.c_double,
+                                        _szp, _f64p]),
             "orc_growth_split": (None, [_vp, _u64p, _szp, _szp]),
             "orc_expect_word": (C.c_double, [C.c_size_t, _f64p, _f64p, _u64p]),
             "orc_expect_sum": (C.c_double, [_f64p, _f64p, _vp]),
@@ -118,7 +119,8 @@ class Oracle:
             "orc_random_qmf": (None, [_vp, C.c_size_t, _f64p, _f64p]),
             "orc_gen_mol": (_vp, [C.c_size_t, C.c_size_t, C.c_uint64]),
             "orc_time_dress_sequence": (C.c_double, [_vp, C.c_size_t, _u64p, _f64p, C.c_double,
-                                                     C.c_size_t, C.c_size_t, C.c_int, _szp, _szp]),
+                                                     C.c_size_t, C.c_size_t, C.c_int, _szp, _szp,
+                                                     C.POINTER(_vp)]),
         }
         if flavor == "reference":
             sig.update({
@@ -171,12 +173,12 @@ class Oracle:
         out = self._wrap(self.lib.orc_sortless_dress(h.handle, _p(g, _u64p), tau, drop, C.byref(nb), C.byref(ns)))
         return out, {"n_buckets": nb.value, "new_stream_sorts": ns.value}
 
-    def dress_sequence(self, h, gens, taus, eps, max_terms=2**64 - 1):
+    def dress_sequence(self, h, gens, taus, eps, max_terms=2**64 - 1, drop=1e-12):
         g = np.ascontiguousarray(gens, dtype=np.uint64)
         t = np.ascontiguousarray(taus, dtype=np.float64)
         dt, dw = C.c_size_t(0), C.c_double(0.0)
         out = self._wrap(self.lib.orc_dress_sequence(h.handle, len(t), _p(g, _u64p), _p(t, _f64p), eps,
-                                                     max_terms, C.byref(dt), C.byref(dw)))
+                                                     max_terms, drop, C.byref(dt), C.byref(dw)))
         return out, {"dropped_terms": dt.value, "dropped_weight": dw.value}
 
     def compress(self, h, eps, max_terms):
@@ -331,12 +333,17 @@ class Oracle:
     def gen_mol(self, n, count, seed):
         return self._wrap(self.lib.orc_gen_mol(n, count, seed))
 
-    def time_dress_sequence(self, h, gens, taus, eps, max_terms, m_bits=0, threads=0):
+    def time_dress_sequence(self, h, gens, taus, eps, max_terms, m_bits=0, threads=0, want_out=False):
+        """Returns (seconds, summed input terms, final size[, final sum])."""
         g = np.ascontiguousarray(gens, dtype=np.uint64)
         t = np.ascontiguousarray(taus, dtype=np.float64)
         tin, fin = C.c_size_t(0), C.c_size_t(0)
+        out = _vp(None)
         secs = self.lib.orc_time_dress_sequence(h.handle, len(t), _p(g, _u64p), _p(t, _f64p), eps, max_terms,
-                                                m_bits, threads, C.byref(tin), C.byref(fin))
+                                                m_bits, threads, C.byref(tin), C.byref(fin),
+                                                C.byref(out) if want_out else None)
+        if want_out:
+            return secs, tin.value, fin.value, self._wrap(out.value)
         return secs, tin.value, fin.value
 
     # reference-only extras -------------------------------------------------

@@ -57,7 +57,7 @@ orc_sum* orc_dress_single(const orc_sum* h, const uint64_t* gen, double tau, dou
 orc_sum* orc_sortless_dress(const orc_sum* h, const uint64_t* gen, double tau, double drop_thr,
                             size_t* n_buckets, size_t* new_stream_sorts);
 orc_sum* orc_dress_sequence(const orc_sum* h, size_t K, const uint64_t* gens, const double* taus,
-                            double eps, size_t max_terms, size_t* dropped_terms,
+                            double eps, size_t max_terms, double drop_thr, size_t* dropped_terms,
                             double* dropped_weight);
 void orc_growth_split(const orc_sum* h, const uint64_t* gen, size_t* n_comm, size_t* n_anti);
 
@@ -116,7 +116,8 @@ orc_sum* orc_gen_mol(size_t n_qubits, size_t n_terms, uint64_t seed);
 /* timing helpers for bench.py's CPU arm (threads = 0 -> hardware) --------- */
 double orc_time_dress_sequence(const orc_sum* h, size_t K, const uint64_t* gens,
                                const double* taus, double eps, size_t max_terms, size_t m_bits,
-                               int threads, size_t* terms_in_total, size_t* final_size);
+                               int threads, size_t* terms_in_total, size_t* final_size,
+                               orc_sum** out /* nullable: the final sum (gathered) */);
 
 #ifdef __cplusplus
 }

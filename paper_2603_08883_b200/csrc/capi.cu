@@ -16,6 +16,7 @@
 #include <random>
 #include <algorithm>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -90,10 +91,9 @@ void count_launch(const char* family) {
   (void)family;
 }
 
-void add_alg_bytes(const char* family, double bytes) {
-  Ctx& c = ctx();
-  if (c.profiling) c.prof[family].alg_bytes += bytes;
-}
+// algorithmic bytes are booked whether or not event profiling is on (a host
+// add per step), so a timed pass reports its own roofline numerator
+void add_alg_bytes(const char* family, double bytes) { ctx().prof[family].alg_bytes += bytes; }
 
 static cudaEvent_t take_event() {
   Ctx& c = ctx();
@@ -581,11 +581,12 @@ int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compre
 }
 
 int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
-                            const double* sin_tau, double eps, size_t max_terms,
+                            const double* sin_tau, double eps, size_t max_terms, double drop_thr,
                             iqcc_compress_stats* stats, size_t* terms_in_total) {
   return guarded([&] {
     need(h);
     if (max_terms < 1) throw std::invalid_argument("dress_sequence: max_terms < 1");
+    if (!(drop_thr >= 0.0)) throw std::invalid_argument("dress_sequence: drop_threshold < 0");
     const uint32_t Bref = ref_blocks(h->s);
     for (size_t k = 0; k < K; ++k)
       if (row_is_identity(gens + k * 2 * Bref, Bref))
@@ -613,14 +614,14 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       if (terms_in_total) *terms_in_total += h->s.logical;
       const bool maybe = eps > 0.0 || max_terms != SIZE_MAX;
       const auto t0 = std::chrono::steady_clock::now();
-      KernelScope* outer = new KernelScope("span_dress");
+      std::optional<KernelScope> outer(std::in_place, "span_dress");
       const double exact = slots && eps > 0.0 ? eps : 0.0;
       // the previous cut, shrunk by what an anticommuting survivor loses (|cos|)
       const double guess = spec * std::min(1.0, std::fabs(cos_tau[k])) * 0.999 * spec_scale;
       const double theta = maybe && guess > eps && max_terms != SIZE_MAX ? guess : exact;
       const size_t M0 = h->s.M, L0 = h->s.logical;
       const Filter F0 = h->s.filt;
-      DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps,
+      DressOutcome o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], drop_thr, maybe, eps,
                                   next.empty() ? nullptr : next.data(), theta);
       if (getenv("IQCC_VERBOSE"))
         fprintf(stderr, "[dress] k=%zu theta=%.3e exact=%.3e n_ge=%zu slots=%zu products=%zu pairs=%zu\n", k,
@@ -636,19 +637,21 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
       if (theta > exact && !spec_ok) {  // speculation failed: redo exactly
         dress_undo(h->s, M0, L0, F0);
         host_ms("spec_redo", std::chrono::steady_clock::now());
-        o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], 1e-12, maybe, eps,
+        o = dress_step(h->s, row.data(), cos_tau[k], sin_tau[k], drop_thr, maybe, eps,
                        next.empty() ? nullptr : next.data(), exact);
         spec = 0.0;  // relearn from the next cut
         h->s.spec_cut = 0.0;
       }
-      delete outer;
+      outer.reset();
       host_ms("host_dress", t0);
       if (eps > 0.0 || h->s.logical > max_terms) {
         const auto t1 = std::chrono::steady_clock::now();
-        KernelScope* outer2 = new KernelScope("span_compress");
-        CompressResult r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr,
-                                          nullptr, nullptr, floor_cut);
-        delete outer2;
+        CompressResult r;
+        {
+          KernelScope outer2("span_compress");
+          r = compress_store(h->s, eps, max_terms, maybe, o.count_eps, stats != nullptr, nullptr, nullptr,
+                             floor_cut);
+        }
         // a compress that cut sets the next guess; one that did not (every
         // slotted term kept) leaves the last verified guess in place
         const double sv = spec_theta(h->s.filt);

@@ -1439,7 +1439,10 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   if (getenv("IQCC_DEBUG") && M > 0) debug_check("present");
   if (products && M > 0) {
     const size_t ntiles = (M + WT - 1) / WT;
-    const int group = ntiles > (size_t)kGroupSmall * 1024 ? kGroupLarge : kGroupSmall;
+    // IQCC_FORCE_GROUP_LARGE (test hook): take the large-shard carry path
+    // (1024-tile groups, > 6.7e7 slots in production) at any size
+    const int group = ntiles > (size_t)kGroupSmall * 1024 || getenv("IQCC_FORCE_GROUP_LARGE") ? kGroupLarge
+                                                                                               : kGroupSmall;
     const size_t ngroups = (ntiles + group - 1) / group;
     if (ngroups > (size_t)kMaxGroups) throw std::runtime_error("dress: more than 2^28 terms per device shard");
     int* tile_cnt = ws.tile_cnt.as<int>(ntiles);

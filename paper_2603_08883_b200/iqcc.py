@@ -313,9 +313,11 @@ class DeviceSum:
             stats.dropped_weight += cs.dropped_weight
 
     def dress_sequence(self, ansatz: Ansatz, eps: float, max_terms: int = U64_MAX,
-                       stats: CompressStats | None = None) -> int:
+                       stats: CompressStats | None = None, opts: MergeOptions | None = None) -> int:
         """In place dress_sequence; returns the summed logical input size of
-        the K dressing steps (the bench metric's unit of work)."""
+        the K dressing steps (the bench metric's unit of work).  opts: the
+        MergeOptions every step merges with (dressing.hpp:319)."""
+        drop = (opts or MergeOptions()).drop_threshold
         K = ansatz.size()
         W = 2 * blocks_for(self.n_qubits)
         gens = np.zeros((max(K, 1), W), np.uint64)
@@ -326,7 +328,7 @@ class DeviceSum:
         st = native.CompressStatsC()
         tin = C.c_size_t(0)
         check(lib.iqcc_gpu_dress_sequence(self.handle, K, _addr(gens), _addr(cs_), _addr(sn_), eps, max_terms,
-                                          C.byref(st) if stats is not None else None, C.byref(tin)))
+                                          drop, C.byref(st) if stats is not None else None, C.byref(tin)))
         if stats is not None:
             stats.dropped_terms += st.dropped_terms
             stats.dropped_weight += st.dropped_weight
@@ -461,16 +463,17 @@ def dress_sequence(h: PauliSum, ansatz: Ansatz, epsilon: float, max_terms: int =
                    out: tuple | None = None) -> PauliSum:
     """iqcc/dressing.hpp:311-324 (device resident across the whole ansatz).
     `out` optionally supplies host (rows, coeffs) buffers for the result."""
-    return dress_sequence_counted(h, ansatz, epsilon, max_terms, stats, out)[0]
+    return dress_sequence_counted(h, ansatz, epsilon, max_terms, stats, out, opts)[0]
 
 
 def dress_sequence_counted(h: PauliSum, ansatz: Ansatz, epsilon: float, max_terms: int = U64_MAX,
-                           stats: CompressStats | None = None, out: tuple | None = None):
+                           stats: CompressStats | None = None, out: tuple | None = None,
+                           opts: MergeOptions = MergeOptions()):
     """dress_sequence that also returns the summed logical input size."""
     if max_terms < 1:
         raise ValueError("dress_sequence: max_terms < 1")
     d = DeviceSum.upload(h)
-    tin = d.dress_sequence(ansatz, epsilon, max_terms, stats)
+    tin = d.dress_sequence(ansatz, epsilon, max_terms, stats, opts)
     if out is None:
         n = d.size()
         rows, coeffs = (pinned_buffers(h.n_qubits, n) if _is_pinned(h) else (None, None))

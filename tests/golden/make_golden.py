@@ -17,6 +17,11 @@ c1_<name>.npz   SURVEY.md §8(d) config C1: the Jordan-Wigner Hamiltonian of
                 dressed sum is stored in full.
 small.npz       random cases from the reference test seeds (dress_single,
                 compress, dress_sequence outputs with checksums).
+c2.npz          SURVEY.md §8(d) config C2 at full size: G_uniform(64, 1e6,
+                seed 1) dressed by one weight-4 entangler at tau = 0.37 (drop
+                1e-12), then compress(1e-3) and compress(0, max_terms=1.2e6);
+                sizes + SHA-256 of each result, plus dress_sequence with
+                MergeOptions{0.0} and {1e-6} on a G_mol(124, 2e4) sum.
 """
 import hashlib
 import math
@@ -113,11 +118,67 @@ def small(ref):
     print("small fixtures", {k: len(v) for k, v in cases.items()})
 
 
+C2_QUBITS, C2_TERMS, C2_SEED, C2_TAU = 64, 1_000_000, 1, 0.37
+
+
+def c2_entangler():
+    """X5 Y21 Z38 X60 (weight 4, reference row layout)."""
+    row = np.zeros(2, np.uint64)
+    for q, (x, z) in {5: (1, 0), 21: (1, 1), 38: (0, 1), 60: (1, 0)}.items():
+        if x:
+            row[0] |= np.uint64(1 << q)
+        if z:
+            row[1] |= np.uint64(1 << q)
+    return row
+
+
+def drop_cases():
+    """(n, terms, seed, gens, taus) of the MergeOptions cases."""
+    rs = np.random.default_rng(99)
+    n, B = 124, 2
+    gens, taus = [], []
+    for _ in range(4):
+        row = np.zeros(2 * B, np.uint64)
+        qs = rs.choice(n, 3, replace=False)
+        for q, (x, z) in zip(qs, [(1, 0), (1, 1), (1, 0)]):
+            if x:
+                row[q // 64] |= np.uint64(1 << int(q % 64))
+            if z:
+                row[B + q // 64] |= np.uint64(1 << int(q % 64))
+        gens.append(row)
+        taus.append(float(rs.uniform(-0.3, 0.3)))
+    return n, 20000, 5, np.stack(gens), np.array(taus)
+
+
+def c2(ref):
+    h = ref.rng(C2_SEED).sum(C2_QUBITS, C2_TERMS)
+    d = ref.dress_single(h, c2_entangler(), C2_TAU)
+    a, sa = ref.compress(d, 1e-3, 2**64 - 1)
+    b, sb = ref.compress(d, 0.0, 1_200_000)
+    out = {"n_in": len(h), "sha_in": digest(*h.export())}
+    for k, s in (("dressed", d), ("eps", a), ("cap", b)):
+        out[f"n_{k}"] = len(s)
+        out[f"sha_{k}"] = digest(*s.export())
+    out["dropped_eps"], out["dropped_cap"] = sa["dropped_terms"], sb["dropped_terms"]
+    n, terms, seed, gens, taus = drop_cases()
+    hm = ref.gen_mol(n, terms, seed)
+    for tag, drop in (("drop0", 0.0), ("drop6", 1e-6), ("drop12", 1e-12)):
+        s, _ = ref.dress_sequence(hm, gens, taus, 0.0, 2**64 - 1, drop=drop)
+        out[f"n_{tag}"] = len(s)
+        out[f"sha_{tag}"] = digest(*s.export())
+    np.savez_compressed(os.path.join(HERE, "c2.npz"), **out)
+    print("c2", {k: v for k, v in out.items() if k.startswith("n_")})
+
+
 def main():
     ref = Oracle("reference")
+    if "--c2" in sys.argv:
+        c2(ref)
+        return
     c1(ref, "h2_sto3g", 5, 1)
     c1(ref, "h2_ccpvdz", 5, 1)
     small(ref)
+    c2(ref)
 
 
 if __name__ == "__main__":

@@ -165,13 +165,25 @@ def test_random_large(eng, port, n):
         check_same(eng.dress_single(hh, eng.DressOp(eng.PauliWord(n, g), tau)), port.dress_single(h, g, tau))
 
 
+@pytest.fixture(params=["group_small", "group_large"])
+def carry_path(request, monkeypatch):
+    """Both carry-scan paths of the product rank (dress.cu plan_impl): the
+    256-tile groups used below 6.7e7 slots and the 1024-tile groups the C3
+    bench shape (1e8+ slots) runs on, forced here by IQCC_FORCE_GROUP_LARGE."""
+    if request.param == "group_large":
+        monkeypatch.setenv("IQCC_FORCE_GROUP_LARGE", "1")
+    else:
+        monkeypatch.delenv("IQCC_FORCE_GROUP_LARGE", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("n,terms,steps,eps,cap", [
     (124, 200_000, 6, 0.0, 2**64 - 1),       # growth, partner pairs (dead slots)
     (124, 200_000, 6, 1e-10, 200_000),       # C3 shape: capped every step
     (64, 100_000, 6, 1e-4, 120_000),         # eps cut + cap
     (200, 50_000, 4, 1e-9, 60_000),          # 4 device blocks
 ])
-def test_gmol_sequence(eng, port, n, terms, steps, eps, cap):
+def test_gmol_sequence(eng, port, n, terms, steps, eps, cap, carry_path):
     h = port.gen_mol(n, terms, 2)
     d = eng.DeviceSum.generate_mol(n, terms, 2)
     check_same(d.download(), h)
@@ -299,7 +311,7 @@ def _entanglers(n, steps, seed, zero_at=()):
     (64, 100_000, 6, 1e-4, 2**64 - 1, ()),     # eps slots only (exact, no speculation)
     (200, 50_000, 5, 1e-9, 55_000, (2,)),      # 4 device blocks
 ])
-def test_sequence_output_slots(eng, port, n, terms, steps, eps, cap, zero_at):
+def test_sequence_output_slots(eng, port, n, terms, steps, eps, cap, zero_at, carry_path):
     """dress_sequence without drop statistics allocates output slots only for
     terms the following compress can keep (speculated cut verified after each
     merge, redone exactly when the check fails): the result must equal the
@@ -332,3 +344,56 @@ def test_sequence_output_slots(eng, port, n, terms, steps, eps, cap, zero_at):
     check_same(d3.download(), ref)
     if cap < 2**63:
         assert redo > 0
+
+
+def test_c2_full_size(eng, port):
+    """SURVEY.md §8(d) C2 at its real size: G_uniform(64, 1e6, seed 1), one
+    weight-4 entangler at tau = 0.37, then compress(1e-3) and
+    compress(0, max_terms = 1.2e6); every result hashed against the
+    unmodified reference's (tests/golden/c2.npz, make_golden.py)."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_golden import C2_QUBITS, C2_SEED, C2_TAU, C2_TERMS, c2_entangler
+    g = load_golden("c2.npz")
+    h = port.rng(C2_SEED).sum(C2_QUBITS, C2_TERMS)
+    hh = host(eng, h)
+    assert digest(hh.rows, hh.coeffs) == g["sha_in"]
+    d = eng.DeviceSum.upload(hh)
+    d.dress(eng.PauliWord(C2_QUBITS, c2_entangler()), C2_TAU)
+    for tag, eps, cap in (("eps", 1e-3, 2**64 - 1), ("cap", 0.0, 1_200_000), ("dressed", None, None)):
+        c = d.clone()
+        if eps is not None:
+            cs = eng.CompressStats()
+            c.compress(eps, cap, cs)
+            assert cs.dropped_terms == g[f"dropped_{tag}"]
+        out = c.download()
+        assert len(out) == g[f"n_{tag}"]
+        assert digest(out.rows, out.coeffs) == g[f"sha_{tag}"], tag
+    # the same through the one-call pipeline (dress_sequence + compress)
+    seq = eng.dress_sequence(hh, eng.Ansatz([eng.PauliWord(C2_QUBITS, c2_entangler())], [C2_TAU]),
+                             0.0, 1_200_000)
+    assert digest(seq.rows, seq.coeffs) == g["sha_cap"]
+
+
+@pytest.mark.parametrize("tag,drop", [("drop0", 0.0), ("drop6", 1e-6), ("drop12", 1e-12)])
+def test_sequence_merge_options(eng, port, tag, drop):
+    """dress_sequence forwards MergeOptions.drop_threshold to every step's
+    merge (iqcc/dressing.hpp:319), device resident and through the host API."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_golden import drop_cases
+    g = load_golden("c2.npz")
+    n, terms, seed, gens, taus = drop_cases()
+    ans = eng.Ansatz([eng.PauliWord(n, r) for r in gens], list(taus))
+    d = eng.DeviceSum.generate_mol(n, terms, seed)
+    d.dress_sequence(ans, 0.0, opts=eng.MergeOptions(drop, True))
+    out = d.download()
+    assert len(out) == g[f"n_{tag}"]
+    assert digest(out.rows, out.coeffs) == g[f"sha_{tag}"]
+    want, _ = port.dress_sequence(port.gen_mol(n, terms, seed), gens, taus, 0.0, drop=drop)
+    check_same(out, want)
+    # with a compress after every step (slot speculation on) as well
+    d2 = eng.DeviceSum.generate_mol(n, terms, seed)
+    d2.dress_sequence(ans, 1e-9, 30000, opts=eng.MergeOptions(drop, True))
+    want2, _ = port.dress_sequence(port.gen_mol(n, terms, seed), gens, taus, 1e-9, 30000, drop=drop)
+    check_same(d2.download(), want2)
