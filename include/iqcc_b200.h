@@ -209,6 +209,71 @@ int iqcc_gpu_parallel_poly_kernels(iqcc_gpu_sum* h, const double* factors, int a
 /* Total logical terms over all ranks. */
 int iqcc_gpu_parallel_size(iqcc_gpu_sum* h, size_t* total);
 
+/* ---- partitioned sums driven from one host thread (iqcc/partition.hpp) --
+ * iqcc_gpu_psum = the reference's PartitionedSum (:145-173) held on the
+ * device: 2^m shards, shard p owned by worker owner[p], worker w running on
+ * CUDA device devices[w] (NULL: w % device count).  One call drives every
+ * shard (one engine context and host worker thread per shard inside the
+ * handle, like run_tasks(kThreaded), :190-204); products cross devices over
+ * NVLink.  Any m (overpartitioning: several partitions per worker/GPU). */
+typedef struct iqcc_gpu_psum iqcc_gpu_psum;
+typedef struct {
+  size_t source;      /* partition id, MessageRecord (:135-140) */
+  size_t destination;
+  size_t terms;
+  size_t bytes;       /* terms * (sizeof(Complex) + 2 * blocks * 8), :419-422 */
+} iqcc_message_record;
+/* distribute (:208-220): a canonical real host sum -> shards by partition key. */
+int iqcc_gpu_psum_distribute(size_t n_qubits, const uint64_t* rows, const double* coeff, size_t M,
+                             size_t m, const size_t* bits, const size_t* owner, size_t n_workers,
+                             const int* devices /* nullable */, iqcc_gpu_psum** out);
+/* From existing host shards (a reference PartitionedSum): rows[p]/coeffs[p]
+ * of sizes[p] terms; a term outside its shard -> IQCC_ERUNTIME ("term in
+ * wrong shard", PartitionedSum::validate :162-172). */
+int iqcc_gpu_psum_create_shards(size_t n_qubits, size_t m, const size_t* bits, const size_t* owner,
+                                size_t n_workers, const int* devices, const uint64_t* const* rows,
+                                const double* const* coeffs, const size_t* sizes, iqcc_gpu_psum** out);
+int iqcc_gpu_psum_destroy(iqcc_gpu_psum* ph);
+/* n_partitions = 2^m; total = total_terms() (:147-151). */
+int iqcc_gpu_psum_info(iqcc_gpu_psum* ph, size_t* n_partitions, size_t* total_terms);
+int iqcc_gpu_psum_shard_sizes(iqcc_gpu_psum* ph, size_t* sizes /* [2^m] */);
+int iqcc_gpu_psum_owner(iqcc_gpu_psum* ph, size_t* owner /* [2^m] */);
+int iqcc_gpu_psum_download_shard(iqcc_gpu_psum* ph, size_t p, uint64_t* rows, double* coeff, size_t cap,
+                                 size_t* M);
+/* gather (:222-230): the canonical union of the shards into host buffers. */
+int iqcc_gpu_psum_gather(iqcc_gpu_psum* ph, uint64_t* rows, double* coeff, size_t cap, size_t* M);
+/* In place ph <- parallel_dress(ph, {gen, tau}, eps, max_terms, log, mode,
+ * stats) (:398-452) with host cos/sin of tau.  log: NULL or log_cap records;
+ * *n_log receives the record count (records past log_cap are dropped);
+ * cstats accumulate ParallelDressStats::compress; *mask = stats->mask. */
+int iqcc_gpu_psum_dress(iqcc_gpu_psum* ph, const uint64_t* gen, double cos_tau, double sin_tau, double eps,
+                        size_t max_terms, iqcc_message_record* log, size_t log_cap, size_t* n_log,
+                        iqcc_compress_stats* cstats, size_t* mask);
+/* parallel_expect (:241-254): worker-order reduction of the shard energies. */
+int iqcc_gpu_psum_expect(iqcc_gpu_psum* ph, const double* factors, double* energy);
+/* qmf_energy_gradient (iqcc/qmf.hpp:94-148) over the shards, energy and 2n
+ * gradients reduced in worker order like parallel_expect. */
+int iqcc_gpu_psum_qmf_energy_gradient(iqcc_gpu_psum* ph, const double* factors, const double* derivs,
+                                      double* energy, double* grad);
+/* DIS gradients (iqcc/dis.hpp:39-52, group_gradient :121-132) of K candidate
+ * words over the shards, reduced in worker order. */
+int iqcc_gpu_psum_gradients(iqcc_gpu_psum* ph, const double* factors, const uint64_t* cands, size_t K,
+                            int flip_group_only, double* g);
+/* rebalance (:457-494) + migration of every shard whose new owner runs on
+ * another device; owner_out (nullable) receives the new map. */
+int iqcc_gpu_psum_rebalance(iqcc_gpu_psum* ph, double threshold, size_t* owner_out);
+
+/* merge_sums (iqcc/pauli.hpp:383-415) of two device sums into a new one
+ * (a's coefficient first on shared words, keep_term with drop_thr). */
+int iqcc_gpu_merge_sums(iqcc_gpu_sum* a, iqcc_gpu_sum* b, double drop_thr, iqcc_gpu_sum** out);
+
+/* Partitioned gradients over the one-process-per-GPU communicator: local
+ * values allgathered and summed in rank order (reduce_scalar, :233-237). */
+int iqcc_gpu_parallel_qmf_energy_gradient(iqcc_gpu_sum* h, const double* factors, const double* derivs,
+                                          double* energy, double* grad);
+int iqcc_gpu_parallel_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* cands, size_t K,
+                                int flip_group_only, double* g);
+
 #ifdef __cplusplus
 }
 #endif

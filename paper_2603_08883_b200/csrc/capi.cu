@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <memory>
 #include <optional>
+#include <atomic>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -38,21 +40,35 @@ struct ProfileEntry {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
 };
 
+// Freed large blocks are cached for reuse (see DevBuf::get); one cache per
+// context, since a context's stream orders every use of its blocks.
+struct BigCache {
+  std::vector<std::pair<void*, size_t>> blocks;
+  size_t bytes = 0;
+};
+
+// One engine context per host thread (a device, a stream, the hot path's
+// scratch and a block cache).  The C-ABI binds the calling thread
+// (iqcc_gpu_init); the partitioned-sum driver (psum.cu) runs one worker
+// thread per shard, each with its own context on the shard's device, so
+// shards on one device never share scratch and shards on different devices
+// run concurrently from one API call.
 struct Ctx {
   int device = -1;
   cudaStream_t own = nullptr;
   cudaStream_t cur = nullptr;
   Workspace ws;
-  uint64_t launches = 0;
   bool profiling = false;
   std::map<std::string, ProfileEntry> prof;
   std::vector<cudaEvent_t> event_pool;
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  BigCache big;
 };
 
-static Ctx* g_ctx = nullptr;
+static thread_local Ctx* g_ctx = nullptr;
 static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};  // every engine kernel launch, all contexts
 
 Ctx& ctx() {
   if (!g_ctx) throw std::runtime_error("iqcc_gpu_init has not been called");
@@ -86,8 +102,7 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 void count_launch(const char* family) {
-  Ctx& c = ctx();
-  ++c.launches;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   (void)family;
 }
 
@@ -109,7 +124,7 @@ static cudaEvent_t take_event() {
 
 KernelScope::KernelScope(const char* f) : family(f) {
   Ctx& c = ctx();
-  ++c.launches;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   if (c.profiling) {
     a = take_event();
     b = take_event();
@@ -215,49 +230,50 @@ static void profile_flush() {
 // kernel.  Small buffers stay stream-ordered.
 constexpr size_t kBigAlloc = (size_t)32 << 20;
 
-// Freed large blocks are cached for reuse (the engine runs on one stream, so
-// a block handed out again is only touched by later work in stream order);
-// a cached block serves requests between a quarter of its size and its size
-// (best fit): chains of stores growing ~1.5x per step then find their blocks
-// again on the next chain instead of missing on a half-size window.
-struct BigCache {
-  std::vector<std::pair<void*, size_t>> blocks;
-  size_t bytes = 0;
-};
-static BigCache g_big;
+// Freed large blocks are cached for reuse (a context runs on one stream, so
+// a block handed out again is only touched by later work in stream order).
+// A cached block serves a request between a quarter of its size and its
+// size (best fit) when it wastes at most kBigSlack bytes, and between half
+// and all of its size otherwise: chains of stores growing ~1.5x per step
+// find their blocks again on the next chain, while a huge block is not
+// pinned under a small live buffer.
+constexpr size_t kBigSlack = (size_t)256 << 20;
 
-static void big_release_all() {
-  if (g_big.blocks.empty()) return;
+static void big_release_all(BigCache& bc) {
+  if (bc.blocks.empty()) return;
   cudaDeviceSynchronize();
-  for (auto& b : g_big.blocks) cudaFree(b.first);
-  g_big.blocks.clear();
-  g_big.bytes = 0;
+  for (auto& b : bc.blocks) cudaFree(b.first);
+  bc.blocks.clear();
+  bc.bytes = 0;
 }
 
 static void* big_take(size_t want, size_t* got) {
+  BigCache& bc = ctx().big;
   size_t best = SIZE_MAX;
-  for (size_t i = 0; i < g_big.blocks.size(); ++i) {
-    const size_t b = g_big.blocks[i].second;
-    if (b >= want && b / 4 <= want && (best == SIZE_MAX || b < g_big.blocks[best].second)) best = i;
+  for (size_t i = 0; i < bc.blocks.size(); ++i) {
+    const size_t b = bc.blocks[i].second;
+    const bool fits = b >= want && (b - want <= kBigSlack ? b / 4 <= want : b / 2 <= want);
+    if (fits && (best == SIZE_MAX || b < bc.blocks[best].second)) best = i;
   }
   if (best == SIZE_MAX) return nullptr;
-  void* p = g_big.blocks[best].first;
-  *got = g_big.blocks[best].second;
-  g_big.bytes -= *got;
-  g_big.blocks.erase(g_big.blocks.begin() + best);
+  void* p = bc.blocks[best].first;
+  *got = bc.blocks[best].second;
+  bc.bytes -= *got;
+  bc.blocks.erase(bc.blocks.begin() + best);
   return p;
 }
 
 static void devbuf_free(void* p, bool big, size_t bytes) {
   if (!p) return;
   if (big) {
-    g_big.blocks.emplace_back(p, bytes);
-    g_big.bytes += bytes;
-    // bound the cache (largest blocks leave last): at most 64 blocks
-    while (g_big.blocks.size() > 64) {
-      IQCC_CUDA(cudaFree(g_big.blocks.front().first));
-      g_big.bytes -= g_big.blocks.front().second;
-      g_big.blocks.erase(g_big.blocks.begin());
+    BigCache& bc = ctx().big;
+    bc.blocks.emplace_back(p, bytes);
+    bc.bytes += bytes;
+    // bound the cache at 64 blocks: the oldest freed block leaves first
+    while (bc.blocks.size() > 64) {
+      IQCC_CUDA(cudaFree(bc.blocks.front().first));
+      bc.bytes -= bc.blocks.front().second;
+      bc.blocks.erase(bc.blocks.begin());
     }
   } else {
     IQCC_CUDA(cudaFreeAsync(p, stream()));
@@ -292,7 +308,7 @@ void* DevBuf::get(size_t n) {
     cudaGetLastError();
     if (verbose) fprintf(stderr, "[alloc] %zu bytes failed: release the caches and retry\n", want);
     IQCC_CUDA(cudaStreamSynchronize(st));
-    big_release_all();
+    big_release_all(ctx().big);
     cudaMemPool_t pool;
     IQCC_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx().device));
     cudaMemPoolTrimTo(pool, 0);
@@ -320,6 +336,55 @@ void DevBuf::release() {
   p = nullptr;
   bytes = 0;
   big = false;
+}
+
+Ctx* ctx_new(int device) {
+  IQCC_CUDA(cudaSetDevice(device));
+  auto* c = new Ctx();
+  c->device = device;
+  IQCC_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->cur = c->own;
+  cudaMemPool_t pool;
+  IQCC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  IQCC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  return c;
+}
+
+Ctx* ctx_bind(Ctx* c) {
+  Ctx* prev = g_ctx;
+  g_ctx = c;
+  if (c) IQCC_CUDA(cudaSetDevice(c->device));
+  return prev;
+}
+
+Ctx* ctx_current() { return g_ctx; }
+
+int ctx_device(const Ctx* c) { return c ? c->device : -1; }
+
+void ctx_free(Ctx* c) {
+  if (!c) return;
+  Ctx* prev = ctx_bind(c);
+  cudaStreamSynchronize(c->cur);
+  c->ws.release_all();
+  cudaStreamSynchronize(c->cur);
+  big_release_all(c->big);
+  for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  cudaStreamDestroy(c->own);
+  delete c;
+  ctx_bind(prev == c ? nullptr : prev);
+}
+
+bool func_attr_once(const void* fn, int device) {
+  // cudaFuncSetAttribute applies per device: remember (kernel, device)
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == fn && d.second == device) return false;
+  done.emplace_back(fn, device);
+  return true;
 }
 
 void Workspace::release_all() {
@@ -395,16 +460,7 @@ int iqcc_gpu_init(int device) {
   return guarded([&] {
     if (g_ctx && g_ctx->device == device) return;
     if (g_ctx) throw std::invalid_argument("engine already initialised on another device");
-    IQCC_CUDA(cudaSetDevice(device));
-    auto* c = new Ctx();
-    c->device = device;
-    IQCC_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
-    c->cur = c->own;
-    cudaMemPool_t pool;
-    IQCC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    IQCC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    g_ctx = c;
+    g_ctx = ctx_new(device);
   });
 }
 
@@ -421,17 +477,12 @@ int iqcc_gpu_finalize(void) {
     if (!g_ctx) return;
     cudaStreamSynchronize(g_ctx->cur);
     multi_shutdown();
-    g_ctx->ws.release_all();
-    cudaStreamSynchronize(g_ctx->cur);
-    big_release_all();
-    if (g_ctx->pinned) cudaFreeHost(g_ctx->pinned);
-    cudaStreamDestroy(g_ctx->own);
-    delete g_ctx;
+    ctx_free(g_ctx);
     g_ctx = nullptr;
   });
 }
 
-uint64_t iqcc_gpu_launch_count(void) { return g_ctx ? g_ctx->launches : 0; }
+uint64_t iqcc_gpu_launch_count(void) { return g_launches.load(); }
 
 int iqcc_gpu_profile_enable(int on) {
   return guarded([&] { ctx().profiling = on != 0; });
@@ -918,6 +969,129 @@ int iqcc_gpu_parallel_poly_kernels(iqcc_gpu_sum* h, const double* factors, int a
     }
     parallel_poly_kernels_store(h->s, factors, at_poles != 0, wide.data(), t, h_kernel, n_kernel);
   });
+}
+
+int iqcc_gpu_parallel_qmf_energy_gradient(iqcc_gpu_sum* h, const double* factors, const double* derivs,
+                                          double* energy, double* grad) {
+  return guarded([&] {
+    need(h);
+    *energy = parallel_qmf_grad_store(h->s, factors, derivs, grad);
+  });
+}
+
+int iqcc_gpu_parallel_gradients(iqcc_gpu_sum* h, const double* factors, const uint64_t* cands, size_t K,
+                                int flip_group_only, double* g) {
+  return guarded([&] {
+    need(h);
+    const uint32_t Bref = ref_blocks(h->s);
+    std::vector<uint64_t> wide(std::max<size_t>(K, 1) * 2 * h->s.B);
+    for (size_t k = 0; k < K; ++k) {
+      auto r = widen_row(cands + k * 2 * Bref, Bref, h->s.B);
+      std::copy(r.begin(), r.end(), wide.begin() + k * 2 * h->s.B);
+    }
+    parallel_gradients_store(h->s, factors, wide.data(), K, flip_group_only != 0, g);
+  });
+}
+
+int iqcc_gpu_merge_sums(iqcc_gpu_sum* a, iqcc_gpu_sum* b, double drop_thr, iqcc_gpu_sum** out) {
+  return guarded([&] {
+    need(a);
+    need(b);
+    if (!(drop_thr >= 0.0)) throw std::invalid_argument("merge_sums: drop_threshold < 0");
+    auto h = std::make_unique<iqcc_gpu_sum>();
+    merge_sums_store(a->s, b->s, drop_thr, h->s);
+    *out = h.release();
+  });
+}
+
+// ---- partitioned sums (psum.cu)
+int iqcc_gpu_psum_distribute(size_t n_qubits, const uint64_t* rows, const double* coeff, size_t M, size_t m,
+                             const size_t* bits, const size_t* owner, size_t n_workers, const int* devices,
+                             iqcc_gpu_psum** out) {
+  return guarded([&] {
+    if (!out || !bits || !owner) throw std::invalid_argument("psum_distribute: null argument");
+    *out = reinterpret_cast<iqcc_gpu_psum*>(
+        psum_distribute(n_qubits, rows, coeff, M, m, bits, owner, n_workers, devices));
+  });
+}
+
+int iqcc_gpu_psum_create_shards(size_t n_qubits, size_t m, const size_t* bits, const size_t* owner,
+                                size_t n_workers, const int* devices, const uint64_t* const* rows,
+                                const double* const* coeffs, const size_t* sizes, iqcc_gpu_psum** out) {
+  return guarded([&] {
+    if (!out || !owner || !sizes || (m && !bits)) throw std::invalid_argument("psum_create_shards: null argument");
+    *out = reinterpret_cast<iqcc_gpu_psum*>(
+        psum_from_shards(n_qubits, m, bits, owner, n_workers, devices, rows, coeffs, sizes));
+  });
+}
+
+static PSum& psum_of(iqcc_gpu_psum* ph) {
+  if (!ph) throw std::invalid_argument("null partitioned-sum handle");
+  return *reinterpret_cast<PSum*>(ph);
+}
+
+int iqcc_gpu_psum_destroy(iqcc_gpu_psum* ph) {
+  return guarded([&] {
+    if (ph) psum_destroy(reinterpret_cast<PSum*>(ph));
+  });
+}
+
+int iqcc_gpu_psum_info(iqcc_gpu_psum* ph, size_t* n_partitions, size_t* total_terms) {
+  return guarded([&] {
+    PSum& P = psum_of(ph);
+    const size_t n = psum_parts(P);
+    std::vector<size_t> sz(n);
+    psum_sizes(P, sz.data());
+    if (n_partitions) *n_partitions = n;
+    if (total_terms) {
+      size_t t = 0;
+      for (size_t v : sz) t += v;
+      *total_terms = t;
+    }
+  });
+}
+
+int iqcc_gpu_psum_shard_sizes(iqcc_gpu_psum* ph, size_t* sizes) {
+  return guarded([&] { psum_sizes(psum_of(ph), sizes); });
+}
+
+int iqcc_gpu_psum_owner(iqcc_gpu_psum* ph, size_t* owner) {
+  return guarded([&] { psum_owner(psum_of(ph), owner); });
+}
+
+int iqcc_gpu_psum_download_shard(iqcc_gpu_psum* ph, size_t p, uint64_t* rows, double* coeff, size_t cap,
+                                 size_t* M) {
+  return guarded([&] { *M = psum_download_shard(psum_of(ph), p, rows, coeff, cap); });
+}
+
+int iqcc_gpu_psum_gather(iqcc_gpu_psum* ph, uint64_t* rows, double* coeff, size_t cap, size_t* M) {
+  return guarded([&] { *M = psum_gather(psum_of(ph), rows, coeff, cap); });
+}
+
+int iqcc_gpu_psum_dress(iqcc_gpu_psum* ph, const uint64_t* gen, double cos_tau, double sin_tau, double eps,
+                        size_t max_terms, iqcc_message_record* log, size_t log_cap, size_t* n_log,
+                        iqcc_compress_stats* cstats, size_t* mask) {
+  return guarded([&] {
+    psum_dress(psum_of(ph), gen, cos_tau, sin_tau, eps, max_terms, log, log_cap, n_log, cstats, mask);
+  });
+}
+
+int iqcc_gpu_psum_expect(iqcc_gpu_psum* ph, const double* factors, double* energy) {
+  return guarded([&] { *energy = psum_expect(psum_of(ph), factors); });
+}
+
+int iqcc_gpu_psum_qmf_energy_gradient(iqcc_gpu_psum* ph, const double* factors, const double* derivs,
+                                      double* energy, double* grad) {
+  return guarded([&] { *energy = psum_qmf_energy_gradient(psum_of(ph), factors, derivs, grad); });
+}
+
+int iqcc_gpu_psum_gradients(iqcc_gpu_psum* ph, const double* factors, const uint64_t* cands, size_t K,
+                            int flip_group_only, double* g) {
+  return guarded([&] { psum_gradients(psum_of(ph), factors, cands, K, flip_group_only != 0, g); });
+}
+
+int iqcc_gpu_psum_rebalance(iqcc_gpu_psum* ph, double threshold, size_t* owner_out) {
+  return guarded([&] { psum_rebalance(psum_of(ph), threshold, owner_out); });
 }
 
 int iqcc_gpu_parallel_size(iqcc_gpu_sum* h, size_t* total) {

@@ -64,6 +64,11 @@ struct Thr {
 #ifndef IQCC_MERGE_MINB
 #define IQCC_MERGE_MINB 6
 #endif
+// resident 256-thread CTAs per SM the merge is compiled for: B = 4 (200-256
+// qubits) rows are twice as wide, so fewer, fatter CTAs (no spills)
+__host__ __device__ constexpr int merge_minb(int B, int NT) {
+  return (B >= 4 ? 3 : IQCC_MERGE_MINB) * 256 / NT > 0 ? (B >= 4 ? 3 : IQCC_MERGE_MINB) * 256 / NT : 1;
+}
 #ifndef IQCC_RANK_MINB
 #define IQCC_RANK_MINB 4
 #endif
@@ -104,7 +109,7 @@ __device__ __forceinline__ bool product_slot(const SlotRule& r, bool anti_presen
 }
 
 template <int B, int IT>
-__global__ void __launch_bounds__(256, IQCC_CLS_MINB) k_classify(const ull* __restrict__ keys,
+__global__ void __launch_bounds__(256, B >= 4 ? 2 : IQCC_CLS_MINB) k_classify(const ull* __restrict__ keys,
                                                   const double* __restrict__ coef, Filter filt,
                                                   size_t M, Key<B> P, short* __restrict__ lcp,
                                                   unsigned* __restrict__ fmask,
@@ -1143,14 +1148,16 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
               put(keep_term(sum, id, g.drop) ? sum : dead_value(), nS + j);
             }
           } else if (qs) {
-            put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
+            put(keep_term(qv, b0 + j == 0 && key_is_identity<B>(kq), g.drop) ? qv : dead_value(), nS + j);
           }
         } else if (sl) {
           put(keep_term(v, id, g.drop) ? v : dead_value(), i);
         }
       } else if (qslot(j)) {
+        // a dressing product is never the identity (T^P = 0 needs T = P,
+        // which commutes); merge_sums' second operand may start with it
         const double qv = qval(j, kq);
-        put(keep_term(qv, false, g.drop) ? qv : dead_value(), nS + j);
+        put(keep_term(qv, b0 + j == 0 && key_is_identity<B>(kq), g.drop) ? qv : dead_value(), nS + j);
       }
       if (c <= 0 && ++i < ia1) ks = sm_key16<B>(sk, i);
       if (c >= 0 && ++j < ib1) kq = qkey(j);
@@ -1250,7 +1257,7 @@ __device__ __forceinline__ void merge_flush(const MergeArgs& g, unsigned* shist,
 /// One tile per CTA (single input stage): the default; enough CTAs stay
 /// resident that load latency of one hides behind the merge of others.
 template <int B, int NT, int IPT>
-__global__ void __launch_bounds__(NT, IQCC_MERGE_MINB * 256 / NT) k_merge1(MergeArgs g, Key<B> P) {
+__global__ void __launch_bounds__(NT, merge_minb(B, NT)) k_merge1(MergeArgs g, Key<B> P) {
   using Cfg = MergeCfg<B, NT, IPT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST - Cfg::STAGE);
@@ -1284,7 +1291,7 @@ __global__ void __launch_bounds__(NT, IQCC_MERGE_MINB * 256 / NT) k_merge1(Merge
 #define IQCC_PMERGE_MINB 4
 #endif
 template <int B, int NT, int IPT>
-__global__ void __launch_bounds__(NT, IQCC_PMERGE_MINB * 256 / NT) k_merge(MergeArgs g, Key<B> P) {
+__global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PMERGE_MINB) * 256 / NT) k_merge(MergeArgs g, Key<B> P) {
   using Cfg = MergeCfg<B, NT, IPT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
@@ -1372,7 +1379,7 @@ struct PlanState {
   const unsigned* qtotal = nullptr;
   size_t Wq = 0;
 };
-PlanState g_plan;
+thread_local PlanState g_plan;  // per host thread (engine context), see capi.cu
 
 template <int B>
 void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = true,
@@ -1581,7 +1588,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
   g_plan = pl;
 }
 
-int g_sub_b0 = -(1 << 20);  // fine-histogram window of the last merge (see kSubBins)
+thread_local int g_sub_b0 = -(1 << 20);  // fine-histogram window of the last merge (see kSubBins)
 
 template <int B, int NT, int IPT>
 void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys, const double* q_vals,
@@ -1659,9 +1666,10 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
   if (persistent) {
     static int ctas_per_sm = 0, n_sm = 0;
-    if (!ctas_per_sm) {
+    if (func_attr_once((const void*)k_merge<B, NT, IPT>, ctx_device(ctx_current())))
       IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::bytes(true, 2)));
+    if (!ctas_per_sm) {
       IQCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_merge<B, NT, IPT>, NT,
                                                               Cfg::bytes(true, 2)));
       IQCC_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0));
@@ -1671,13 +1679,11 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     const unsigned grid = (unsigned)std::min<size_t>(ntm, (size_t)n_sm * ctas_per_sm);
     k_merge<B, NT, IPT><<<grid, NT, Cfg::bytes(want_hist, 2), st>>>(g, P);
   } else {
-    static bool attr1 = false;
-    if (!attr1) {
+    if (func_attr_once((const void*)k_merge1<B, NT, IPT>, ctx_device(ctx_current()))) {
       IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::bytes(true, 1)));
       IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      (int)cudaSharedmemCarveoutMaxShared));
-      attr1 = true;
     }
     KernelScope ks("merge");
     k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
@@ -1690,7 +1696,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   if (getenv("IQCC_DEBUG")) debug_check("merge");
 }
 
-Reducer* g_merge_red = nullptr;
+thread_local Reducer* g_merge_red = nullptr;
 
 __global__ void k_pack_glob(ull* ctr, ull identity) {
   if (threadIdx.x == 0) {
@@ -1944,6 +1950,22 @@ DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, 
     case 2: return merge_products_t<2>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
     default: return merge_products_t<4>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
   }
+}
+
+/// merge_sums (iqcc/pauli.hpp:383-415): out = a's terms merged with b's
+/// through the merge kernel with an all-zero "entangler" (it commutes with
+/// every word, so a's values pass unchanged and b enters as received,
+/// final products): a + b (a first) on shared words, keep_term(drop) on
+/// every output, identity always kept.
+void merge_sums_store(DeviceStore& a, DeviceStore& b, double drop, DeviceStore& out) {
+  if (a.n_qubits != b.n_qubits) throw std::invalid_argument("merge_sums: mismatched qubit counts");
+  store_materialize(b);  // plain sorted live terms (same logical content)
+  store_clone(a, out);
+  const std::vector<uint64_t> zero(2 * out.B, 0);
+  plan_survivors(out, zero.data(), 1.0, 0.0, 0.0);
+  recv_slot_bits(b.coef(), b.M, 0.0);
+  merge_products(out, zero.data(), 1.0, 0.0, drop, false, 0.0, b.M, b.keys(), b.coef());
+  out.has_identity = a.has_identity || b.has_identity;
 }
 
 void dress_undo(DeviceStore& s, size_t M, size_t logical, const Filter& filt) {

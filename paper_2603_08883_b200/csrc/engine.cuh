@@ -16,8 +16,11 @@
 
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
+
+#include "../../include/iqcc_b200.h"
 
 namespace iqcc_b200 {
 
@@ -330,6 +333,17 @@ __device__ __forceinline__ bool dbg_ok(ull* dbg, unsigned site, ull idx, ull bou
 struct Ctx;
 Ctx& ctx();
 cudaStream_t stream();
+/// Engine contexts (one per host thread, see capi.cu): create one on a
+/// device, bind it to the calling thread (returns the previous binding),
+/// free it (its stream, scratch and cached blocks).
+Ctx* ctx_new(int device);
+Ctx* ctx_bind(Ctx* c);
+Ctx* ctx_current();
+int ctx_device(const Ctx* c);
+void ctx_free(Ctx* c);
+/// True the first time (kernel, device) is seen: cudaFuncSetAttribute is a
+/// per-device setting.
+bool func_attr_once(const void* fn, int device);
 void count_launch(const char* family);
 void add_alg_bytes(const char* family, double bytes);
 void check_cuda(cudaError_t e, const char* what);
@@ -521,6 +535,31 @@ void poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const
 void parallel_poly_kernels_store(DeviceStore& s, const double* factors, bool poles, const uint64_t* words,
                                  size_t t, double* hk, double* nk);
 void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* owner, int rank);
+
+/// merge_sums (iqcc/pauli.hpp:383-415) of two stores into `out`.
+void merge_sums_store(DeviceStore& a, DeviceStore& b, double drop, DeviceStore& out);
+
+/// Partitioned sums on the device driven from one host thread (psum.cu).
+struct PSum;
+PSum* psum_distribute(size_t n_qubits, const uint64_t* rows, const double* coeff, size_t M,
+                                      size_t m, const size_t* bits, const size_t* owner, size_t n_workers,
+                                      const int* devices);
+PSum* psum_from_shards(size_t n_qubits, size_t m, const size_t* bits, const size_t* owner,
+                                       size_t n_workers, const int* devices, const uint64_t* const* rows,
+                                       const double* const* coeffs, const size_t* sizes);
+void psum_destroy(PSum* ps);
+size_t psum_parts(const PSum& P);
+void psum_sizes(PSum& P, size_t* sizes);
+void psum_owner(const PSum& P, size_t* owner);
+size_t psum_download_shard(PSum& P, size_t p, uint64_t* rows, double* coeff, size_t cap);
+size_t psum_gather(PSum& P, uint64_t* rows, double* coeff, size_t cap);
+void psum_dress(PSum& P, const uint64_t* gen, double cs, double sn, double eps, size_t max_terms,
+                iqcc_message_record* log, size_t log_cap, size_t* n_log, iqcc_compress_stats* cstats,
+                size_t* mask_out);
+double psum_expect(PSum& P, const double* factors);
+double psum_qmf_energy_gradient(PSum& P, const double* factors, const double* derivs, double* grad);
+void psum_gradients(PSum& P, const double* factors, const uint64_t* cands, size_t K, bool flip_only, double* g);
+void psum_rebalance(PSum& P, double threshold, size_t* owner_out);
 
 /// Partition bits as (device word, bit) pairs (iqcc/partition.hpp:40-42).
 struct PartSpecHost {

@@ -434,6 +434,48 @@ double parallel_expect_store(DeviceStore& s, const double* factors) {
   return e;
 }
 
+/// Allgather of n doubles per rank; returns [world][n] in rank order.
+static std::vector<double> allgather_doubles(const double* local, size_t n) {
+  Comm& c = comm();
+  cudaStream_t st = stream();
+  double* d = workspace().partials.as<double>((c.world + 1) * std::max<size_t>(n, 1));
+  IQCC_CUDA(cudaMemcpyAsync(d + c.world * n, local, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  IQCC_NCCL(ncclAllGather(d + c.world * n, d, n, ncclFloat64, c.comm, st));
+  std::vector<double> parts(c.world * n);
+  IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  host_sync(st);
+  return parts;
+}
+
+double parallel_qmf_grad_store(DeviceStore& s, const double* factors, const double* derivs, double* grad) {
+  Comm& c = comm();
+  const size_t n2 = 2 * (size_t)s.n_qubits;
+  std::vector<double> local(n2 + 1, 0.0);
+  if (s.logical) local[n2] = qmf_grad_store(s, factors, derivs, local.data());
+  const auto parts = allgather_doubles(local.data(), n2 + 1);
+  for (size_t k = 0; k <= n2; ++k) {
+    double v = 0.0;
+    for (int w = 0; w < c.world; ++w) v += parts[w * (n2 + 1) + k];  // rank order (reduce_scalar)
+    if (k < n2) grad[k] = v;
+    else local[n2] = v;
+  }
+  return local[n2];
+}
+
+void parallel_gradients_store(DeviceStore& s, const double* factors, const uint64_t* cands, size_t K,
+                              bool flip_only, double* g) {
+  Comm& c = comm();
+  if (K == 0) return;
+  std::vector<double> local(K, 0.0);
+  if (s.logical) gradients_store(s, factors, cands, K, flip_only, local.data());
+  const auto parts = allgather_doubles(local.data(), K);
+  for (size_t k = 0; k < K; ++k) {
+    double v = 0.0;
+    for (int w = 0; w < c.world; ++w) v += parts[w * K + k];
+    g[k] = v;
+  }
+}
+
 size_t parallel_sum(size_t v) {
   ull a[1] = {(ull)v};
   NcclReducer red;

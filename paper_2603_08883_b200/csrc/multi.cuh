@@ -18,5 +18,10 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
 /// Sum of a host value over the ranks (one allreduce).
 size_t parallel_sum(size_t v);
 double parallel_expect_store(DeviceStore& s, const double* factors);
+/// Partitioned QMF energy + 2n gradients and DIS gradients of K candidates:
+/// local values allgathered, summed element by element in rank order.
+double parallel_qmf_grad_store(DeviceStore& s, const double* factors, const double* derivs, double* grad);
+void parallel_gradients_store(DeviceStore& s, const double* factors, const uint64_t* cands, size_t K,
+                              bool flip_only, double* g);
 size_t parallel_size(DeviceStore& s);
 }  // namespace iqcc_b200

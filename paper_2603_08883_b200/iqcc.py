@@ -681,6 +681,273 @@ class Partition:
         sandwiches, allgathered over NCCL, summed in worker order.  Collective."""
         return d.poly_kernels(omega, ex, partitioned=True)
 
+    def qmf_energy_gradient(self, d: DeviceSum, omega: QmfState):
+        """qmf_energy_gradient (iqcc/qmf.hpp:94-148) of the global sum: each
+        rank's energy and 2n gradients, allgathered and summed in rank order
+        (reduce_scalar, iqcc/partition.hpp:233-237).  Collective."""
+        t, dt = qmf_factor_table(omega), qmf_deriv_table(omega)
+        g = np.zeros(2 * self.n_qubits, np.float64)
+        e = C.c_double()
+        check(lib.iqcc_gpu_parallel_qmf_energy_gradient(d.handle, _addr(t), _addr(dt), C.byref(e), _addr(g)))
+        return e.value, g
+
+    def gradients(self, d: DeviceSum, omega: QmfState, cands: np.ndarray, flip_group_only: bool = False):
+        """DIS gradients (iqcc/dis.hpp:39-52) of K candidates over the global
+        sum: local vectors allgathered and summed in rank order.  Collective."""
+        t = qmf_factor_table(omega)
+        c = np.ascontiguousarray(cands, np.uint64).reshape(-1, 2 * blocks_for(self.n_qubits))
+        g = np.zeros(max(1, c.shape[0]), np.float64)
+        check(lib.iqcc_gpu_parallel_gradients(d.handle, _addr(t), _addr(c), c.shape[0], int(flip_group_only),
+                                              _addr(g)))
+        return g[: c.shape[0]]
+
+
+# ------------------------------- PartitionedSum on the device (one caller)
+@dataclass
+class PartitionMap:
+    """iqcc/partition.hpp:20-38."""
+    n_qubits: int
+    partition_bits: List[int]
+    owner: List[int]
+    n_workers: int = 1
+
+    def n_partitions(self) -> int:
+        return len(self.owner)
+
+    def validate(self) -> None:
+        if len(self.owner) != 1 << len(self.partition_bits):
+            raise ValueError("PartitionMap: owner table size")
+        if any(p >= 2 * self.n_qubits for p in self.partition_bits):
+            raise ValueError("PartitionMap: bit position out of range")
+        if any(w >= self.n_workers for w in self.owner):
+            raise ValueError("PartitionMap: owner out of range")
+
+
+def make_partition_map(h, m: int, n_workers: int) -> PartitionMap:
+    """iqcc/partition.hpp:111-123: greedy bits (on the device), round-robin owners."""
+    if n_workers < 1:
+        raise ValueError("make_partition_map: no workers")
+    bits, _ = choose_partition_bits(h, m)
+    return PartitionMap(h.n_qubits, bits, [p % n_workers for p in range(1 << m)], n_workers)
+
+
+@dataclass
+class MessageRecord:
+    """iqcc/partition.hpp:135-140."""
+    source: int
+    destination: int
+    terms: int
+    bytes: int
+
+
+@dataclass
+class MessageLog:
+    """iqcc/partition.hpp:143-165."""
+    records: List[MessageRecord] = field(default_factory=list)
+
+    def total_terms(self) -> int:
+        return sum(r.terms for r in self.records)
+
+    def total_bytes(self) -> int:
+        return sum(r.bytes for r in self.records)
+
+    def to_csv(self) -> str:
+        return "source,destination,terms,bytes\n" + "".join(
+            f"{r.source},{r.destination},{r.terms},{r.bytes}\n" for r in self.records)
+
+
+@dataclass
+class ParallelDressStats:
+    """iqcc/partition.hpp:303-306."""
+    compress: CompressStats = field(default_factory=lambda: CompressStats())
+    mask: int = 0
+
+
+class PartitionedSum:
+    """The reference's PartitionedSum (iqcc/partition.hpp:145-173) resident on
+    the GPUs: 2^m shards, shard p owned by worker map.owner[p], worker w on
+    CUDA device devices[w] (default w % device count).  One call drives all
+    shards (a worker thread and engine context per shard inside the handle);
+    any m, so several partitions may share a worker or a GPU."""
+
+    def __init__(self, handle: int, pmap: PartitionMap):
+        self.handle, self.map = handle, pmap
+        self.n_qubits = pmap.n_qubits
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            lib.iqcc_gpu_psum_destroy(h)
+            self.handle = None
+
+    def _map_arrays(self):
+        b = np.array(self.map.partition_bits or [0], np.uintp)
+        o = np.array(self.map.owner, np.uintp)
+        return b, o
+
+    @staticmethod
+    def distribute(h: PauliSum, pmap: PartitionMap, devices: Optional[Sequence[int]] = None) -> "PartitionedSum":
+        """distribute (iqcc/partition.hpp:208-220)."""
+        native.init()
+        pmap.validate()
+        if pmap.n_qubits != h.n_qubits:
+            raise ValueError("distribute: mismatched qubit counts")
+        rows = np.ascontiguousarray(h.rows, np.uint64)
+        cf = np.ascontiguousarray(h.coeffs, np.complex128)
+        b = np.array(pmap.partition_bits or [0], np.uintp)
+        o = np.array(pmap.owner, np.uintp)
+        dv = None if devices is None else np.array(devices, np.int32)
+        out = C.c_void_p()
+        check(lib.iqcc_gpu_psum_distribute(h.n_qubits, _addr(rows), _addr(cf), len(h), len(pmap.partition_bits),
+                                           _addr(b), _addr(o), pmap.n_workers,
+                                           None if dv is None else _addr(dv), C.byref(out)))
+        return PartitionedSum(out.value, pmap)
+
+    @staticmethod
+    def from_shards(shards: Sequence[PauliSum], pmap: PartitionMap,
+                    devices: Optional[Sequence[int]] = None) -> "PartitionedSum":
+        """A reference PartitionedSum's shards uploaded as they are (each term
+        must carry its shard's key, PartitionedSum::validate)."""
+        native.init()
+        pmap.validate()
+        if len(shards) != pmap.n_partitions():
+            raise ValueError("PartitionedSum: shard count != 2^m")
+        rows = [np.ascontiguousarray(s.rows, np.uint64) for s in shards]
+        cfs = [np.ascontiguousarray(s.coeffs, np.complex128) for s in shards]
+        rp = (C.c_void_p * len(shards))(*[_addr(r) for r in rows])
+        cp = (C.c_void_p * len(shards))(*[_addr(c) for c in cfs])
+        sz = np.array([len(s) for s in shards], np.uintp)
+        b, o = (np.array(pmap.partition_bits or [0], np.uintp), np.array(pmap.owner, np.uintp))
+        dv = None if devices is None else np.array(devices, np.int32)
+        out = C.c_void_p()
+        check(lib.iqcc_gpu_psum_create_shards(pmap.n_qubits, len(pmap.partition_bits), _addr(b), _addr(o),
+                                              pmap.n_workers, None if dv is None else _addr(dv), rp, cp,
+                                              _addr(sz), C.byref(out)))
+        return PartitionedSum(out.value, pmap)
+
+    def shard_sizes(self) -> List[int]:
+        sz = np.zeros(self.map.n_partitions(), np.uintp)
+        check(lib.iqcc_gpu_psum_shard_sizes(self.handle, _addr(sz)))
+        return [int(v) for v in sz]
+
+    def total_terms(self) -> int:
+        return sum(self.shard_sizes())
+
+    def worker_loads(self) -> List[int]:
+        loads = [0] * self.map.n_workers
+        for p, n in enumerate(self.shard_sizes()):
+            loads[self.map.owner[p]] += n
+        return loads
+
+    def shard(self, p: int) -> PauliSum:
+        n = self.shard_sizes()[p]
+        B = blocks_for(self.n_qubits)
+        rows = np.zeros((max(n, 1), 2 * B), np.uint64)
+        cf = np.zeros(max(n, 1), np.complex128)
+        got = C.c_size_t()
+        check(lib.iqcc_gpu_psum_download_shard(self.handle, p, _addr(rows), _addr(cf), n, C.byref(got)))
+        return PauliSum(self.n_qubits, rows[: got.value], cf[: got.value])
+
+    def gather(self) -> PauliSum:
+        """gather (iqcc/partition.hpp:222-230), merged on the device."""
+        n = self.total_terms()
+        B = blocks_for(self.n_qubits)
+        rows = np.zeros((max(n, 1), 2 * B), np.uint64)
+        cf = np.zeros(max(n, 1), np.complex128)
+        got = C.c_size_t()
+        check(lib.iqcc_gpu_psum_gather(self.handle, _addr(rows), _addr(cf), n, C.byref(got)))
+        return PauliSum(self.n_qubits, rows[: got.value], cf[: got.value])
+
+    def dress(self, op: DressOp, epsilon: float, max_terms: int = U64_MAX, log: Optional[MessageLog] = None,
+              stats: Optional[ParallelDressStats] = None) -> None:
+        """In place parallel_dress (iqcc/partition.hpp:398-452)."""
+        if op.generator.n_qubits != self.n_qubits:
+            raise ValueError("parallel_dress: mismatched qubit counts")
+        g = np.ascontiguousarray(op.generator.row, np.uint64)
+        cap = self.map.n_partitions()
+        recs = (native.MessageRecord * cap)()
+        nl, mask = C.c_size_t(), C.c_size_t()
+        cs = native.CompressStatsC()
+        check(lib.iqcc_gpu_psum_dress(self.handle, _addr(g), math.cos(op.amplitude), math.sin(op.amplitude),
+                                      epsilon, max_terms, recs, cap, C.byref(nl),
+                                      C.byref(cs) if stats is not None else None, C.byref(mask)))
+        if log is not None:
+            log.records.extend(MessageRecord(recs[i].source, recs[i].destination, recs[i].terms, recs[i].bytes)
+                               for i in range(min(nl.value, cap)))
+        if stats is not None:
+            stats.compress.dropped_terms += cs.dropped_terms
+            stats.compress.dropped_weight += cs.dropped_weight
+            stats.mask = mask.value
+
+    def expect(self, omega: QmfState) -> float:
+        t = qmf_factor_table(omega)
+        e = C.c_double()
+        check(lib.iqcc_gpu_psum_expect(self.handle, _addr(t), C.byref(e)))
+        return e.value
+
+    def qmf_energy_gradient(self, omega: QmfState):
+        t, dt = qmf_factor_table(omega), qmf_deriv_table(omega)
+        g = np.zeros(2 * self.n_qubits, np.float64)
+        e = C.c_double()
+        check(lib.iqcc_gpu_psum_qmf_energy_gradient(self.handle, _addr(t), _addr(dt), C.byref(e), _addr(g)))
+        return e.value, g
+
+    def gradients(self, omega: QmfState, cands: np.ndarray, flip_group_only: bool = False) -> np.ndarray:
+        t = qmf_factor_table(omega)
+        c = np.ascontiguousarray(cands, np.uint64).reshape(-1, 2 * blocks_for(self.n_qubits))
+        g = np.zeros(max(1, c.shape[0]), np.float64)
+        check(lib.iqcc_gpu_psum_gradients(self.handle, _addr(t), _addr(c), c.shape[0], int(flip_group_only),
+                                          _addr(g)))
+        return g[: c.shape[0]]
+
+    def rebalance(self, threshold: float) -> PartitionMap:
+        """rebalance (iqcc/partition.hpp:457-494) + device migration of moved shards."""
+        o = np.zeros(self.map.n_partitions(), np.uintp)
+        check(lib.iqcc_gpu_psum_rebalance(self.handle, threshold, _addr(o)))
+        self.map = PartitionMap(self.map.n_qubits, list(self.map.partition_bits), [int(v) for v in o],
+                                self.map.n_workers)
+        return self.map
+
+
+def distribute(h: PauliSum, pmap: PartitionMap, devices: Optional[Sequence[int]] = None) -> PartitionedSum:
+    """iqcc/partition.hpp:208-220."""
+    return PartitionedSum.distribute(h, pmap, devices)
+
+
+def gather(ph: PartitionedSum) -> PauliSum:
+    """iqcc/partition.hpp:222-230."""
+    return ph.gather()
+
+
+def parallel_dress(ph: PartitionedSum, op: DressOp, epsilon: float, max_terms: int = U64_MAX,
+                   log: Optional[MessageLog] = None, mode=None,
+                   stats: Optional[ParallelDressStats] = None) -> PartitionedSum:
+    """iqcc/partition.hpp:398-452, in place on the device handle (returned).
+    `mode` (ExecutionMode) is accepted for signature parity: shards always
+    run concurrently and the result is the same either way."""
+    ph.dress(op, epsilon, max_terms, log, stats)
+    return ph
+
+
+def parallel_expect(ph: PartitionedSum, omega: QmfState, mode=None) -> float:
+    """iqcc/partition.hpp:241-254."""
+    return ph.expect(omega)
+
+
+def rebalance(ph: PartitionedSum, threshold: float) -> PartitionMap:
+    """iqcc/partition.hpp:457-494."""
+    return ph.rebalance(threshold)
+
+
+def merge_sums(a: PauliSum, b: PauliSum, opts: MergeOptions = MergeOptions()) -> PauliSum:
+    """iqcc/pauli.hpp:383-415 on the device (check_hermitian is moot: real sums)."""
+    if a.n_qubits != b.n_qubits:
+        raise ValueError("merge_sums: mismatched qubit counts")
+    da, db = DeviceSum.upload(a), DeviceSum.upload(b)
+    out = C.c_void_p()
+    check(lib.iqcc_gpu_merge_sums(da.handle, db.handle, opts.drop_threshold, C.byref(out)))
+    return DeviceSum(out.value, a.n_qubits).download()
+
 
 def partition_key(row, n_qubits: int, bits) -> int:
     """partition_key (iqcc/partition.hpp:40-42) of a reference row."""

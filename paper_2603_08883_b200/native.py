@@ -38,6 +38,12 @@ class ExchangeStats(C.Structure):
                 ("bytes_wire", C.c_size_t), ("bytes_reference", C.c_size_t)]
 
 
+class MessageRecord(C.Structure):
+    """iqcc_message_record = MessageRecord (iqcc/partition.hpp:135-140)."""
+    _fields_ = [("source", C.c_size_t), ("destination", C.c_size_t), ("terms", C.c_size_t),
+                ("bytes", C.c_size_t)]
+
+
 _vp = C.c_void_p
 _u64p = C.c_void_p  # raw addresses (numpy .ctypes.data or device pointers)
 _f64p = C.c_void_p
@@ -90,6 +96,27 @@ _SIGS = {
                                                    C.POINTER(CompressStatsC), C.POINTER(C.c_size_t)]),
     "iqcc_gpu_parallel_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
     "iqcc_gpu_parallel_size": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_parallel_qmf_energy_gradient": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(C.c_double), _f64p]),
+    "iqcc_gpu_parallel_gradients": (C.c_int, [_vp, _f64p, _u64p, C.c_size_t, C.c_int, _f64p]),
+    "iqcc_gpu_merge_sums": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(_vp)]),
+    "iqcc_gpu_psum_distribute": (C.c_int, [C.c_size_t, _u64p, _f64p, C.c_size_t, C.c_size_t, _szp, _szp,
+                                           C.c_size_t, _vp, C.POINTER(_vp)]),
+    "iqcc_gpu_psum_create_shards": (C.c_int, [C.c_size_t, C.c_size_t, _szp, _szp, C.c_size_t, _vp, _vp, _vp,
+                                              _szp, C.POINTER(_vp)]),
+    "iqcc_gpu_psum_destroy": (C.c_int, [_vp]),
+    "iqcc_gpu_psum_info": (C.c_int, [_vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_psum_shard_sizes": (C.c_int, [_vp, _szp]),
+    "iqcc_gpu_psum_owner": (C.c_int, [_vp, _szp]),
+    "iqcc_gpu_psum_download_shard": (C.c_int, [_vp, C.c_size_t, _u64p, _f64p, C.c_size_t,
+                                               C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_psum_gather": (C.c_int, [_vp, _u64p, _f64p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_psum_dress": (C.c_int, [_vp, _u64p, C.c_double, C.c_double, C.c_double, C.c_size_t, _vp,
+                                      C.c_size_t, C.POINTER(C.c_size_t), C.POINTER(CompressStatsC),
+                                      C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_psum_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
+    "iqcc_gpu_psum_qmf_energy_gradient": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(C.c_double), _f64p]),
+    "iqcc_gpu_psum_gradients": (C.c_int, [_vp, _f64p, _u64p, C.c_size_t, C.c_int, _f64p]),
+    "iqcc_gpu_psum_rebalance": (C.c_int, [_vp, C.c_double, _szp]),
 }
 
 EXPORTED = tuple(_SIGS)
