@@ -120,6 +120,15 @@ int iqcc_gpu_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compre
 int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, const double* cos_tau,
                             const double* sin_tau, double eps, size_t max_terms, double drop_thr,
                             iqcc_compress_stats* stats, size_t* terms_in_total /* nullable */);
+/* SortlessStats of sortless_dress (iqcc/dressing.hpp:182-189, 248-305) for
+ * dressing h by gen with sin(tau) = sin_tau: n_buckets = support buckets
+ * (bucket_by_support, :159-177), new_term_streams = anticommuting buckets
+ * when sin_tau != 0, else 0.  The device never sorts products, so
+ * new_stream_sorts is 0; merge_comparisons (the reference's heap k-way merge
+ * compare count) has no device counterpart and is reported as 0.
+ * > 64 support bits -> IQCC_ERUNTIME as the reference throws. */
+int iqcc_gpu_sortless_stats(iqcc_gpu_sum* h, const uint64_t* gen, double sin_tau, size_t* n_buckets,
+                            size_t* new_term_streams);
 /* growth_split (iqcc/dressing.hpp:41-50). */
 int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* n_commuting,
                           size_t* n_anticommuting);

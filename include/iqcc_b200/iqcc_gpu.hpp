@@ -21,6 +21,7 @@
 #include <complex>
 #include <cstdint>
 #include <limits>
+#include <memory>
 #include <random>
 #include <span>
 #include <stdexcept>
@@ -30,6 +31,7 @@
 #include "iqcc/dis.hpp"
 #include "iqcc/dressing.hpp"
 #include "iqcc/optimizer.hpp"
+#include "iqcc/partition.hpp"
 #include "iqcc/pauli.hpp"
 #include "iqcc/qmf.hpp"
 #include "iqcc_b200.h"
@@ -45,9 +47,10 @@ inline void check(int rc) {
   throw std::runtime_error(msg);
 }
 
-/// Engine bound to one device per process (iqcc_gpu_init is idempotent).
+/// Engine context of the calling thread (iqcc_gpu_init binds one per host
+/// thread and is idempotent).
 inline void ensure_engine(int device = 0) {
-  static const int rc = iqcc_gpu_init(device);
+  static thread_local const int rc = iqcc_gpu_init(device);
   check(rc);
 }
 
@@ -88,6 +91,17 @@ inline PauliSum download(const Handle& d, std::size_t n_qubits) {
   std::vector<double> coeff(std::max<std::size_t>(n, 1) * 2);
   std::size_t got = 0;
   check(iqcc_gpu_sum_download(d.get(), rows.data(), coeff.data(), n, &got));
+  PauliSum out(n_qubits);
+  out.reserve(got);
+  for (std::size_t i = 0; i < got; ++i)
+    out.append(PauliView{{rows.data() + i * 2 * B, B}, {rows.data() + i * 2 * B + B, B}},
+               Complex(coeff[2 * i], coeff[2 * i + 1]));
+  return out;
+}
+
+inline PauliSum from_rows(std::size_t n_qubits, const std::vector<uint64_t>& rows,
+                          const std::vector<double>& coeff, std::size_t got) {
+  const std::size_t B = blocks_for(n_qubits);
   PauliSum out(n_qubits);
   out.reserve(got);
   for (std::size_t i = 0; i < got; ++i)
@@ -233,9 +247,17 @@ inline PauliSum sortless_dress(const PauliSum& h, const DressOp& op, const Merge
   if (op.generator.is_identity()) throw std::invalid_argument("sortless_dress: identity generator");
   const auto pos = iqcc::detail::support_positions(op.generator.view(), h.n_qubits());
   if (pos.size() > 64) throw std::runtime_error("entangler support exceeds 64 bits; not supported");
-  PauliSum out = gpu::dress_single(h, op, opts);
-  if (stats) *stats = SortlessStats{};
-  return out;
+  DeviceSum d(h);
+  if (stats) {
+    // buckets / new-term streams counted on the device (dressing.hpp:248-268);
+    // no stream is ever sorted; merge_comparisons (heap compares) stays 0
+    *stats = SortlessStats{};
+    const auto row = detail::row_of(op.generator.view());
+    detail::check(iqcc_gpu_sortless_stats(d.handle(), row.data(), std::sin(op.amplitude), &stats->n_buckets,
+                                          &stats->new_term_streams));
+  }
+  d.dress(op, opts);
+  return d.download();
 }
 
 /// iqcc::dress_sequence (iqcc/dressing.hpp:311-324), device resident.
@@ -368,6 +390,187 @@ inline PolyKernels build_poly_kernels(const PauliSum& h, const QmfState& omega, 
     ker.n_kernel[i] = Complex(nk[2 * i], nk[2 * i + 1]);
   }
   return ker;
+}
+
+/// iqcc::merge_sums (iqcc/pauli.hpp:383-415): a + b (a first) on shared words,
+/// keep_term(opts.drop_threshold) on every output (check_hermitian is moot:
+/// the device holds real coefficients).
+inline PauliSum merge_sums(const PauliSum& a, const PauliSum& b, const MergeOptions& opts = {}) {
+  if (a.n_qubits() != b.n_qubits()) throw std::invalid_argument("merge_sums: mismatched qubit counts");
+  DeviceSum da(a), db(b);
+  iqcc_gpu_sum* out = nullptr;
+  detail::check(iqcc_gpu_merge_sums(da.handle(), db.handle(), opts.drop_threshold, &out));
+  return detail::download(detail::Handle(out), a.n_qubits());
+}
+
+// ------------------------------------------------------------ partitioning
+/// A PartitionedSum (iqcc/partition.hpp:145-173) resident on the GPUs: 2^m
+/// device shards, worker w on CUDA device devices[w] (default w % count).
+/// One call drives every shard; any m (several partitions per GPU).
+class DevicePartitionedSum {
+ public:
+  DevicePartitionedSum(const PauliSum& h, const PartitionMap& map, std::vector<int> devices = {})
+      : map_(map) {
+    map.validate();
+    if (map.n_qubits != h.n_qubits()) throw std::invalid_argument("distribute: mismatched qubit counts");
+    detail::ensure_engine();
+    const uint64_t* rows = h.empty() ? nullptr : h.word(0).x.data();
+    const double* coeff =
+        h.empty() ? nullptr : reinterpret_cast<const double*>(&const_cast<PauliSum&>(h).coeff(0));
+    iqcc_gpu_psum* out = nullptr;
+    detail::check(iqcc_gpu_psum_distribute(h.n_qubits(), rows, coeff, h.size(), map.partition_bits.size(),
+                                           map.partition_bits.data(), map.owner.data(), map.n_workers,
+                                           devices.empty() ? nullptr : devices.data(), &out));
+    h_ = out;
+  }
+  explicit DevicePartitionedSum(const PartitionedSum& ph, std::vector<int> devices = {}) : map_(ph.map) {
+    ph.map.validate();
+    detail::ensure_engine();
+    std::vector<const uint64_t*> rows;
+    std::vector<const double*> coeffs;
+    std::vector<std::size_t> sizes;
+    for (const auto& s : ph.shards) {
+      rows.push_back(s.empty() ? nullptr : s.word(0).x.data());
+      coeffs.push_back(s.empty() ? nullptr : reinterpret_cast<const double*>(&const_cast<PauliSum&>(s).coeff(0)));
+      sizes.push_back(s.size());
+    }
+    if (ph.shards.size() != ph.map.n_partitions()) throw std::invalid_argument("PartitionMap: owner table size");
+    iqcc_gpu_psum* out = nullptr;
+    detail::check(iqcc_gpu_psum_create_shards(ph.map.n_qubits, ph.map.partition_bits.size(),
+                                              ph.map.partition_bits.data(), ph.map.owner.data(),
+                                              ph.map.n_workers, devices.empty() ? nullptr : devices.data(),
+                                              rows.data(), coeffs.data(), sizes.data(), &out));
+    h_ = out;
+  }
+  DevicePartitionedSum(const DevicePartitionedSum&) = delete;
+  DevicePartitionedSum& operator=(const DevicePartitionedSum&) = delete;
+  ~DevicePartitionedSum() {
+    if (h_) iqcc_gpu_psum_destroy(h_);
+  }
+  const PartitionMap& map() const { return map_; }
+  std::vector<std::size_t> shard_sizes() const {
+    std::vector<std::size_t> s(map_.n_partitions());
+    detail::check(iqcc_gpu_psum_shard_sizes(h_, s.data()));
+    return s;
+  }
+  std::size_t total_terms() const {
+    std::size_t t = 0;
+    for (std::size_t v : shard_sizes()) t += v;
+    return t;
+  }
+  /// parallel_dress (iqcc/partition.hpp:398-452), in place.
+  void dress(const DressOp& op, double epsilon, std::size_t max_terms = std::numeric_limits<std::size_t>::max(),
+             MessageLog* log = nullptr, ParallelDressStats* stats = nullptr) {
+    if (map_.n_qubits != op.generator.n_qubits())
+      throw std::invalid_argument("parallel_dress: mismatched qubit counts");
+    const auto row = detail::row_of(op.generator.view());
+    std::vector<iqcc_message_record> recs(map_.n_partitions());
+    std::size_t nl = 0, mask = 0;
+    iqcc_compress_stats cs{0, 0.0};
+    detail::check(iqcc_gpu_psum_dress(h_, row.data(), std::cos(op.amplitude), std::sin(op.amplitude), epsilon,
+                                      max_terms, recs.data(), recs.size(), &nl, stats ? &cs : nullptr, &mask));
+    if (log)
+      for (std::size_t i = 0; i < std::min(nl, recs.size()); ++i)
+        log->records.push_back({recs[i].source, recs[i].destination, recs[i].terms, recs[i].bytes});
+    if (stats) {
+      stats->compress.dropped_terms += cs.dropped_terms;
+      stats->compress.dropped_weight += cs.dropped_weight;
+      stats->mask = mask;
+    }
+  }
+  double expect(const QmfState& omega) const {
+    const auto t = detail::factor_table(omega);
+    double e = 0.0;
+    detail::check(iqcc_gpu_psum_expect(h_, t.data(), &e));
+    return e;
+  }
+  double qmf_energy_gradient(const QmfState& omega, std::span<double> grad) const {
+    const auto t = detail::factor_table(omega);
+    const auto dt = detail::deriv_table(omega);
+    double e = 0.0;
+    detail::check(iqcc_gpu_psum_qmf_energy_gradient(h_, t.data(), dt.data(), &e, grad.data()));
+    return e;
+  }
+  std::vector<double> gradients(const QmfState& omega, const std::vector<PauliWord>& cands,
+                                bool flip_group_only = false) const {
+    const auto t = detail::factor_table(omega);
+    std::vector<uint64_t> rows;
+    for (const auto& c : cands) {
+      const auto r = detail::row_of(c.view());
+      rows.insert(rows.end(), r.begin(), r.end());
+    }
+    std::vector<double> g(std::max<std::size_t>(cands.size(), 1));
+    detail::check(iqcc_gpu_psum_gradients(h_, t.data(), rows.data(), cands.size(), flip_group_only, g.data()));
+    g.resize(cands.size());
+    return g;
+  }
+  /// rebalance (iqcc/partition.hpp:457-494) + migration of moved shards.
+  PartitionMap rebalance(double threshold) {
+    detail::check(iqcc_gpu_psum_rebalance(h_, threshold, map_.owner.data()));
+    return map_;
+  }
+  PauliSum shard(std::size_t p) const {
+    const std::size_t n = shard_sizes().at(p), B = blocks_for(map_.n_qubits);
+    std::vector<uint64_t> rows(std::max<std::size_t>(n, 1) * 2 * B);
+    std::vector<double> coeff(std::max<std::size_t>(n, 1) * 2);
+    std::size_t got = 0;
+    detail::check(iqcc_gpu_psum_download_shard(h_, p, rows.data(), coeff.data(), n, &got));
+    return detail::from_rows(map_.n_qubits, rows, coeff, got);
+  }
+  /// gather (iqcc/partition.hpp:222-230), merged on the device.
+  PauliSum gather() const {
+    const std::size_t n = total_terms(), B = blocks_for(map_.n_qubits);
+    std::vector<uint64_t> rows(std::max<std::size_t>(n, 1) * 2 * B);
+    std::vector<double> coeff(std::max<std::size_t>(n, 1) * 2);
+    std::size_t got = 0;
+    detail::check(iqcc_gpu_psum_gather(h_, rows.data(), coeff.data(), n, &got));
+    return detail::from_rows(map_.n_qubits, rows, coeff, got);
+  }
+  /// The shards as a reference PartitionedSum on the host.
+  PartitionedSum to_host() const {
+    PartitionedSum ph;
+    ph.map = map_;
+    for (std::size_t p = 0; p < map_.n_partitions(); ++p) ph.shards.push_back(shard(p));
+    return ph;
+  }
+
+ private:
+  PartitionMap map_;
+  iqcc_gpu_psum* h_ = nullptr;
+};
+
+/// iqcc::distribute (iqcc/partition.hpp:208-220) onto the devices.
+inline std::unique_ptr<DevicePartitionedSum> distribute(const PauliSum& h, const PartitionMap& map,
+                                                        std::vector<int> devices = {}) {
+  return std::make_unique<DevicePartitionedSum>(h, map, std::move(devices));
+}
+
+/// iqcc::gather of a device partitioned sum.
+inline PauliSum gather(const DevicePartitionedSum& ph) { return ph.gather(); }
+
+/// iqcc::parallel_dress (iqcc/partition.hpp:398-452) with the reference's
+/// signature: the shards go to the devices, one dressing step runs there
+/// (any mode gives the same sum: shards always run concurrently), and the
+/// dressed shards come back as a host PartitionedSum.
+inline PartitionedSum parallel_dress(const PartitionedSum& ph, const DressOp& op, double epsilon,
+                                     std::size_t max_terms = std::numeric_limits<std::size_t>::max(),
+                                     MessageLog* log = nullptr, ExecutionMode mode = ExecutionMode::kDeterministic,
+                                     ParallelDressStats* stats = nullptr) {
+  (void)mode;
+  if (ph.map.n_qubits != op.generator.n_qubits())
+    throw std::invalid_argument("parallel_dress: mismatched qubit counts");
+  if (op.generator.is_identity()) throw std::invalid_argument("parallel_dress: identity generator");
+  DevicePartitionedSum d(ph);
+  d.dress(op, epsilon, max_terms, log, stats);
+  return d.to_host();
+}
+
+/// iqcc::parallel_expect (iqcc/partition.hpp:241-254): worker-order reduction.
+inline double parallel_expect(const PartitionedSum& ph, const QmfState& omega,
+                              ExecutionMode mode = ExecutionMode::kDeterministic) {
+  (void)mode;
+  DevicePartitionedSum d(ph);
+  return d.expect(omega);
 }
 
 }  // namespace iqcc::gpu

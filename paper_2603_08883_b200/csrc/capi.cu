@@ -717,6 +717,18 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
   });
 }
 
+int iqcc_gpu_sortless_stats(iqcc_gpu_sum* h, const uint64_t* gen, double sin_tau, size_t* n_buckets,
+                            size_t* new_term_streams) {
+  return guarded([&] {
+    need(h);
+    auto row = widen_row(gen, ref_blocks(h->s), h->s.B);
+    size_t nb = 0, na = 0;
+    sortless_stats(h->s, row.data(), &nb, &na);
+    if (n_buckets) *n_buckets = nb;
+    if (new_term_streams) *new_term_streams = sin_tau != 0.0 ? na : 0;
+  });
+}
+
 int iqcc_gpu_growth_split(iqcc_gpu_sum* h, const uint64_t* gen, size_t* nc, size_t* na) {
   return guarded([&] {
     need(h);

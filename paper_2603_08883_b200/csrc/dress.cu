@@ -2031,4 +2031,150 @@ void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* n
   *nc = h[1];
 }
 
+// ---------------------------------------------------------- sortless stats
+// SortlessStats of sortless_dress (iqcc/dressing.hpp:182-189, 248-305): the
+// support buckets (bucket_by_support, :159-177) are the distinct bit
+// patterns of the terms on the entangler's support positions (x and z bit
+// of every qubit P touches, key bit i = position i, :115-147); a bucket
+// anticommutes iff its pattern does (commutation only sees the support), and
+// every anticommuting bucket yields one new-term stream when sin != 0.
+// Distinct patterns: a device bitmap over all 2^(2w) patterns for w <= 11
+// support qubits, else an open-addressing hash set of 64-bit patterns.
+struct SupportSpec {
+  int npos;
+  short word[64];  // device key word of position i
+  short bit[64];   // bit index in that word (LSB 0)
+};
+
+template <int B>
+__device__ __forceinline__ ull support_key(const Key<B>& k, const SupportSpec& sp) {
+  ull key = 0;
+  for (int i = 0; i < sp.npos; ++i) {
+    ull v = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * B; ++j) v = (j == sp.word[i]) ? k.w[j] : v;
+    key |= ((v >> sp.bit[i]) & 1ull) << i;
+  }
+  return key;
+}
+
+template <int B>
+__global__ void k_support_bitmap(const ull* __restrict__ keys, const double* __restrict__ coef, size_t M,
+                                 Filter filt, SupportSpec sp, unsigned* __restrict__ bitmap) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const Key<B> k = load_key<B>(keys, i);
+  if (!filter_keep(filt, i, coef[i], i == 0 && key_is_identity<B>(k))) return;
+  const ull key = support_key<B>(k, sp);
+  atomicOr(bitmap + (key >> 5), 1u << (key & 31));
+}
+
+template <int B>
+__global__ void k_support_hash(const ull* __restrict__ keys, const double* __restrict__ coef, size_t M,
+                               Filter filt, SupportSpec sp, ull* __restrict__ table, ull mask,
+                               ull anti_mask, ull* __restrict__ ctr) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const Key<B> k = load_key<B>(keys, i);
+  if (!filter_keep(filt, i, coef[i], i == 0 && key_is_identity<B>(k))) return;
+  const ull key = support_key<B>(k, sp);
+  const ull stored = key + 1;  // 0 marks an empty slot
+  ull h = (key * 0x9E3779B97F4A7C15ull) & mask;
+  for (;;) {
+    const ull prev = atomicCAS(table + h, 0ull, stored);
+    if (prev == 0ull) {  // first occurrence of the pattern
+      atomicAdd(ctr, 1ull);
+      if (__popcll(key & anti_mask) & 1) atomicAdd(ctr + 1, 1ull);
+      return;
+    }
+    if (prev == stored) return;
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void k_bitmap_count(const unsigned* __restrict__ bitmap, size_t words, ull anti_mask,
+                               ull* __restrict__ ctr) {
+  const size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  unsigned n = 0, a = 0;
+  if (w < words) {
+    unsigned v = bitmap[w];
+    n = __popc(v);
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1;
+      a += __popcll(((ull)w * 32 + b) & anti_mask) & 1;
+    }
+  }
+  n = __reduce_add_sync(0xffffffffu, n);
+  a = __reduce_add_sync(0xffffffffu, a);
+  if ((threadIdx.x & 31) == 0 && n) {
+    atomicAdd(ctr, (ull)n);
+    if (a) atomicAdd(ctr + 1, (ull)a);
+  }
+}
+
+void sortless_stats(DeviceStore& s, const uint64_t* gen_row, size_t* n_buckets, size_t* n_anti_buckets) {
+  // support positions in the reference's order (:115-128): for every qubit j
+  // of supp(P) ascending, x bit (position j) then z bit (position n + j)
+  const uint32_t B = s.B;
+  SupportSpec sp{};
+  ull anti = 0;
+  std::vector<int> qubits;
+  for (uint32_t blk = 0; blk < B; ++blk) {
+    const uint64_t b = gen_row[blk] | gen_row[B + blk];
+    for (int t = 0; t < 64; ++t)
+      if ((b >> t) & 1ull) qubits.push_back((int)(blk * 64 + t));
+  }
+  if (2 * qubits.size() > 64) throw std::runtime_error("entangler support exceeds 64 bits; not supported");
+  sp.npos = (int)(2 * qubits.size());
+  for (size_t k = 0; k < qubits.size(); ++k) {
+    const int j = qubits[k];
+    // device keys are bit-reversed words: qubit j of block j/64 sits at bit 63 - j%64
+    sp.word[2 * k] = (short)(j / 64);
+    sp.bit[2 * k] = (short)(63 - j % 64);
+    sp.word[2 * k + 1] = (short)(B + j / 64);
+    sp.bit[2 * k + 1] = (short)(63 - j % 64);
+    const bool px = (gen_row[j / 64] >> (j % 64)) & 1ull, pz = (gen_row[B + j / 64] >> (j % 64)) & 1ull;
+    // T anticommutes iff sum_j (tx_j pz_j + tz_j px_j) is odd
+    if (pz) anti |= 1ull << (2 * k);
+    if (px) anti |= 1ull << (2 * k + 1);
+  }
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  ull* ctr = ws.counters.as<ull>(16);
+  IQCC_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(ull), st));
+  const unsigned grid = (unsigned)std::max<size_t>(1, (s.M + 255) / 256);
+  KernelScope ks("sortless_stats");
+  if (sp.npos <= 22) {
+    const size_t words = std::max<size_t>(1, ((size_t)1 << sp.npos) / 32);
+    unsigned* bm = ws.misc2.as<unsigned>(words);
+    IQCC_CUDA(cudaMemsetAsync(bm, 0, words * sizeof(unsigned), st));
+    if (s.M) {
+      switch (B) {
+        case 1: k_support_bitmap<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, sp, bm); break;
+        case 2: k_support_bitmap<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, sp, bm); break;
+        default: k_support_bitmap<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, sp, bm); break;
+      }
+    }
+    k_bitmap_count<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(bm, words, anti, ctr);
+  } else {
+    size_t cap = 1024;
+    while (cap < 2 * s.M) cap <<= 1;
+    ull* table = ws.misc3.as<ull>(cap);
+    IQCC_CUDA(cudaMemsetAsync(table, 0, cap * sizeof(ull), st));
+    if (s.M) {
+      switch (B) {
+        case 1: k_support_hash<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, sp, table, cap - 1, anti, ctr); break;
+        case 2: k_support_hash<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, sp, table, cap - 1, anti, ctr); break;
+        default: k_support_hash<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, sp, table, cap - 1, anti, ctr); break;
+      }
+    }
+  }
+  ull h[2];
+  IQCC_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  host_sync(st);
+  *n_buckets = h[0];
+  *n_anti_buckets = h[1];
+}
+
 }  // namespace iqcc_b200

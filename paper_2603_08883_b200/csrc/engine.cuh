@@ -519,6 +519,9 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
                               size_t count_eps, bool want_stats, Reducer* red = nullptr,
                               const ull* glob_known = nullptr, double cand_floor = 0.0);
 void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* na);
+/// SortlessStats buckets (iqcc/dressing.hpp:159-189): distinct support
+/// patterns of the present terms, and how many of them anticommute.
+void sortless_stats(DeviceStore& s, const uint64_t* gen_row, size_t* n_buckets, size_t* n_anti_buckets);
 
 double expect_store(DeviceStore& s, const double* factors);
 double qmf_grad_store(DeviceStore& s, const double* factors, const double* derivs, double* grad);

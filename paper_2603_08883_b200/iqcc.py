@@ -452,10 +452,18 @@ def sortless_dress(h: PauliSum, op: DressOp, opts: MergeOptions = MergeOptions()
     support = sum(bin(int(op.generator.row[b]) | int(op.generator.row[B + b])).count("1") for b in range(B))
     if 2 * support > 64:
         raise RuntimeError("entangler support exceeds 64 bits; not supported")
-    out = dress_single(h, op, opts)
+    d = DeviceSum.upload(h)
     if stats is not None:
-        stats.new_stream_sorts = 0
-    return out
+        # support buckets and new-term streams (dressing.hpp:248-268) counted
+        # on the device; no product stream is ever sorted; the heap merge's
+        # comparison count has no device counterpart (0)
+        g = np.ascontiguousarray(op.generator.row, np.uint64)
+        nb, ns = C.c_size_t(), C.c_size_t()
+        check(lib.iqcc_gpu_sortless_stats(d.handle, _addr(g), math.sin(op.amplitude), C.byref(nb), C.byref(ns)))
+        stats.n_buckets, stats.new_term_streams = nb.value, ns.value
+        stats.new_stream_sorts, stats.merge_comparisons = 0, 0
+    d.dress(op.generator, op.amplitude, opts.drop_threshold)
+    return d.download()
 
 
 def dress_sequence(h: PauliSum, ansatz: Ansatz, epsilon: float, max_terms: int = U64_MAX,

@@ -74,6 +74,8 @@ _SIGS = {
     "iqcc_gpu_dress_sequence": (C.c_int, [_vp, C.c_size_t, _u64p, _f64p, _f64p, C.c_double, C.c_size_t,
                                           C.c_double, C.POINTER(CompressStatsC), C.POINTER(C.c_size_t)]),
     "iqcc_gpu_growth_split": (C.c_int, [_vp, _u64p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "iqcc_gpu_sortless_stats": (C.c_int, [_vp, _u64p, C.c_double, C.POINTER(C.c_size_t),
+                                          C.POINTER(C.c_size_t)]),
     "iqcc_gpu_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
     "iqcc_gpu_qmf_energy_gradient": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(C.c_double), _f64p]),
     "iqcc_gpu_qcc_energy": (C.c_int, [_vp, C.c_size_t, _u64p, _f64p, _f64p, _f64p, C.POINTER(C.c_double)]),

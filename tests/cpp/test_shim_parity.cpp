@@ -13,6 +13,7 @@
 #include "iqcc/dressing.hpp"
 #include "iqcc/io.hpp"
 #include "iqcc/optimizer.hpp"
+#include "iqcc/partition.hpp"
 #include "iqcc/pauli.hpp"
 #include "iqcc/qmf.hpp"
 #include "iqcc_b200/iqcc_gpu.hpp"
@@ -61,7 +62,11 @@ int main(int argc, char** argv) {
       auto h = rand_sum(rng, n, 12 * n);
       iqcc::DressOp op{rand_word(rng, n, false), amp(rng)};
       expect(iqcc::gpu::dress_single(h, op) == iqcc::dress_single(h, op), "dress_single/557", t);
-      expect(iqcc::gpu::sortless_dress(h, op) == iqcc::sortless_dress(h, op), "sortless_dress/557", t);
+      iqcc::SortlessStats sa, sb;
+      expect(iqcc::gpu::sortless_dress(h, op, {}, &sa) == iqcc::sortless_dress(h, op, {}, &sb), "sortless_dress/557", t);
+      expect(sa.n_buckets == sb.n_buckets && sa.new_term_streams == sb.new_term_streams &&
+                 sa.new_stream_sorts == sb.new_stream_sorts,
+             "sortless_stats/557", t);
     }
     std::printf("ok dress_single 120\n");
   }
@@ -157,6 +162,104 @@ int main(int argc, char** argv) {
       ++cases;
     }
     std::printf("ok build_poly_kernels %d\n", cases);
+  }
+  // parallel_dress with the reference's signature, tests/test_partition.cpp:180-208
+  // (seed 631): gathered sums AND message logs equal for every worker count
+  {
+    std::mt19937_64 rng(631);
+    std::uniform_real_distribution<double> amp(-3.0, 3.0);
+    int cases = 0;
+    for (int t = 0; t < 16; ++t) {
+      std::size_t n = 3 + t % 4;
+      auto h = rand_sum(rng, n, 25 * n);
+      iqcc::DressOp op{rand_word(rng, n, false), amp(rng)};
+      double eps = (t % 3 == 0) ? 1e-3 : 0.0;
+      std::size_t mt = (t % 4 == 0) ? 40 : 100000;
+      for (std::size_t workers : {1, 2, 4, 8}) {
+        const std::size_t m = workers == 1 ? 2 : 3;
+        auto ph = iqcc::distribute(h, iqcc::make_partition_map(h, m, workers));
+        iqcc::MessageLog la, lb;
+        iqcc::ParallelDressStats sa, sb;
+        auto a = iqcc::gpu::parallel_dress(ph, op, eps, mt, &la, iqcc::ExecutionMode::kThreaded, &sa);
+        auto b = iqcc::parallel_dress(ph, op, eps, mt, &lb, iqcc::ExecutionMode::kDeterministic, &sb);
+        expect(iqcc::gather(a) == iqcc::gather(b), "parallel_dress/631 gather", t);
+        bool shards_equal = a.shards.size() == b.shards.size();
+        for (std::size_t p = 0; shards_equal && p < a.shards.size(); ++p) shards_equal = a.shards[p] == b.shards[p];
+        expect(shards_equal, "parallel_dress/631 shards", t);
+        bool logs = la.records.size() == lb.records.size();
+        for (std::size_t i = 0; logs && i < la.records.size(); ++i)
+          logs = la.records[i].source == lb.records[i].source &&
+                 la.records[i].destination == lb.records[i].destination &&
+                 la.records[i].terms == lb.records[i].terms && la.records[i].bytes == lb.records[i].bytes;
+        expect(logs && la.total_bytes() == lb.total_bytes(), "parallel_dress/631 message log", t);
+        expect(sa.mask == sb.mask && sa.compress.dropped_terms == sb.compress.dropped_terms,
+               "parallel_dress/631 stats", t);
+        ++cases;
+      }
+    }
+    std::printf("ok parallel_dress %d\n", cases);
+  }
+  // parallel_expect + rebalance (tests/test_partition.cpp:257-309, seeds 647, 653)
+  {
+    std::mt19937_64 rng(647);
+    std::uniform_real_distribution<double> ang(-3.0, 3.0);
+    int cases = 0;
+    for (int t = 0; t < 8; ++t) {
+      auto h = rand_sum(rng, 6, 100);
+      iqcc::QmfState om(6);
+      for (std::size_t j = 0; j < 6; ++j) {
+        om.theta[j] = ang(rng);
+        om.phi[j] = ang(rng);
+      }
+      for (std::size_t workers : {1, 2, 4}) {
+        auto ph = iqcc::distribute(h, iqcc::make_partition_map(h, 3, workers));
+        const double a = iqcc::gpu::parallel_expect(ph, om), b = iqcc::parallel_expect(ph, om);
+        expect(std::fabs(a - b) <= 1e-10 * std::max(1.0, std::fabs(b)), "parallel_expect/647", t);
+        ++cases;
+      }
+    }
+    std::mt19937_64 rng2(653);
+    auto h = rand_sum(rng2, 6, 160);
+    iqcc::PartitionMap map;
+    map.n_qubits = 6;
+    map.partition_bits = {0, 1, 2};
+    map.n_workers = 4;
+    map.owner.assign(8, 0);
+    auto ph = iqcc::distribute(h, map);
+    iqcc::gpu::DevicePartitionedSum d(h, map);
+    expect(d.rebalance(1.5).owner == iqcc::rebalance(ph, 1.5).owner, "rebalance/653", 0);
+    expect(d.gather() == h, "rebalance/653 gather", 0);
+    std::printf("ok parallel_expect_rebalance %d\n", cases + 1);
+  }
+  // merge_sums, iqcc/pauli.hpp:383-415 (tests/test_pauli.cpp seed 37)
+  {
+    std::mt19937_64 rng(37);
+    for (int t = 0; t < 30; ++t) {
+      std::size_t n = 2 + t % 6;
+      auto a = rand_sum(rng, n, 40), b = rand_sum(rng, n, 40);
+      for (double drop : {1e-12, 0.0, 0.3}) {
+        iqcc::MergeOptions o;
+        o.drop_threshold = drop;
+        expect(iqcc::gpu::merge_sums(a, b, o) == iqcc::merge_sums(a, b, o), "merge_sums/37", t);
+      }
+    }
+    std::printf("ok merge_sums 90\n");
+  }
+  // dress_sequence forwards MergeOptions (iqcc/dressing.hpp:311-324)
+  {
+    std::mt19937_64 rng(29);
+    std::uniform_real_distribution<double> amp(-1.0, 1.0);
+    for (int t = 0; t < 12; ++t) {
+      std::size_t n = 4 + t % 5;
+      auto h = rand_sum(rng, n, 30 * n);
+      iqcc::Ansatz a;
+      for (int k = 0; k < 3; ++k) a.push(rand_word(rng, n, false), amp(rng));
+      iqcc::MergeOptions o;
+      o.drop_threshold = t % 2 ? 0.0 : 0.05;
+      expect(iqcc::gpu::dress_sequence(h, a, 0.0, 1000, nullptr, o) == iqcc::dress_sequence(h, a, 0.0, 1000, nullptr, o),
+             "dress_sequence merge options", t);
+    }
+    std::printf("ok dress_sequence_options 12\n");
   }
   // identity generator rejected with std::invalid_argument
   {

@@ -107,6 +107,8 @@ def test_sortless_equals_dress_single(eng, port):  # test_dressing.cpp:177-196 (
         d = eng.sortless_dress(host(eng, h), eng.DressOp(eng.PauliWord(n, g), tau), stats=st)
         assert st.new_stream_sorts == 0
         assert digest(d.rows, d.coeffs) == g_sha[t]  # reference output (golden)
+        _, ref_st = port.sortless_dress(h, g, tau)  # bucket count of bucket_by_support
+        assert st.n_buckets == ref_st["n_buckets"]
 
 
 def test_growth_bound(eng, port):  # test_dressing.cpp:241-252 (seed 563)
