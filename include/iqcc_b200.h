@@ -89,6 +89,24 @@ int iqcc_gpu_sum_download_device(iqcc_gpu_sum* h, uint64_t* d_rows, double* d_co
  * B' in {1,2,4}; raw coefficients incl. dead-slot NaNs) to host buffers. */
 int iqcc_gpu_sum_raw(iqcc_gpu_sum* h, uint64_t* keys, double* coeff, size_t cap, size_t* M);
 
+/* ---- Pauli text files and the FCIDUMP ingest (iqcc/io.hpp) ------------- */
+/* parse_pauli_file (io.hpp:31-87): '#' comments, `# qubits: N`, one
+ * `<coefficient> <letters>` term per line (qubit 0 leftmost); the same
+ * grammar and "path:line: ..." errors (IQCC_ERUNTIME).  Letters become rows
+ * on the device; duplicates are combined on the device (from_terms,
+ * pauli.hpp:302-326, drop 1e-12) in file order. */
+int iqcc_gpu_read_pauli_file(const char* path, iqcc_gpu_sum** out);
+/* write_pauli_file (io.hpp:90-101): "# qubits: N" then "%.17g <letters>" in
+ * canonical order; letter strings rendered on the device chunk by chunk
+ * while the host writes the previous chunk. */
+int iqcc_gpu_write_pauli_file(iqcc_gpu_sum* h, const char* path);
+/* jordan_wigner(read_fcidump(path)) (io.hpp:154-276): integrals parsed on the
+ * host, the ladder-operator expansion and from_terms on the device.
+ * *n_electrons (nullable) receives NELEC.  Equal words are combined in
+ * emission order (the reference's std::sort leaves that order unspecified:
+ * a word with >= 3 contributions may differ in its last bits). */
+int iqcc_gpu_jordan_wigner_fcidump(const char* path, size_t* n_electrons, iqcc_gpu_sum** out);
+
 /* ---- dressing (iqcc/dressing.hpp) ------------------------------------- */
 typedef struct {
   size_t n_in;             /* logical terms before the step */

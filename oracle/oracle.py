@@ -126,6 +126,8 @@ class Oracle:
             sig.update({
                 "orc_ref_jordan_wigner_fcidump": (_vp, [C.c_char_p, _szp]),
                 "orc_ref_ground_energy": (C.c_double, [_vp]),
+                "orc_ref_parse_pauli_file": (_vp, [C.c_char_p]),
+                "orc_ref_write_pauli_file": (C.c_int, [_vp, C.c_char_p]),
                 "orc_ref_iqcc_iteration": (_vp, [_vp, _f64p, _f64p, C.c_size_t, C.c_double, C.c_size_t,
                                                  _u64p, _f64p, _szp, _f64p]),
             })
@@ -351,6 +353,13 @@ class Oracle:
         ne = C.c_size_t(0)
         h = self._wrap(self.lib.orc_ref_jordan_wigner_fcidump(path.encode(), C.byref(ne)))
         return h, ne.value
+
+    def parse_pauli_file(self, path):
+        return self._wrap(self.lib.orc_ref_parse_pauli_file(path.encode()))
+
+    def write_pauli_file(self, h, path):
+        if self.lib.orc_ref_write_pauli_file(h.handle, path.encode()) != 0:
+            self._raise()
 
     def ground_energy(self, h):
         return self.lib.orc_ref_ground_energy(h.handle)

@@ -426,6 +426,17 @@ orc_sum* orc_ref_jordan_wigner_fcidump(const char* path, size_t* n_electrons) {
   }, nullptr);
 }
 
+orc_sum* orc_ref_parse_pauli_file(const char* path) {
+  return guard([&]() -> orc_sum* { return box(iqcc::parse_pauli_file(path)); }, nullptr);
+}
+
+int orc_ref_write_pauli_file(const orc_sum* h, const char* path) {
+  return guard([&]() -> int {
+    iqcc::write_pauli_file(h->h, path);
+    return 0;
+  }, -1);
+}
+
 double orc_ref_ground_energy(const orc_sum* h) {
   return guard([&]() -> double { return iqcc::oracle::ground_energy(h->h); }, 0.0);
 }

@@ -542,6 +542,35 @@ int iqcc_gpu_sum_generate_mol(size_t n_qubits, size_t n_terms, uint64_t seed, iq
   });
 }
 
+int iqcc_gpu_read_pauli_file(const char* path, iqcc_gpu_sum** out) {
+  return guarded([&] {
+    ctx();
+    if (!path || !out) throw std::invalid_argument("read_pauli_file: null argument");
+    auto h = std::make_unique<iqcc_gpu_sum>();
+    store_read_pauli_file(h->s, path);
+    *out = h.release();
+  });
+}
+
+int iqcc_gpu_write_pauli_file(iqcc_gpu_sum* h, const char* path) {
+  return guarded([&] {
+    need(h);
+    if (!path) throw std::invalid_argument("write_pauli_file: null path");
+    store_write_pauli_file(h->s, path);
+  });
+}
+
+int iqcc_gpu_jordan_wigner_fcidump(const char* path, size_t* n_electrons, iqcc_gpu_sum** out) {
+  return guarded([&] {
+    ctx();
+    if (!path || !out) throw std::invalid_argument("jordan_wigner_fcidump: null argument");
+    auto h = std::make_unique<iqcc_gpu_sum>();
+    const size_t ne = store_jordan_wigner_fcidump(h->s, path);
+    if (n_electrons) *n_electrons = ne;
+    *out = h.release();
+  });
+}
+
 int iqcc_gpu_sum_clone(const iqcc_gpu_sum* h, iqcc_gpu_sum** out) {
   return guarded([&] {
     need(h);

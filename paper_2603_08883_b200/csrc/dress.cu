@@ -883,8 +883,11 @@ struct MergeCfg {
   static constexpr int CAP = TILE + 8;  // tiles absorb short runs of equal survivors
   static constexpr size_t KEYB = (size_t)CAP * 16 * B;
   // one input stage: survivor rows [0,nS) then product rows [nS, nS+nQ);
-  // S coefs [coff, coff+nS), Q coefs [nS+4, ...)
-  static constexpr size_t STAGE = (KEYB + (size_t)(CAP + 4) * 8 + 127) & ~(size_t)127;
+  // S coefs [coff, coff+nS), Q coefs [nS+4, ...); then the tile's plan bit
+  // words (pmask, fmask, product slots; BW words each) fetched with the rows
+  static constexpr int BW = (CAP + 31) / 32 + 3;
+  static constexpr size_t OFF_SBITS = KEYB + (size_t)(CAP + 4) * 8;
+  static constexpr size_t STAGE = (OFF_SBITS + (size_t)3 * BW * 4 + 127) & ~(size_t)127;
   static constexpr size_t OFF_OUTV = 2 * STAGE;
   static constexpr size_t OFF_OUTE = OFF_OUTV + (size_t)CAP * 8;
   static constexpr size_t OFF_TA = (OFF_OUTE + (size_t)CAP * 2 + 15) & ~(size_t)15;
@@ -952,9 +955,13 @@ struct MergeArgs {
 /// Issue the loads of one tile into one stage: survivors by the TMA bulk
 /// engine (thread 0, completion on *mb), products by per-thread cp.async
 /// gathers (one commit group).
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+
 template <int B, int NT>
 __device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull* sk, double* sc,
-                                            unsigned long long* mb) {
+                                            unsigned long long* mb, unsigned* sbits = nullptr, int BW = 0) {
   const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
   const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
   const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0);
@@ -985,6 +992,16 @@ __device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull
       cp_async8(sc + qc0 + j, g.coef + src);
     }
   }
+  if (sbits) {  // the tile's plan bit words ride along (no dependent load after the wait)
+    const size_t pw0 = a0 >> 5, qw0 = b0 >> 5;
+    const int npw = (int)(((a1 + 31) >> 5) - pw0) + 1, nqw = (int)(((b1 + 31) >> 5) - qw0) + 1;
+    for (int w = threadIdx.x; w < npw; w += NT) {
+      cp_async4(sbits + w, g.pmask + pw0 + w);
+      cp_async4(sbits + BW + w, g.fmask + pw0 + w);
+    }
+    if (g.qbits)
+      for (int w = threadIdx.x; w < nqw; w += NT) cp_async4(sbits + 2 * BW + w, g.qbits + qw0 + w);
+  }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
@@ -993,10 +1010,25 @@ __device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull
 // the combined value into the survivor's slot and a dead slot after it;
 // a value failing keep_term leaves a dead slot.  So the tile's output
 // offset is present_before(a0) + b0, known before the tile runs.
+struct TileBounds {
+  size_t a0, a1, b0, b1, o0, o1;
+};
+/// Plan bits of one tile staged in shared memory by the pipelined merge:
+/// pm/fm hold pmask/fmask words from word pw0 on, qb the product slot words
+/// from qw0 on.
+struct StagedBits {
+  const unsigned* pm;
+  const unsigned* fm;
+  const unsigned* qb;
+  size_t pw0, qw0;
+};
+
 template <int B, int NT, int IPT>
 __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, const Key<B>& P,
                                               ull* sk, double* sc, unsigned char* smem_raw,
-                                              int& n_eps, int& n_dead, int& n_coll, int& n_ge) {
+                                              int& n_eps, int& n_dead, int& n_coll, int& n_ge,
+                                              const TileBounds* tbp = nullptr,
+                                              const StagedBits* sb = nullptr) {
   using Cfg = MergeCfg<B, NT, IPT>;
   double* outv = reinterpret_cast<double*>(smem_raw + Cfg::OFF_OUTV);
   unsigned short* oute = reinterpret_cast<unsigned short*>(smem_raw + Cfg::OFF_OUTE);
@@ -1009,13 +1041,19 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   unsigned* sqp = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_QP);
   unsigned* sam = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_AM);
   unsigned* shist = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_HIST);
-  const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
-  const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
-  const size_t o0 = g.part_o[tile], o1 = g.part_o[tile + 1];
+  const TileBounds tb = tbp ? *tbp
+                            : TileBounds{g.part_a[tile], g.part_a[tile + 1], g.part_b[tile],
+                                         g.part_b[tile + 1], g.part_o[tile], g.part_o[tile + 1]};
+  const size_t a0 = tb.a0, a1 = tb.a1, b0 = tb.b0, b1 = tb.b1, o0 = tb.o0, o1 = tb.o1;
   const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0), n = nS + nQ;
   const int nslots = (int)(o1 - o0);
   const int coff = (int)(a0 & 1);
   const int qc0 = nS + 4;
+  // plan bits: global, or the tile's words staged in shared memory (indexed
+  // through a base shifted by the first staged word)
+  const unsigned* PMASK = sb ? sb->pm - sb->pw0 : g.pmask;
+  const unsigned* FMASK = sb ? sb->fm - sb->pw0 : g.fmask;
+  const unsigned* QBITS = g.qbits ? (sb ? sb->qb - sb->qw0 : g.qbits) : nullptr;
 
   // survivor bits from the plan: slot (pmask, also "present": see MergeArgs)
   // and present & anticommuting (fmask); slot bits of the products
@@ -1029,17 +1067,17 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
     for (int w = threadIdx.x; w < (nS + 31) >> 5; w += NT) {
       const size_t gb = a0 + (size_t)w * 32;
       const int rem = nS - w * 32;
-      const unsigned sl = bits_at(g.pmask, gb, rem);
+      const unsigned sl = bits_at(PMASK, gb, rem);
       spm[w] = sl;
       ssm[w] = sl;
-      sam[w] = bits_at(g.fmask, gb, rem);
+      sam[w] = bits_at(FMASK, gb, rem);
     }
-    if (g.qbits)
+    if (QBITS)
       for (int w = threadIdx.x; w < (nQ + 31) >> 5; w += NT) {
         const size_t gb = b0 + (size_t)w * 32;
         const unsigned sh = (unsigned)(gb & 31);
-        unsigned x = g.qbits[gb >> 5] >> sh;
-        if (sh) x |= g.qbits[(gb >> 5) + 1] << (32 - sh);
+        unsigned x = QBITS[gb >> 5] >> sh;
+        if (sh) x |= QBITS[(gb >> 5) + 1] << (32 - sh);
         const int rem = nQ - w * 32;
         if (rem < 32) x &= (1u << rem) - 1u;
         sqm[w] = x;
@@ -1273,14 +1311,18 @@ __global__ void __launch_bounds__(NT, merge_minb(B, NT)) k_merge1(MergeArgs g, K
   __syncthreads();
   ull* sk = reinterpret_cast<ull*>(smem_raw);
   double* sc = reinterpret_cast<double*>(smem_raw + Cfg::KEYB);
-  merge_issue<B, NT>(g, tile, sk, sc, &mbar);
+  unsigned* sbits = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_SBITS);
+  const TileBounds tb{g.part_a[tile], g.part_a[tile + 1], g.part_b[tile],
+                      g.part_b[tile + 1], g.part_o[tile], g.part_o[tile + 1]};
+  merge_issue<B, NT>(g, tile, sk, sc, &mbar, sbits, Cfg::BW);
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  if (g.part_a[tile + 1] > g.part_a[tile]) mbar_wait(&mbar, 0);
+  if (tb.a1 > tb.a0) mbar_wait(&mbar, 0);
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar)) : "memory");
   int n_eps = 0, n_dead = 0, n_coll = 0, n_ge = 0;
+  const StagedBits sb{sbits, sbits + Cfg::BW, sbits + 2 * Cfg::BW, tb.a0 >> 5, tb.b0 >> 5};
   // shared layout past the single stage is shifted down by one STAGE
-  merge_compute<B, NT, IPT>(g, tile, P, sk, sc, smem_raw - Cfg::STAGE, n_eps, n_dead, n_coll, n_ge);
+  merge_compute<B, NT, IPT>(g, tile, P, sk, sc, smem_raw - Cfg::STAGE, n_eps, n_dead, n_coll, n_ge, &tb, &sb);
   merge_flush<B, NT>(g, shist, n_eps, n_dead, n_coll, n_ge, s_cnt);
 }
 
@@ -1326,6 +1368,178 @@ __global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PMERGE_MINB) * 256 / NT
     merge_compute<B, NT, IPT>(g, tile, P, stage_k(cur), stage_c(cur), smem_raw, n_eps, n_dead, n_coll, n_ge);
     __syncthreads();  // stage `cur` and the staging list are free again
   }
+  merge_flush<B, NT>(g, shist, n_eps, n_dead, n_coll, n_ge, s_cnt);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[0])) : "memory");
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[1])) : "memory");
+  }
+}
+
+// ---------------------------------------------------------- pipelined merge
+// Persistent CTAs walk tiles blockIdx.x, +gridDim.x, ... with every global
+// dependency of a tile issued ahead of its merge, so a CTA never waits on
+// memory between tiles:
+//   tile k+3: merge-path bounds loaded into registers (parked in a 3-slot
+//             shared ring after the merge of tile k)
+//   tile k+2: inv_perm slice fetched into shared memory by cp.async
+//   tile k+1: survivors by TMA bulk copy (mbarrier), products gathered by
+//             cp.async through the staged inv_perm, plan bit words by cp.async
+//   tile k  : merged from shared memory (merge_compute)
+// The |c| histogram and the counters are flushed once per CTA.
+template <int B, int NT, int IPT>
+struct PipeCfg {
+  using M = MergeCfg<B, NT, IPT>;
+  static constexpr int BW = M::PMW + 3;  // staged plan words per mask (a shifted window + 1)
+  static constexpr size_t STAGE = (M::KEYB + (size_t)(M::CAP + 4) * 8 + (size_t)3 * BW * 4 + 127) & ~(size_t)127;
+  static constexpr size_t OFF_BITS = M::KEYB + (size_t)(M::CAP + 4) * 8;  // within a stage
+  static constexpr int IDXW = M::CAP + 8;  // staged inv_perm words per slot
+  static constexpr size_t OFF_IDX = 2 * STAGE;
+  static constexpr size_t OFF_REST = (OFF_IDX + (size_t)2 * IDXW * 4 + 127) & ~(size_t)127;
+  // merge_compute's layout (outv ...) starts at OFF_REST: it addresses it as
+  // smem_raw + M::OFF_OUTV with smem_raw shifted by OFF_REST - M::OFF_OUTV
+  static constexpr size_t bytes(bool hist) {
+    return OFF_REST + (M::OFF_HIST - M::OFF_OUTV) + (hist ? M::HBINS * 4 : 0);
+  }
+};
+
+#ifndef IQCC_PIPE_MINB
+#define IQCC_PIPE_MINB 4
+#endif
+template <int B, int NT, int IPT>
+__global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PIPE_MINB) * 256 / NT) k_merge_pipe(MergeArgs g, Key<B> P) {
+  using Cfg = PipeCfg<B, NT, IPT>;
+  using M = MergeCfg<B, NT, IPT>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* rest = smem_raw + Cfg::OFF_REST - M::OFF_OUTV;  // merge_compute's base
+  unsigned* shist = reinterpret_cast<unsigned*>(rest + M::OFF_HIST);
+  __shared__ __align__(8) unsigned long long mbar[2];
+  __shared__ int s_cnt[4];
+  __shared__ TileBounds s_tb[3];
+  auto stage = [&](int st) { return smem_raw + st * Cfg::STAGE; };
+  auto idx_slot = [&](int sl) { return reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_IDX) + sl * Cfg::IDXW; };
+  const size_t G = gridDim.x;
+  const size_t t0 = blockIdx.x;
+  auto tile_of = [&](size_t k) { return t0 + k * G; };
+  auto load_bounds = [&](size_t t, ull* r) {  // threads 0..5: one bound each
+    const int i = threadIdx.x;
+    if (t < g.ntiles && i < 6) {
+      const ull* src = i < 2 ? g.part_a : (i < 4 ? g.part_b : g.part_o);
+      r[0] = src[t + (i & 1)];
+    }
+  };
+  auto park_bounds = [&](int slot, ull v) {
+    if (threadIdx.x < 6) reinterpret_cast<size_t*>(&s_tb[slot])[threadIdx.x] = (size_t)v;
+  };
+  // inv_perm[b0, b1) -> idx slot (16-byte aligned superset; local products only)
+  auto issue_idx = [&](size_t t, int slot) {
+    if (t >= g.ntiles || g.q_keys) return;
+    const TileBounds& tb = s_tb[(t - t0) / G % 3];
+    const size_t e0 = tb.b0 & ~(size_t)3, e1 = (tb.b1 + 3) & ~(size_t)3;
+    unsigned* dst = idx_slot(slot);
+    for (size_t j = threadIdx.x; j < (e1 - e0) / 4; j += NT) cp_async16(dst + 4 * j, g.inv_perm + e0 + 4 * j);
+  };
+  // survivors (TMA), products (cp.async gathers through the staged idx), plan bits
+  auto issue_data = [&](size_t t, int st, int slot) {
+    if (t >= g.ntiles) return;
+    const TileBounds& tb = s_tb[(t - t0) / G % 3];
+    unsigned char* base = stage(st);
+    ull* sk = reinterpret_cast<ull*>(base);
+    double* sc = reinterpret_cast<double*>(base + M::KEYB);
+    unsigned* bits = reinterpret_cast<unsigned*>(base + Cfg::OFF_BITS);
+    const int nS = (int)(tb.a1 - tb.a0), nQ = (int)(tb.b1 - tb.b0);
+    if (threadIdx.x == 0 && nS > 0) {
+      const unsigned kb = (unsigned)nS * 16u * B;
+      const size_t c0 = tb.a0 & ~(size_t)1, c1 = (tb.a1 + 1) & ~(size_t)1;
+      const unsigned cb = (unsigned)((c1 - c0) * 8);
+      mbar_expect_tx(&mbar[st], kb + cb);
+      bulk_g2s(sk, g.keys + tb.a0 * 2 * B, kb, &mbar[st]);
+      bulk_g2s(sc, g.coef + c0, cb, &mbar[st]);
+    }
+    const int qc0 = nS + 4;
+    if (g.q_keys) {
+      for (int j = threadIdx.x; j < nQ; j += NT) {
+        const ull* gk = g.q_keys + (tb.b0 + j) * 2 * B;
+        ull* d = sk + (size_t)(nS + j) * 2 * B;
+#pragma unroll
+        for (int h = 0; h < B; ++h) cp_async16(d + 2 * h, gk + 2 * h);
+        cp_async8(sc + qc0 + j, g.q_vals + tb.b0 + j);
+      }
+    } else {
+      const unsigned* ix = idx_slot(slot) + (tb.b0 & 3);
+      for (int j = threadIdx.x; j < nQ; j += NT) {
+        const size_t src = ix[j];
+        const ull* gk = g.keys + src * 2 * B;
+        ull* d = sk + (size_t)(nS + j) * 2 * B;
+#pragma unroll
+        for (int h = 0; h < B; ++h) cp_async16(d + 2 * h, gk + 2 * h);
+        cp_async8(sc + qc0 + j, g.coef + src);
+      }
+    }
+    // plan bit words: pmask/fmask from word a0/32 on, product slot words from b0/32 on
+    const size_t pw0 = tb.a0 >> 5, qw0 = tb.b0 >> 5;
+    const int npw = (int)(((tb.a1 + 31) >> 5) - pw0) + 1, nqw = (int)(((tb.b1 + 31) >> 5) - qw0) + 1;
+    for (int w = threadIdx.x; w < npw; w += NT) {
+      cp_async4(bits + w, g.pmask + pw0 + w);
+      cp_async4(bits + Cfg::BW + w, g.fmask + pw0 + w);
+    }
+    if (g.qbits)
+      for (int w = threadIdx.x; w < nqw; w += NT) cp_async4(bits + 2 * Cfg::BW + w, g.qbits + qw0 + w);
+  };
+  auto commit = [] { asm volatile("cp.async.commit_group;\n" ::: "memory"); };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
+  }
+  if (g.want_hist)
+    for (int b = threadIdx.x; b < M::HBINS; b += NT) shist[b] = 0;
+  // prologue: bounds of tiles 0..2 (0, 1 parked, 2 in registers), idx of
+  // tile 0 (waited), data of tile 0, idx of tile 1
+  ull r0 = 0, r1 = 0, rn = 0;
+  load_bounds(tile_of(0), &r0);
+  load_bounds(tile_of(1), &r1);
+  load_bounds(tile_of(2), &rn);
+  park_bounds(0, r0);
+  park_bounds(1, r1);
+  __syncthreads();
+  issue_idx(tile_of(0), 0);
+  commit();
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  issue_data(tile_of(0), 0, 0);
+  commit();
+  issue_idx(tile_of(1), 1);
+  commit();
+  unsigned phase[2] = {0u, 0u};
+  int n_eps = 0, n_dead = 0, n_coll = 0, n_ge = 0;
+  for (size_t k = 0; tile_of(k) < g.ntiles; ++k) {
+    const int cur = (int)(k & 1);
+    const size_t t = tile_of(k);
+    // data(k) and idx(k+1) landed; bounds(k+2) parked by the previous iteration
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    const TileBounds tb = s_tb[k % 3];
+    if (tb.a1 > tb.a0) {
+      mbar_wait(&mbar[cur], phase[cur]);
+      phase[cur] ^= 1u;
+    }
+    if (k == 0) park_bounds(2, rn);
+    __syncthreads();
+    issue_data(tile_of(k + 1), cur ^ 1, (int)((k + 1) & 1));
+    commit();
+    issue_idx(tile_of(k + 2), cur);  // the slot of idx(k), consumed by data(k)
+    commit();
+    ull rb = 0;
+    load_bounds(tile_of(k + 3), &rb);  // lands while tile k is merged
+    unsigned char* base = stage(cur);
+    const unsigned* bits = reinterpret_cast<const unsigned*>(base + Cfg::OFF_BITS);
+    const StagedBits sb{bits, bits + Cfg::BW, bits + 2 * Cfg::BW, tb.a0 >> 5, tb.b0 >> 5};
+    merge_compute<B, NT, IPT>(g, t, P, reinterpret_cast<ull*>(base), reinterpret_cast<double*>(base + M::KEYB),
+                              rest, n_eps, n_dead, n_coll, n_ge, &tb, &sb);
+    __syncthreads();  // stage cur, the staging list and the ring slot k % 3 are free
+    park_bounds((int)(k % 3), rb);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   merge_flush<B, NT>(g, shist, n_eps, n_dead, n_coll, n_ge, s_cnt);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[0])) : "memory");
@@ -1464,7 +1678,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
     long long* g_bwd = g_fwd + ngroups * kThrPerChunk;
     long long* a_total = g_bwd + ngroups * kThrPerChunk;
     int* rdelta = nch > 1 ? ws.rdelta.as<int>(M) : nullptr;
-    pl.inv_perm = ws.inv_perm.as<unsigned>(M);
+    pl.inv_perm = ws.inv_perm.as<unsigned>(M + 8);  // +8: the pipelined merge fetches 16-byte groups
     // product slot flags in rank order (only when some products lose their slot)
     unsigned char* qflag = rule.thq != 0.0 ? ws.qflag.as<unsigned char>(M + 64) : nullptr;
     ull* dbg = debug_buffer();
@@ -1664,7 +1878,27 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     for (int w = 0; w < 2 * B; ++w) g.pn[w] = PN->w[w];
   }
   static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
-  if (persistent) {
+  static const bool pipelined = getenv("IQCC_MERGE_PIPE") != nullptr && atoi(getenv("IQCC_MERGE_PIPE")) != 0;
+  if (pipelined) {
+    using PC = PipeCfg<B, NT, IPT>;
+    static int ctas_per_sm = 0, n_sm = 0;
+    const int dev = ctx_device(ctx_current());
+    if (func_attr_once((const void*)k_merge_pipe<B, NT, IPT>, dev)) {
+      IQCC_CUDA(cudaFuncSetAttribute(k_merge_pipe<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)PC::bytes(true)));
+      IQCC_CUDA(cudaFuncSetAttribute(k_merge_pipe<B, NT, IPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared));
+    }
+    if (!ctas_per_sm) {
+      IQCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_merge_pipe<B, NT, IPT>, NT,
+                                                              PC::bytes(true)));
+      IQCC_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+      ctas_per_sm = std::max(ctas_per_sm, 1);
+    }
+    KernelScope ks("merge");
+    const unsigned grid = (unsigned)std::min<size_t>(ntm, (size_t)n_sm * ctas_per_sm);
+    k_merge_pipe<B, NT, IPT><<<grid, NT, PC::bytes(want_hist), st>>>(g, P);
+  } else if (persistent) {
     static int ctas_per_sm = 0, n_sm = 0;
     if (func_attr_once((const void*)k_merge<B, NT, IPT>, ctx_device(ctx_current())))
       IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -436,6 +436,10 @@ size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap,
 void store_generate_mol(DeviceStore& s, size_t n_qubits, size_t n_terms, uint64_t seed);
 void store_materialize(DeviceStore& s);
 void store_clone(const DeviceStore& src, DeviceStore& dst);
+/// Pauli text I/O and the FCIDUMP -> JW ingest (io.cu, iqcc/io.hpp).
+void store_read_pauli_file(DeviceStore& s, const std::string& path);
+void store_write_pauli_file(DeviceStore& s, const std::string& path);
+size_t store_jordan_wigner_fcidump(DeviceStore& s, const std::string& path);
 
 struct DressOutcome {
   size_t n_anticommuting = 0;

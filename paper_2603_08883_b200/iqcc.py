@@ -571,6 +571,42 @@ def _dis_on(d: "DeviceSum", omega: QmfState, top_k: int, opts: DisOptions) -> li
 DeviceSum.dis_candidates = lambda self, omega, top_k, opts=DisOptions(): _dis_on(self, omega, top_k, opts)
 
 
+# ------------------------------------------- Pauli text files, FCIDUMP ingest
+def _device_of(out: C.c_void_p, n_qubits_hint: int = 0) -> DeviceSum:
+    n = C.c_size_t()
+    check(lib.iqcc_gpu_sum_qubits(out, C.byref(n)))
+    return DeviceSum(out.value, n.value)
+
+
+def read_pauli_file_device(path: str) -> DeviceSum:
+    """parse_pauli_file (iqcc/io.hpp:31-87) into a device sum."""
+    native.init()
+    out = C.c_void_p()
+    check(lib.iqcc_gpu_read_pauli_file(str(path).encode(), C.byref(out)))
+    return _device_of(out)
+
+
+def parse_pauli_file(path: str) -> PauliSum:
+    """iqcc/io.hpp:31-87: same grammar and "path:line: ..." errors (RuntimeError)."""
+    return read_pauli_file_device(path).download()
+
+
+def write_pauli_file(h, path: str) -> None:
+    """iqcc/io.hpp:90-101 ("# qubits: N", then "%.17g <letters>" per term)."""
+    d = h if isinstance(h, DeviceSum) else DeviceSum.upload(h)
+    check(lib.iqcc_gpu_write_pauli_file(d.handle, str(path).encode()))
+
+
+def jordan_wigner_fcidump(path: str, device: bool = False):
+    """jordan_wigner(read_fcidump(path)) (iqcc/io.hpp:154-276) built on the
+    device; returns (sum, n_electrons) (a DeviceSum when device=True)."""
+    native.init()
+    out, ne = C.c_void_p(), C.c_size_t()
+    check(lib.iqcc_gpu_jordan_wigner_fcidump(str(path).encode(), C.byref(ne), C.byref(out)))
+    d = _device_of(out)
+    return (d if device else d.download()), ne.value
+
+
 def choose_partition_bits(h, m: int):
     """iqcc/partition.hpp:52-108 on the device; returns (bits, imbalance)."""
     d = h if isinstance(h, DeviceSum) else DeviceSum.upload(h)

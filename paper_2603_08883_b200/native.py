@@ -63,6 +63,9 @@ _SIGS = {
     "iqcc_gpu_sum_create_device": (C.c_int, [C.c_size_t, _u64p, _f64p, C.c_size_t, C.POINTER(_vp)]),
     "iqcc_gpu_sum_generate_mol": (C.c_int, [C.c_size_t, C.c_size_t, C.c_uint64, C.POINTER(_vp)]),
     "iqcc_gpu_sum_clone": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "iqcc_gpu_read_pauli_file": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "iqcc_gpu_write_pauli_file": (C.c_int, [_vp, C.c_char_p]),
+    "iqcc_gpu_jordan_wigner_fcidump": (C.c_int, [C.c_char_p, C.POINTER(C.c_size_t), C.POINTER(_vp)]),
     "iqcc_gpu_sum_destroy": (C.c_int, [_vp]),
     "iqcc_gpu_sum_qubits": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_sum_size": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),

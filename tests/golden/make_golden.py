@@ -17,6 +17,11 @@ c1_<name>.npz   SURVEY.md §8(d) config C1: the Jordan-Wigner Hamiltonian of
                 dressed sum is stored in full.
 small.npz       random cases from the reference test seeds (dress_single,
                 compress, dress_sequence outputs with checksums).
+io.npz + io_*.txt / fcidump_*.txt   iqcc/io.hpp fixtures: a Pauli text file
+                written by the reference's write_pauli_file, a hand-made one with
+                comments, blank lines and duplicate words, two synthetic FCIDUMPs
+                (random integrals with the 8-fold symmetry, made here), and the
+                reference's parse_pauli_file / jordan_wigner(read_fcidump) results.
 c2.npz          SURVEY.md §8(d) config C2 at full size: G_uniform(64, 1e6,
                 seed 1) dressed by one weight-4 entangler at tau = 0.37 (drop
                 1e-12), then compress(1e-3) and compress(0, max_terms=1.2e6);
@@ -170,15 +175,68 @@ def c2(ref):
     print("c2", {k: v for k, v in out.items() if k.startswith("n_")})
 
 
+def synthetic_fcidump(path, norb, nelec, seed):
+    """Random real integrals with h symmetric and (pq|rs) 8-fold symmetric,
+    each unique element written once (FCIDUMP convention)."""
+    rs = np.random.default_rng(seed)
+    lines = [f" &FCI NORB={norb},NELEC={nelec},MS2=0,", "  ORBSYM=" + "1," * norb, "  ISYM=1,", " &END"]
+    for i in range(1, norb + 1):
+        for j in range(1, i + 1):
+            for k in range(1, norb + 1):
+                for l in range(1, k + 1):
+                    if (i * (i - 1) // 2 + j) < (k * (k - 1) // 2 + l):
+                        continue
+                    if rs.random() < 0.3:
+                        continue  # sparse, like real integral files
+                    lines.append(f"{rs.normal(0, 0.3):.16e} {i} {j} {k} {l}")
+    for i in range(1, norb + 1):
+        for j in range(1, i + 1):
+            lines.append(f"{rs.normal(0, 1.0):.16e} {i} {j} 0 0")
+    lines.append(f"{rs.normal(0, 1.0):.16e} 0 0 0 0")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+def io_fixtures(ref):
+    out = {}
+    h = ref.rng(71).sum(10, 300)
+    p1 = os.path.join(HERE, "io_sum10.txt")
+    ref.write_pauli_file(h, p1)
+    out["sha_sum10"] = digest(*h.export())
+    out["n_sum10"] = len(h)
+    p2 = os.path.join(HERE, "io_dups.txt")
+    with open(p2, "w") as f:
+        f.write("# a hand-made Pauli file\n# qubits: 6\n\n"
+                "0.5 XXIIZZ\n-0.25 IIIIII\n  1e-13 ZZZZZZ\n0.125 XXIIZZ\n"
+                "# duplicates merge (0.5 + 0.125), 1e-13 < 1e-12 is dropped\n"
+                "3 YIYIYI\n-3 YIYIYI\n0.75 IIIIIX\n")
+    d = ref.parse_pauli_file(p2)
+    out["rows_dups"], out["coeffs_dups"] = d.export()
+    r = ref.parse_pauli_file(p1)
+    out["sha_sum10_parsed"] = digest(*r.export())
+    for name, norb, ne, seed in (("fcidump_4", 4, 2, 81), ("fcidump_6", 6, 4, 83)):
+        path = os.path.join(HERE, f"{name}.txt")
+        synthetic_fcidump(path, norb, ne, seed)
+        jw, nel = ref.jordan_wigner_fcidump(path)
+        out[f"rows_{name}"], out[f"coeffs_{name}"] = jw.export()
+        out[f"nelec_{name}"] = nel
+    np.savez_compressed(os.path.join(HERE, "io.npz"), **out)
+    print("io", {k: (v.shape if hasattr(v, "shape") else v) for k, v in out.items()})
+
+
 def main():
     ref = Oracle("reference")
     if "--c2" in sys.argv:
         c2(ref)
         return
+    if "--io" in sys.argv:
+        io_fixtures(ref)
+        return
     c1(ref, "h2_sto3g", 5, 1)
     c1(ref, "h2_ccpvdz", 5, 1)
     small(ref)
     c2(ref)
+    io_fixtures(ref)
 
 
 if __name__ == "__main__":

@@ -75,6 +75,14 @@ def main():
     for tt, pp in ((th, ph), (th2, ph)):
         om = iqcc.QmfState(tt, pp)
         kers.append(part.poly_kernels(d, om, iqcc.build_poly(ents, om, 2)))
+    # partitioned QMF energy/gradient and DIS gradients (allgather, rank order)
+    th3 = np.random.default_rng(9).uniform(-3, 3, n)
+    ph3 = np.random.default_rng(10).uniform(-3, 3, n)
+    om3 = iqcc.QmfState(th3, ph3)
+    e_qmf, g_qmf = part.qmf_energy_gradient(d, om3)
+    cands = np.stack(gens[:4])
+    g_dis = part.gradients(d, om3, cands)
+    g_dis_poles = part.gradients(d, iqcc.QmfState(th, ph), cands, flip_group_only=True)
     objs = [None] * world
     dist.all_gather_object(objs, (shard.rows, shard.coeffs, exch))
     if rank == 0:
@@ -94,6 +102,13 @@ def main():
             _, _, hc, nc, _ = port.poly_kernels(h, tt, ph, np.stack(gens[:3]), 2)
             scale = max(1e-300, np.abs(hc).max())
             e_ok = e_ok and np.abs(ker.h_kernel - hc).max() <= 1e-12 * scale and np.array_equal(ker.n_kernel, nc)
+        e1, g1 = port.qmf_energy_gradient(h, th3, ph3)
+        e_ok = e_ok and abs(e_qmf - e1) <= 1e-10 * max(1.0, abs(e1))
+        e_ok = e_ok and np.abs(g_qmf - g1).max() <= 1e-10 * max(1.0, np.abs(g1).max())
+        gd = np.array([port.gradient(h, th3, ph3, c) for c in cands])
+        e_ok = e_ok and np.abs(g_dis - gd).max() <= 1e-10 * max(1.0, np.abs(gd).max())
+        gp = np.array([port.gradient(h, th, ph, c) for c in cands])  # exact at the poles
+        e_ok = e_ok and np.abs(g_dis_poles - gp).max() <= 1e-10 * max(1.0, np.abs(gp).max())
         print(f"MULTI world={world} terms={len(r)} exchanged={sum(o[2] for o in objs)} "
               f"bitexact={ok} energy_ok={e_ok}", flush=True)
         if not (ok and e_ok):
