@@ -70,7 +70,7 @@ __host__ __device__ constexpr int merge_minb(int B, int NT) {
   return (B >= 4 ? 3 : IQCC_MERGE_MINB) * 256 / NT > 0 ? (B >= 4 ? 3 : IQCC_MERGE_MINB) * 256 / NT : 1;
 }
 #ifndef IQCC_RANK_MINB
-#define IQCC_RANK_MINB 4
+#define IQCC_RANK_MINB 5
 #endif
 // Output slots.  Every present survivor and every product owns an output
 // slot ("pmask" / "qmask" bits) unless a compress whose cut is at least theta
@@ -573,15 +573,11 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
   const int cnt = __popc(it.bits);
   const int inc = warp_inclusive(cnt, OpAdd());
   const int cl = inc - cnt + tile_pfx[wt];
-  int C[WI], delta[WI];
-  unsigned used[WI];
+  // C(k) = anticommuting terms before item k (recomputed, not stored)
+  auto Cof = [&](int k) { return cl + __popc(it.bits & ((1u << k) - 1u)); };
+  int delta[WI];
 #pragma unroll
-  for (int k = 0; k < WI; ++k) {
-    C[k] = cl + __popc(it.bits & ((1u << k) - 1u));
-    delta[k] = 0;
-    used[k] = 0;
-  }
-  int st[NTHR];
+  for (int k = 0; k < WI; ++k) delta[k] = 0;
   // a threshold below every LCP of the warp tile has no boundary in it: its
   // scans reduce to the carries (warp-uniform skip; common for shallow
   // levels inside runs of equal x planes)
@@ -589,100 +585,91 @@ __global__ void __launch_bounds__(256, IQCC_RANK_MINB) k_rank_w(const short* __r
 #pragma unroll
   for (int k = 0; k < WI; ++k) lmin = min(lmin, it.l[k]);
   lmin = __reduce_min_sync(0xffffffffu, lmin);
-  // forward: last boundary at or before the term
-#pragma unroll
-  for (int j = 0; j < NTHR; ++j) {
+  // forward scan of one threshold: last boundary at or before each item
+  auto fwd = [&](int j) {
     const int fc = fwd_carry[wt * kThrPerChunk + j];
-    if (thr.t[j] < lmin) {
-      st[j] = fc;
-      continue;
-    }
+    if (thr.t[j] < lmin) return fc;
     int a = -1;
 #pragma unroll
     for (int k = 0; k < WI; ++k)
-      if (it.l[k] <= thr.t[j]) a = C[k];
+      if (it.l[k] <= thr.t[j]) a = Cof(k);
     a = warp_inclusive(a, OpMax());
     int ex = __shfl_up_sync(0xffffffffu, a, 1);
     if (lane == 0) ex = -1;
-    st[j] = max(ex, fc);
-  }
-  // per level (thresholds 2lv, 2lv+1) the item walk only needs that level's
-  // two running boundaries, so levels run one after another and a level
-  // without any boundary in the tile (both thresholds below lmin) costs no
-  // compares: its D is the constant carry difference
-  const int nlev = thr.nlev;
+    return max(ex, fc);
+  };
+  // backward scan: first boundary strictly after each item
+  auto bwd = [&](int j) {
+    const int bc = bwd_carry[wt * kThrPerChunk + j];
+    if (thr.t[j] < lmin) return bc;
+    int b = INT_MAX;
 #pragma unroll
+    for (int k = WI - 1; k >= 0; --k)
+      if (it.l[k] <= thr.t[j]) b = Cof(k);
+    b = warp_inclusive_rev(b, OpMin());
+    int ex = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == 31) ex = INT_MAX;
+    return min(ex, bc);
+  };
+  // levels one at a time (thresholds 2lv: node start, 2lv+1: child split):
+  // only that level's scans and one bit per item ("D > 0 seen") stay live,
+  // so the kernel fits 40 registers; a level without any boundary in the
+  // tile (both thresholds below lmin) costs no compares
+  const int nlev = thr.nlev;
+#pragma unroll 1
   for (int lv = 0; lv < NTHR / 2; ++lv) {
     if (lv >= nlev) break;  // padded levels: D == 0 everywhere
-    int a = st[2 * lv], b = st[2 * lv + 1];
-    if (thr.t[2 * lv + 1] < lmin) {
+    unsigned used = 0;
+    int a = fwd(2 * lv), b = fwd(2 * lv + 1);
+    const bool flat = thr.t[2 * lv + 1] < lmin;
+    if (flat) {
       const int D = b - a;
       if (D > 0) {
 #pragma unroll
         for (int k = 0; k < WI; ++k)
-          if ((it.bits >> k) & 1u) {
-            delta[k] -= D;
-            used[k] |= 1u << lv;
-          }
+          if ((it.bits >> k) & 1u) delta[k] -= D;
+        used = it.bits;
       }
-      continue;
-    }
+    } else {
 #pragma unroll
-    for (int k = 0; k < WI; ++k) {
-      if (it.l[k] <= thr.t[2 * lv]) a = C[k];
-      if (it.l[k] <= thr.t[2 * lv + 1]) b = C[k];
-      const int D = b - a;
-      if (((it.bits >> k) & 1u) && D > 0) {
-        delta[k] -= D;
-        used[k] |= 1u << lv;
+      for (int k = 0; k < WI; ++k) {
+        if (it.l[k] <= thr.t[2 * lv]) a = Cof(k);
+        if (it.l[k] <= thr.t[2 * lv + 1]) b = Cof(k);
+        const int D = b - a;
+        if (((it.bits >> k) & 1u) && D > 0) {
+          delta[k] -= D;
+          used |= 1u << k;
+        }
       }
     }
-  }
-  // backward: first boundary strictly after the term
-#pragma unroll
-  for (int j = 0; j < NTHR; ++j) {
-    const int bc = bwd_carry[wt * kThrPerChunk + j];
-    if (thr.t[j] < lmin) {
-      st[j] = bc;
-      continue;
-    }
-    int b = INT_MAX;
-#pragma unroll
-    for (int k = WI - 1; k >= 0; --k)
-      if (it.l[k] <= thr.t[j]) b = C[k];
-    b = warp_inclusive_rev(b, OpMin());
-    int ex = __shfl_down_sync(0xffffffffu, b, 1);
-    if (lane == 31) ex = INT_MAX;
-    st[j] = min(ex, bc);
-  }
-#pragma unroll
-  for (int lv = 0; lv < NTHR / 2; ++lv) {
-    if (lv >= nlev) break;
-    int a = st[2 * lv], b = st[2 * lv + 1];
-    if (thr.t[2 * lv + 1] < lmin) {
+    a = bwd(2 * lv);
+    b = bwd(2 * lv + 1);
+    const unsigned rest = it.bits & ~used;
+    if (flat) {
       const int E = a - b;
 #pragma unroll
       for (int k = 0; k < WI; ++k)
-        if (((it.bits >> k) & 1u) && !((used[k] >> lv) & 1u)) delta[k] += E;
-      continue;
-    }
+        if ((rest >> k) & 1u) delta[k] += E;
+    } else {
 #pragma unroll
-    for (int k = WI - 1; k >= 0; --k) {
-      if (((it.bits >> k) & 1u) && !((used[k] >> lv) & 1u)) delta[k] += a - b;
-      if (it.l[k] <= thr.t[2 * lv]) a = C[k];
-      if (it.l[k] <= thr.t[2 * lv + 1]) b = C[k];
+      for (int k = WI - 1; k >= 0; --k) {
+        if ((rest >> k) & 1u) delta[k] += a - b;
+        if (it.l[k] <= thr.t[2 * lv]) a = Cof(k);
+        if (it.l[k] <= thr.t[2 * lv + 1]) b = Cof(k);
+      }
     }
   }
-#pragma unroll
   const unsigned qm = FINAL && qflag && first < M ? (qmask[first >> 5] >> (first & 31)) : 0u;
+#pragma unroll
   for (int k = 0; k < WI; ++k) {
     if (!((it.bits >> k) & 1u)) continue;
     const size_t g = first + k;
     const int d = delta[k] + (has_rdelta ? rdelta[g] : 0);
+    const int Ck = Cof(k);
     if (FINAL) {
-      if (dbg_ok(dbg, 1, (ull)(long long)(C[k] + d), (ull)*a_total)) {
-        inv_perm[C[k] + d] = (unsigned)g;
-        if (qflag) qflag[C[k] + d] = (unsigned char)((qm >> k) & 1u);
+      if (dbg_ok(dbg, 1, (ull)(long long)(Ck + d), (ull)*a_total)) {
+        inv_perm[Ck + d] = (unsigned)g;
+        if (qflag) qflag[Ck + d] = (unsigned char)((qm >> k) & 1u);
       }
     } else {
       rdelta[g] = d;

@@ -130,6 +130,79 @@ __global__ void __launch_bounds__(256) k_expect(const ull* __restrict__ keys,
   }
 }
 
+// Nibble tables: the qubit slots in groups of four; for group g the 256
+// products of its four factors, indexed by the group's z nibble | x nibble
+// << 4 (nibbles as they sit in the bit-reversed device words: bit 3 =
+// qubit 4g).  A term's value is the product of its 16B group entries in
+// ascending group order: 16B dmuls and table reads instead of 64B, at the
+// price of the per-term rounding order (the sum is within 1e-15 relative of
+// expect_word's; the engine's energies are specified to 1e-10).  With the z
+// nibble in the low index bits, terms whose x nibble is 0 (most groups of a
+// molecular Hamiltonian) read 16 consecutive entries: distinct banks.
+__global__ void k_nibble_table(const double* __restrict__ f4, int ngroups, double* __restrict__ tab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ngroups * 256) return;
+  const int g = i >> 8, idx = i & 255, zn = idx & 15, xn = idx >> 4;
+  double v = 1.0;
+  for (int j = 3; j >= 0; --j) {  // nibble bit 3 = qubit 4g: ascending qubit order
+    const int q = 4 * g + (3 - j);
+    const unsigned code = ((xn >> j) & 1u) | (((zn >> j) & 1u) << 1);
+    v = __dmul_rn(v, f4[4 * q + code]);
+  }
+  tab[i] = v;
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) k_expect_nib(const ull* __restrict__ keys,
+                                                    const double* __restrict__ coef, size_t M,
+                                                    Filter filt, const double* __restrict__ tab_g,
+                                                    double* __restrict__ partial) {
+  constexpr int NG = 16 * B;  // groups of four qubit slots
+  extern __shared__ double tab[];  // [NG][256]
+  __shared__ double rs[256], rc[256];
+  for (int i = threadIdx.x; i < NG * 256; i += blockDim.x) tab[i] = tab_g[i];
+  __syncthreads();
+  TwoSum acc;
+  const size_t per = (M + gridDim.x - 1) / gridDim.x;
+  const size_t lo = blockIdx.x * per, hi = min(M, lo + per);
+  for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const Key<B> k = load_key<B>(keys, i);
+    const double c = coef[i];
+    if (!filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k))) continue;
+    double v = 1.0;
+#pragma unroll
+    for (int w = 0; w < B; ++w) {
+#pragma unroll
+      for (int h = 1; h >= 0; --h) {
+        const unsigned xh = (unsigned)(k.w[w] >> (32 * h)), zh = (unsigned)(k.w[B + w] >> (32 * h));
+#pragma unroll
+        for (int n = 7; n >= 0; --n) {  // bits 31..28 hold the lowest qubits of the half
+          const int g = 16 * w + 8 * (1 - h) + (7 - n);
+          const unsigned idx = ((zh >> (4 * n)) & 15u) | (((xh >> (4 * n)) & 15u) << 4);
+          v = __dmul_rn(v, tab[g * 256 + idx]);
+        }
+      }
+    }
+    acc.add(__dmul_rn(c, v));
+  }
+  rs[threadIdx.x] = acc.s;
+  rc[threadIdx.x] = acc.c;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {  // fixed tree: deterministic
+    if (threadIdx.x < o) {
+      TwoSum a{rs[threadIdx.x], rc[threadIdx.x]}, b{rs[threadIdx.x + o], rc[threadIdx.x + o]};
+      a.merge(b);
+      rs[threadIdx.x] = a.s;
+      rc[threadIdx.x] = a.c;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = rs[0];
+    partial[2 * blockIdx.x + 1] = rc[0];
+  }
+}
+
 /// F4 rows from the host factor table [nq][3] = (X, Z, Y).
 static std::vector<double> factor_rows(const double* factors, int nq, uint32_t B) {
   std::vector<double> f4((size_t)4 * 64 * B, 1.0);
@@ -168,14 +241,39 @@ double expect_store(DeviceStore& s, const double* factors) {
   const std::vector<double> f4 = factor_rows(factors, nq, s.B);
   double* tab = ws.tables.as<double>(f4.size());
   IQCC_CUDA(cudaMemcpyAsync(tab, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-  const unsigned grid = (unsigned)std::min<size_t>(148 * 8, std::max<size_t>(1, (s.M + 1023) / 1024));
+  // IQCC_EXPECT_EXACT=1: the lockstep product over every qubit slot (each
+  // term's value bit-identical to expect_word); default: nibble tables
+  const bool exact = getenv("IQCC_EXPECT_EXACT") && atoi(getenv("IQCC_EXPECT_EXACT")) != 0;
+  // nibble tables take 32 KB per device block of the key: 2-3 CTAs per SM
+  const unsigned per_sm = exact ? 8u : (s.B >= 4 ? 1u : (s.B == 2 ? 3u : 6u));
+  const unsigned grid = (unsigned)std::min<size_t>(148 * per_sm, std::max<size_t>(1, (s.M + 1023) / 1024));
   double* part = ws.partials.as<double>(2 * grid);
-  {
+  if (exact) {
     KernelScope ks("expect");
     switch (s.B) {
       case 1: k_expect<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, part); break;
       case 2: k_expect<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, part); break;
       default: k_expect<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, tab, part); break;
+    }
+  } else {
+    const int ng = 16 * (int)s.B;
+    double* nib = ws.misc2.as<double>((size_t)ng * 256);
+    const size_t smem = (size_t)ng * 256 * sizeof(double);
+    KernelScope ks("expect");
+    k_nibble_table<<<(ng * 256 + 255) / 256, 256, 0, st>>>(tab, ng, nib);
+    switch (s.B) {
+      case 1:
+        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_expect_nib<1><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
+        break;
+      case 2:
+        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_expect_nib<2><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
+        break;
+      default:
+        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_expect_nib<4><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
+        break;
     }
   }
   return host_sum_pairs(fetch(part, 2 * grid));
@@ -315,6 +413,137 @@ __global__ void __launch_bounds__(kQB) k_qmf_grad(const ull* __restrict__ keys,
   }
 }
 
+// ---------------------------------------- QMF gradient, no zero factors
+// H[k][code] = sum of w = c*P over the terms whose letter at qubit k is
+// `code` (see above).  One warp takes 32 terms at a time (one per lane):
+//  * every lane's 32-bit slice of its x and z words is transposed across the
+//    warp (5 butterfly shuffles), so lane k holds, for qubit k of the slice,
+//    the 32-term masks of X (x & ~z), Z (z & ~x) and Y (x & z) letters;
+//  * the 32 weights form 8 groups of 4 whose 16 subset sums sit in shared
+//    memory (Four Russians): each group adds S_u[mask nibble] to the lane's
+//    three bins with one conflict-free read instead of four adds per term.
+// Work per term is O(qubit slots / 32) instead of O(qubits); the order of
+// every sum is fixed (deterministic).  P is the nibble-table product.
+__device__ __forceinline__ unsigned transpose32(unsigned x) {
+  const int lane = threadIdx.x & 31;
+  const unsigned hi[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int sft = 16 >> t;
+    const unsigned y = __shfl_xor_sync(0xffffffffu, x, sft);
+    x = (lane & sft) ? ((x & hi[t]) | ((y >> sft) & ~hi[t])) : ((x & ~hi[t]) | ((y << sft) & hi[t]));
+  }
+  return x;
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) k_qmf_grad_fr(const ull* __restrict__ keys, const double* __restrict__ coef,
+                                                     size_t M, Filter filt, const double* __restrict__ nib_g,
+                                                     double* __restrict__ partial) {
+  constexpr int NG = 16 * B, NS = 2 * B;  // nibble groups; 32-qubit slices
+  extern __shared__ double shq[];
+  double* tab = shq;                       // [NG][256]
+  double* St = shq + NG * 256;             // [8 warps][8 groups][16]
+  double* Wt = St + 8 * 128;               // [8 warps][32]
+  double* red = Wt + 8 * 32;               // [8 warps][NS][32][3] block reduction
+  for (int i = threadIdx.x; i < NG * 256; i += blockDim.x) tab[i] = nib_g[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* S = St + warp * 128;
+  double* Wl = Wt + warp * 32;
+  double acc[NS][3];
+#pragma unroll
+  for (int a = 0; a < NS; ++a) acc[a][0] = acc[a][1] = acc[a][2] = 0.0;
+  TwoSum e;
+  const size_t nchunk = (M + 31) / 32;
+  for (size_t ch = (size_t)blockIdx.x * 8 + warp; ch < nchunk; ch += (size_t)gridDim.x * 8) {
+    const size_t i = ch * 32 + lane;
+    Key<B> k;
+#pragma unroll
+    for (int w = 0; w < 2 * B; ++w) k.w[w] = 0;
+    double wt = 0.0;
+    if (i < M) {
+      const Key<B> kk = load_key<B>(keys, i);
+      const double c = coef[i];
+      if (filter_keep(filt, i, c, i == 0 && key_is_identity<B>(kk))) {
+        k = kk;
+        double v = 1.0;
+#pragma unroll
+        for (int w = 0; w < B; ++w)
+#pragma unroll
+          for (int h = 1; h >= 0; --h) {
+            const unsigned xh = (unsigned)(k.w[w] >> (32 * h)), zh = (unsigned)(k.w[B + w] >> (32 * h));
+#pragma unroll
+            for (int n = 7; n >= 0; --n) {
+              const int g = 16 * w + 8 * (1 - h) + (7 - n);
+              v = __dmul_rn(v, tab[g * 256 + (((zh >> (4 * n)) & 15u) | (((xh >> (4 * n)) & 15u) << 4))]);
+            }
+          }
+        wt = __dmul_rn(c, v);
+        e.add(wt);
+      }
+    }
+    Wl[lane] = wt;
+    __syncwarp();
+    // subset sums of the 8 groups of 4 terms: lane -> (group 2r + lane/16, subset lane%16)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int u = 2 * r + (lane >> 4), sub = lane & 15;
+      double sum = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if ((sub >> b) & 1) sum = __dadd_rn(sum, Wl[4 * u + b]);
+      S[u * 16 + sub] = sum;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < B; ++w)
+#pragma unroll
+      for (int h = 1; h >= 0; --h) {
+        const int sl = 2 * w + (1 - h);
+        const unsigned xt = transpose32((unsigned)(k.w[w] >> (32 * h)));
+        const unsigned zt = transpose32((unsigned)(k.w[B + w] >> (32 * h)));
+        const unsigned mx = xt & ~zt, mz = zt & ~xt, my = xt & zt;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc[sl][0] = __dadd_rn(acc[sl][0], S[u * 16 + ((mx >> (4 * u)) & 15u)]);
+          acc[sl][1] = __dadd_rn(acc[sl][1], S[u * 16 + ((mz >> (4 * u)) & 15u)]);
+          acc[sl][2] = __dadd_rn(acc[sl][2], S[u * 16 + ((my >> (4 * u)) & 15u)]);
+        }
+      }
+    __syncwarp();
+  }
+  // lane k of slice sl holds qubit 32*sl + (31 - k); warps summed in order
+#pragma unroll
+  for (int a = 0; a < NS; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) red[((warp * NS + a) * 32 + lane) * 3 + c] = acc[a][c];
+  __shared__ double rs[256], rc[256];
+  rs[threadIdx.x] = e.s;
+  rc[threadIdx.x] = e.c;
+  __syncthreads();
+  for (int j = threadIdx.x; j < NS * 32 * 3; j += blockDim.x) {
+    double v = 0.0;
+    for (int wp = 0; wp < 8; ++wp) v = __dadd_rn(v, red[wp * NS * 96 + j]);
+    const int a = j / 96, r = j % 96, ln = r / 3, c = r % 3;
+    const int q = 32 * a + (31 - ln);
+    partial[(size_t)blockIdx.x * (NS * 96 + 2) + 3 * q + c] = v;
+  }
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      TwoSum x{rs[threadIdx.x], rc[threadIdx.x]}, y{rs[threadIdx.x + o], rc[threadIdx.x + o]};
+      x.merge(y);
+      rs[threadIdx.x] = x.s;
+      rc[threadIdx.x] = x.c;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[(size_t)blockIdx.x * (NS * 96 + 2) + NS * 96] = rs[0];
+    partial[(size_t)blockIdx.x * (NS * 96 + 2) + NS * 96 + 1] = rc[0];
+  }
+}
+
 double qmf_grad_store(DeviceStore& s, const double* factors, const double* derivs, double* grad) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
@@ -334,6 +563,49 @@ double qmf_grad_store(DeviceStore& s, const double* factors, const double* deriv
   unsigned char* zmd = reinterpret_cast<unsigned char*>(tab + f4.size());
   IQCC_CUDA(cudaMemcpyAsync(tab, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
   IQCC_CUDA(cudaMemcpyAsync(zmd, zm.data(), zm.size(), cudaMemcpyHostToDevice, st));
+  if (!zeros && !(getenv("IQCC_QMF_GRAD_BINS") && atoi(getenv("IQCC_QMF_GRAD_BINS")))) {
+    // no zero factor anywhere: every term is a c*P weight (bit-sliced kernel)
+    const int ng = 16 * (int)s.B, ns = 2 * (int)s.B;
+    double* nib = ws.misc2.as<double>((size_t)ng * 256);
+    const size_t smem = ((size_t)ng * 256 + 8 * 128 + 8 * 32 + (size_t)8 * ns * 96) * sizeof(double);
+    const unsigned per_sm = s.B >= 4 ? 1u : 2u;
+    const unsigned grid = (unsigned)std::min<size_t>(148 * per_sm, std::max<size_t>(1, (s.M + 255) / 256));
+    const size_t stride = (size_t)ns * 96 + 2;
+    double* part = ws.grad_part.as<double>((size_t)grid * stride);
+    {
+      KernelScope ks("qmf_grad");
+      k_nibble_table<<<(ng * 256 + 255) / 256, 256, 0, st>>>(tab, ng, nib);
+#define IQCC_QF(B_)                                                                                        \
+  IQCC_CUDA(cudaFuncSetAttribute(k_qmf_grad_fr<B_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+  k_qmf_grad_fr<B_><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part)
+      switch (s.B) {
+        case 1: IQCC_QF(1); break;
+        case 2: IQCC_QF(2); break;
+        default: IQCC_QF(4); break;
+      }
+#undef IQCC_QF
+    }
+    const std::vector<double> h = fetch(part, (size_t)grid * stride);
+    std::vector<double> H(3 * (size_t)64 * s.B, 0.0);
+    double es = 0.0, ec = 0.0;
+    for (unsigned b = 0; b < grid; ++b) {
+      const double* p = h.data() + (size_t)b * stride;
+      for (size_t j = 0; j < (size_t)ns * 96; ++j) H[j] += p[j];
+      const double x = p[stride - 2];
+      const double t = es + x;
+      ec += std::fabs(es) >= std::fabs(x) ? (es - t) + x : (x - t) + es;
+      es = t;
+      ec += p[stride - 1];
+    }
+    for (int q = 0; q < nq; ++q)
+      for (int c = 0; c < 3; ++c) {  // bins (X, Z, Y) = codes 1, 2, 3
+        const double f = f4[4 * q + 1 + c];
+        const double dth = derivs[6 * q + 2 * c], dph = derivs[6 * q + 2 * c + 1];
+        grad[q] += H[3 * q + c] * (dth / f);
+        grad[nq + q] += H[3 * q + c] * (dph / f);
+      }
+    return es + ec;
+  }
   const unsigned grid = (unsigned)std::min<size_t>(148 * 6, std::max<size_t>(1, (s.M + kQB - 1) / kQB));
   const size_t tpq = 4 / s.B;  // threads per qubit slot in the kernel's phase 2
   const size_t stride = 6 * (size_t)nq * tpq + 2;

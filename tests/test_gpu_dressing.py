@@ -5,6 +5,7 @@ plus the golden C1 iQCC traces and large G_mol runs (124/200 qubits)."""
 import math
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -399,3 +400,17 @@ def test_sequence_merge_options(eng, port, tag, drop):
     d2.dress_sequence(ans, 1e-9, 30000, opts=eng.MergeOptions(drop, True))
     want2, _ = port.dress_sequence(port.gen_mol(n, terms, seed), gens, taus, 1e-9, 30000, drop=drop)
     check_same(d2.download(), want2)
+
+
+def test_debug_bounds_checks_pass():
+    """IQCC_DEBUG=1 turns on the engine's bounds checks on every scattered
+    write (merge slots, rank permutation, bijection check of inv_perm) and a
+    synchronize after every kernel family; the workload must run clean and
+    produce the same sums (tools/sanitize_run.py, also run under
+    compute-sanitizer: profiles/r2_sanitizer_*.log)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IQCC_DEBUG="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_run.py"), "--small"],
+                       capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "SANITIZE RUN OK" in r.stdout

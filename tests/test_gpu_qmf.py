@@ -45,12 +45,23 @@ def test_expect_sum_random(eng, port):
         th, ph = rng.qmf(n)
         got = eng.expect_sum(eng.QmfState(th, ph), host(eng, h))
         assert close(got, port.expect_sum(th, ph, h))
-    # per-term values are bit-exact: one-term sums
+
+def test_expect_word_values(eng, port, monkeypatch):
+    """One-term sums: the nibble-table product (default) agrees with
+    expect_word to 1e-14; the lockstep mode (IQCC_EXPECT_EXACT=1) is bit-exact."""
+    rng = port.rng(203)
+    cases = []
     for t in range(100):
-        n = 1 + t % 70
+        n = 1 + t % 200
         w = rng.word(n)
+        cases.append((n, w, rng.qmf(n)))
+    for n, w, (th, ph) in cases:
         h = port.sum(n, w[None, :], [1.0])
-        th, ph = rng.qmf(n)
+        want = port.expect_word(n, th, ph, w)
+        assert abs(eng.expect_sum(eng.QmfState(th, ph), host(eng, h)) - want) <= 1e-13 * max(1e-300, abs(want))
+    monkeypatch.setenv("IQCC_EXPECT_EXACT", "1")
+    for n, w, (th, ph) in cases:
+        h = port.sum(n, w[None, :], [1.0])
         assert eng.expect_sum(eng.QmfState(th, ph), host(eng, h)) == port.expect_word(n, th, ph, w)
 
 
@@ -72,6 +83,41 @@ def test_qmf_energy_gradient(eng, port, n):
     assert close(e, er)
     scale = max(1.0, np.abs(gr).max())
     assert np.abs(g - gr).max() <= REL * scale
+
+
+@pytest.mark.parametrize("mode", ["bitsliced", "bins"])
+def test_qmf_gradient_near_poles(eng, port, monkeypatch, mode):
+    """|sin theta| ~ 1e-8 (a QMF state next to the HF poles): the c*P*(f'/f)
+    rearrangement must still match the reference's prefix/suffix products
+    (iqcc/qmf.hpp:94-148), on a Hamiltonian and on its G_mol-like shape;
+    both kernels (the bit-sliced default and the per-qubit bins)."""
+    if mode == "bins":
+        monkeypatch.setenv("IQCC_QMF_GRAD_BINS", "1")
+    rng = port.rng(223)
+    for n, h in ((12, rng.sum(12, 800)), (124, port.gen_mol(124, 20000, 7))):
+        th, ph = rng.qmf(n)
+        occ = np.arange(n) < n // 3
+        th = np.where(occ, np.pi - 1e-8 * (1 + np.arange(n) % 3), 1e-8 * (1 + np.arange(n) % 5))
+        th[::7] += 0.3  # and some generic angles
+        e, g = eng.qmf_energy_gradient(host(eng, h), eng.QmfState(th, ph))
+        er, gr = port.qmf_energy_gradient(h, th, ph)
+        assert close(e, er)
+        assert np.abs(g - gr).max() <= REL * max(1.0, np.abs(gr).max())
+
+
+@pytest.mark.parametrize("n", [64, 124, 200])
+def test_qmf_gradient_gmol_kernels_agree(eng, port, monkeypatch, n):
+    """The bit-sliced kernel against the reference at G_mol shapes (sparse x
+    planes, the benchmark's shape) and against the per-qubit-bin kernel."""
+    h = port.gen_mol(n, 30000, 3)
+    th, ph = port.rng(227).qmf(n)
+    d = eng.DeviceSum.upload(host(eng, h))
+    e1, g1 = d.qmf_energy_gradient(eng.QmfState(th, ph))
+    er, gr = port.qmf_energy_gradient(h, th, ph)
+    assert close(e1, er) and np.abs(g1 - gr).max() <= REL * max(1.0, np.abs(gr).max())
+    monkeypatch.setenv("IQCC_QMF_GRAD_BINS", "1")
+    e2, g2 = d.qmf_energy_gradient(eng.QmfState(th, ph))
+    assert close(e2, er) and np.abs(g2 - gr).max() <= REL * max(1.0, np.abs(gr).max())
 
 
 def test_qmf_gradient_finite_difference(eng, port):  # test_qmf.cpp:68-87
