@@ -347,19 +347,36 @@ def run_gpu_arm(args, rank, world, local_rank):
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         h2d = h_host.rows.nbytes + h_host.coeffs.nbytes
         tin_e2e, d2h = 0, 0
+        split = {"upload": 0.0, "dress": 0.0, "download": 0.0}
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for s in range(e2e_steps):
             ents = step_entanglers(N_QUBITS, args.warmup + 2 * args.steps + s)
             ans = iqcc.Ansatz([iqcc.PauliWord(N_QUBITS, r) for r, _ in ents], [t for _, t in ents])
-            out, tin = iqcc.dress_sequence_counted(h_host, ans, EPS, n_terms, out=out_bufs)
+            # iqcc.dress_sequence_counted in its three phases (each call ends
+            # device-synchronous): H2D + upload check, the 10 steps, D2H
+            ta = time.perf_counter()
+            dev = iqcc.DeviceSum.upload(h_host)
+            tb = time.perf_counter()
+            tin = dev.dress_sequence(ans, EPS, n_terms)
+            torch.cuda.synchronize()
+            tc = time.perf_counter()
+            out = dev.download(*out_bufs)
+            td = time.perf_counter()
+            del dev
+            split["upload"] += tb - ta
+            split["dress"] += tc - tb
+            split["download"] += td - tc
             tin_e2e += tin
             d2h += out.rows.nbytes + out.coeffs.nbytes
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
         e2e = {"value": tin_e2e / secs, "unit": "terms/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps,
-               "ms_per_step": 1e3 * secs / e2e_steps}
+               "ms_per_step": 1e3 * secs / e2e_steps,
+               "split_ms_per_step": {k: round(1e3 * v / e2e_steps, 2) for k, v in split.items()},
+               "split_note": "upload = pinned H2D of rows + complex coefficients and the device check/convert; "
+                             "download = device compaction to the reference layout + D2H (PCIe bound)"}
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_reference(SAMPLE_TERMS, 1, want_digest=True)

@@ -1301,8 +1301,11 @@ static void poly_impl(DeviceStore& s, const double* factors, bool poles, const u
   // chunks of >= 4096 terms, only as many as needed to fill 8 blocks (32
   // warps) per SM: the per-lane product is a dependent dmul chain, so the
   // kernel needs warps to hide its latency
+  // IQCC_POLY_EXACT=1: one chunk, each pair summed in canonical order over
+  // the whole store (bit-identical to the reference at any size, slower)
+  const bool exact = getenv("IQCC_POLY_EXACT") && atoi(getenv("IQCC_POLY_EXACT")) != 0;
   size_t chunks = 1;
-  if (!poles && s.M > 4096)
+  if (!poles && !exact && s.M > 4096)
     chunks = std::min<size_t>((s.M + 4095) / 4096, std::max<size_t>(1, (148 * 8 + pblocks - 1) / pblocks));
   chunks = std::min<size_t>(chunks, 65535);
   const size_t chunk = chunks == 1 ? std::max<size_t>(s.M, 1) : (s.M + chunks - 1) / chunks;

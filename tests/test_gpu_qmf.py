@@ -298,6 +298,14 @@ def test_poly_kernels_chunked_large(eng, port):
     scale = max(1e-300, np.abs(hc).max())
     assert np.abs(ker.h_kernel - hc).max() <= 1e-12 * scale
     assert np.array_equal(_bits(np.stack([ker.n_kernel.real.ravel(), ker.n_kernel.imag.ravel()], 1)), _bits(raw[1]))
+    # exact mode: one chunk, bit-identical to the reference at this size too
+    import os
+    os.environ["IQCC_POLY_EXACT"] = "1"
+    try:
+        kx = d.poly_kernels(om, ex)
+    finally:
+        del os.environ["IQCC_POLY_EXACT"]
+    assert _kernels_equal(kx, port.poly_kernels(hm, th, ph, rows, 2))
 
 
 def test_poly_energy_full_order_is_qcc_energy(eng, port):
