@@ -435,6 +435,8 @@ def main():
         run_reference_arm(args, rank)
         return
     if world > 1:
+        # NCCL's banner / INFO lines go to stderr: stdout carries the JSON line only
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
