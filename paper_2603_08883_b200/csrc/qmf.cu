@@ -152,22 +152,34 @@ __global__ void k_nibble_table(const double* __restrict__ f4, int ngroups, doubl
   tab[i] = v;
 }
 
-template <int B>
-__global__ void __launch_bounds__(256) k_expect_nib(const ull* __restrict__ keys,
-                                                    const double* __restrict__ coef, size_t M,
-                                                    Filter filt, const double* __restrict__ tab_g,
-                                                    double* __restrict__ partial) {
+template <int B, int NT>
+__global__ void __launch_bounds__(NT) k_expect_nib(const ull* __restrict__ keys,
+                                                   const double* __restrict__ coef, size_t M,
+                                                   Filter filt, const double* __restrict__ tab_g,
+                                                   double* __restrict__ partial) {
   constexpr int NG = 16 * B;  // groups of four qubit slots
   extern __shared__ double tab[];  // [NG][256]
-  __shared__ double rs[256], rc[256];
+  __shared__ double rs[NT], rc[NT];
   for (int i = threadIdx.x; i < NG * 256; i += blockDim.x) tab[i] = tab_g[i];
   __syncthreads();
   TwoSum acc;
   const size_t per = (M + gridDim.x - 1) / gridDim.x;
   const size_t lo = blockIdx.x * per, hi = min(M, lo + per);
+  // the next term's row and coefficient are in flight while this one is
+  // multiplied out (the loop is otherwise one dependent load per term)
+  Key<B> kn;
+  double cn = 0.0;
+  if (lo + threadIdx.x < hi) {
+    kn = load_key<B>(keys, lo + threadIdx.x);
+    cn = coef[lo + threadIdx.x];
+  }
   for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const Key<B> k = load_key<B>(keys, i);
-    const double c = coef[i];
+    const Key<B> k = kn;
+    const double c = cn;
+    if (i + blockDim.x < hi) {
+      kn = load_key<B>(keys, i + blockDim.x);
+      cn = coef[i + blockDim.x];
+    }
     if (!filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k))) continue;
     double v = 1.0;
 #pragma unroll
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(256) k_expect_nib(const ull* __restrict__ keys
   rs[threadIdx.x] = acc.s;
   rc[threadIdx.x] = acc.c;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {  // fixed tree: deterministic
+  for (int o = NT / 2; o > 0; o >>= 1) {  // fixed tree: deterministic
     if (threadIdx.x < o) {
       TwoSum a{rs[threadIdx.x], rc[threadIdx.x]}, b{rs[threadIdx.x + o], rc[threadIdx.x + o]};
       a.merge(b);
@@ -244,9 +256,12 @@ double expect_store(DeviceStore& s, const double* factors) {
   // IQCC_EXPECT_EXACT=1: the lockstep product over every qubit slot (each
   // term's value bit-identical to expect_word); default: nibble tables
   const bool exact = getenv("IQCC_EXPECT_EXACT") && atoi(getenv("IQCC_EXPECT_EXACT")) != 0;
-  // nibble tables take 32 KB per device block of the key: 2-3 CTAs per SM
+  // nibble tables take 32 KB per device block of the key: 512-thread CTAs,
+  // 2 per SM at B <= 2 (32 warps), 1 at B = 4
   const unsigned per_sm = exact ? 8u : (s.B >= 4 ? 1u : (s.B == 2 ? 3u : 6u));
-  const unsigned grid = (unsigned)std::min<size_t>(148 * per_sm, std::max<size_t>(1, (s.M + 1023) / 1024));
+  const unsigned grid = (unsigned)std::min<size_t>(148 * (exact ? 8u : (s.B >= 4 ? 1u : 2u)),
+                                                   std::max<size_t>(1, (s.M + 1023) / 1024));
+  (void)per_sm;
   double* part = ws.partials.as<double>(2 * grid);
   if (exact) {
     KernelScope ks("expect");
@@ -263,16 +278,16 @@ double expect_store(DeviceStore& s, const double* factors) {
     k_nibble_table<<<(ng * 256 + 255) / 256, 256, 0, st>>>(tab, ng, nib);
     switch (s.B) {
       case 1:
-        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_expect_nib<1><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
+        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<1, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_expect_nib<1, 512><<<grid, 512, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
         break;
       case 2:
-        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_expect_nib<2><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
+        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<2, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_expect_nib<2, 512><<<grid, 512, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
         break;
       default:
-        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_expect_nib<4><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
+        IQCC_CUDA(cudaFuncSetAttribute(k_expect_nib<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_expect_nib<4, 512><<<grid, 512, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part);
         break;
     }
   }
@@ -436,16 +451,17 @@ __device__ __forceinline__ unsigned transpose32(unsigned x) {
   return x;
 }
 
-template <int B>
-__global__ void __launch_bounds__(256) k_qmf_grad_fr(const ull* __restrict__ keys, const double* __restrict__ coef,
-                                                     size_t M, Filter filt, const double* __restrict__ nib_g,
-                                                     double* __restrict__ partial) {
+template <int B, int NT>
+__global__ void __launch_bounds__(NT) k_qmf_grad_fr(const ull* __restrict__ keys, const double* __restrict__ coef,
+                                                    size_t M, Filter filt, const double* __restrict__ nib_g,
+                                                    double* __restrict__ partial) {
   constexpr int NG = 16 * B, NS = 2 * B;  // nibble groups; 32-qubit slices
+  constexpr int NW = NT / 32;              // warps sharing one nibble table
   extern __shared__ double shq[];
   double* tab = shq;                       // [NG][256]
-  double* St = shq + NG * 256;             // [8 warps][8 groups][16]
-  double* Wt = St + 8 * 128;               // [8 warps][32]
-  double* red = Wt + 8 * 32;               // [8 warps][NS][32][3] block reduction
+  double* St = shq + NG * 256;             // [NW][8 groups][16]
+  double* Wt = St + NW * 128;              // [NW][32]
+  double* red = Wt + NW * 32;              // [NW][NS][32][3] block reduction
   for (int i = threadIdx.x; i < NG * 256; i += blockDim.x) tab[i] = nib_g[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -456,15 +472,29 @@ __global__ void __launch_bounds__(256) k_qmf_grad_fr(const ull* __restrict__ key
   for (int a = 0; a < NS; ++a) acc[a][0] = acc[a][1] = acc[a][2] = 0.0;
   TwoSum e;
   const size_t nchunk = (M + 31) / 32;
-  for (size_t ch = (size_t)blockIdx.x * 8 + warp; ch < nchunk; ch += (size_t)gridDim.x * 8) {
+  const size_t cstep = (size_t)gridDim.x * NW;
+  Key<B> kn;
+  double cn = 0.0;
+  {
+    const size_t i0 = ((size_t)blockIdx.x * NW + warp) * 32 + lane;
+    if (i0 < M) {
+      kn = load_key<B>(keys, i0);
+      cn = coef[i0];
+    }
+  }
+  for (size_t ch = (size_t)blockIdx.x * NW + warp; ch < nchunk; ch += cstep) {
     const size_t i = ch * 32 + lane;
     Key<B> k;
 #pragma unroll
     for (int w = 0; w < 2 * B; ++w) k.w[w] = 0;
     double wt = 0.0;
+    const Key<B> kk = kn;
+    const double c = cn;
+    if ((ch + cstep) * 32 + lane < M) {  // the next chunk's row in flight
+      kn = load_key<B>(keys, (ch + cstep) * 32 + lane);
+      cn = coef[(ch + cstep) * 32 + lane];
+    }
     if (i < M) {
-      const Key<B> kk = load_key<B>(keys, i);
-      const double c = coef[i];
       if (filter_keep(filt, i, c, i == 0 && key_is_identity<B>(kk))) {
         k = kk;
         double v = 1.0;
@@ -518,18 +548,18 @@ __global__ void __launch_bounds__(256) k_qmf_grad_fr(const ull* __restrict__ key
   for (int a = 0; a < NS; ++a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) red[((warp * NS + a) * 32 + lane) * 3 + c] = acc[a][c];
-  __shared__ double rs[256], rc[256];
+  __shared__ double rs[NT], rc[NT];
   rs[threadIdx.x] = e.s;
   rc[threadIdx.x] = e.c;
   __syncthreads();
   for (int j = threadIdx.x; j < NS * 32 * 3; j += blockDim.x) {
     double v = 0.0;
-    for (int wp = 0; wp < 8; ++wp) v = __dadd_rn(v, red[wp * NS * 96 + j]);
+    for (int wp = 0; wp < NW; ++wp) v = __dadd_rn(v, red[wp * NS * 96 + j]);
     const int a = j / 96, r = j % 96, ln = r / 3, c = r % 3;
     const int q = 32 * a + (31 - ln);
     partial[(size_t)blockIdx.x * (NS * 96 + 2) + 3 * q + c] = v;
   }
-  for (int o = 128; o > 0; o >>= 1) {
+  for (int o = NT / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
       TwoSum x{rs[threadIdx.x], rc[threadIdx.x]}, y{rs[threadIdx.x + o], rc[threadIdx.x + o]};
       x.merge(y);
@@ -565,23 +595,25 @@ double qmf_grad_store(DeviceStore& s, const double* factors, const double* deriv
   IQCC_CUDA(cudaMemcpyAsync(zmd, zm.data(), zm.size(), cudaMemcpyHostToDevice, st));
   if (!zeros && !(getenv("IQCC_QMF_GRAD_BINS") && atoi(getenv("IQCC_QMF_GRAD_BINS")))) {
     // no zero factor anywhere: every term is a c*P weight (bit-sliced kernel)
+    // B <= 2: one 1024-thread CTA per SM shares one nibble table (32 warps);
+    // B = 4 (a 128 KB table): 256 threads
     const int ng = 16 * (int)s.B, ns = 2 * (int)s.B;
+    const int nt = s.B >= 4 ? 256 : 1024, nw = nt / 32;
     double* nib = ws.misc2.as<double>((size_t)ng * 256);
-    const size_t smem = ((size_t)ng * 256 + 8 * 128 + 8 * 32 + (size_t)8 * ns * 96) * sizeof(double);
-    const unsigned per_sm = s.B >= 4 ? 1u : 2u;
-    const unsigned grid = (unsigned)std::min<size_t>(148 * per_sm, std::max<size_t>(1, (s.M + 255) / 256));
+    const size_t smem = ((size_t)ng * 256 + (size_t)nw * 128 + (size_t)nw * 32 + (size_t)nw * ns * 96) * sizeof(double);
+    const unsigned grid = (unsigned)std::min<size_t>(148, std::max<size_t>(1, (s.M + nt - 1) / nt));
     const size_t stride = (size_t)ns * 96 + 2;
     double* part = ws.grad_part.as<double>((size_t)grid * stride);
     {
       KernelScope ks("qmf_grad");
       k_nibble_table<<<(ng * 256 + 255) / 256, 256, 0, st>>>(tab, ng, nib);
-#define IQCC_QF(B_)                                                                                        \
-  IQCC_CUDA(cudaFuncSetAttribute(k_qmf_grad_fr<B_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-  k_qmf_grad_fr<B_><<<grid, 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part)
+#define IQCC_QF(B_, NT_)                                                                                        \
+  IQCC_CUDA(cudaFuncSetAttribute(k_qmf_grad_fr<B_, NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+  k_qmf_grad_fr<B_, NT_><<<grid, NT_, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nib, part)
       switch (s.B) {
-        case 1: IQCC_QF(1); break;
-        case 2: IQCC_QF(2); break;
-        default: IQCC_QF(4); break;
+        case 1: IQCC_QF(1, 1024); break;
+        case 2: IQCC_QF(2, 1024); break;
+        default: IQCC_QF(4, 256); break;
       }
 #undef IQCC_QF
     }
