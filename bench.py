@@ -151,13 +151,15 @@ def measured_peaks():
 
 def profile_traffic():
     """DRAM bytes (read + write) per merge launch from the committed
-    `ncu --set full` capture at this workload (profiles/merge_traffic.json)."""
+    `ncu --set full` capture at this workload (profiles/merge_traffic.json),
+    and which capture it came from."""
     path = os.path.join(ROOT, "profiles", "merge_traffic.json")
     try:
         with open(path) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
+            t = json.load(f)
+        return float(t["dram_bytes_per_launch"]), t.get("capture")
     except Exception:
-        return None
+        return None, None
 
 
 # ----------------------------------------------------------------- CPU arm
@@ -334,7 +336,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     peak, peak_kind = measured_peaks()
     alg_bytes = native.profile_bytes("merge")
     achieved = alg_bytes / (merge_ms / 1e3) / 1e9 if merge_ms > 0 else 0.0
-    traffic = profile_traffic()
+    traffic, traffic_src = profile_traffic()
     # whole dressing step (plan + merge + compress) against the same peak:
     # the timed pass's algorithmic bytes over its device time (per rank)
     step_achieved = step_bytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
@@ -399,7 +401,7 @@ def run_gpu_arm(args, rank, world, local_rank):
             "clocks": clk.summary(),
             "roofline": {"bound": "hbm", "kernel": "k_merge1", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "launches": merge_n,
+                         "traffic": traffic, "traffic_source": traffic_src, "launches": merge_n,
                          "algorithmic_bytes": alg_bytes, "bytes_per_term": S},
             "step_roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
                               "frac": step_achieved / peak,
