@@ -23,6 +23,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/iqcc_b200.h"
 #include "engine.cuh"
 #include "multi.cuh"
@@ -122,9 +124,17 @@ static cudaEvent_t take_event() {
   return e;
 }
 
+// NVTX ranges (IQCC_NVTX=1): one range per kernel family launch and per
+// host scope, named by family, for nsys / ncu --nvtx timelines.
+static bool nvtx_on() {
+  static const bool on = getenv("IQCC_NVTX") && atoi(getenv("IQCC_NVTX")) != 0;
+  return on;
+}
+
 KernelScope::KernelScope(const char* f) : family(f) {
   Ctx& c = ctx();
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (nvtx_on()) nvtxRangePushA(f);
   if (c.profiling) {
     a = take_event();
     b = take_event();
@@ -134,6 +144,7 @@ KernelScope::KernelScope(const char* f) : family(f) {
 
 KernelScope::~KernelScope() {
   Ctx& c = ctx();
+  if (nvtx_on()) nvtxRangePop();
   cudaError_t le = cudaPeekAtLastError();
   if (a) {
     cudaEventRecord(b, c.cur);
@@ -198,8 +209,11 @@ static void host_ms(const char* fam, std::chrono::steady_clock::time_point t0) {
 static double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
-HostScope::HostScope(const char* f) : family(f), t0(now_ms()) {}
+HostScope::HostScope(const char* f) : family(f), t0(now_ms()) {
+  if (nvtx_on()) nvtxRangePushA(f);
+}
 HostScope::~HostScope() {
+  if (nvtx_on()) nvtxRangePop();
   Ctx& c = ctx();
   if (!c.profiling) return;
   auto& e = c.prof[family];

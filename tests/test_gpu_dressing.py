@@ -414,3 +414,24 @@ def test_debug_bounds_checks_pass():
                        capture_output=True, text=True, timeout=900, cwd=root, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "SANITIZE RUN OK" in r.stdout
+
+
+def test_c5_shape_uncapped_growth_then_cap(eng, port):
+    """SURVEY.md §8(d) C5 shape at a checkable size: G_mol(200 qubits, seed 5)
+    dressed without a cap for three steps (the store grows ~1.5x per step),
+    then compress(max_terms) — the memory-bounded truncation — bit-exact
+    against the reference pipeline."""
+    n, terms = 200, 300_000
+    gens, taus = _entanglers(n, 3, 55)
+    h = port.gen_mol(n, terms, 5)
+    d = eng.DeviceSum.generate_mol(n, terms, 5)
+    for g, t in zip(gens, taus):
+        h, _ = port.dress_sequence(h, g[None, :], [t], 0.0)
+        d.dress_sequence(eng.Ansatz([eng.PauliWord(n, g)], [t]), 0.0)
+        assert d.size() == len(h)
+    cap = int(0.8 * len(h))
+    want, st = port.compress(h, 1e-10, cap)
+    cs = eng.CompressStats()
+    d.compress(1e-10, cap, cs)
+    check_same(d.download(), want)
+    assert cs.dropped_terms == st["dropped_terms"]

@@ -6,6 +6,7 @@ DIS gradients are summed in the reference's order and compared bit-exactly;
 energies and QMF gradients are sums in a different order, compared at
 1e-10 relative (north_star's fp64 tolerance)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -357,3 +358,28 @@ def test_poly_kernels_edge_cases(eng, port):
 def ker_n(eng, port, n, th, ph, ents):
     z = port.sum(n, np.zeros((0, 2 * eng.blocks_for(n)), np.uint64), np.zeros(0, np.complex128))
     return port.poly_kernels(z, th, ph, ents, 2)[3]
+
+
+def test_c4_shape_gradients_bit_exact(eng, port):
+    """SURVEY.md §8(d) C4 shape: G_mol(100 qubits, seed 3) against odd-Y
+    candidates (seed 4) at a generic Omega and, flip-group restricted, at HF
+    poles.  Gradients are summed in canonical order like the reference's
+    gradient / group_gradient (dis.hpp:39-52, 121-132): bit-exact.  1e6 terms
+    here (the checker's pace); bench_aux runs the config's 1e7 x 1e5."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench_aux import odd_y_candidates
+    n, terms = 100, 1_000_000
+    h = port.gen_mol(n, terms, 3)
+    d = eng.DeviceSum.generate_mol(n, terms, 3)
+    cands = odd_y_candidates(n, 64, 4)
+    rs = np.random.default_rng(9)
+    th, ph = rs.uniform(-3, 3, n), rs.uniform(-3, 3, n)
+    sel = [0, 1, 9, 17, 40, 63]
+    g = d.gradients(eng.QmfState(th, ph), cands)
+    for k in sel:
+        assert g[k] == port.gradient(h, th, ph, cands[k]), k
+    thp = np.where(np.arange(n) < n // 4, np.pi, 0.0)
+    gp = d.gradients(eng.QmfState(thp, np.zeros(n)), cands, flip_group_only=True)
+    for k in sel:  # exact at the poles (every other term's contribution vanishes)
+        assert abs(gp[k] - port.gradient(h, thp, np.zeros(n), cands[k])) <= 1e-12 * max(1.0, abs(gp[k]))
