@@ -892,17 +892,31 @@ struct MergeCfg {
   }
 };
 
-template <int B>
+// Staged key rows in shared memory are split into 16-byte chunks: chunk h
+// (words 2h, 2h+1 of the device row) of element e at chunk index h*CAPR + e,
+// so a warp reading consecutive elements touches consecutive 16-byte slots
+// (conflict-free); row-major 32-byte rows made every such read 2-way bank
+// conflicted (ncu: 76% of the merge's excess shared wavefronts).
+// IQCC_SPLIT_SMEM=0 restores row-major rows filled by the TMA bulk engine.
+#ifndef IQCC_SPLIT_SMEM
+#define IQCC_SPLIT_SMEM 1
+#endif
+template <int B, int CAPR>
 __device__ __forceinline__ Key<B> sm_key16(const ull* sk, int e) {
   Key<B> k;
-  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(sk + (size_t)e * 2 * B);
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(sk);
 #pragma unroll
   for (int h = 0; h < B; ++h) {
-    ulonglong2 v = p[h];
+    const ulonglong2 v = IQCC_SPLIT_SMEM ? p[h * CAPR + e] : p[(size_t)e * B + h];
     k.w[2 * h] = v.x;
     k.w[2 * h + 1] = v.y;
   }
   return k;
+}
+/// 16-byte chunk h of staged element e (see sm_key16).
+template <int B, int CAPR>
+__device__ __forceinline__ ull* sm_chunk(ull* sk, int e, int h) {
+  return IQCC_SPLIT_SMEM ? sk + 2 * ((size_t)h * CAPR + e) : sk + (size_t)e * 2 * B + 2 * h;
 }
 
 struct MergeArgs {
@@ -946,36 +960,52 @@ __device__ __forceinline__ void cp_async4(void* s, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
 }
 
-template <int B, int NT>
-__device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull* sk, double* sc,
-                                            unsigned long long* mb, unsigned* sbits = nullptr, int BW = 0) {
-  const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
-  const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
-  const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0);
-  if (threadIdx.x == 0 && nS > 0) {
+/// Survivor rows [a0, a1) and their coefficients into a stage: split
+/// 16-byte chunks by per-thread cp.async (IQCC_SPLIT_SMEM), else one TMA
+/// bulk copy each (thread 0, completion on *mb).
+template <int B, int NT, int CAPR>
+__device__ __forceinline__ void stage_survivors(const MergeArgs& g, size_t a0, size_t a1, ull* sk, double* sc,
+                                                unsigned long long* mb) {
+  const int nS = (int)(a1 - a0);
+  if (nS <= 0) return;
+  const size_t c0 = a0 & ~(size_t)1, c1 = (a1 + 1) & ~(size_t)1;
+  if (IQCC_SPLIT_SMEM) {
+    for (int i = threadIdx.x; i < nS; i += NT) {
+      const ull* gk = g.keys + (a0 + i) * 2 * B;
+#pragma unroll
+      for (int h = 0; h < B; ++h) cp_async16(sm_chunk<B, CAPR>(sk, i, h), gk + 2 * h);
+    }
+    for (int i = threadIdx.x; i < (int)((c1 - c0) >> 1); i += NT) cp_async16(sc + 2 * i, g.coef + c0 + 2 * i);
+  } else if (threadIdx.x == 0) {
     const unsigned kb = (unsigned)nS * 16u * B;
-    const size_t c0 = a0 & ~(size_t)1, c1 = (a1 + 1) & ~(size_t)1;
     const unsigned cb = (unsigned)((c1 - c0) * 8);
     mbar_expect_tx(mb, kb + cb);
     bulk_g2s(sk, g.keys + a0 * 2 * B, kb, mb);
     bulk_g2s(sc, g.coef + c0, cb, mb);
   }
+}
+
+template <int B, int NT, int CAPR>
+__device__ __forceinline__ void merge_issue(const MergeArgs& g, size_t tile, ull* sk, double* sc,
+                                            unsigned long long* mb, unsigned* sbits = nullptr, int BW = 0) {
+  const size_t a0 = g.part_a[tile], a1 = g.part_a[tile + 1];
+  const size_t b0 = g.part_b[tile], b1 = g.part_b[tile + 1];
+  const int nS = (int)(a1 - a0), nQ = (int)(b1 - b0);
+  stage_survivors<B, NT, CAPR>(g, a0, a1, sk, sc, mb);
   const int qc0 = nS + 4;
   if (g.q_keys) {  // contiguous received products
     for (int j = threadIdx.x; j < nQ; j += NT) {
       const ull* gk = g.q_keys + (b0 + j) * 2 * B;
-      ull* s = sk + (size_t)(nS + j) * 2 * B;
 #pragma unroll
-      for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, gk + 2 * h);
+      for (int h = 0; h < B; ++h) cp_async16(sm_chunk<B, CAPR>(sk, nS + j, h), gk + 2 * h);
       cp_async8(sc + qc0 + j, g.q_vals + b0 + j);
     }
   } else {
     for (int j = threadIdx.x; j < nQ; j += NT) {
       const size_t src = __ldg(g.inv_perm + b0 + j);
       const ull* gk = g.keys + src * 2 * B;
-      ull* s = sk + (size_t)(nS + j) * 2 * B;
 #pragma unroll
-      for (int h = 0; h < B; ++h) cp_async16(s + 2 * h, gk + 2 * h);
+      for (int h = 0; h < B; ++h) cp_async16(sm_chunk<B, CAPR>(sk, nS + j, h), gk + 2 * h);
       cp_async8(sc + qc0 + j, g.coef + src);
     }
   }
@@ -1074,7 +1104,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   // received products arrive as final keys and values
   const bool qdirect = g.q_keys != nullptr;
   const Key<B> PX = qdirect ? Key<B>{} : P;
-  auto qkey = [&](int j) { return key_xor<B>(sm_key16<B>(sk, nS + j), PX); };
+  auto qkey = [&](int j) { return key_xor<B>(sm_key16<B, Cfg::CAP>(sk, nS + j), PX); };
   auto qval = [&](int j, const Key<B>& kq) {
     if (qdirect) return sc[qc0 + j];
     const double pr = __dmul_rn(sc[qc0 + j], g.sn);
@@ -1085,7 +1115,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
     int lo = max(0, d - nQ), hi = min(d, nS);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (key_cmp<B>(sm_key16<B>(sk, mid), qkey(d - 1 - mid)) <= 0)
+      if (key_cmp<B>(sm_key16<B, Cfg::CAP>(sk, mid), qkey(d - 1 - mid)) <= 0)
         lo = mid + 1;
       else
         hi = mid;
@@ -1094,7 +1124,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
     const int b = d - lo;
     if (b < nQ) {
       const Key<B> q = qkey(b);
-      while (a > 0 && key_cmp<B>(sm_key16<B>(sk, a - 1), q) == 0) --a;
+      while (a > 0 && key_cmp<B>(sm_key16<B, Cfg::CAP>(sk, a - 1), q) == 0) --a;
     }
     s_ta[threadIdx.x] = a;
     s_tb[threadIdx.x] = b;
@@ -1137,7 +1167,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
   {
     int i = ia0, j = ib0;
     Key<B> ks, kq;
-    if (i < ia1) ks = sm_key16<B>(sk, i);
+    if (i < ia1) ks = sm_key16<B, Cfg::CAP>(sk, i);
     if (j < ib1) kq = qkey(j);
     auto put = [&](double v, int e) {
       if (dbg_ok(g.dbg, 2, (ull)slot, (ull)nslots)) {
@@ -1184,7 +1214,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
         const double qv = qval(j, kq);
         put(keep_term(qv, b0 + j == 0 && key_is_identity<B>(kq), g.drop) ? qv : dead_value(), nS + j);
       }
-      if (c <= 0 && ++i < ia1) ks = sm_key16<B>(sk, i);
+      if (c <= 0 && ++i < ia1) ks = sm_key16<B, Cfg::CAP>(sk, i);
       if (c >= 0 && ++j < ib1) kq = qkey(j);
     }
   }
@@ -1199,7 +1229,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
     if (q < nslots) {
       const int e = oute[q];
       const double v = outv[q];
-      const Key<B> k = e < nS ? sm_key16<B>(sk, e) : qkey(e - nS);
+      const Key<B> k = e < nS ? sm_key16<B, Cfg::CAP>(sk, e) : qkey(e - nS);
       store_key<B>(g.out_keys, o0 + q, k);
       g.out_coef[o0 + q] = v;
       if (is_dead(v)) {
@@ -1223,7 +1253,7 @@ __device__ __forceinline__ void merge_compute(const MergeArgs& g, size_t tile, c
         short l = -1;  // tile-first slot: fixed up by k_meta_fix
         if (q > 0) {
           const int ep = oute[q - 1];
-          l = (short)key_lcp<B>(ep < nS ? sm_key16<B>(sk, ep) : qkey(ep - nS), k);
+          l = (short)key_lcp<B>(ep < nS ? sm_key16<B, Cfg::CAP>(sk, ep) : qkey(ep - nS), k);
         }
         g.out_lcp[o0 + q] = l;
         anti = anticommutes<B>(k, PN);
@@ -1301,9 +1331,9 @@ __global__ void __launch_bounds__(NT, merge_minb(B, NT)) k_merge1(MergeArgs g, K
   unsigned* sbits = reinterpret_cast<unsigned*>(smem_raw + Cfg::OFF_SBITS);
   const TileBounds tb{g.part_a[tile], g.part_a[tile + 1], g.part_b[tile],
                       g.part_b[tile + 1], g.part_o[tile], g.part_o[tile + 1]};
-  merge_issue<B, NT>(g, tile, sk, sc, &mbar, sbits, Cfg::BW);
+  merge_issue<B, NT, Cfg::CAP>(g, tile, sk, sc, &mbar, sbits, Cfg::BW);
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  if (tb.a1 > tb.a0) mbar_wait(&mbar, 0);
+  if (!IQCC_SPLIT_SMEM && tb.a1 > tb.a0) mbar_wait(&mbar, 0);
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar)) : "memory");
   int n_eps = 0, n_dead = 0, n_coll = 0, n_ge = 0;
@@ -1339,19 +1369,19 @@ __global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PMERGE_MINB) * 256 / NT
     return reinterpret_cast<double*>(smem_raw + st * Cfg::STAGE + Cfg::KEYB);
   };
   size_t tile = blockIdx.x;
-  if (tile < g.ntiles) merge_issue<B, NT>(g, tile, stage_k(0), stage_c(0), &mbar[0]);
+  if (tile < g.ntiles) merge_issue<B, NT, Cfg::CAP>(g, tile, stage_k(0), stage_c(0), &mbar[0]);
   unsigned phase[2] = {0u, 0u};
   int n_eps = 0, n_dead = 0, n_coll = 0, n_ge = 0;
   for (int it = 0; tile < g.ntiles; ++it, tile += gridDim.x) {
     const int cur = it & 1;
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    if (g.part_a[tile + 1] > g.part_a[tile]) {
+    if (!IQCC_SPLIT_SMEM && g.part_a[tile + 1] > g.part_a[tile]) {
       mbar_wait(&mbar[cur], phase[cur]);
       phase[cur] ^= 1u;
     }
     __syncthreads();
     const size_t next = tile + gridDim.x;
-    if (next < g.ntiles) merge_issue<B, NT>(g, next, stage_k(cur ^ 1), stage_c(cur ^ 1), &mbar[cur ^ 1]);
+    if (next < g.ntiles) merge_issue<B, NT, Cfg::CAP>(g, next, stage_k(cur ^ 1), stage_c(cur ^ 1), &mbar[cur ^ 1]);
     merge_compute<B, NT, IPT>(g, tile, P, stage_k(cur), stage_c(cur), smem_raw, n_eps, n_dead, n_coll, n_ge);
     __syncthreads();  // stage `cur` and the staging list are free again
   }
@@ -1434,21 +1464,13 @@ __global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PIPE_MINB) * 256 / NT) 
     double* sc = reinterpret_cast<double*>(base + M::KEYB);
     unsigned* bits = reinterpret_cast<unsigned*>(base + Cfg::OFF_BITS);
     const int nS = (int)(tb.a1 - tb.a0), nQ = (int)(tb.b1 - tb.b0);
-    if (threadIdx.x == 0 && nS > 0) {
-      const unsigned kb = (unsigned)nS * 16u * B;
-      const size_t c0 = tb.a0 & ~(size_t)1, c1 = (tb.a1 + 1) & ~(size_t)1;
-      const unsigned cb = (unsigned)((c1 - c0) * 8);
-      mbar_expect_tx(&mbar[st], kb + cb);
-      bulk_g2s(sk, g.keys + tb.a0 * 2 * B, kb, &mbar[st]);
-      bulk_g2s(sc, g.coef + c0, cb, &mbar[st]);
-    }
+    stage_survivors<B, NT, M::CAP>(g, tb.a0, tb.a1, sk, sc, &mbar[st]);
     const int qc0 = nS + 4;
     if (g.q_keys) {
       for (int j = threadIdx.x; j < nQ; j += NT) {
         const ull* gk = g.q_keys + (tb.b0 + j) * 2 * B;
-        ull* d = sk + (size_t)(nS + j) * 2 * B;
 #pragma unroll
-        for (int h = 0; h < B; ++h) cp_async16(d + 2 * h, gk + 2 * h);
+        for (int h = 0; h < B; ++h) cp_async16(sm_chunk<B, M::CAP>(sk, nS + j, h), gk + 2 * h);
         cp_async8(sc + qc0 + j, g.q_vals + tb.b0 + j);
       }
     } else {
@@ -1456,9 +1478,8 @@ __global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PIPE_MINB) * 256 / NT) 
       for (int j = threadIdx.x; j < nQ; j += NT) {
         const size_t src = ix[j];
         const ull* gk = g.keys + src * 2 * B;
-        ull* d = sk + (size_t)(nS + j) * 2 * B;
 #pragma unroll
-        for (int h = 0; h < B; ++h) cp_async16(d + 2 * h, gk + 2 * h);
+        for (int h = 0; h < B; ++h) cp_async16(sm_chunk<B, M::CAP>(sk, nS + j, h), gk + 2 * h);
         cp_async8(sc + qc0 + j, g.coef + src);
       }
     }
@@ -1506,7 +1527,7 @@ __global__ void __launch_bounds__(NT, (B >= 4 ? 2 : IQCC_PIPE_MINB) * 256 / NT) 
     // data(k) and idx(k+1) landed; bounds(k+2) parked by the previous iteration
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     const TileBounds tb = s_tb[k % 3];
-    if (tb.a1 > tb.a0) {
+    if (!IQCC_SPLIT_SMEM && tb.a1 > tb.a0) {
       mbar_wait(&mbar[cur], phase[cur]);
       phase[cur] ^= 1u;
     }
