@@ -307,14 +307,7 @@ void* DevBuf::get(size_t n) {
   devbuf_free(p, big, bytes);
   p = nullptr;
   bytes = 0;
-  // generous slack: stores grow ~1.5x per uncapped step; blocks of 1 GB and
-  // up double (a fresh cudaMalloc of that size costs tens of milliseconds,
-  // more than a dressing step; HBM holds 180 GB)
-#ifndef IQCC_BIG_SLACK_2X
-#define IQCC_BIG_SLACK_2X 1
-#endif
-  const size_t slack = IQCC_BIG_SLACK_2X && n >= ((size_t)1 << 30) ? n : n / 2;
-  size_t want = std::max<size_t>(n + slack, 256);
+  size_t want = std::max<size_t>(n + n / 2, 256);  // generous slack: stores grow ~1.5x per step
   big = want >= kBigAlloc;
   if (big) {
     size_t got = 0;

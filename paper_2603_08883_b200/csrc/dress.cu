@@ -892,14 +892,15 @@ struct MergeCfg {
   }
 };
 
-// Staged key rows in shared memory are split into 16-byte chunks: chunk h
-// (words 2h, 2h+1 of the device row) of element e at chunk index h*CAPR + e,
-// so a warp reading consecutive elements touches consecutive 16-byte slots
-// (conflict-free); row-major 32-byte rows made every such read 2-way bank
-// conflicted (ncu: 76% of the merge's excess shared wavefronts).
-// IQCC_SPLIT_SMEM=0 restores row-major rows filled by the TMA bulk engine.
+// Staged key rows in shared memory: row-major (default; survivors land by
+// one TMA bulk copy), or with IQCC_SPLIT_SMEM=1 split into 16-byte chunks
+// (chunk h of element e at chunk index h*CAPR + e), which makes a warp's
+// reads of consecutive elements bank-conflict free (row-major 32-byte rows
+// are 2-way conflicted: 76% of the merge's excess shared wavefronts under
+// ncu) but needs per-thread cp.async for the survivors: measured 1.6 ms per
+// bench step slower (profiles/r2_summary.md), so row-major stays.
 #ifndef IQCC_SPLIT_SMEM
-#define IQCC_SPLIT_SMEM 1
+#define IQCC_SPLIT_SMEM 0
 #endif
 template <int B, int CAPR>
 __device__ __forceinline__ Key<B> sm_key16(const ull* sk, int e) {
