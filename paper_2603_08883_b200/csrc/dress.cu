@@ -2023,14 +2023,22 @@ DressOutcome dress_impl(DeviceStore& s, const uint64_t* gen_row, double cs, doub
 template <int B>
 __global__ void k_materialize(const ull* __restrict__ keys, const double* __restrict__ coef,
                               const unsigned* __restrict__ inv_perm, size_t r0, size_t A, Key<B> P,
-                              double sn, ull* __restrict__ okeys, double* __restrict__ ovals) {
+                              double sn, ull* __restrict__ okeys, double* __restrict__ ovals,
+                              double thq, unsigned* __restrict__ obits) {
   const size_t r = r0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (r >= A) return;
-  const unsigned src = inv_perm[r];
-  const Key<B> k = load_key<B>(keys, src);
-  const double pr = __dmul_rn(coef[src], sn);
-  store_key<B>(okeys, r, key_xor<B>(k, P));
-  ovals[r] = product_phase<B>(k, P) == 1 ? pr : -pr;
+  double v = 0.0;
+  if (r < A) {
+    const unsigned src = inv_perm[r];
+    const Key<B> k = load_key<B>(keys, src);
+    const double pr = __dmul_rn(coef[src], sn);
+    store_key<B>(okeys, r, key_xor<B>(k, P));
+    v = product_phase<B>(k, P) == 1 ? pr : -pr;
+    ovals[r] = v;
+  }
+  if (obits) {  // the receiver's slot bits (SlotRule: |v| >= thq), r0 % 32 == 0
+    const unsigned b = __ballot_sync(0xffffffffu, r < A && fabs(v) >= thq);
+    if ((threadIdx.x & 31) == 0 && r < A) obits[r >> 5] = b;
+  }
 }
 
 /// Products pushed straight into a peer's receive buffer over NVLink (CUDA
@@ -2162,17 +2170,45 @@ size_t plan_products(DeviceStore& s, const uint64_t* gen_row, bool products) {
 }
 
 void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
-                          double* ovals, size_t r0, size_t r1, const char* family) {
+                          double* ovals, size_t r0, size_t r1, const char* family, double thq,
+                          unsigned* obits) {
   r1 = std::min(r1, g_plan.A);
   if (r1 <= r0) return;
   cudaStream_t st = stream();
   KernelScope ks(family);
   const unsigned grid = (unsigned)((r1 - r0 + 255) / 256);
   switch (s.B) {
-    case 1: k_materialize<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<1>(gen_row), sn, okeys, ovals); break;
-    case 2: k_materialize<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<2>(gen_row), sn, okeys, ovals); break;
-    default: k_materialize<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<4>(gen_row), sn, okeys, ovals); break;
+    case 1: k_materialize<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<1>(gen_row), sn, okeys, ovals, thq, obits); break;
+    case 2: k_materialize<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<2>(gen_row), sn, okeys, ovals, thq, obits); break;
+    default: k_materialize<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, r0, r1, make_key<4>(gen_row), sn, okeys, ovals, thq, obits); break;
   }
+}
+
+/// Slot bits of n received products already packed by the sender (bits
+/// words, possibly in a peer's memory): the local prefix for the merge.
+void recv_slot_bits_packed(const unsigned* bits, size_t n, double thq) {
+  g_plan.qbits = g_plan.qpre = g_plan.qtotal = nullptr;
+  g_plan.Wq = 0;
+  if (thq == 0.0) return;
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const size_t Wq = (n + 31) / 32, nbq = (Wq + PW - 1) / PW;
+  unsigned* qpre = ws.qbits.as<unsigned>(std::max<size_t>(Wq, 1) + nbq + 64);
+  unsigned* qbs = qpre + std::max<size_t>(Wq, 1);
+  unsigned* qtot = qbs + nbq + 4;
+  IQCC_CUDA(cudaMemsetAsync(qtot, 0, sizeof(unsigned), st));
+  if (n > 0) {
+    KernelScope ks("present");
+    k_popc_blocks<<<(unsigned)nbq, 256, 0, st>>>(bits, Wq, qbs);
+    k_scan_blocks<<<1, 1024, 0, st>>>(qbs, nbq, qtot);
+    k_popc_prefix<<<(unsigned)nbq, 256, 0, st>>>(bits, Wq, qbs, qpre);
+    count_launch("present");
+    count_launch("present");
+  }
+  g_plan.qbits = bits;
+  g_plan.qpre = qpre;
+  g_plan.qtotal = qtot;
+  g_plan.Wq = Wq;
 }
 
 template <int B>

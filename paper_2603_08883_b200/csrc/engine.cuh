@@ -494,9 +494,14 @@ void plan_set_products(size_t A);
 /// (okeys/ovals: CUDA IPC mapping over NVLink), staged per 256-product tile.
 void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals);
 /// Products [r0, r1) of the planned order (clamped to the product count).
+/// thq / obits (optional): also pack the receiver's product slot bits
+/// (|v| >= thq) into obits (one bit per product, r0 % 32 == 0).
 void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys,
                           double* ovals, size_t r0 = 0, size_t r1 = SIZE_MAX,
-                          const char* family = "materialize");
+                          const char* family = "materialize", double thq = 0.0,
+                          unsigned* obits = nullptr);
+/// recv_slot_bits from bits the sender packed (possibly in peer memory).
+void recv_slot_bits_packed(const unsigned* bits, size_t n, double thq);
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
                             const double* q_vals, const uint64_t* next_row = nullptr,

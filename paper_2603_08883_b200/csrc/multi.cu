@@ -157,7 +157,7 @@ void p2p_prepare(size_t need, size_t W) {
   p2p_free();
   g_p2p.tried = true;
   const size_t cap = (size_t)need_g + need_g / 4 + 1024;
-  bool ok = cudaMalloc(&g_p2p.mine, cap * (W * 8 + 8)) == cudaSuccess;
+  bool ok = cudaMalloc(&g_p2p.mine, cap * (W * 8 + 8) + (cap / 32 + 64) * 4) == cudaSuccess;
   cudaIpcMemHandle_t h;
   std::memset(&h, 0, sizeof(h));
   if (ok) ok = cudaIpcGetMemHandle(&h, g_p2p.mine) == cudaSuccess;
@@ -333,7 +333,29 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     const size_t xcap = std::max<size_t>({A, nrecv, s.M, 1});
     ull* sk = p2p ? nullptr : ws.xbuf_keys.as<ull>(xcap * W);
     double* sv = p2p ? nullptr : ws.xbuf_coef.as<double>(xcap);
-    if (p2p) {
+    // IQCC_XCHG=pull: each rank writes its sorted products (and the
+    // receiver's slot bits) into its OWN peer-visible buffer at HBM speed,
+    // and the partner's merge reads them over NVLink while it merges (no
+    // separate transfer pass); default: push them into the partner's buffer
+    static const bool pull = getenv("IQCC_XCHG") && std::string(getenv("IQCC_XCHG")) == "pull";
+    const unsigned* rbits = nullptr;
+    if (p2p && pull) {
+      char* mine = g_p2p.mine;
+      unsigned* mbits = reinterpret_cast<unsigned*>(mine + g_p2p.cap * (W * 8 + 8));
+      materialize_products(s, gen_row, sn, reinterpret_cast<ull*>(mine),
+                           reinterpret_cast<double*>(mine + g_p2p.cap * W * 8), 0, SIZE_MAX, "exchange", theta,
+                           theta != 0.0 ? mbits : nullptr);
+      KernelScope ks2("exch_signal");
+      char* src = g_p2p.peer[peer];
+      rk = reinterpret_cast<ull*>(src);
+      rv = reinterpret_cast<double*>(src + g_p2p.cap * W * 8);
+      rbits = reinterpret_cast<const unsigned*>(src + g_p2p.cap * (W * 8 + 8));
+      // my products are written -> the partner may read them (and its are ready)
+      IQCC_NCCL(ncclGroupStart());
+      IQCC_NCCL(ncclSend(cnt, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclRecv(cnt + 2, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclGroupEnd());
+    } else if (p2p) {
       // the SMs gather the sorted products and write them, tile by tile,
       // straight into the partner's receive buffer over NVLink
       char* dst = g_p2p.peer[peer];
@@ -369,7 +391,10 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     x.recv_terms = nrecv;
     x.bytes_wire = A * (W * 8 + 8);
     x.bytes_reference = A * (16 + Bref * 16);  // MessageLog formula, partition.hpp:420-422
-    recv_slot_bits(rv, nrecv, theta);
+    if (rbits)
+      recv_slot_bits_packed(rbits, nrecv, theta);
+    else
+      recv_slot_bits(rv, nrecv, theta);
     o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, theta);
   }
   if (xs) *xs = x;

@@ -22,21 +22,27 @@ def n_gpus():
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq"),
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "badspec"),
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "nccl"),
+                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "pull"),
+                                  ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "pull", "badspec"),
                                   ("200", "1e5", "6", "1e-10", "1.2e5", "seq")])
 def test_partitioned_dressing_matches_serial(world, args):
     """The sequence cases exercise the output-slot speculation on the
     exchange and the local steps; "badspec" forces every guess too high
     (IQCC_SPEC_SCALE), so every step is undone and redone exactly; "nccl"
     moves the products with NCCL send/recv (the fallback of the CUDA-IPC
-    NVLink push)."""
+    NVLink push); "pull" lets the partner's merge read them in place over
+    NVLink (IQCC_XCHG=pull)."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ)
     if args[-1] == "badspec":
         env["IQCC_SPEC_SCALE"] = "64"
         args = args[:-1]
-    elif args[-1] == "nccl":  # products over NCCL send/recv instead of the NVLink push
+    if args[-1] == "nccl":  # products over NCCL send/recv instead of the NVLink push
         env["IQCC_NO_P2P"] = "1"
+        args = args[:-1]
+    elif args[-1] == "pull":  # the partner's merge reads the products over NVLink
+        env["IQCC_XCHG"] = "pull"
         args = args[:-1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "multi_worker.py"),
