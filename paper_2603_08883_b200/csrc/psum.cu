@@ -49,6 +49,11 @@
 namespace iqcc_b200 {
 namespace {
 
+/// Thrown by a barrier another shard aborted (a secondary failure).
+struct ShardAborted : std::runtime_error {
+  ShardAborted() : std::runtime_error("partitioned sum: another shard failed") {}
+};
+
 /// Generation barrier over the shard threads; abort() releases every waiter
 /// with an exception so one failing shard cannot hang the others.
 class Barrier {
@@ -61,7 +66,7 @@ class Barrier {
   }
   void wait() {
     std::unique_lock<std::mutex> lk(mu_);
-    if (aborted_) throw std::runtime_error("partitioned sum: another shard failed");
+    if (aborted_) throw ShardAborted();
     const uint64_t g = gen_;
     if (++count_ == n_) {
       count_ = 0;
@@ -70,7 +75,7 @@ class Barrier {
       return;
     }
     cv_.wait(lk, [&] { return gen_ != g || aborted_; });
-    if (gen_ == g) throw std::runtime_error("partitioned sum: another shard failed");
+    if (gen_ == g) throw ShardAborted();
   }
   void abort() {
     std::lock_guard<std::mutex> lk(mu_);
@@ -166,8 +171,20 @@ struct PSum {
     cv.notify_all();
     std::unique_lock<std::mutex> lk(mu);
     done_cv.wait(lk, [&] { return done == n_parts(); });
-    for (auto& e : err)
-      if (e) std::rethrow_exception(e);
+    // the first primary failure in shard order (not the aborts it caused)
+    std::exception_ptr first;
+    for (auto& e : err) {
+      if (!e) continue;
+      if (!first) first = e;
+      try {
+        std::rethrow_exception(e);
+      } catch (const ShardAborted&) {
+        continue;
+      } catch (...) {
+        std::rethrow_exception(e);
+      }
+    }
+    if (first) std::rethrow_exception(first);
   }
 
   void start() {

@@ -81,6 +81,12 @@ def test_wrong_shard_rejected(eng, port):  # PartitionedSum::validate (partition
         eng.PartitionedSum.from_shards([h, eng.PauliSum(5), eng.PauliSum(5), eng.PauliSum(5)], pm)
     with pytest.raises(ValueError):  # owner out of range
         eng.distribute(h, eng.PartitionMap(5, [0, 2], [0, 1, 2, 3], 2))
+    # a non-canonical input fails with the upload's invalid_argument (not the
+    # "another shard failed" of the shards it released), on any device layout
+    u = eng.PauliSum(5, h.rows[::-1].copy(), h.coeffs[::-1].copy())
+    for devs in device_layouts(2):
+        with pytest.raises(ValueError):
+            eng.distribute(u, fixed_map(eng, 5, [0, 2], 2), devs)
 
 
 def test_local_entangler_moves_nothing(eng, port):  # test_partition.cpp:136-155 (seed 617)
