@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <climits>
 #include <cstring>
+#include <optional>
 #include <stdexcept>
 
 #include "engine.cuh"
@@ -174,15 +175,19 @@ __global__ void __launch_bounds__(256) k_popc_blocks(const unsigned* __restrict_
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
+// in-place exclusive scan of nb block counts; `base` (optional, device)
+// offsets the prefix and the total (a chunk continuing the previous one)
 __global__ void __launch_bounds__(1024) k_scan_blocks(unsigned* __restrict__ bsum, size_t nb,
-                                                      unsigned* __restrict__ total) {
+                                                      unsigned* total, const unsigned* base = nullptr) {
   __shared__ unsigned sm[1024 / 32 + 2];
   const size_t per = (nb + 1023) / 1024;
   const size_t lo = threadIdx.x * per, hi = min(nb, lo + per);
+  const unsigned b0 = base ? *base : 0u;
   unsigned c = 0;
   for (size_t k = lo; k < hi; ++k) c += bsum[k];
   unsigned tot;
-  unsigned run = block_exclusive<1024>(c, 0u, OpAdd(), sm, &tot);
+  unsigned run = block_exclusive<1024>(c, 0u, OpAdd(), sm, &tot) + b0;
+  tot += b0;
   for (size_t k = lo; k < hi; ++k) {
     const unsigned v = bsum[k];
     bsum[k] = run;
@@ -735,10 +740,12 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
                             const unsigned* __restrict__ ptotal, const unsigned* __restrict__ qbits,
                             const unsigned* __restrict__ qpre, size_t Wq,
                             const unsigned* __restrict__ qtotal, int coarse_shift,
-                            ull* __restrict__ raw_a) {
+                            ull* __restrict__ raw_a, size_t a_base = 0, size_t b_base = 0) {
   // two passes: coarse_shift > 0 searches every 2^shift-th boundary over the
   // whole range and records the raw split; coarse_shift == 0 searches every
-  // boundary inside the window between its two coarse neighbours
+  // boundary inside the window between its two coarse neighbours.  A chunk
+  // of a chunked merge is the sub-merge of S[a_base, a_base + nS) and
+  // Q[b_base, b_base + nQ) (outputs absolute)
   const size_t t = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) << coarse_shift;
   if (t > ntiles) return;
   const size_t d = min(t * tile_items, nS + nQ);
@@ -750,7 +757,8 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
   }
   while (lo < hi) {
     size_t mid = (lo + hi) >> 1;
-    if (key_cmp<B>(load_key<B>(keys, mid), q_key<B>(keys, inv_perm, q_keys, d - 1 - mid, P)) <= 0)
+    if (key_cmp<B>(load_key<B>(keys, a_base + mid),
+                   q_key<B>(keys, inv_perm, q_keys, b_base + d - 1 - mid, P)) <= 0)
       lo = mid + 1;
     else
       hi = mid;
@@ -762,9 +770,11 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
   }
   // never split a run of equal survivors (live + dead slot) from its product
   if (b < nQ) {
-    const Key<B> q = q_key<B>(keys, inv_perm, q_keys, b, P);
-    while (a > 0 && key_cmp<B>(load_key<B>(keys, a - 1), q) == 0) --a;
+    const Key<B> q = q_key<B>(keys, inv_perm, q_keys, b_base + b, P);
+    while (a > 0 && key_cmp<B>(load_key<B>(keys, a_base + a - 1), q) == 0) --a;
   }
+  a += a_base;
+  b += b_base;
   part_a[t] = a;
   part_b[t] = b;
   // output slots before this tile: survivors and products that own a slot
@@ -780,7 +790,8 @@ __global__ void k_partition(const ull* __restrict__ keys, const unsigned* __rest
 template <int B>
 __global__ void k_partition_coarse(const ull* __restrict__ keys, const unsigned* __restrict__ inv_perm,
                                    const ull* __restrict__ q_keys, size_t nS, size_t nQ, Key<B> P,
-                                   size_t tile_items, size_t ntiles, ull* __restrict__ raw_a) {
+                                   size_t tile_items, size_t ntiles, ull* __restrict__ raw_a,
+                                   size_t a_base = 0, size_t b_base = 0) {
   const size_t c = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const size_t t = c << kPartShift;
@@ -793,7 +804,8 @@ __global__ void k_partition_coarse(const ull* __restrict__ keys, const unsigned*
     const size_t step = (span + 31) / 32;  // probe lo + step*(lane+1) - 1
     const size_t m = lo + step * (lane + 1) - 1;
     bool pr = true;
-    if (m < hi) pr = key_cmp<B>(load_key<B>(keys, m), q_key<B>(keys, inv_perm, q_keys, d - 1 - m, P)) <= 0;
+    if (m < hi)
+      pr = key_cmp<B>(load_key<B>(keys, a_base + m), q_key<B>(keys, inv_perm, q_keys, b_base + d - 1 - m, P)) <= 0;
     const unsigned fails = __ballot_sync(0xffffffffu, !pr);
     if (fails == 0) {
       // every probe below hi held: the split lies past the last of them
@@ -1816,29 +1828,44 @@ thread_local int g_sub_b0 = -(1 << 20);  // fine-histogram window of the last me
 template <int B, int NT, int IPT>
 void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys, const double* q_vals,
                     double cs, double sn, double drop, bool want_hist, double eps, const Key<B>* PN,
-                    double theta) {
+                    double theta, const ChunkPlan* cp) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   const PlanState& pl = g_plan;
   constexpr int TILEM = NT * IPT;
   const size_t M = s.M;
   const size_t total = M + nQ;
-  const size_t ntm = std::max<size_t>(1, (total + TILEM - 1) / TILEM);
-  const size_t nco = (ntm >> kPartShift) + 1;  // coarse boundaries 0, 32, 64, ... <= ntm
-  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1) + nco + 8);
+  // tiles: one range, or per chunk of a chunked merge (chunk c = S[a_c,
+  // a_c+1) with Q[r_c, r_c+1), tiles [T_c, T_c+1) of one global tile list)
+  const int C = cp ? cp->C : 1;
+  std::vector<size_t> tc(C + 1, 0);
+  size_t nco_max = 1;
+  for (int c = 0; c < C; ++c) {
+    const size_t len = cp ? (cp->a[c + 1] - cp->a[c]) + (cp->r[c + 1] - cp->r[c]) : total;
+    const size_t n = cp ? (len + TILEM - 1) / TILEM : std::max<size_t>(1, (total + TILEM - 1) / TILEM);
+    tc[c + 1] = tc[c] + n;
+    nco_max = std::max(nco_max, (n >> kPartShift) + 1);
+  }
+  const size_t ntm = tc[C];
+  if (cp && (ntm == 0 || cp->a[C] != M || cp->r[C] != nQ))
+    throw std::logic_error("chunked merge: chunk bounds do not cover the inputs");
+  ull* pa = ws.part_a.as<ull>(3 * (ntm + 1) + nco_max + 8);
   ull* pb = pa + (ntm + 1);
   ull* po = pb + (ntm + 1);
-  {
+  auto partition = [&](int c, const unsigned* qtotal, size_t Wq) {
     KernelScope ks("partition");
     ull* raw = po + (ntm + 1);
-    const unsigned* qb = pl.qbits;
+    const size_t a0 = cp ? cp->a[c] : 0, b0 = cp ? cp->r[c] : 0;
+    const size_t nS = cp ? cp->a[c + 1] - a0 : M, nq = cp ? cp->r[c + 1] - b0 : nQ;
+    const size_t n = tc[c + 1] - tc[c], nco = (n >> kPartShift) + 1;
     k_partition_coarse<B><<<(unsigned)((nco * 32 + 255) / 256), 256, 0, st>>>(
-        s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, raw);
-    k_partition<B><<<(unsigned)((ntm + 1 + 255) / 256), 256, 0, st>>>(
-        s.keys(), pl.inv_perm, q_keys, M, nQ, P, TILEM, ntm, pa, pb, po, pl.pmask, pl.ppre, pl.W,
-        pl.ptotal, qb, pl.qpre, pl.Wq, pl.qtotal, 0, raw);
+        s.keys(), pl.inv_perm, q_keys, nS, nq, P, TILEM, n, raw, a0, b0);
+    k_partition<B><<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(
+        s.keys(), pl.inv_perm, q_keys, nS, nq, P, TILEM, n, pa + tc[c], pb + tc[c], po + tc[c], pl.pmask,
+        pl.ppre, pl.W, pl.ptotal, pl.qbits, pl.qpre, Wq, qtotal, 0, raw, a0, b0);
     count_launch("partition");
-  }
+  };
+  if (!cp) partition(0, pl.qtotal, pl.Wq);
   ull* out_keys = ws.out_keys.as<ull>(std::max<size_t>(total, 1) * 2 * B);
   double* out_coef = ws.out_coef.as<double>(std::max<size_t>(total, 1));
   ull* ctr = ws.counters.as<ull>(16);
@@ -1888,7 +1915,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
   }
   static const bool persistent = getenv("IQCC_MERGE_PERSIST") != nullptr;
   static const bool pipelined = getenv("IQCC_MERGE_PIPE") != nullptr && atoi(getenv("IQCC_MERGE_PIPE")) != 0;
-  if (pipelined) {
+  if (pipelined && !cp) {
     using PC = PipeCfg<B, NT, IPT>;
     static int ctas_per_sm = 0, n_sm = 0;
     const int dev = ctx_device(ctx_current());
@@ -1907,7 +1934,7 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
     KernelScope ks("merge");
     const unsigned grid = (unsigned)std::min<size_t>(ntm, (size_t)n_sm * ctas_per_sm);
     k_merge_pipe<B, NT, IPT><<<grid, NT, PC::bytes(want_hist), st>>>(g, P);
-  } else if (persistent) {
+  } else if (persistent && !cp) {
     static int ctas_per_sm = 0, n_sm = 0;
     if (func_attr_once((const void*)k_merge<B, NT, IPT>, ctx_device(ctx_current())))
       IQCC_CUDA(cudaFuncSetAttribute(k_merge<B, NT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1928,8 +1955,28 @@ void launch_merge_t(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_key
       IQCC_CUDA(cudaFuncSetAttribute(k_merge1<B, NT, IPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      (int)cudaSharedmemCarveoutMaxShared));
     }
-    KernelScope ks("merge");
-    k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
+    if (!cp) {
+      KernelScope ks("merge");
+      k_merge1<B, NT, IPT><<<(unsigned)ntm, NT, Cfg::bytes(want_hist, 1), st>>>(g, P);
+    } else {
+      // chunk by chunk as the products land: the wait for chunk c (and its
+      // slot bits) is enqueued by the caller, then its partition and merge
+      for (int c = 0; c < C; ++c) {
+        const unsigned* qtotal = pl.qtotal;
+        size_t Wq = pl.Wq;
+        cp->arrive(c, &qtotal, &Wq);
+        const size_t n = tc[c + 1] - tc[c];
+        if (n == 0) continue;
+        partition(c, qtotal, Wq);
+        MergeArgs gc = g;
+        gc.part_a = pa + tc[c];
+        gc.part_b = pb + tc[c];
+        gc.part_o = po + tc[c];
+        gc.ntiles = n;
+        KernelScope ks("merge");
+        k_merge1<B, NT, IPT><<<(unsigned)n, NT, Cfg::bytes(want_hist, 1), st>>>(gc, P);
+      }
+    }
   }
   if (PN) {
     KernelScope ks("meta_fix");
@@ -1952,14 +1999,15 @@ __global__ void k_pack_glob(ull* ctr, ull identity) {
 template <int B>
 DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q_keys,
                         const double* q_vals, double cs, double sn, double drop, bool want_hist,
-                        double eps, const Key<B>* PN = nullptr, double theta = 0.0) {
+                        double eps, const Key<B>* PN = nullptr, double theta = 0.0,
+                        const ChunkPlan* cp = nullptr) {
   static int shape = -1;
   if (shape < 0) {
     const char* env = getenv("IQCC_MERGE_CFG");
     shape = env ? atoi(env) : 3;
     if (shape < 0 || shape >= (int)(sizeof(kMergeShapes) / sizeof(kMergeShapes[0]))) shape = 3;
   }
-#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps, PN, theta)
+#define IQCC_MERGE(NT_, IPT_) launch_merge_t<B, NT_, IPT_>(s, P, nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps, PN, theta, cp)
   switch (shape) {
     case 0: IQCC_MERGE(256, 4); break;
     case 1: IQCC_MERGE(128, 4); break;
@@ -2049,11 +2097,12 @@ __global__ void k_materialize(const ull* __restrict__ keys, const double* __rest
 template <int B>
 __global__ void __launch_bounds__(256) k_push(const ull* __restrict__ keys, const double* __restrict__ coef,
                                               const unsigned* __restrict__ inv_perm, size_t A, Key<B> P,
-                                              double sn, ull* __restrict__ okeys, double* __restrict__ ovals) {
+                                              double sn, ull* __restrict__ okeys, double* __restrict__ ovals,
+                                              size_t r_begin = 0) {
   __shared__ __align__(16) ull sk[256 * 2 * B];
   __shared__ __align__(16) double sv[256];
-  for (size_t t = blockIdx.x; t * 256 < A; t += gridDim.x) {
-    const size_t r0 = t * 256;
+  for (size_t t = blockIdx.x; r_begin + t * 256 < A; t += gridDim.x) {
+    const size_t r0 = r_begin + t * 256;
     const int n = (int)min((size_t)256, A - r0);
     if ((int)threadIdx.x < n) {
       const unsigned src = inv_perm[r0 + threadIdx.x];
@@ -2076,20 +2125,23 @@ __global__ void __launch_bounds__(256) k_push(const ull* __restrict__ keys, cons
     }
     __syncthreads();
   }
+  __threadfence_system();  // the remote stores land before a ready flag raised after this kernel
 }
 
 }  // namespace
 
-void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals) {
-  const size_t A = g_plan.A;
-  if (A == 0) return;
-  cudaStream_t st = stream();
-  KernelScope ks("exchange");
-  const unsigned grid = (unsigned)std::min<size_t>((A + 255) / 256, 148 * 8);
+void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals,
+                   size_t r0, size_t r1, cudaStream_t on, unsigned max_grid) {
+  const size_t A = std::min(r1, g_plan.A);
+  if (A <= r0) return;
+  cudaStream_t st = on ? on : stream();
+  std::optional<KernelScope> ks;
+  if (!on) ks.emplace("exchange");
+  const unsigned grid = (unsigned)std::min<size_t>((A - r0 + 255) / 256, max_grid ? max_grid : 148 * 8);
   switch (s.B) {
-    case 1: k_push<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<1>(gen_row), sn, okeys, ovals); break;
-    case 2: k_push<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<2>(gen_row), sn, okeys, ovals); break;
-    default: k_push<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<4>(gen_row), sn, okeys, ovals); break;
+    case 1: k_push<1><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<1>(gen_row), sn, okeys, ovals, r0); break;
+    case 2: k_push<2><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<2>(gen_row), sn, okeys, ovals, r0); break;
+    default: k_push<4><<<grid, 256, 0, st>>>(s.keys(), s.coef(), g_plan.inv_perm, A, make_key<4>(gen_row), sn, okeys, ovals, r0); break;
   }
 }
 
@@ -2154,7 +2206,60 @@ void recv_slot_bits(const double* rv, size_t n, double thq) {
   g_plan.Wq = Wq;
 }
 
+thread_local double g_rs_thq = 0.0;
+thread_local unsigned* g_qtc = nullptr;  // running slot totals through each chunk
+
+void recv_slot_bits_begin(size_t n, double thq, int chunks) {
+  g_plan.qbits = g_plan.qpre = g_plan.qtotal = nullptr;
+  g_plan.Wq = 0;
+  g_rs_thq = thq;
+  if (thq == 0.0) return;  // every received product owns a slot
+  Workspace& ws = workspace();
+  cudaStream_t st = stream();
+  const size_t Wq = (n + 31) / 32, nbq = (Wq + PW - 1) / PW;
+  unsigned* qb = ws.qbits.as<unsigned>(2 * std::max<size_t>(Wq, 1) + nbq + 64 + chunks);
+  unsigned* qpre = qb + std::max<size_t>(Wq, 1) + 2;
+  unsigned* qbs = qpre + std::max<size_t>(Wq, 1);
+  g_qtc = qbs + nbq + 8;
+  IQCC_CUDA(cudaMemsetAsync(qb, 0, (std::max<size_t>(Wq, 1) + 2) * sizeof(unsigned), st));
+  g_plan.qbits = qb;
+  g_plan.qpre = qpre;
+  g_plan.qtotal = g_qtc + (chunks - 1);
+  g_plan.Wq = Wq;
+}
+
+void recv_slot_bits_chunk(const double* rv, size_t r0, size_t r1, size_t n, int c,
+                          const unsigned** qtotal, size_t* Wq) {
+  if (!g_plan.qbits) return;
+  if (r0 % (32 * (size_t)PW)) throw std::logic_error("recv_slot_bits_chunk: unaligned chunk");
+  cudaStream_t st = stream();
+  const size_t Wall = (n + 31) / 32, nbq = (Wall + PW - 1) / PW;
+  unsigned* qb = const_cast<unsigned*>(g_plan.qbits);  // this context's workspace arrays
+  unsigned* qpre = const_cast<unsigned*>(g_plan.qpre);
+  unsigned* qbs = qpre + std::max<size_t>(Wall, 1);
+  const size_t w0 = r0 / 32, w1 = (r1 + 31) / 32;
+  if (r1 > r0) {
+    KernelScope ks("present");
+    const size_t b0 = w0 / PW, b1 = std::min(nbq, (w1 + PW - 1) / PW);
+    k_value_slots<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(rv + r0, r1 - r0, g_rs_thq, qb + w0);
+    k_popc_blocks<<<(unsigned)(b1 - b0), 256, 0, st>>>(qb + w0, w1 - w0, qbs + b0);
+    k_scan_blocks<<<1, 1024, 0, st>>>(qbs + b0, b1 - b0, g_qtc + c, c ? g_qtc + c - 1 : nullptr);
+    k_popc_prefix<<<(unsigned)(b1 - b0), 256, 0, st>>>(qb + w0, w1 - w0, qbs + b0, qpre + w0);
+    count_launch("present");
+    count_launch("present");
+    count_launch("present");
+  } else if (c == 0) {
+    IQCC_CUDA(cudaMemsetAsync(g_qtc, 0, sizeof(unsigned), st));
+  } else {
+    IQCC_CUDA(cudaMemcpyAsync(g_qtc + c, g_qtc + c - 1, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+  }
+  *qtotal = g_qtc + c;
+  *Wq = std::max(w0, w1);
+}
+
 void plan_set_products(size_t A) { g_plan.A = A; }
+
+const unsigned* plan_inv_perm() { return g_plan.inv_perm; }
 
 void set_merge_reducer(Reducer* red) { g_merge_red = red; }
 
@@ -2214,20 +2319,22 @@ void recv_slot_bits_packed(const unsigned* bits, size_t n, double thq) {
 template <int B>
 DressOutcome merge_products_t(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                               double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                              const double* q_vals, const uint64_t* next_row, double theta) {
+                              const double* q_vals, const uint64_t* next_row, double theta,
+                              const ChunkPlan* cp) {
   Key<B> PN;
   if (next_row) PN = make_key<B>(next_row);
   return merge_impl<B>(s, make_key<B>(gen_row), nQ, q_keys, q_vals, cs, sn, drop, want_hist, eps,
-                       next_row ? &PN : nullptr, theta);
+                       next_row ? &PN : nullptr, theta, cp);
 }
 
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
-                            const double* q_vals, const uint64_t* next_row, double theta) {
+                            const double* q_vals, const uint64_t* next_row, double theta,
+                            const ChunkPlan* cp) {
   switch (s.B) {
-    case 1: return merge_products_t<1>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
-    case 2: return merge_products_t<2>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
-    default: return merge_products_t<4>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta);
+    case 1: return merge_products_t<1>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta, cp);
+    case 2: return merge_products_t<2>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta, cp);
+    default: return merge_products_t<4>(s, gen_row, cs, sn, drop, want_hist, eps, nQ, q_keys, q_vals, next_row, theta, cp);
   }
 }
 

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/iqcc_b200.h"
@@ -490,9 +491,14 @@ void plan_survivors(DeviceStore& s, const uint64_t* gen_row, double cs, double s
 /// Slot bits of n received products (values rv): |v| >= thq; thq = 0: all.
 void recv_slot_bits(const double* rv, size_t n, double thq);
 void plan_set_products(size_t A);
+/// The planned product order (sorted rank -> store index) of the last plan.
+const unsigned* plan_inv_perm();
 /// All planned products written straight into a peer's receive buffer
 /// (okeys/ovals: CUDA IPC mapping over NVLink), staged per 256-product tile.
-void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals);
+/// [r0, r1) only, on stream `on` (nullptr: the engine stream, profiled as
+/// "exchange"), with at most max_grid CTAs (0: 8 per SM).
+void push_products(DeviceStore& s, const uint64_t* gen_row, double sn, ull* okeys, double* ovals,
+                   size_t r0 = 0, size_t r1 = SIZE_MAX, cudaStream_t on = nullptr, unsigned max_grid = 0);
 /// Products [r0, r1) of the planned order (clamped to the product count).
 /// thq / obits (optional): also pack the receiver's product slot bits
 /// (|v| >= thq) into obits (one bit per product, r0 % 32 == 0).
@@ -502,10 +508,29 @@ void materialize_products(DeviceStore& s, const uint64_t* gen_row, double sn, ul
                           unsigned* obits = nullptr);
 /// recv_slot_bits from bits the sender packed (possibly in peer memory).
 void recv_slot_bits_packed(const unsigned* bits, size_t n, double thq);
+/// Received products merged chunk by chunk as they land (multi.cu's chunked
+/// exchange): chunk c merges survivors [a[c], a[c+1]) with products
+/// [r[c], r[c+1]); a[C] = store size, r[C] = product count, every r[c]
+/// (c < C) a multiple of 32 * 1024 (whole slot-bit scan blocks).  arrive(c,
+/// &qtotal, &Wq) enqueues what must precede chunk c (the wait for its data,
+/// its product slot bits) and may narrow the slot-bit view to the words
+/// ready so far.
+struct ChunkPlan {
+  int C = 1;
+  std::vector<size_t> a, r;
+  std::function<void(int, const unsigned**, size_t*)> arrive;
+};
+/// Slot bits of n received products computed chunk by chunk:
+/// recv_slot_bits_begin sizes the arrays; recv_slot_bits_chunk adds
+/// products [r0, r1) (r0 a multiple of 32 * 1024, chunks in order) and
+/// returns the prefix total and word count through r1.
+void recv_slot_bits_begin(size_t n, double thq, int chunks);
+void recv_slot_bits_chunk(const double* rv, size_t r0, size_t r1, size_t n, int c,
+                          const unsigned** qtotal, size_t* Wq);
 DressOutcome merge_products(DeviceStore& s, const uint64_t* gen_row, double cs, double sn,
                             double drop, bool want_hist, double eps, size_t nQ, const ull* q_keys,
                             const double* q_vals, const uint64_t* next_row = nullptr,
-                            double theta = 0.0);
+                            double theta = 0.0, const ChunkPlan* cp = nullptr);
 /// Selects the compress filter on a store without a filter.  If hist_ready,
 /// the histogram/count_eps of the last dress_step are used.
 /// Cross-rank hooks for compress_partitioned (iqcc/partition.hpp:325-396);

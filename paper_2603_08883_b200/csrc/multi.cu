@@ -114,6 +114,129 @@ struct P2P {
 };
 P2P g_p2p;
 
+// Chunked exchange (the default push): each rank materializes its sorted
+// products chunk by chunk into local HBM, the copy engines move each chunk
+// into the partner's receive buffer over NVLink (no SM time), and a
+// one-thread kernel behind the copy raises the chunk's ready flag in the
+// partner's buffer; the partner's merge waits for chunk c's flag only and
+// merges chunk c while later chunks are still on the wire.
+constexpr int kMaxChunks = 32;
+constexpr size_t kChunkAlign = 32 * 1024;  // whole slot-bit scan blocks (PW words)
+
+/// Byte offset of the ready flags (kMaxChunks u32) in a receive buffer.
+size_t p2p_flag_off(size_t cap, size_t W) {
+  return (cap * (W * 8 + 8) + (cap / 32 + 64) * 4 + 255) & ~(size_t)255;
+}
+
+struct XState {
+  cudaStream_t xst = nullptr;  // copy-engine stream
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t done = nullptr;
+  unsigned* err = nullptr;  // device: a ready-flag wait timed out
+  unsigned epoch = 0;       // exchanges so far (same on every rank)
+};
+XState g_x;
+
+XState& xstate() {
+  if (!g_x.xst) {
+    IQCC_CUDA(cudaStreamCreateWithFlags(&g_x.xst, cudaStreamNonBlocking));
+    g_x.ev.resize(kMaxChunks);
+    for (auto& e : g_x.ev) IQCC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    IQCC_CUDA(cudaEventCreateWithFlags(&g_x.done, cudaEventDisableTiming));
+    IQCC_CUDA(cudaMalloc(&g_x.err, sizeof(unsigned)));
+    IQCC_CUDA(cudaMemset(g_x.err, 0, sizeof(unsigned)));
+  }
+  return g_x;
+}
+
+int exchange_chunks() {
+  static const int c = [] {
+    const char* e = getenv("IQCC_XCHG_CHUNKS");
+    const int v = e ? atoi(e) : 4;
+    return std::max(1, std::min(v, kMaxChunks));
+  }();
+  return c;
+}
+
+struct KeyWords {
+  ull w[8];
+};
+
+/// Sender: [A, r_1..r_{C-1}, key(r_1)..key(r_{C-1})] with r_c = c*A/C rounded
+/// down to kChunkAlign, key(r) = the r-th sorted product's key (all ones
+/// past the end).
+__global__ void k_chunk_send(const long long* __restrict__ a_dev, const ull* __restrict__ keys,
+                             const unsigned* __restrict__ inv_perm, int W, KeyWords P, int C,
+                             ull* __restrict__ out) {
+  const int c = threadIdx.x;
+  const ull A = a_dev ? (ull)*a_dev : 0ull;
+  if (c == 0) out[0] = A;
+  if (c < 1 || c >= C) return;
+  const ull r = ((A * (ull)c / (ull)C) / kChunkAlign) * kChunkAlign;
+  out[c] = r;
+  for (int w = 0; w < W; ++w)
+    out[C + (size_t)(c - 1) * W + w] = r < A ? keys[(size_t)inv_perm[r] * W + w] ^ P.w[w] : ~0ull;
+}
+
+/// Receiver: where the partner's chunk split keys fall in this store
+/// (lower bound: a run of equal survivors stays with its product), plus
+/// both sides' counts and chunk starts for the host:
+/// hb = [A, my r_1..r_{C-1}, nrecv, their r_1..r_{C-1}, a_1..a_{C-1}].
+__global__ void k_chunk_bounds(const ull* __restrict__ mine, const ull* __restrict__ recv,
+                               const ull* __restrict__ keys, size_t M, int W, int C,
+                               ull* __restrict__ hb) {
+  const int c = threadIdx.x;
+  if (c < C) {
+    hb[c] = mine[c];
+    hb[C + c] = recv[c];
+  }
+  if (c < 1 || c >= C) return;
+  const ull nrecv = recv[0], r = recv[c];
+  size_t a = M;
+  if (r < nrecv) {
+    const ull* k = recv + C + (size_t)(c - 1) * W;
+    size_t lo = 0, hi = M;
+    while (lo < hi) {  // first store key >= k
+      const size_t mid = (lo + hi) >> 1;
+      int cmp = 0;
+      for (int w = 0; w < W && cmp == 0; ++w) {
+        const ull x = keys[mid * W + w];
+        cmp = x < k[w] ? -1 : (x > k[w] ? 1 : 0);
+      }
+      if (cmp < 0)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    a = lo;
+  }
+  hb[2 * C + c - 1] = a;
+}
+
+/// Raised behind a chunk's copy (stream order: the copy is complete).
+__global__ void k_flag_signal(unsigned* flag, unsigned epoch) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(flag), "r"(epoch) : "memory");
+}
+
+/// Blocks the engine stream until the partner raised chunk c's flag; gives
+/// up after 60 s (err) rather than hang the device.
+__global__ void k_flag_wait(const unsigned* flag, unsigned epoch, unsigned* err) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - epoch) >= 0) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60ull * 1000000000ull) {
+      atomicExch(err, 1u);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
 ull allreduce_host(ull v, ncclRedOp_t op) {
   Comm& c = comm();
   cudaStream_t st = stream();
@@ -157,7 +280,8 @@ void p2p_prepare(size_t need, size_t W) {
   p2p_free();
   g_p2p.tried = true;
   const size_t cap = (size_t)need_g + need_g / 4 + 1024;
-  bool ok = cudaMalloc(&g_p2p.mine, cap * (W * 8 + 8) + (cap / 32 + 64) * 4) == cudaSuccess;
+  bool ok = cudaMalloc(&g_p2p.mine, p2p_flag_off(cap, W) + kMaxChunks * sizeof(unsigned)) == cudaSuccess;
+  if (ok) ok = cudaMemset(g_p2p.mine + p2p_flag_off(cap, W), 0, kMaxChunks * sizeof(unsigned)) == cudaSuccess;
   cudaIpcMemHandle_t h;
   std::memset(&h, 0, sizeof(h));
   if (ok) ok = cudaIpcGetMemHandle(&h, g_p2p.mine) == cudaSuccess;
@@ -255,6 +379,13 @@ void multi_prepare(DeviceStore& s) { p2p_prepare(s.M, 2 * (size_t)s.B); }
 void multi_shutdown() {
   if (g_comm.comm) {
     cudaDeviceSynchronize();
+    if (g_x.xst) {
+      for (auto e : g_x.ev) cudaEventDestroy(e);
+      cudaEventDestroy(g_x.done);
+      cudaFree(g_x.err);
+      cudaStreamDestroy(g_x.xst);
+      g_x = XState{};
+    }
     p2p_close();
     p2p_free();
     g_p2p = P2P{};
@@ -307,25 +438,50 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     // device memory: one round trip gives both A and the receive count
     const long long* a_dev = plan_products_async(s, gen_row, cs, sn, theta);
     const int peer = (int)owner[mine ^ mask];
-    ull* cnt = scratch(4);
-    if (a_dev)
+    const size_t W = 2 * s.B;
+    static const bool pull = getenv("IQCC_XCHG") && std::string(getenv("IQCC_XCHG")) == "pull";
+    // chunked push (every rank decides alike: the P2P state is agreed)
+    const int C = (g_p2p.ok && g_p2p.W == W && !pull) ? exchange_chunks() : 1;
+    const bool chunked = C > 1;
+    // one swap gives A and the receive count (chunked: also both sides'
+    // chunk starts and where the partner's chunk keys fall in this store)
+    const size_t S = chunked ? (size_t)C + (size_t)(C - 1) * W : 1;
+    ull* cnt = scratch(2 * S + 3 * (size_t)C + 8);
+    ull* hbd = cnt + 2 * S;
+    if (chunked) {
+      KeyWords Pw{};
+      row_to_device_key(gen_row, s.B, Pw.w);
+      k_chunk_send<<<1, 32, 0, st>>>(a_dev, s.keys(), plan_inv_perm(), (int)W, Pw, C, cnt);
+    } else if (a_dev) {
       IQCC_CUDA(cudaMemcpyAsync(cnt, a_dev, sizeof(ull), cudaMemcpyDeviceToDevice, st));
-    else
+    } else {
       IQCC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(ull), st));
+    }
     {
       KernelScope ks("exch_count");
       IQCC_NCCL(ncclGroupStart());
-      IQCC_NCCL(ncclSend(cnt, 1, ncclUint64, peer, c.comm, st));
-      IQCC_NCCL(ncclRecv(cnt + 1, 1, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclSend(cnt, S, ncclUint64, peer, c.comm, st));
+      IQCC_NCCL(ncclRecv(cnt + S, S, ncclUint64, peer, c.comm, st));
       IQCC_NCCL(ncclGroupEnd());
     }
-    ull* hp = static_cast<ull*>(host_pinned(2 * sizeof(ull)));
-    IQCC_CUDA(cudaMemcpyAsync(hp, cnt, 2 * sizeof(ull), cudaMemcpyDeviceToHost, st));
-    host_sync(st);
-    const size_t A = hp[0];
-    nrecv = hp[1];
+    std::vector<ull> hb(3 * (size_t)C);
+    if (chunked) {
+      k_chunk_bounds<<<1, 32, 0, st>>>(cnt, cnt + S, s.keys(), s.M, (int)W, C, hbd);
+      ull* hp = static_cast<ull*>(host_pinned((3 * (size_t)C - 1) * sizeof(ull)));
+      IQCC_CUDA(cudaMemcpyAsync(hp, hbd, (3 * (size_t)C - 1) * sizeof(ull), cudaMemcpyDeviceToHost, st));
+      host_sync(st);
+      std::copy(hp, hp + 3 * C - 1, hb.begin());
+    } else {
+      ull* hp = static_cast<ull*>(host_pinned(2 * sizeof(ull)));
+      IQCC_CUDA(cudaMemcpyAsync(hp, cnt, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      IQCC_CUDA(cudaMemcpyAsync(hp + 1, cnt + S, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      host_sync(st);
+      hb[0] = hp[0];
+      hb[1] = hp[1];  // (chunked layout: hb[C])
+    }
+    const size_t A = hb[0];
+    nrecv = chunked ? hb[C] : hb[1];
     plan_set_products(A);
-    const size_t W = 2 * s.B;
     // both ends see the same (A, nrecv) and the same agreed capacity
     const bool p2p = g_p2p.ok && g_p2p.W == W && A <= g_p2p.cap && nrecv <= g_p2p.cap;
     // exchange buffers sized by the shard (products <= terms), so they do
@@ -336,10 +492,71 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     // IQCC_XCHG=pull: each rank writes its sorted products (and the
     // receiver's slot bits) into its OWN peer-visible buffer at HBM speed,
     // and the partner's merge reads them over NVLink while it merges (no
-    // separate transfer pass); default: push them into the partner's buffer
-    static const bool pull = getenv("IQCC_XCHG") && std::string(getenv("IQCC_XCHG")) == "pull";
+    // separate transfer pass); default: the chunked push (IQCC_XCHG_CHUNKS=1:
+    // one SM push of everything, then the merge)
     const unsigned* rbits = nullptr;
-    if (p2p && pull) {
+    ChunkPlan cp;
+    if (p2p && chunked) {
+      XState& xs = xstate();
+      const unsigned epoch = ++xs.epoch;
+      ull* stk = ws.xbuf_keys.as<ull>(std::max<size_t>(A, 1) * W);
+      double* stv = ws.xbuf_coef.as<double>(std::max<size_t>(A, 1));
+      char* dst = g_p2p.peer[peer];
+      ull* dk = reinterpret_cast<ull*>(dst);
+      double* dv = reinterpret_cast<double*>(dst + g_p2p.cap * W * 8);
+      unsigned* pflag = reinterpret_cast<unsigned*>(dst + p2p_flag_off(g_p2p.cap, W));
+      const unsigned* mflag = reinterpret_cast<const unsigned*>(g_p2p.mine + p2p_flag_off(g_p2p.cap, W));
+      std::vector<size_t> mr(C + 1);
+      mr[0] = 0;
+      mr[C] = A;
+      for (int k = 1; k < C; ++k) mr[k] = hb[k];
+      // IQCC_XCHG_SM=<CTAs>: the chunks leave through SM stores into the
+      // partner's buffer (a push kernel with that many CTAs beside the merge)
+      // instead of local staging + copy engine
+      static const unsigned sm_push = getenv("IQCC_XCHG_SM") ? (unsigned)atoi(getenv("IQCC_XCHG_SM")) : 0u;
+      if (sm_push) {
+        IQCC_CUDA(cudaEventRecord(xs.ev[0], st));  // the plan is done
+        IQCC_CUDA(cudaStreamWaitEvent(xs.xst, xs.ev[0], 0));
+      }
+      for (int k = 0; k < C && sm_push; ++k) {
+        push_products(s, gen_row, sn, dk, dv, mr[k], mr[k + 1], xs.xst, sm_push);
+        k_flag_signal<<<1, 1, 0, xs.xst>>>(pflag + k, epoch);
+      }
+      for (int k = 0; k < C && !sm_push; ++k) {
+        // chunk k into local HBM (SMs), then onto the wire (copy engine)
+        materialize_products(s, gen_row, sn, stk, stv, mr[k], mr[k + 1], "exchange");
+        IQCC_CUDA(cudaEventRecord(xs.ev[k], st));
+        IQCC_CUDA(cudaStreamWaitEvent(xs.xst, xs.ev[k], 0));
+        if (mr[k + 1] > mr[k]) {
+          IQCC_CUDA(cudaMemcpyAsync(dk + mr[k] * W, stk + mr[k] * W, (mr[k + 1] - mr[k]) * W * 8,
+                                    cudaMemcpyDeviceToDevice, xs.xst));
+          IQCC_CUDA(cudaMemcpyAsync(dv + mr[k], stv + mr[k], (mr[k + 1] - mr[k]) * 8,
+                                    cudaMemcpyDeviceToDevice, xs.xst));
+        }
+        k_flag_signal<<<1, 1, 0, xs.xst>>>(pflag + k, epoch);
+      }
+      IQCC_CUDA(cudaEventRecord(xs.done, xs.xst));
+      rk = reinterpret_cast<ull*>(g_p2p.mine);
+      rv = reinterpret_cast<double*>(g_p2p.mine + g_p2p.cap * W * 8);
+      cp.C = C;
+      cp.a.assign(C + 1, 0);
+      cp.r.assign(C + 1, 0);
+      for (int k = 1; k < C; ++k) {
+        cp.r[k] = hb[C + k];
+        cp.a[k] = hb[2 * C + k - 1];
+      }
+      cp.a[C] = s.M;
+      cp.r[C] = nrecv;
+      recv_slot_bits_begin(nrecv, theta, C);
+      const unsigned* err = xs.err;
+      cp.arrive = [&cp, mflag, epoch, err, rv, nrecv, st](int k, const unsigned** qt, size_t* wq) {
+        {
+          KernelScope ks("exchange");
+          k_flag_wait<<<1, 1, 0, st>>>(mflag + k, epoch, const_cast<unsigned*>(err));
+        }
+        recv_slot_bits_chunk(rv, cp.r[k], cp.r[k + 1], nrecv, k, qt, wq);
+      };
+    } else if (p2p && pull) {
       char* mine = g_p2p.mine;
       unsigned* mbits = reinterpret_cast<unsigned*>(mine + g_p2p.cap * (W * 8 + 8));
       materialize_products(s, gen_row, sn, reinterpret_cast<ull*>(mine),
@@ -391,11 +608,22 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     x.recv_terms = nrecv;
     x.bytes_wire = A * (W * 8 + 8);
     x.bytes_reference = A * (16 + Bref * 16);  // MessageLog formula, partition.hpp:420-422
-    if (rbits)
-      recv_slot_bits_packed(rbits, nrecv, theta);
-    else
-      recv_slot_bits(rv, nrecv, theta);
-    o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, theta);
+    if (cp.C > 1) {
+      o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, theta, &cp);
+      // the staging buffer is free again once the copies are done; and a
+      // timed-out wait means the partner never delivered
+      IQCC_CUDA(cudaStreamWaitEvent(st, g_x.done, 0));
+      unsigned* he = static_cast<unsigned*>(host_pinned(sizeof(unsigned)));
+      IQCC_CUDA(cudaMemcpyAsync(he, g_x.err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      host_sync(st);
+      if (*he) throw std::runtime_error("parallel_dress: the partner's products did not arrive (60 s)");
+    } else {
+      if (rbits)
+        recv_slot_bits_packed(rbits, nrecv, theta);
+      else
+        recv_slot_bits(rv, nrecv, theta);
+      o = merge_products(s, gen_row, cs, sn, 1e-12, want_hist, eps, nrecv, rk, rv, next_row, theta);
+    }
   }
   if (xs) *xs = x;
   if (!want_hist) return;  // eps == 0 and no cap: compress_partitioned is a no-op

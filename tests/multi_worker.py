@@ -87,7 +87,9 @@ def main():
     dist.all_gather_object(objs, (shard.rows, shard.coeffs, exch))
     if rank == 0:
         from oracle.oracle import Oracle
-        port = Oracle("port")
+        # the unmodified reference (oracle/_ref, built here and shipped with
+        # the snapshot) when present, else its pinned restatement
+        port = Oracle("reference") if Oracle.available("reference") else Oracle("port")
         h = port.gen_mol(n, N, 2)
         h, _ = port.dress_sequence(h, np.stack(gens), taus, eps, cap)
         r, c = h.export()
@@ -109,7 +111,7 @@ def main():
         e_ok = e_ok and np.abs(g_dis - gd).max() <= 1e-10 * max(1.0, np.abs(gd).max())
         gp = np.array([port.gradient(h, th, ph, c) for c in cands])  # exact at the poles
         e_ok = e_ok and np.abs(g_dis_poles - gp).max() <= 1e-10 * max(1.0, np.abs(gp).max())
-        print(f"MULTI world={world} terms={len(r)} exchanged={sum(o[2] for o in objs)} "
+        print(f"MULTI world={world} checker={port.flavor} terms={len(r)} exchanged={sum(o[2] for o in objs)} "
               f"bitexact={ok} energy_ok={e_ok}", flush=True)
         if not (ok and e_ok):
             sys.exit(1)

@@ -24,11 +24,20 @@ def n_gpus():
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "nccl"),
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "pull"),
                                   ("124", "2e5", "7", "1e-10", "1.5e5", "seq", "pull", "badspec"),
-                                  ("200", "1e5", "6", "1e-10", "1.2e5", "seq")])
+                                  ("200", "1e5", "6", "1e-10", "1.2e5", "seq"),
+                                  ("124", "1e6", "5", "1e-10", "8e5", "seq"),
+                                  ("124", "1e6", "5", "1e-10", "8e5", "seq", "chunks16"),
+                                  ("124", "1e6", "5", "1e-10", "8e5", "seq", "chunks16", "badspec"),
+                                  ("124", "1e6", "5", "1e-10", "8e5", "seq", "chunks1"),
+                                  ("124", "1e6", "5", "1e-10", "8e5", "seq", "smpush")])
 def test_partitioned_dressing_matches_serial(world, args):
     """The sequence cases exercise the output-slot speculation on the
     exchange and the local steps; "badspec" forces every guess too high
-    (IQCC_SPEC_SCALE), so every step is undone and redone exactly; "nccl"
+    (IQCC_SPEC_SCALE), so every step is undone and redone exactly; the
+    1e6-term cases are large enough for the chunked exchange to split the
+    products (the partner's merge starts on chunk 0 while later chunks are
+    on the wire; chunks16: many chunks, some empty; chunks1: one SM push
+    then the merge); "nccl"
     moves the products with NCCL send/recv (the fallback of the CUDA-IPC
     NVLink push); "pull" lets the partner's merge read them in place over
     NVLink (IQCC_XCHG=pull)."""
@@ -37,6 +46,12 @@ def test_partitioned_dressing_matches_serial(world, args):
     env = dict(os.environ)
     if args[-1] == "badspec":
         env["IQCC_SPEC_SCALE"] = "64"
+        args = args[:-1]
+    if args[-1] == "smpush":  # chunks leave through a 148-CTA SM push kernel beside the merge
+        env["IQCC_XCHG_SM"] = "148"
+        args = args[:-1]
+    if args[-1].startswith("chunks"):  # exchange chunk count (1: one SM push, then the merge)
+        env["IQCC_XCHG_CHUNKS"] = args[-1][6:]
         args = args[:-1]
     if args[-1] == "nccl":  # products over NCCL send/recv instead of the NVLink push
         env["IQCC_NO_P2P"] = "1"
@@ -50,3 +65,5 @@ def test_partitioned_dressing_matches_serial(world, args):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "bitexact=True" in r.stdout and "energy_ok=True" in r.stdout
+    if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libiqcc_ref.so")):
+        assert "checker=reference" in r.stdout  # the unmodified reference is the checker
