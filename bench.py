@@ -318,7 +318,9 @@ def run_gpu_arm(args, rank, world, local_rank):
         fam[f] = native.profile_get(f)[0]
     native.profile(False)
     if dist:
-        print(f"[bench] rank {rank}: shard {d.size()} terms, sent {sent[0]} products, ms {ms:.2f}, kernel_ms "
+        print(f"[bench] rank {rank}: shard {d.size()} terms, sent {sent[0]} products, ms {ms:.2f}, "
+              f"host syncs {native.profile_get('host_wait')[1]}, tie gathers "
+              f"{native.profile_get('host_tie_gather')[1]}, kernel_ms "
               + json.dumps({k: round(v, 2) for k, v in fam.items() if v}), file=sys.stderr)
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -226,6 +226,14 @@ int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bi
                                      const double* cos_tau, const double* sin_tau, double eps,
                                      size_t max_terms, iqcc_exchange_stats* xstats,
                                      iqcc_compress_stats* cstats, size_t* terms_in_total);
+/* Collective: reserve every rank's NVLink receive buffer for shards of up
+ * to `terms` terms (a store about to grow uncapped maps its peer buffers
+ * once instead of at every growth step). */
+int iqcc_gpu_parallel_reserve(iqcc_gpu_sum* h, size_t terms);
+/* compress_partitioned (iqcc/partition.hpp:325-396) alone, collective:
+ * keep identity or |c| >= eps; over max_terms globally, the global top
+ * max_terms - 1 by |c| with the canonical tie-break across ranks. */
+int iqcc_gpu_parallel_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compress_stats* cstats);
 /* Partitioned energy: local expect + allreduce (parallel_expect, :241-254). */
 int iqcc_gpu_parallel_expect(iqcc_gpu_sum* h, const double* factors, double* energy);
 /* Partitioned build_poly_kernels (iqcc/optimizer.hpp:371-422): local

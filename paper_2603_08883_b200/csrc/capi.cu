@@ -961,6 +961,22 @@ int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const
   });
 }
 
+int iqcc_gpu_parallel_reserve(iqcc_gpu_sum* h, size_t terms) {
+  return guarded([&] {
+    need(h);
+    parallel_reserve(h->s, terms);
+  });
+}
+
+int iqcc_gpu_parallel_compress(iqcc_gpu_sum* h, double eps, size_t max_terms, iqcc_compress_stats* cs) {
+  return guarded([&] {
+    need(h);
+    if (!(eps >= 0.0)) throw std::invalid_argument("compress_partitioned: epsilon < 0");
+    if (max_terms < 1) throw std::invalid_argument("compress_partitioned: max_terms < 1");
+    parallel_compress_store(h->s, eps, max_terms, cs);
+  });
+}
+
 int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bits,
                                      const size_t* owner, size_t K, const uint64_t* gens,
                                      const double* cos_tau, const double* sin_tau, double eps,

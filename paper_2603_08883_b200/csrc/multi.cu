@@ -113,6 +113,7 @@ struct P2P {
   std::vector<char*> peer;  // mapping of every rank's buffer (own rank: mine)
 };
 P2P g_p2p;
+size_t g_p2p_last_cap = 0;
 
 // Chunked exchange (the default push): each rank materializes its sorted
 // products chunk by chunk into local HBM, the copy engines move each chunk
@@ -273,13 +274,18 @@ void p2p_prepare(size_t need, size_t W) {
   if (off || (g_p2p.tried && !g_p2p.ok && g_p2p.cap == 0 && g_p2p.W == (size_t)-1)) return;
   const ull need_g = allreduce_host((ull)need, ncclMax);
   if (g_p2p.ok && need_g <= g_p2p.cap && W == g_p2p.W) return;
+  HostScope hs("host_p2p_prepare");
+  // a store that outgrew its buffer keeps growing (uncapped dressing, C5):
+  // regrow by 2x so the (costly) remap happens every other step at most
+  const bool regrow = g_p2p.ok && W == g_p2p.W;
   cudaStream_t st = stream();
   IQCC_CUDA(cudaStreamSynchronize(st));
   p2p_close();
   allreduce_host(0, ncclSum);  // every mapping of the old buffers is closed
   p2p_free();
   g_p2p.tried = true;
-  const size_t cap = (size_t)need_g + need_g / 4 + 1024;
+  const size_t cap = regrow ? std::max<size_t>(2 * (size_t)need_g, 2 * g_p2p_last_cap) + 1024
+                            : (size_t)need_g + need_g / 4 + 1024;
   bool ok = cudaMalloc(&g_p2p.mine, p2p_flag_off(cap, W) + kMaxChunks * sizeof(unsigned)) == cudaSuccess;
   if (ok) ok = cudaMemset(g_p2p.mine + p2p_flag_off(cap, W), 0, kMaxChunks * sizeof(unsigned)) == cudaSuccess;
   cudaIpcMemHandle_t h;
@@ -318,6 +324,7 @@ void p2p_prepare(size_t need, size_t W) {
   if (allreduce_host(ok ? 1 : 0, ncclMin) == 1) {
     g_p2p.ok = true;
     g_p2p.cap = cap;
+    g_p2p_last_cap = cap;
     g_p2p.W = W;
     return;
   }
@@ -669,6 +676,18 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
       cs_out->dropped_terms += r.dropped_terms;
       cs_out->dropped_weight += r.dropped_weight;
     }
+  }
+}
+
+void parallel_reserve(DeviceStore& s, size_t terms) { p2p_prepare(std::max(terms, s.M), 2 * (size_t)s.B); }
+
+void parallel_compress_store(DeviceStore& s, double eps, size_t max_terms, iqcc_compress_stats* cs) {
+  comm();
+  NcclReducer red;
+  CompressResult r = compress_store(s, eps, max_terms, false, 0, cs != nullptr, &red);
+  if (cs) {
+    cs->dropped_terms += r.dropped_terms;
+    cs->dropped_weight += r.dropped_weight;
   }
 }
 

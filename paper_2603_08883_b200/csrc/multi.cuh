@@ -18,6 +18,13 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
 /// Sum of a host value over the ranks (one allreduce).
 size_t parallel_sum(size_t v);
 double parallel_expect_store(DeviceStore& s, const double* factors);
+/// compress_partitioned (iqcc/partition.hpp:325-396) on its own: global
+/// counts and histograms allreduced, canonical tie-break across ranks.
+void parallel_compress_store(DeviceStore& s, double eps, size_t max_terms, iqcc_compress_stats* cs);
+/// Collective: size every rank's NVLink receive buffer for shards of up to
+/// `terms` terms now (mapping a peer buffer costs ~1 s per 10 GB, so a
+/// store that will grow uncapped reserves once instead of regrowing).
+void parallel_reserve(DeviceStore& s, size_t terms);
 /// Partitioned QMF energy + 2n gradients and DIS gradients of K candidates:
 /// local values allgathered, summed element by element in rank order.
 double parallel_qmf_grad_store(DeviceStore& s, const double* factors, const double* derivs, double* grad);

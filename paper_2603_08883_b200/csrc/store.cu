@@ -1131,6 +1131,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         // canonical tie-break across shards (partition.hpp:350-361): the
         // globally first r tied words are kept; local index order is
         // canonical order
+        HostScope tscope("host_tie_gather");
         std::sort(th.begin(), th.end());
         const size_t W = 2 * s.B;
         std::vector<ull> mine(th.size() * W);

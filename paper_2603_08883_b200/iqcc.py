@@ -709,6 +709,21 @@ class Partition:
             exchange.extend(xs[k] for k in range(K))
         return tin.value
 
+    def reserve(self, d: DeviceSum, terms: int) -> None:
+        """Size the NVLink receive buffers for shards of up to `terms` terms
+        (collective), before a run that grows the store uncapped."""
+        check(lib.iqcc_gpu_parallel_reserve(d.handle, int(terms)))
+
+    def compress(self, d: DeviceSum, eps: float, max_terms: int = U64_MAX,
+                 stats: CompressStats | None = None) -> None:
+        """compress_partitioned (iqcc/partition.hpp:325-396) on this rank's
+        shard: collective over the communicator."""
+        cs = native.CompressStatsC()
+        check(lib.iqcc_gpu_parallel_compress(d.handle, eps, max_terms, C.byref(cs)))
+        if stats is not None:
+            stats.dropped_terms += cs.dropped_terms
+            stats.dropped_weight += cs.dropped_weight
+
     def total_size(self, d: DeviceSum) -> int:
         n = C.c_size_t()
         check(lib.iqcc_gpu_parallel_size(d.handle, C.byref(n)))

@@ -100,6 +100,8 @@ _SIGS = {
                                                    _f64p, C.c_double, C.c_size_t, C.POINTER(ExchangeStats),
                                                    C.POINTER(CompressStatsC), C.POINTER(C.c_size_t)]),
     "iqcc_gpu_parallel_expect": (C.c_int, [_vp, _f64p, C.POINTER(C.c_double)]),
+    "iqcc_gpu_parallel_compress": (C.c_int, [_vp, C.c_double, C.c_size_t, C.POINTER(CompressStatsC)]),
+    "iqcc_gpu_parallel_reserve": (C.c_int, [_vp, C.c_size_t]),
     "iqcc_gpu_parallel_size": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),
     "iqcc_gpu_parallel_qmf_energy_gradient": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(C.c_double), _f64p]),
     "iqcc_gpu_parallel_gradients": (C.c_int, [_vp, _f64p, _u64p, C.c_size_t, C.c_int, _f64p]),

@@ -83,8 +83,13 @@ def main():
     cands = np.stack(gens[:4])
     g_dis = part.gradients(d, om3, cands)
     g_dis_poles = part.gradients(d, iqcc.QmfState(th, ph), cands, flip_group_only=True)
+    # compress_partitioned alone (partition.hpp:325-396): a cut between
+    # the eps floor and a global cap, canonical tie-break across ranks
+    cap2 = max(1, (part.total_size(d) * 3) // 5)
+    part.compress(d, 1e-6, cap2)
+    shard_c = d.download()
     objs = [None] * world
-    dist.all_gather_object(objs, (shard.rows, shard.coeffs, exch))
+    dist.all_gather_object(objs, (shard.rows, shard.coeffs, exch, shard_c.rows, shard_c.coeffs))
     if rank == 0:
         from oracle.oracle import Oracle
         # the unmodified reference (oracle/_ref, built here and shipped with
@@ -98,6 +103,11 @@ def main():
         # gather (partition.hpp:224-230): canonical merge of disjoint shards
         rows, coeffs = port.from_terms(n, rows, coeffs, drop=0.0, check=False).export()
         ok = rows.shape == r.shape and np.array_equal(rows, r) and np.array_equal(coeffs, c)
+        rc, cc = port.compress(h, 1e-6, max(1, (len(r) * 3) // 5))[0].export()
+        rows2 = np.concatenate([o[3] for o in objs])
+        coeffs2 = np.concatenate([o[4] for o in objs])
+        rows2, coeffs2 = port.from_terms(n, rows2, coeffs2, drop=0.0, check=False).export()
+        ok = ok and rows2.shape == rc.shape and np.array_equal(rows2, rc) and np.array_equal(coeffs2, cc)
         e_ref = port.expect_sum(th, ph, h)
         e_ok = abs(e_par - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
         for ker, tt in zip(kers, (th, th2)):
