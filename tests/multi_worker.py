@@ -29,6 +29,7 @@ def main():
     native.init(local)
     d = iqcc.DeviceSum.generate_mol(n, N, 2)
     part = iqcc.Partition.setup(d, world, rank)
+    part.reserve(d, 2 * len(d))  # receive buffers mapped once, before the steps
     B = iqcc.blocks_for(n)
     rs = np.random.default_rng(11)
     gens, taus, exch = [], [], 0
