@@ -379,8 +379,11 @@ def run_gpu_arm(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps,
                "ms_per_step": 1e3 * secs / e2e_steps,
                "split_ms_per_step": {k: round(1e3 * v / e2e_steps, 2) for k, v in split.items()},
-               "split_note": "upload = pinned H2D of rows + complex coefficients and the device check/convert; "
-                             "download = device compaction to the reference layout + D2H (PCIe bound)"}
+               "h2d_wire_bytes_per_step": h2d - h_host.coeffs.nbytes // 2,
+               "split_note": "upload = pinned H2D of the rows while host threads keep the real parts of the "
+                             "complex coefficients (checking every imaginary part is zero), then H2D of those "
+                             "and the device check/convert; download = device compaction to the reference "
+                             "layout + D2H of rows and complex coefficients (PCIe bound)"}
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_reference(SAMPLE_TERMS, 1, want_digest=True)

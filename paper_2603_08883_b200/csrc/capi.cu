@@ -65,6 +65,8 @@ struct Ctx {
   std::vector<cudaEvent_t> event_pool;
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  void* staging = nullptr;  // large page-locked buffer for host<->device reformatting
+  size_t staging_bytes = 0;
   BigCache big;
 };
 
@@ -172,6 +174,17 @@ void* host_pinned(size_t bytes) {
     IQCC_CUDA(cudaMallocHost(&c.pinned, c.pinned_bytes));
   }
   return c.pinned;
+}
+
+void* host_staging(size_t bytes) {
+  Ctx& c = ctx();
+  if (bytes > c.staging_bytes) {
+    if (c.staging) IQCC_CUDA(cudaFreeHost(c.staging));
+    c.staging = nullptr;
+    c.staging_bytes = std::max<size_t>(bytes + bytes / 4, 1 << 20);
+    IQCC_CUDA(cudaMallocHost(&c.staging, c.staging_bytes));
+  }
+  return c.staging;
 }
 
 // Busy-wait: a blocking/yielding synchronize can leave the GPU idle for a
@@ -385,6 +398,7 @@ void ctx_free(Ctx* c) {
   big_release_all(c->big);
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->staging) cudaFreeHost(c->staging);
   cudaStreamDestroy(c->own);
   delete c;
   ctx_bind(prev == c ? nullptr : prev);

@@ -358,6 +358,9 @@ void host_sync(cudaStream_t st);
 /// Page-locked host scratch (>= 8 KiB) for small device->host reads, so the
 /// copies stay asynchronous; valid until the next call.
 void* host_pinned(size_t bytes);
+/// A second, large page-locked buffer of the context (grows, reused): the
+/// staging of the host-side coefficient reformatting in upload/download.
+void* host_staging(size_t bytes);
 
 /// Host wall time of a region, booked under a profile family (profiling on).
 struct HostScope {
