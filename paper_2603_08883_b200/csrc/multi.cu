@@ -67,6 +67,8 @@ struct NcclReducer : Reducer {
     std::memcpy(vals, hp, n * sizeof(ull));
   }
   void sum_device(ull* d, size_t n) override {
+    // (a one-kernel allreduce over NVLink mailboxes measured no faster than
+    // NCCL here: the time in these collectives is the ranks' skew)
     IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, comm().comm, stream()));
   }
   std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t W, size_t* mine_off) override {
@@ -129,11 +131,15 @@ size_t p2p_flag_off(size_t cap, size_t W) {
   return (cap * (W * 8 + 8) + (cap / 32 + 64) * 4 + 255) & ~(size_t)255;
 }
 
+constexpr size_t kP2PTail = 256;  // chunk flags
+static_assert(kMaxChunks * sizeof(unsigned) <= kP2PTail, "chunk flags");
+
 struct XState {
   cudaStream_t xst = nullptr;  // copy-engine stream
   std::vector<cudaEvent_t> ev;
   cudaEvent_t done = nullptr;
-  unsigned* err = nullptr;  // device: a ready-flag wait timed out
+  unsigned* err = nullptr;  // mapped host word (device view): a ready-flag wait timed out
+  unsigned* err_host = nullptr;
   unsigned epoch = 0;       // exchanges so far (same on every rank)
 };
 XState g_x;
@@ -144,8 +150,10 @@ XState& xstate() {
     g_x.ev.resize(kMaxChunks);
     for (auto& e : g_x.ev) IQCC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     IQCC_CUDA(cudaEventCreateWithFlags(&g_x.done, cudaEventDisableTiming));
-    IQCC_CUDA(cudaMalloc(&g_x.err, sizeof(unsigned)));
-    IQCC_CUDA(cudaMemset(g_x.err, 0, sizeof(unsigned)));
+    // read by the host after the step's own synchronizations: no extra round trip
+    IQCC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_x.err_host), sizeof(unsigned), cudaHostAllocMapped));
+    *g_x.err_host = 0;
+    IQCC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_x.err), g_x.err_host, 0));
   }
   return g_x;
 }
@@ -231,10 +239,19 @@ __global__ void k_flag_wait(const unsigned* flag, unsigned epoch, unsigned* err)
     if ((int)(v - epoch) >= 0) return;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > 60ull * 1000000000ull) {
-      atomicExch(err, 1u);
+      *(volatile unsigned*)err = 1u;
       return;
     }
     __nanosleep(256);
+  }
+}
+
+/// A ready-flag wait that gave up means the partner stopped
+/// participating: fail loudly (checked after the step's synchronizations).
+void check_wait_timeout() {
+  if (g_x.err_host && *(volatile unsigned*)g_x.err_host) {
+    *g_x.err_host = 0;
+    throw std::runtime_error("parallel_dress: the partner's products did not arrive (60 s)");
   }
 }
 
@@ -286,8 +303,8 @@ void p2p_prepare(size_t need, size_t W) {
   g_p2p.tried = true;
   const size_t cap = regrow ? std::max<size_t>(2 * (size_t)need_g, 2 * g_p2p_last_cap) + 1024
                             : (size_t)need_g + need_g / 4 + 1024;
-  bool ok = cudaMalloc(&g_p2p.mine, p2p_flag_off(cap, W) + kMaxChunks * sizeof(unsigned)) == cudaSuccess;
-  if (ok) ok = cudaMemset(g_p2p.mine + p2p_flag_off(cap, W), 0, kMaxChunks * sizeof(unsigned)) == cudaSuccess;
+  bool ok = cudaMalloc(&g_p2p.mine, p2p_flag_off(cap, W) + kP2PTail) == cudaSuccess;
+  if (ok) ok = cudaMemset(g_p2p.mine + p2p_flag_off(cap, W), 0, kP2PTail) == cudaSuccess;
   cudaIpcMemHandle_t h;
   std::memset(&h, 0, sizeof(h));
   if (ok) ok = cudaIpcGetMemHandle(&h, g_p2p.mine) == cudaSuccess;
@@ -389,7 +406,7 @@ void multi_shutdown() {
     if (g_x.xst) {
       for (auto e : g_x.ev) cudaEventDestroy(e);
       cudaEventDestroy(g_x.done);
-      cudaFree(g_x.err);
+      cudaFreeHost(g_x.err_host);
       cudaStreamDestroy(g_x.xst);
       g_x = XState{};
     }
@@ -620,10 +637,7 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
       // the staging buffer is free again once the copies are done; and a
       // timed-out wait means the partner never delivered
       IQCC_CUDA(cudaStreamWaitEvent(st, g_x.done, 0));
-      unsigned* he = static_cast<unsigned*>(host_pinned(sizeof(unsigned)));
-      IQCC_CUDA(cudaMemcpyAsync(he, g_x.err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      host_sync(st);
-      if (*he) throw std::runtime_error("parallel_dress: the partner's products did not arrive (60 s)");
+      check_wait_timeout();  // (the merge ended with a synchronize)
     } else {
       if (rbits)
         recv_slot_bits_packed(rbits, nrecv, theta);
@@ -677,6 +691,7 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
       cs_out->dropped_weight += r.dropped_weight;
     }
   }
+  check_wait_timeout();  // (the compress select ended with a synchronize)
 }
 
 void parallel_reserve(DeviceStore& s, size_t terms) { p2p_prepare(std::max(terms, s.M), 2 * (size_t)s.B); }
