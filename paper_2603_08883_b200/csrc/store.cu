@@ -712,7 +712,7 @@ template <class HG>
 __device__ __forceinline__ bool block_pick(const HG* __restrict__ hg, const unsigned* __restrict__ hl,
                                            int nbins, ull r, int* x_out, ull* before_g,
                                            ull* before_l) {
-  __shared__ ull sg[256], sl[256];
+  __shared__ ull scr[256 / 32 + 2];
   __shared__ int s_x;
   __shared__ ull s_bg, s_bl;
   const int per = (nbins + 255) / 256;
@@ -725,19 +725,11 @@ __device__ __forceinline__ bool block_pick(const HG* __restrict__ hg, const unsi
       tl += hl[x];
     }
   }
-  sg[threadIdx.x] = tg;
-  sl[threadIdx.x] = tl;
   if (threadIdx.x == 0) s_x = -1;
-  __syncthreads();
-  // exclusive prefix over threads (thread 0 holds the top bins)
-  for (int o = 1; o < 256; o <<= 1) {
-    ull vg = threadIdx.x >= o ? sg[threadIdx.x - o] : 0, vl = threadIdx.x >= o ? sl[threadIdx.x - o] : 0;
-    __syncthreads();
-    sg[threadIdx.x] += vg;
-    sl[threadIdx.x] += vl;
-    __syncthreads();
-  }
-  const ull eg = sg[threadIdx.x] - tg, el = sl[threadIdx.x] - tl;
+  // exclusive prefixes over threads (thread 0 holds the top bins): warp
+  // shuffles plus one pass over the warp totals
+  const ull eg = block_exclusive<256>(tg, 0ull, OpAdd(), scr, (ull*)nullptr);
+  const ull el = block_exclusive<256>(tl, 0ull, OpAdd(), scr, (ull*)nullptr);
   if (eg < r && eg + tg >= r) {  // the crossing lies in this thread's run
     ull cg = eg, cl = el;
     for (int k = 0; k < per; ++k) {
@@ -988,6 +980,66 @@ __global__ void __launch_bounds__(256) k_cand_filter(const ull* __restrict__ cv,
   hist_end(do_hist, dmask, sh, hist);
 }
 
+// Single store: the digit rounds after the first over a small candidate
+// set in one CTA (the set in shared memory, one histogram, pick and filter
+// per round, no launches between rounds), then the ties.  More than
+// kFinishCap candidates: leaves the state alone (top >= 0) and the host
+// runs the rounds kernel by kernel.
+constexpr int kFinishCap = 3584;  // 28 KB of candidates + a 16 KB digit histogram (static shared)
+__global__ void __launch_bounds__(256) k_select_finish(const ull* __restrict__ cv, const ull* __restrict__ ci,
+                                                       const ull* __restrict__ n_in, SelState* __restrict__ st,
+                                                       ull* __restrict__ ov, ull* __restrict__ oi,
+                                                       ull* __restrict__ n_out) {
+  __shared__ ull sv[kFinishCap];
+  __shared__ unsigned sh[1 << kDigitBits];
+  __shared__ unsigned s_n;
+  if (st->fail || st->top < 0) return;
+  const ull n = *n_in;
+  if (n > (ull)kFinishCap) return;
+  for (int i = threadIdx.x; i < (int)n; i += blockDim.x) sv[i] = cv[i];
+  ull km = st->known_mask, kv = st->known_val, r = st->r, above = st->local_above;
+  int top = st->top;
+  __syncthreads();
+  while (top >= 0) {
+    const int width = min(kDigitBits, top + 1);
+    const int shift = top + 1 - width;
+    const unsigned dmask = (1u << width) - 1u;
+    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < (int)n; i += blockDim.x)
+      if ((sv[i] & km) == kv) atomicAdd(sh + ((sv[i] >> shift) & dmask), 1u);
+    __syncthreads();
+    int x;
+    ull bg, bl;
+    if (!block_pick(sh, sh, (int)dmask + 1, r, &x, &bg, &bl)) {
+      if (threadIdx.x == 0) st->fail = 2;
+      return;
+    }
+    r -= bg;
+    above += bl;
+    km |= (ull)dmask << shift;
+    kv |= (ull)x << shift;
+    top = shift - 1;
+  }
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)n; i += blockDim.x)
+    if (sv[i] == kv) {  // every bit fixed: the ties
+      const unsigned pos = atomicAdd(&s_n, 1u);
+      ov[pos] = sv[i];
+      oi[pos] = ci[i];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->r = r;
+    st->local_above = above;
+    st->known_mask = km;
+    st->known_val = kv;
+    st->top = -1;
+    *n_out = s_n;
+  }
+}
+
 template <int B>
 __global__ void k_dropped_weight(const ull* __restrict__ keys, const double* __restrict__ coef,
                                  size_t M, Filter filt, double* __restrict__ partial) {
@@ -1136,8 +1188,20 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
           cur = nxt;
         }
       };
-      run_rounds(0, kPlanned);
+      // single store: round 0 by kernels, the rest in one CTA
+      // (k_select_finish) unless more than kFinishCap candidates survive it
+      static const bool by_rounds = getenv("IQCC_SELECT_ROUNDS") != nullptr;
+      const bool finish = red == nullptr && !by_rounds;
       int rounds = kPlanned;
+      if (finish) {
+        run_rounds(0, 1);
+        KernelScope ks("select_digits");
+        k_select_finish<<<1, 256, 0, st>>>(av[1], ai[1], cnt + 1, sel, av[0], ai[0], cnt + kMaxRounds);
+        cur = 0;
+        rounds = kMaxRounds;
+      } else {
+        run_rounds(0, kPlanned);
+      }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
       // local and global tie counts come back with the select state; the
       // first kTieSpec tied indices travel speculatively in the same copy
@@ -1159,8 +1223,11 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         host_sync(st);
       };
       read_back();
-      if (!hsp->fail && hsp->top >= 0) {  // edge bin: finish the remaining bits
-        run_rounds(kPlanned, kMaxRounds);
+      if (!hsp->fail && hsp->top >= 0) {
+        // edge bin: finish the remaining bits; or the one-CTA finish had too
+        // many candidates: the rounds after round 0
+        cur = finish ? 1 : cur;
+        run_rounds(finish ? 1 : kPlanned, kMaxRounds);
         rounds = kMaxRounds;
         read_back();
       }
