@@ -180,7 +180,7 @@ def run_c4(args):
     cands = odd_y_candidates(n, max(kg, int(args.dis_poles)), 4)
     mg = int(args.dis_generic_terms)
     dg = iqcc.DeviceSum.generate_mol(n, mg, 3) if mg != m else d
-    t, g = timed(lambda: dg.gradients(generic, cands[:kg]), reps=1)
+    t, g = timed(lambda: dg.gradients(generic, cands[:kg]), reps=1)  # nibble tables (default)
     # useful multiplies per pair: expect_word over supp(T ^ P) = supp(T) | supp(P)
     # for the anticommuting pairs (others are skipped), from a 2e4 x 256 sample
     hs = dg.download()
@@ -204,14 +204,32 @@ def run_c4(args):
         fp64 = json.loads(subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout)
     except Exception:
         pass
-    achieved = kg * mg / t * mul_per_pair
-    out.append(row("C4", omega="generic", n_qubits=n, terms=mg, candidates=kg, s=t,
-                   pairs_per_s=kg * mg / t, useful_dmul_per_pair=mul_per_pair, useful_dmul_per_s=achieved,
-                   fp64_dmul_peak_per_s=fp64["dmul_per_s"] if fp64 else None,
+    # the nibble kernel multiplies ceil(n/4) group values per anticommuting pair (+2)
+    anti_frac = float(anti.mean())
+    nib_per_pair = anti_frac * ((n + 3) // 4 + 2)
+    achieved = kg * mg / t * nib_per_pair
+    out.append(row("C4", omega="generic", kernel="nibble tables", n_qubits=n, terms=mg, candidates=kg, s=t,
+                   pairs_per_s=kg * mg / t, anticommuting_frac=anti_frac, dmul_per_pair=nib_per_pair,
+                   dmul_per_s=achieved, fp64_dmul_peak_per_s=fp64["dmul_per_s"] if fp64 else None,
                    fp64_frac=achieved / fp64["dmul_per_s"] if fp64 else None,
-                   note="bit-exact per candidate (sequential canonical-order sum); compute-bound: "
-                        "one fp64 multiply per qubit of supp(T) | supp(P) per anticommuting pair; peak "
-                        "from tools/fp64_peak.cu (measured on this box)"))
+                   note="within 1e-13 of the reference per candidate (canonical-order sum, nibble-group "
+                        "products); per anticommuting pair ceil(n/4) table reads + multiplies; peak from "
+                        "tools/fp64_peak.cu (measured on this box)"))
+    # the bit-exact ascending-qubit kernel (IQCC_DIS_EXACT=1) on a slice of the terms
+    me = min(mg, int(args.dis_exact_terms))
+    de = iqcc.DeviceSum.generate_mol(n, me, 3)
+    os.environ["IQCC_DIS_EXACT"] = "1"
+    try:
+        te, _ = timed(lambda: de.gradients(generic, cands[:kg]), reps=1)
+    finally:
+        del os.environ["IQCC_DIS_EXACT"]
+    del de
+    out.append(row("C4", omega="generic", kernel="exact (IQCC_DIS_EXACT=1)", n_qubits=n, terms=me, candidates=kg,
+                   s=te, pairs_per_s=kg * me / te, useful_dmul_per_pair=mul_per_pair,
+                   dmul_per_s=kg * me / te * mul_per_pair,
+                   fp64_frac=kg * me / te * mul_per_pair / fp64["dmul_per_s"] if fp64 else None,
+                   note="bit-exact per candidate: one multiply per qubit of supp(T) | supp(P) per "
+                        "anticommuting pair, ascending qubit order"))
     del dg
     kp = int(args.dis_poles)
     t, g = timed(lambda: d.gradients(hf, cands[:kp], True), reps=1)
@@ -324,6 +342,7 @@ def main():
     ap.add_argument("--dis-generic", type=float, default=1e5)
     ap.add_argument("--dis-generic-terms", type=float, default=1e7)
     ap.add_argument("--dis-poles", type=float, default=1e5)
+    ap.add_argument("--dis-exact-terms", type=float, default=1e6)
     ap.add_argument("--c5-terms", type=float, default=5e7)
     ap.add_argument("--c5-target", type=float, default=1.25e8)
     ap.add_argument("--poly-terms", type=float, default=1e7)

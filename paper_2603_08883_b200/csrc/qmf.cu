@@ -766,6 +766,107 @@ __global__ void __launch_bounds__(128) k_dis_full(const ull* __restrict__ keys,
   if (cid < K) g_out[cid] = g;
 }
 
+// The generic-Omega gradient with nibble tables (about
+// n/4 table reads and multiplies per pair): <omega|T^P|omega> is the
+// product of the tables of T^P's 4-qubit groups (k_nibble_table), in two
+// interleaved partial products for instruction-level parallelism.  The
+// rounding order differs from expect_word's ascending-qubit product, so a
+// gradient is within ~1e-15 relative of the reference's (the engine's
+// energies and gradients are specified to 1e-10); IQCC_DIS_EXACT=1 (and
+// dis_candidates, whose ranking must match the reference's bit for bit)
+// takes k_dis_full.
+template <int B>
+__global__ void __launch_bounds__(256) k_dis_nib(const ull* __restrict__ keys, const double* __restrict__ coef,
+                                                 size_t M, Filter filt, const double* __restrict__ tab_g, int ng,
+                                                 const ull* __restrict__ cands, size_t K,
+                                                 double* __restrict__ g_part) {
+  constexpr int TT = 256;
+  extern __shared__ double tab[];  // [ng][256]
+  __shared__ ull tk[TT * 2 * B];
+  __shared__ double tc[TT];
+  for (int i = threadIdx.x; i < ng * 256; i += blockDim.x) tab[i] = tab_g[i];
+  const size_t cid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  // term slice blockIdx.y of gridDim.y (partial sums, added in slice order)
+  const size_t per = ((M + gridDim.y - 1) / gridDim.y + TT - 1) / TT * TT;
+  const size_t lo = blockIdx.y * per, hi = min(M, lo + per);
+  Key<B> P;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) P.w[w] = 0;
+  if (cid < K) P = load_key<B>(cands, cid);
+  double g = 0.0;
+  for (size_t base = lo; base < hi; base += TT) {
+    __syncthreads();
+    const size_t i = base + threadIdx.x;
+    if (i < hi) {
+      const Key<B> k = load_key<B>(keys, i);
+      double c = coef[i];
+      if (!filter_keep(filt, i, c, i == 0 && key_is_identity<B>(k))) c = 0.0;  // Im(0) == 0: skipped
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) tk[(size_t)threadIdx.x * 2 * B + w] = k.w[w];
+      tc[threadIdx.x] = c;
+    }
+    __syncthreads();
+    const int n = (int)min((size_t)TT, hi - base);
+    // two terms per iteration: two independent sets of multiply chains
+    // (the loop is bound by table-read and multiply latency, with the
+    // table capping residency at 3 blocks per SM)
+    for (int j = 0; j < n; j += 2) {
+      Key<B> k[2];
+      double c[2];
+      bool anti[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int jj = min(j + t, n - 1);
+#pragma unroll
+        for (int w = 0; w < 2 * B; ++w) k[t].w[w] = tk[(size_t)jj * 2 * B + w];
+        c[t] = j + t < n ? tc[jj] : 0.0;
+        anti[t] = cid < K && c[t] != 0.0 && anticommutes<B>(k[t], P);
+      }
+      if (!__any_sync(0xffffffffu, anti[0] || anti[1])) continue;  // warp-uniform
+      double v[2][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) v[t][0] = v[t][1] = v[t][2] = v[t][3] = 1.0;
+#pragma unroll
+      for (int w = 0; w < B; ++w)
+#pragma unroll
+        for (int h = 1; h >= 0; --h) {
+          unsigned xh[2], zh[2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            xh[t] = (unsigned)((k[t].w[w] ^ P.w[w]) >> (32 * h));
+            zh[t] = (unsigned)((k[t].w[B + w] ^ P.w[B + w]) >> (32 * h));
+          }
+#pragma unroll
+          for (int nn = 7; nn >= 0; --nn) {
+            const int q = 16 * w + 8 * (1 - h) + (7 - nn);
+            if (q < ng) {
+#pragma unroll
+              for (int t = 0; t < 2; ++t)
+                v[t][q & 3] = __dmul_rn(
+                    v[t][q & 3], tab[q * 256 + (((zh[t] >> (4 * nn)) & 15u) | (((xh[t] >> (4 * nn)) & 15u) << 4))]);
+            }
+          }
+        }
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (anti[t]) {
+          const double im = product_phase<B>(k[t], P) == 1 ? c[t] : -c[t];
+          g = __dadd_rn(g, __dmul_rn(im, __dmul_rn(__dmul_rn(v[t][0], v[t][1]), __dmul_rn(v[t][2], v[t][3]))));
+        }
+    }
+  }
+  if (cid < K) g_part[blockIdx.y * K + cid] = g;
+}
+
+/// g[k] = the slices' partial sums in slice order.
+__global__ void k_dis_fold(const double* __restrict__ g_part, size_t K, int S, double* __restrict__ g) {
+  const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double v = g_part[k];
+  for (int s = 1; s < S; ++s) v = __dadd_rn(v, g_part[s * K + k]);
+  g[k] = v;
+}
+
 // Candidate restricted to its flip group [lo, hi) (group_gradient).
 template <int B>
 __global__ void k_dis_group(const ull* __restrict__ keys, const double* __restrict__ coef,
@@ -824,7 +925,7 @@ __global__ void k_group_range(const ull* __restrict__ keys, size_t M, const ull*
 
 template <int B>
 static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t* cands_rows,
-                           size_t K, bool flip_group_only, double* g) {
+                           size_t K, bool flip_group_only, double* g, bool exact = false) {
   Workspace& ws = workspace();
   cudaStream_t st = stream();
   const int nq = (int)s.n_qubits;
@@ -845,11 +946,34 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
     count_launch("dis_gradient");
   } else {
     const std::vector<double> f4 = factor_rows(factors, nq, B);
-    double* f4d = ws.grad_part.as<double>(f4.size());
+    // nibble path: term slices so that the candidate blocks fill the SMs
+    // (the table limits a SM to a few resident blocks); partials after f4
+    const unsigned cb = (unsigned)((K + 255) / 256);
+    const int S = (int)std::max<size_t>(1, std::min<size_t>({8, (148 * 4 + cb - 1) / cb, (s.M + 4095) / 4096}));
+    double* f4d = ws.grad_part.as<double>(f4.size() + (size_t)S * K);
+    double* gpart = f4d + f4.size();
     IQCC_CUDA(cudaMemcpyAsync(f4d, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-    KernelScope ks("dis_gradient");
-    k_dis_full<B><<<(unsigned)((K + 127) / 128), 128, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, f4d, dc,
-                                                                K, dg);
+    const char* ex = getenv("IQCC_DIS_EXACT");
+    if (exact || (ex && atoi(ex))) {
+      KernelScope ks("dis_gradient");
+      k_dis_full<B><<<(unsigned)((K + 127) / 128), 128, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, f4d, dc,
+                                                                  K, dg);
+    } else {
+      // nibble tables of the groups holding qubits (the rest are all 1.0)
+      const int ng = std::max(1, (nq + 3) / 4);
+      double* nibt = ws.misc2.as<double>((size_t)ng * 256);
+      k_nibble_table<<<(unsigned)((ng * 256 + 255) / 256), 256, 0, st>>>(f4d, ng, nibt);
+      const size_t smem = (size_t)ng * 256 * sizeof(double);
+      if (func_attr_once((const void*)k_dis_nib<B>, ctx_device(ctx_current())))
+        IQCC_CUDA(cudaFuncSetAttribute(k_dis_nib<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(16 * B * 256 * sizeof(double))));
+      KernelScope ks("dis_gradient");
+      k_dis_nib<B><<<dim3(cb, (unsigned)S), 256, smem, st>>>(s.keys(), s.coef(), s.M, s.filt, nibt, ng, dc, K,
+                                                             gpart);
+      k_dis_fold<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(gpart, K, S, dg);
+      count_launch("dis_gradient");
+      count_launch("dis_gradient");
+    }
   }
   IQCC_CUDA(cudaMemcpyAsync(g, dg, K * sizeof(double), cudaMemcpyDeviceToHost, st));
   IQCC_CUDA(cudaStreamSynchronize(st));
@@ -979,7 +1103,7 @@ static size_t dis_impl(DeviceStore& s, const double* factors, bool poles, size_t
   std::vector<uint64_t> crow(K * 2 * B);
   for (size_t k = 0; k < K; ++k) device_key_to_row(cand.data() + k * 2 * B, B, crow.data() + k * 2 * B);
   std::vector<double> g(K);
-  gradients_impl<B>(s, factors, crow.data(), K, poles, g.data());
+  gradients_impl<B>(s, factors, crow.data(), K, poles, g.data(), true);  // the ranking: exact values
   // best per group (|g| desc, canonical asc), screen, rank
   struct Pick {
     size_t c;

@@ -147,16 +147,23 @@ def test_gradient_known_answer(eng):  # test_dis.cpp:108-114
     assert eng.gradient(h, eng.QmfState.zeros(1), eng.PauliWord.from_string("Y")) == pytest.approx(1.0)
 
 
-@pytest.mark.parametrize("n", [5, 64, 124])
-def test_gradient_bit_exact(eng, port, n):
+@pytest.mark.parametrize("n", [5, 64, 124, 200])
+def test_gradient_bit_exact(eng, port, monkeypatch, n):
+    """DIS gradients at a generic Omega: the nibble-table kernel (default)
+    within 1e-13 of the reference, the ascending-qubit kernel
+    (IQCC_DIS_EXACT=1) bit for bit."""
     rng = port.rng(419 + n)
     h = rng.sum(n, 2000)
     th, ph = rng.qmf(n)
     d = eng.DeviceSum.upload(host(eng, h))
     cands = np.stack([rng.word(n, False) for _ in range(64)])
+    want = np.array([port.gradient(h, th, ph, c) for c in cands])
+    g = d.gradients(eng.QmfState(th, ph), cands)
+    assert np.abs(g - want).max() <= 1e-13 * max(1.0, np.abs(want).max())
+    monkeypatch.setenv("IQCC_DIS_EXACT", "1")
     g = d.gradients(eng.QmfState(th, ph), cands)
     for k in range(len(cands)):
-        assert g[k] == port.gradient(h, th, ph, cands[k])
+        assert g[k] == want[k]
 
 
 def test_dis_candidates_random(eng, port):  # test_dis.cpp:231-263 shapes
@@ -360,7 +367,7 @@ def ker_n(eng, port, n, th, ph, ents):
     return port.poly_kernels(z, th, ph, ents, 2)[3]
 
 
-def test_c4_shape_gradients_bit_exact(eng, port):
+def test_c4_shape_gradients_bit_exact(eng, port, monkeypatch):
     """SURVEY.md §8(d) C4 shape: G_mol(100 qubits, seed 3) against odd-Y
     candidates (seed 4) at a generic Omega and, flip-group restricted, at HF
     poles.  Gradients are summed in canonical order like the reference's
@@ -376,9 +383,15 @@ def test_c4_shape_gradients_bit_exact(eng, port):
     rs = np.random.default_rng(9)
     th, ph = rs.uniform(-3, 3, n), rs.uniform(-3, 3, n)
     sel = [0, 1, 9, 17, 40, 63]
+    want = {k: port.gradient(h, th, ph, cands[k]) for k in sel}
+    g = d.gradients(eng.QmfState(th, ph), cands)  # nibble tables (default)
+    for k in sel:
+        assert abs(g[k] - want[k]) <= 1e-13 * max(1.0, abs(want[k])), k
+    monkeypatch.setenv("IQCC_DIS_EXACT", "1")  # ascending-qubit products: bit-exact
     g = d.gradients(eng.QmfState(th, ph), cands)
     for k in sel:
-        assert g[k] == port.gradient(h, th, ph, cands[k]), k
+        assert g[k] == want[k], k
+    monkeypatch.delenv("IQCC_DIS_EXACT")
     thp = np.where(np.arange(n) < n // 4, np.pi, 0.0)
     gp = d.gradients(eng.QmfState(thp, np.zeros(n)), cands, flip_group_only=True)
     for k in sel:  # exact at the poles (every other term's contribution vanishes)
