@@ -1,10 +1,11 @@
 """GPU parity for the energy / gradient / DIS rows:
 expect_sum, qmf_energy_gradient, gradient, dis_candidates and
 choose_partition_bits against the CPU checker, restating tests/test_qmf.cpp
-and tests/test_dis.cpp.  Tolerances: per-term values of expect_word and the
-DIS gradients are summed in the reference's order and compared bit-exactly;
-energies and QMF gradients are sums in a different order, compared at
-1e-10 relative (north_star's fp64 tolerance)."""
+and tests/test_dis.cpp.  Tolerances: the exact modes (per-term expect_word
+values, IQCC_DIS_EXACT gradients, dis_candidates) are summed in the
+reference's order and compared bit-exactly; the nibble-table DIS gradients
+within 1e-13; energies and QMF gradients are sums in a different order,
+compared at 1e-10 relative (north_star's fp64 tolerance)."""
 import math
 import os
 
