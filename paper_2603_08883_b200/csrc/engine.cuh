@@ -546,6 +546,12 @@ struct Reducer {
   /// order; *mine_offset receives where this rank's keys start.
   virtual std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t words_per_key,
                                        size_t* mine_offset) = 0;
+  /// Device allgather of n u64 per rank into recv[world][n] on the stream
+  /// (false: not offered; the caller falls back).  world/rank: this group.
+  virtual bool allgather_device(const ull* /*send*/, ull* /*recv*/, size_t /*n*/) { return false; }
+  virtual bool can_allgather() const { return false; }
+  virtual int group_size() const { return 1; }
+  virtual int group_rank() const { return 0; }
 };
 /// glob_known (partitioned, optional): {global count_eps, global identity
 /// count} already reduced by the caller, saving the first reduction.

@@ -71,6 +71,13 @@ struct NcclReducer : Reducer {
     // NCCL here: the time in these collectives is the ranks' skew)
     IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, comm().comm, stream()));
   }
+  bool allgather_device(const ull* send, ull* recv, size_t n) override {
+    IQCC_NCCL(ncclAllGather(send, recv, n, ncclUint64, comm().comm, stream()));
+    return true;
+  }
+  bool can_allgather() const override { return true; }
+  int group_size() const override { return g_comm.world; }
+  int group_rank() const override { return g_comm.rank; }
   std::vector<ull> gather_keys(const std::vector<ull>& mine, size_t W, size_t* mine_off) override {
     Comm& c = comm();
     cudaStream_t st = stream();

@@ -993,9 +993,9 @@ __global__ void __launch_bounds__(256) k_select_finish(const ull* __restrict__ c
   __shared__ ull sv[kFinishCap];
   __shared__ unsigned sh[1 << kDigitBits];
   __shared__ unsigned s_n;
-  if (st->fail || st->top < 0) return;
+  if (st->fail) return;
   const ull n = *n_in;
-  if (n > (ull)kFinishCap) return;
+  if (n > (ull)kFinishCap) return;  // (top >= 0 here: one round fixes at most 12 of >= 48 bits)
   for (int i = threadIdx.x; i < (int)n; i += blockDim.x) sv[i] = cv[i];
   ull km = st->known_mask, kv = st->known_val, r = st->r, above = st->local_above;
   int top = st->top;
@@ -1032,6 +1032,87 @@ __global__ void __launch_bounds__(256) k_select_finish(const ull* __restrict__ c
   __syncthreads();
   if (threadIdx.x == 0) {
     st->r = r;
+    st->local_above = above;
+    st->known_mask = km;
+    st->known_val = kv;
+    st->top = -1;
+    *n_out = s_n;
+  }
+}
+
+// Ranks: after the first filter round every rank's few candidates are
+// allgathered (count, then up to kFinishCapRank values); each rank then
+// runs the remaining digit rounds redundantly over the same gathered
+// multiset (global histogram) and its own slice of it (local histogram),
+// exactly as the allreduced rounds would, and extracts its local ties.
+// Any rank over the cap: the state is left alone (top >= 0) and the host
+// runs the allreduced rounds.
+constexpr int kFinishCapRank = 1024;
+__global__ void k_pack_cands(const ull* __restrict__ cv, const ull* __restrict__ n_in, ull* __restrict__ out) {
+  const ull n = *n_in;
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = n;
+  const int m = (int)min(n, (ull)kFinishCapRank);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) out[1 + i] = cv[i];
+}
+
+__global__ void __launch_bounds__(256) k_select_finish_ranks(const ull* __restrict__ gath, int world, int rank,
+                                                             const ull* __restrict__ cv, const ull* __restrict__ ci,
+                                                             SelState* __restrict__ st, ull* __restrict__ ov,
+                                                             ull* __restrict__ oi, ull* __restrict__ n_out) {
+  extern __shared__ ull gv[];  // [world][kFinishCapRank]
+  __shared__ unsigned hgl[1 << kDigitBits], hlo[1 << kDigitBits];
+  __shared__ unsigned s_n;
+  if (st->fail) return;
+  constexpr int S = kFinishCapRank + 1;
+  for (int r = 0; r < world; ++r)
+    if (gath[(size_t)r * S] > (ull)kFinishCapRank) return;  // uniform: every rank sees the same counts
+  int cnt[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) cnt[r] = r < world ? (int)gath[(size_t)r * S] : 0;
+  for (int r = 0; r < world; ++r)
+    for (int i = threadIdx.x; i < cnt[r]; i += blockDim.x) gv[r * kFinishCapRank + i] = gath[(size_t)r * S + 1 + i];
+  ull km = st->known_mask, kv = st->known_val, rr = st->r, above = st->local_above;
+  int top = st->top;
+  __syncthreads();
+  while (top >= 0) {
+    const int width = min(kDigitBits, top + 1);
+    const int shift = top + 1 - width;
+    const unsigned dmask = (1u << width) - 1u;
+    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x) hgl[b] = hlo[b] = 0;
+    __syncthreads();
+    for (int r = 0; r < world; ++r)
+      for (int i = threadIdx.x; i < cnt[r]; i += blockDim.x) {
+        const ull v = gv[r * kFinishCapRank + i];
+        if ((v & km) == kv) {
+          const unsigned d = (unsigned)((v >> shift) & dmask);
+          atomicAdd(hgl + d, 1u);
+          if (r == rank) atomicAdd(hlo + d, 1u);
+        }
+      }
+    __syncthreads();
+    int x;
+    ull bg, bl;
+    if (!block_pick(hgl, hlo, (int)dmask + 1, rr, &x, &bg, &bl)) {
+      if (threadIdx.x == 0) st->fail = 2;
+      return;
+    }
+    rr -= bg;
+    above += bl;
+    km |= (ull)dmask << shift;
+    kv |= (ull)x << shift;
+    top = shift - 1;
+  }
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt[rank]; i += blockDim.x)
+    if (cv[i] == kv) {  // this rank's ties (its candidates are its gathered slice)
+      const unsigned pos = atomicAdd(&s_n, 1u);
+      ov[pos] = cv[i];
+      oi[pos] = ci[i];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->r = rr;
     st->local_above = above;
     st->known_mask = km;
     st->known_val = kv;
@@ -1191,16 +1272,36 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       // single store: round 0 by kernels, the rest in one CTA
       // (k_select_finish) unless more than kFinishCap candidates survive it
       static const bool by_rounds = getenv("IQCC_SELECT_ROUNDS") != nullptr;
-      const bool finish = red == nullptr && !by_rounds;
-      int rounds = kPlanned;
-      if (finish) {
+      // ranks: round 0 allreduced, then the rest on an allgather of the
+      // few surviving candidates (k_select_finish_ranks)
+      const int world = red ? red->group_size() : 1;
+      ull* gsend = nullptr;
+      bool finish = !by_rounds && (red == nullptr || (world <= 8 && red->can_allgather()));
+      if (finish && red) {
+        const size_t S = (size_t)kFinishCapRank + 1;
+        gsend = ws.misc3.as<ull>(S * (world + 1));
+        run_rounds(0, 1);
+        KernelScope ks("select_digits");
+        k_pack_cands<<<4, 256, 0, st>>>(av[1], cnt + 1, gsend + S * world);
+        if (!red->allgather_device(gsend + S * world, gsend, S)) throw std::logic_error("compress: no allgather");
+        const size_t smem = (size_t)world * kFinishCapRank * sizeof(ull);
+        if (func_attr_once((const void*)k_select_finish_ranks, ctx_device(ctx_current())))
+          IQCC_CUDA(cudaFuncSetAttribute(k_select_finish_ranks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(8 * kFinishCapRank * sizeof(ull))));
+        k_select_finish_ranks<<<1, 256, smem, st>>>(gsend, world, red->group_rank(), av[1], ai[1], sel, av[0], ai[0],
+                                                     cnt + kMaxRounds);
+        count_launch("select_digits");
+      } else if (finish) {
         run_rounds(0, 1);
         KernelScope ks("select_digits");
         k_select_finish<<<1, 256, 0, st>>>(av[1], ai[1], cnt + 1, sel, av[0], ai[0], cnt + kMaxRounds);
-        cur = 0;
-        rounds = kMaxRounds;
       } else {
         run_rounds(0, kPlanned);
+      }
+      int rounds = kPlanned;
+      if (finish) {
+        cur = 0;
+        rounds = kMaxRounds;
       }
       if (getenv("IQCC_DEBUG")) debug_check("select digits");
       // local and global tie counts come back with the select state; the
