@@ -67,3 +67,21 @@ def test_partitioned_dressing_matches_serial(world, args):
     assert "bitexact=True" in r.stdout and "energy_ok=True" in r.stdout
     if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libiqcc_ref.so")):
         assert "checker=reference" in r.stdout  # the unmodified reference is the checker
+
+
+@pytest.mark.parametrize("world", [2])
+def test_c5_script_small(world):
+    """bench_c5.py (SURVEY.md §8(d) C5 across GPUs) at a small size: uncapped
+    growth over the chunked exchange, receive buffers reserved up front, then
+    compress_partitioned to the target; the kept count is the target."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "bench_c5.py"),
+           "--terms", "4e5", "--target", "1e6"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["grown_to"] > 1_000_000 and line["kept"] == 1_000_000
+    assert any(s["exchanged"] > 0 for s in line["steps"])
