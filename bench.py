@@ -316,6 +316,9 @@ def run_gpu_arm(args, rank, world, local_rank):
             "select_gather", "select_digits", "exchange", "host_wait", "host_dress", "host_compress", "span_dress", "span_compress", "host_alloc", "host_compress_inner", "spec_redo"]}
     for f in ["materialize", "exch_count", "exch_signal"]:
         fam[f] = native.profile_get(f)[0]
+    # N > 1: time per dressing step by kind (mask != 0: products exchanged)
+    steps_by_kind = {k: (lambda t: {"steps": t[1], "ms_per_step": t[0] / t[1] if t[1] else None})(
+        native.profile_get(f)) for k, f in (("exchange", "step_exchange"), ("local", "step_local"))}
     native.profile(False)
     if dist:
         print(f"[bench] rank {rank}: shard {d.size()} terms, sent {sent[0]} products, ms {ms:.2f}, "
@@ -426,6 +429,7 @@ def run_gpu_arm(args, rank, world, local_rank):
             "spec_redos": native.profile_get("spec_redo")[1],
             "kernel_ms": fam,
             "kernel_ms_note": "CUDA events per kernel family over a second, profiled pass of the same K steps (the timed pass runs with profiling off)",
+            "dressing_steps_by_kind": steps_by_kind if world > 1 else None,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "parity": parity,

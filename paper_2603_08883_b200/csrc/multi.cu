@@ -448,6 +448,10 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
   const bool want_hist = eps > 0.0 || max_terms != SIZE_MAX;
   if (!want_hist) theta = exact = 0.0;  // no compress follows: every term keeps a slot
   const bool exch = !(mask == 0 || sn == 0.0);
+  // host wall time per step kind (each step ends with a synchronize, so it
+  // tracks the device time): SURVEY §8(d) C3 reports mask = 0 and mask != 0
+  // steps separately
+  HostScope step_scope(exch ? "step_exchange" : "step_local");
   const size_t M0 = s.M, L0 = s.logical;
   const Filter F0 = s.filt;
   DressOutcome o;
