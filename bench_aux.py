@@ -5,6 +5,9 @@ bench.py carries the driver's one-line contract (C3 dressing throughput);
 this script measures the remaining §8(d) rows on one B200 and prints one
 JSON object per row (profiles/r1_aux_*.json keeps the committed copy):
 
+  C1      the recorded 5-iteration iQCC trace of h2_ccpvdz (20 qubits) replayed:
+          DIS screening + dressing + energy per iteration ("s per iQCC
+          iter"); the reference's full iteration timed beside it
   C2      G_uniform(64, 1e6, seed 1): one 4-qubit entangler (tau 0.37, drop
           1e-12) + compress(1e-3), and the max_terms = 1.2e6 variant
           (latency-dominated; roofline (M_in + M_out) * 24 B)
@@ -302,6 +305,59 @@ def run_qcc(args):
     return [r1, r2]
 
 
+def run_c1(args):
+    """C1: the recorded iQCC trace of h2_ccpvdz (20 qubits,
+    tests/golden/c1_h2_ccpvdz.npz, made from the reference) replayed on the
+    device, one iteration at a time: DIS screening at the HF state
+    (dis_candidates, top 1), dressing with that iteration's generator and
+    its recorded amplitude, the energy.  The amplitude optimizer is not on
+    the device path (out of scope), so the device figure is an
+    iteration without it; the reference's full iteration (DIS, optimize,
+    dress, energy; oracle/_ref) is timed beside it for context."""
+    from paper_2603_08883_b200 import iqcc
+    from oracle.oracle import Oracle
+    import torch
+    g = np.load(os.path.join(ROOT, "tests", "golden", "c1_h2_ccpvdz.npz"))
+    n, ne = int(g["n_qubits"]), int(g["n_electrons"])
+    hf = iqcc.hf_reference([j < ne for j in range(n)])
+    gens, taus, it = g["gens"], g["taus"], g["gen_iter"]
+    iters = int(it.max()) + 1
+
+    def replay():
+        d = iqcc.DeviceSum.upload(iqcc.PauliSum(n, g["rows0"], g["coeffs0"]))
+        secs, picks_ok, energies = [], True, []
+        for i in range(iters):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            picks = d.dis_candidates(hf, 1)
+            sel = np.flatnonzero(it == i)
+            ans = iqcc.Ansatz([iqcc.PauliWord(n, gens[k]) for k in sel], [float(taus[k]) for k in sel])
+            d.dress_sequence(ans, 0.0)
+            e = d.expect(hf)
+            torch.cuda.synchronize()
+            secs.append(time.perf_counter() - t0)
+            picks_ok = picks_ok and len(picks) >= 1 and np.array_equal(picks[0].word.row, gens[sel[0]])
+            energies.append(e)
+        return secs, picks_ok, energies, len(d)
+
+    replay()
+    secs, picks_ok, energies, terms = replay()
+    e_err = float(np.max(np.abs(np.array(energies) - g["energies"][:iters])))
+    kind = "reference" if Oracle.available("reference") else "port"
+    orc = Oracle(kind)
+    h0 = orc.sum(n, np.ascontiguousarray(g["rows0"], np.uint64), np.ascontiguousarray(g["coeffs0"], np.complex128))
+    th = np.where(np.arange(n) < ne, np.pi, 0.0)
+    t0 = time.perf_counter()
+    orc.iqcc_iteration(h0, th, np.zeros(n), 1)
+    tc = time.perf_counter() - t0
+    return [row("C1", system="h2_ccpvdz", n_qubits=n, iterations=iters, terms_final=terms,
+                s_per_iter=float(np.mean(secs)), s_per_iter_each=[round(x, 6) for x in secs],
+                dis_pick_matches_reference=bool(picks_ok), max_energy_err=e_err,
+                cpu={"kind": kind, "cores": 1, "s_per_iter_incl_amplitude_optimization": tc},
+                note="device: DIS screening + dressing + energy per iteration with the recorded amplitudes "
+                     "(the optimizer is out of scope); cpu: the reference's full iqcc_iteration")]
+
+
 def run_poly(args):
     """build_poly_kernels (iqcc/optimizer.hpp:340-368, SURVEY.md §8(f) rank
     2): t(t+1)/2 sandwiches <omega|W_a H W_b|omega> over a G_mol sum at a
@@ -335,7 +391,7 @@ def run_poly(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c2,energy,c4,c5,qcc,poly")
+    ap.add_argument("--only", default="c1,c2,energy,c4,c5,qcc,poly")
     ap.add_argument("--qcc-terms", type=float, default=1e7)
     ap.add_argument("--energy-terms", type=float, default=1e8)
     ap.add_argument("--dis-terms", type=float, default=1e7)
@@ -355,7 +411,8 @@ def main():
     native.init(0)
     rows = []
     for part in args.only.split(","):
-        rows += {"c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5, "qcc": run_qcc, "poly": run_poly}[part](args)
+        rows += {"c1": run_c1, "c2": run_c2, "energy": run_energy, "c4": run_c4, "c5": run_c5, "qcc": run_qcc,
+                 "poly": run_poly}[part](args)
     if args.out:
         with open(args.out, "w") as f:
             json.dump(rows, f, indent=1)
