@@ -6,6 +6,8 @@
 // std::invalid_argument for precondition violations),
 // std::runtime_error -> IQCC_ERUNTIME, CUDA failures -> IQCC_ECUDA.
 #include <chrono>
+#include <tuple>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -68,6 +70,11 @@ struct Ctx {
   void* staging = nullptr;  // large page-locked buffer for host<->device reformatting
   size_t staging_bytes = 0;
   BigCache big;
+  // d2h_small: mapped page-locked landing buffer and the reads pending on it
+  unsigned char* peek_host = nullptr;
+  unsigned char* peek_dev = nullptr;
+  size_t peek_used = 0;
+  std::vector<std::tuple<void*, size_t, size_t>> peek_pending;  // (dst, offset, bytes)
 };
 
 static thread_local Ctx* g_ctx = nullptr;
@@ -187,6 +194,37 @@ void* host_staging(size_t bytes) {
   return c.staging;
 }
 
+constexpr size_t kPeekCap = (size_t)64 << 10;
+
+__global__ void k_peek(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, size_t n) {
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  Ctx& c = ctx();
+  const size_t off = (c.peek_used + 15) & ~(size_t)15;
+  if (bytes > kPeekCap || off + bytes > kPeekCap) {
+    IQCC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    return;
+  }
+  if (!c.peek_host) {
+    IQCC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c.peek_host), kPeekCap, cudaHostAllocMapped));
+    IQCC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.peek_dev), c.peek_host, 0));
+  }
+  count_launch("peek");
+  k_peek<<<1, 256, 0, st>>>(static_cast<const unsigned char*>(src), c.peek_dev + off, bytes);
+  IQCC_CUDA(cudaGetLastError());
+  c.peek_pending.emplace_back(dst, off, bytes);
+  c.peek_used = off + bytes;
+}
+
+static void peek_flush(Ctx& c) {
+  for (auto& [dst, off, n] : c.peek_pending) std::memcpy(dst, c.peek_host + off, n);
+  c.peek_pending.clear();
+  c.peek_used = 0;
+}
+
 // Busy-wait: a blocking/yielding synchronize can leave the GPU idle for a
 // scheduler quantum after every step boundary.
 static void spin_sync(cudaStream_t st) {
@@ -201,10 +239,12 @@ void host_sync(cudaStream_t st) {
   Ctx& c = ctx();
   if (!c.profiling) {
     spin_sync(st);
+    peek_flush(c);
     return;
   }
   const auto t0 = std::chrono::steady_clock::now();
   spin_sync(st);
+  peek_flush(c);
   const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   auto& e = c.prof["host_wait"];
   e.ms += ms;
@@ -399,6 +439,7 @@ void ctx_free(Ctx* c) {
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->staging) cudaFreeHost(c->staging);
+  if (c->peek_host) cudaFreeHost(c->peek_host);
   cudaStreamDestroy(c->own);
   delete c;
   ctx_bind(prev == c ? nullptr : prev);
@@ -436,6 +477,10 @@ namespace {
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
+  if (g_ctx) {  // reads queued by the failed call must not land later
+    g_ctx->peek_pending.clear();
+    g_ctx->peek_used = 0;
+  }
   return code;
 }
 

@@ -1787,7 +1787,7 @@ void plan_impl(DeviceStore& s, const Key<B>& P, bool products, bool read_A = tru
       return;
     }
     long long* a_host = static_cast<long long*>(host_pinned(sizeof(long long)));
-    IQCC_CUDA(cudaMemcpyAsync(a_host, a_total, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    d2h_small(a_host, a_total, sizeof(long long), st);
     host_sync(st);
     pl.A = (size_t)*a_host;
     if (qflag) {  // flags -> bits + popcount prefix (like the survivor slot bits)
@@ -2025,7 +2025,7 @@ DressOutcome merge_impl(DeviceStore& s, const Key<B>& P, size_t nQ, const ull* q
     k_pack_glob<<<1, 32, 0, st>>>(ctr, s.has_identity ? 1ull : 0ull);
     g_merge_red->sum_device(ctr + 8, 3);
   }
-  IQCC_CUDA(cudaMemcpyAsync(hc, ctr, (g_merge_red ? 11 : 8) * sizeof(ull), cudaMemcpyDeviceToHost, st));
+  d2h_small(hc, ctr, (g_merge_red ? 11 : 8) * sizeof(ull), st);
   host_sync(st);
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
@@ -2411,7 +2411,7 @@ void growth_split(DeviceStore& s, const uint64_t* gen_row, size_t* nc, size_t* n
     }
   }
   ull h[2];
-  IQCC_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  d2h_small(h, ctr, sizeof(h), st);
   host_sync(st);
   *na = h[0];
   *nc = h[1];
@@ -2557,7 +2557,7 @@ void sortless_stats(DeviceStore& s, const uint64_t* gen_row, size_t* n_buckets, 
     }
   }
   ull h[2];
-  IQCC_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  d2h_small(h, ctr, sizeof(h), st);
   host_sync(st);
   *n_buckets = h[0];
   *n_anti_buckets = h[1];

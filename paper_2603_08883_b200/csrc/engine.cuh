@@ -358,6 +358,14 @@ void host_sync(cudaStream_t st);
 /// Page-locked host scratch (>= 8 KiB) for small device->host reads, so the
 /// copies stay asynchronous; valid until the next call.
 void* host_pinned(size_t bytes);
+/// Small device->host read (<= 64 KiB) that does not go through a copy
+/// engine: a one-block kernel stores the bytes into the context's mapped
+/// page-locked buffer, and the next host_sync() copies them to dst.  Copy
+/// engines run their queues in order, so a 4-byte cudaMemcpy D2H of one
+/// context waits behind another context's multi-GB download; SM stores
+/// over PCIe do not.  Larger reads fall back to cudaMemcpyAsync.  dst must
+/// stay valid until that host_sync().
+void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st);
 /// A second, large page-locked buffer of the context (grows, reused): the
 /// staging of the host-side coefficient reformatting in upload/download.
 void* host_staging(size_t bytes);

@@ -173,8 +173,8 @@ void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const d
   }
   ull h[2];
   ull first_key[kMaxB * 2];
-  IQCC_CUDA(cudaMemcpyAsync(h, err, sizeof(h), cudaMemcpyDeviceToHost, st));
-  IQCC_CUDA(cudaMemcpyAsync(first_key, s.keys(), 2 * s.B * sizeof(ull), cudaMemcpyDeviceToHost, st));
+  d2h_small(h, err, sizeof(h), st);
+  d2h_small(first_key, s.keys(), 2 * s.B * sizeof(ull), st);
   host_sync(st);
   if (host_bad && (h[0] == ULLONG_MAX || host_bad < h[0])) h[0] = host_bad;
   if (h[0] != ULLONG_MAX)
@@ -267,7 +267,7 @@ static size_t run_compact(DeviceStore& s, int mode, uint32_t Bout, ull* okeys, d
     }
   }
   ull n = 0;
-  IQCC_CUDA(cudaMemcpyAsync(&n, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  d2h_small(&n, ctr, sizeof(ull), st);
   host_sync(st);
   return (size_t)n;
 }
@@ -441,7 +441,7 @@ void restrict_store(DeviceStore& s, size_t m, const size_t* bits, const size_t* 
     }
   }
   ull n = 0;
-  IQCC_CUDA(cudaMemcpyAsync(&n, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  d2h_small(&n, ctr, sizeof(ull), st);
   host_sync(st);
   std::swap(s.kbuf, ws.out_keys);
   std::swap(s.cbuf, ws.out_coef);
@@ -637,7 +637,7 @@ static void gen_impl(DeviceStore& s, size_t n, size_t N, uint64_t seed) {
                                                         tstat, reinterpret_cast<unsigned*>(ctr + 4), ctr);
   }
   ull m = 0;
-  IQCC_CUDA(cudaMemcpyAsync(&m, ctr, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  d2h_small(&m, ctr, sizeof(ull), st);
   host_sync(st);
   s.M = m;
   s.meta_valid = false;
@@ -1169,7 +1169,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
       }
     }
     ull* h = static_cast<ull*>(host_pinned(sizeof(ull)));
-    IQCC_CUDA(cudaMemcpyAsync(h, ctr + 1, sizeof(ull), cudaMemcpyDeviceToHost, st));
+    d2h_small(h, ctr + 1, sizeof(ull), st);
     host_sync(st);
     count_eps = (size_t)*h;
   }
@@ -1317,10 +1317,10 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
           IQCC_CUDA(cudaMemcpyAsync(gtie, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToDevice, st));
           red->sum_device(gtie, 1);
         }
-        IQCC_CUDA(cudaMemcpyAsync(hsp, sel, sizeof(SelState), cudaMemcpyDeviceToHost, st));
-        IQCC_CUDA(cudaMemcpyAsync(ntp, cnt + rounds, sizeof(ull), cudaMemcpyDeviceToHost, st));
-        if (red) IQCC_CUDA(cudaMemcpyAsync(ntp + 1, gtie, sizeof(ull), cudaMemcpyDeviceToHost, st));
-        IQCC_CUDA(cudaMemcpyAsync(ntp + 2, ties, spec * sizeof(ull), cudaMemcpyDeviceToHost, st));
+        d2h_small(hsp, sel, sizeof(SelState), st);
+        d2h_small(ntp, cnt + rounds, sizeof(ull), st);
+        if (red) d2h_small(ntp + 1, gtie, sizeof(ull), st);
+        d2h_small(ntp + 2, ties, spec * sizeof(ull), st);
         host_sync(st);
       };
       read_back();
@@ -1346,7 +1346,7 @@ CompressResult compress_store(DeviceStore& s, double eps, size_t max_terms, bool
         std::copy(ntp + 2, ntp + 2 + hs.ntie, th.begin());
       } else {
         ull* tp = static_cast<ull*>(host_pinned(hs.ntie * sizeof(ull)));
-        IQCC_CUDA(cudaMemcpyAsync(tp, ties, hs.ntie * sizeof(ull), cudaMemcpyDeviceToHost, st));
+        d2h_small(tp, ties, hs.ntie * sizeof(ull), st);
         host_sync(st);
         std::copy(tp, tp + hs.ntie, th.begin());
       }

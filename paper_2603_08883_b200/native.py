@@ -181,6 +181,20 @@ def init(device: int | None = None) -> None:
     _initialised_device = device
 
 
+def init_thread(device: int) -> None:
+    """Give the calling host thread its own engine context on `device` (its
+    own stream, scratch, block cache and page-locked staging; the C-ABI's
+    contexts are per host thread).  Calls from different threads then run
+    concurrently on the device: one call's uploads overlap another's
+    dressing and downloads.  Pair with finalize_thread()."""
+    check(lib.iqcc_gpu_init(device))
+
+
+def finalize_thread() -> None:
+    """Release the calling thread's engine context (device memory, caches)."""
+    check(lib.iqcc_gpu_finalize())
+
+
 def launch_count() -> int:
     return int(lib.iqcc_gpu_launch_count())
 
