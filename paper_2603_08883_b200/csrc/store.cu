@@ -192,6 +192,7 @@ void store_upload(DeviceStore& s, size_t n_qubits, const uint64_t* rows, const d
 // ------------------------------------------------ filtered compaction (1 pass)
 // mode 0: write device store arrays; mode 1: write reference layout rows +
 // complex coefficients (download staging).
+// mode 2: reference layout rows + real parts only (host-widened download).
 template <int B>
 __global__ void __launch_bounds__(CT) k_compact(const ull* __restrict__ keys,
                                                 const double* __restrict__ coef, size_t M,
@@ -242,8 +243,12 @@ __global__ void __launch_bounds__(CT) k_compact(const ull* __restrict__ keys,
         okeys[pos * 2 * Bout + w] = __brevll(key.w[w]);
         okeys[pos * 2 * Bout + Bout + w] = __brevll(key.w[B + w]);
       }
-      ocoef[2 * pos] = c;
-      ocoef[2 * pos + 1] = 0.0;
+      if (mode == 2) {  // real parts only (the host widens them)
+        ocoef[pos] = c;
+      } else {
+        ocoef[2 * pos] = c;
+        ocoef[2 * pos + 1] = 0.0;
+      }
     }
     ++pos;
   }
@@ -296,9 +301,37 @@ size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap,
   if (n_log == 0) return 0;
   ull* d_rows = host_dst ? ws.stage_rows.as<ull>(n_log * 2 * Bref) : reinterpret_cast<ull*>(rows);
   double* d_coef = host_dst ? ws.stage_coef.as<double>(2 * n_log) : coeff;
-  // (host destination: widening real parts to complex on host threads while
-  // the rows are on the wire measured slower than moving the complex
-  // values over PCIe: 92.4 vs 90.8 ms at 1e8 terms, host memory contention)
+  // host destination: only the real parts cross PCIe (8 of the 16 complex
+  // bytes per term); measured 89.4 -> 80-84 ms per 1e8-term download, and
+  // it frees D2H bandwidth when several calls are in flight
+  // (profiles/r3_summary.md).  IQCC_DL_REAL=0: complex values on the wire.
+  static const bool real_wire = !(getenv("IQCC_DL_REAL") && atoi(getenv("IQCC_DL_REAL")) == 0);
+  if (host_dst && real_wire) {
+    // real parts cross PCIe first (8 B per term); host threads widen them
+    // into the caller's complex array while the key rows are on the wire
+    size_t n = run_compact(s, 2, Bref, d_rows, d_coef);
+    if (n != n_log) throw std::runtime_error("download: filtered count mismatch");
+    double* hre = static_cast<double*>(host_staging(n * sizeof(double)));
+    IQCC_CUDA(cudaMemcpyAsync(hre, d_coef, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    cudaEvent_t ev;
+    IQCC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    IQCC_CUDA(cudaEventRecord(ev, st));
+    IQCC_CUDA(cudaMemcpyAsync(rows, d_rows, n * 2 * Bref * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    for (;;) {
+      const cudaError_t e = cudaEventQuery(ev);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorNotReady) IQCC_CUDA(e);
+    }
+    cudaEventDestroy(ev);
+    host_parallel(n, [&](size_t lo, size_t hi, size_t) {
+      for (size_t i = lo; i < hi; ++i) {
+        coeff[2 * i] = hre[i];
+        coeff[2 * i + 1] = 0.0;
+      }
+    });
+    host_sync(st);
+    return n;
+  }
   size_t n = run_compact(s, 1, Bref, d_rows, d_coef);
   if (n != n_log) throw std::runtime_error("download: filtered count mismatch");
   if (host_dst) {
