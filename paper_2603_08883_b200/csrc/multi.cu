@@ -62,7 +62,7 @@ struct NcclReducer : Reducer {
     std::memcpy(hp, vals, n * sizeof(ull));
     IQCC_CUDA(cudaMemcpyAsync(d, hp, n * sizeof(ull), cudaMemcpyHostToDevice, st));
     IQCC_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclSum, c.comm, st));
-    IQCC_CUDA(cudaMemcpyAsync(hp, d, n * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    d2h_small(hp, d, n * sizeof(ull), st);
     host_sync(st);
     std::memcpy(vals, hp, n * sizeof(ull));
   }
@@ -99,7 +99,7 @@ struct NcclReducer : Reducer {
       IQCC_CUDA(cudaMemcpyAsync(dm, mine.data(), mine.size() * sizeof(ull), cudaMemcpyHostToDevice, st));
     IQCC_NCCL(ncclAllGather(dm, d, mx * W, ncclUint64, c.comm, st));
     std::vector<ull> padded((size_t)mx * W * c.world);
-    IQCC_CUDA(cudaMemcpyAsync(padded.data(), d, padded.size() * sizeof(ull), cudaMemcpyDeviceToHost, st));
+    d2h_small(padded.data(), d, padded.size() * sizeof(ull), st);
     host_sync(st);
     for (int r = 0; r < c.world; ++r)
       all.insert(all.end(), padded.begin() + (size_t)r * mx * W,
@@ -270,7 +270,7 @@ ull allreduce_host(ull v, ncclRedOp_t op) {
   *hp = v;
   IQCC_CUDA(cudaMemcpyAsync(d, hp, sizeof(ull), cudaMemcpyHostToDevice, st));
   IQCC_NCCL(ncclAllReduce(d, d, 1, ncclUint64, op, c.comm, st));
-  IQCC_CUDA(cudaMemcpyAsync(hp, d, sizeof(ull), cudaMemcpyDeviceToHost, st));
+  d2h_small(hp, d, sizeof(ull), st);
   host_sync(st);
   return *hp;
 }
@@ -324,7 +324,7 @@ void p2p_prepare(size_t need, size_t W) {
     std::memcpy(hp, &h, 64);
     IQCC_CUDA(cudaMemcpyAsync(d + 8 * c.world, hp, 64, cudaMemcpyHostToDevice, st));
     IQCC_NCCL(ncclAllGather(d + 8 * c.world, d, 8, ncclUint64, c.comm, st));
-    IQCC_CUDA(cudaMemcpyAsync(hp, d, 64 * c.world, cudaMemcpyDeviceToHost, st));
+    d2h_small(hp, d, 64 * c.world, st);
     host_sync(st);
     std::memcpy(all.data(), hp, 64 * c.world);
   }
@@ -503,13 +503,13 @@ void parallel_dress_step(DeviceStore& s, size_t m, const size_t* bits, const siz
     if (chunked) {
       k_chunk_bounds<<<1, 32, 0, st>>>(cnt, cnt + S, s.keys(), s.M, (int)W, C, hbd);
       ull* hp = static_cast<ull*>(host_pinned((3 * (size_t)C - 1) * sizeof(ull)));
-      IQCC_CUDA(cudaMemcpyAsync(hp, hbd, (3 * (size_t)C - 1) * sizeof(ull), cudaMemcpyDeviceToHost, st));
+      d2h_small(hp, hbd, (3 * (size_t)C - 1) * sizeof(ull), st);
       host_sync(st);
       std::copy(hp, hp + 3 * C - 1, hb.begin());
     } else {
       ull* hp = static_cast<ull*>(host_pinned(2 * sizeof(ull)));
-      IQCC_CUDA(cudaMemcpyAsync(hp, cnt, sizeof(ull), cudaMemcpyDeviceToHost, st));
-      IQCC_CUDA(cudaMemcpyAsync(hp + 1, cnt + S, sizeof(ull), cudaMemcpyDeviceToHost, st));
+      d2h_small(hp, cnt, sizeof(ull), st);
+      d2h_small(hp + 1, cnt + S, sizeof(ull), st);
       host_sync(st);
       hb[0] = hp[0];
       hb[1] = hp[1];  // (chunked layout: hb[C])
@@ -725,7 +725,7 @@ double parallel_expect_store(DeviceStore& s, const double* factors) {
   IQCC_CUDA(cudaMemcpyAsync(d + c.world, &local, sizeof(double), cudaMemcpyHostToDevice, st));
   IQCC_NCCL(ncclAllGather(d + c.world, d, 1, ncclFloat64, c.comm, st));
   std::vector<double> parts(c.world);
-  IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, c.world * sizeof(double), cudaMemcpyDeviceToHost, st));
+  d2h_small(parts.data(), d, c.world * sizeof(double), st);
   host_sync(st);
   double e = 0.0;
   for (double v : parts) e += v;  // worker order (reduce_scalar)
@@ -740,7 +740,7 @@ static std::vector<double> allgather_doubles(const double* local, size_t n) {
   IQCC_CUDA(cudaMemcpyAsync(d + c.world * n, local, n * sizeof(double), cudaMemcpyHostToDevice, st));
   IQCC_NCCL(ncclAllGather(d + c.world * n, d, n, ncclFloat64, c.comm, st));
   std::vector<double> parts(c.world * n);
-  IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  d2h_small(parts.data(), d, parts.size() * sizeof(double), st);
   host_sync(st);
   return parts;
 }
@@ -804,7 +804,7 @@ void parallel_poly_kernels_store(DeviceStore& s, const double* factors, bool pol
   IQCC_CUDA(cudaMemcpyAsync(d + c.world * n, local.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
   IQCC_NCCL(ncclAllGather(d + c.world * n, d, n, ncclFloat64, c.comm, st));
   std::vector<double> parts(c.world * n);
-  IQCC_CUDA(cudaMemcpyAsync(parts.data(), d, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  d2h_small(parts.data(), d, parts.size() * sizeof(double), st);
   host_sync(st);
   for (size_t i = 0; i < n; ++i) {
     double v = 0.0;
