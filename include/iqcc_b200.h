@@ -45,11 +45,17 @@ typedef struct iqcc_gpu_sum iqcc_gpu_sum;
 
 /* ---- engine ---------------------------------------------------------- */
 const char* iqcc_gpu_last_error(void);
-/* Binds the calling thread to `device` and creates the engine context. */
+/* Binds the calling thread to `device` and creates the engine context.
+ * Contexts are per host thread (own stream, scratch, block cache and
+ * page-locked staging); a handle is used from the thread that created it.
+ * Several threads, each with its own context, run their calls concurrently
+ * on one device (bench.py's e2e keeps three upload/dress/download calls in
+ * flight this way). */
 int iqcc_gpu_init(int device);
 /* Run all engine work on an existing cudaStream_t (e.g. torch's current
  * stream) instead of the engine's own; NULL restores the default. */
 int iqcc_gpu_set_stream(void* cuda_stream);
+/* Releases the calling thread's context (device memory, caches, staging). */
 int iqcc_gpu_finalize(void);
 /* Number of engine kernel launches so far (bench.py's gpu_launches). */
 uint64_t iqcc_gpu_launch_count(void);

@@ -806,9 +806,16 @@ int iqcc_gpu_dress_sequence(iqcc_gpu_sum* h, size_t K, const uint64_t* gens, con
                              floor_cut);
         }
         // a compress that cut sets the next guess; one that did not (every
-        // slotted term kept) leaves the last verified guess in place
+        // slotted term kept) hands on the verified floor theta
         const double sv = spec_theta(h->s.filt);
-        if (sv > 0.0) spec = h->s.spec_cut = sv;
+        if (sv > 0.0) {
+          spec = h->s.spec_cut = sv;
+        } else if (floor_cut > 0.0) {
+          // no cut: every live term holds a slot, so |c| >= theta is the
+          // store's verified floor (it decays by |cos| per uncut step; the
+          // last cut would overestimate it and fail the next guess)
+          spec = h->s.spec_cut = floor_cut;
+        }
         host_ms("host_compress", t1);
         if (stats) {
           stats->dropped_terms += r.dropped_terms;
@@ -1072,7 +1079,10 @@ int iqcc_gpu_parallel_dress_sequence(iqcc_gpu_sum* h, size_t m, const size_t* bi
                           exact, &failed);
       if (failed) spec = h->s.spec_cut = 0.0;
       const Filter& f = h->s.filt;
-      if (slots && f.active && f.has_v && f.v > 0.0 && std::isfinite(f.v)) spec = h->s.spec_cut = f.v;
+      if (slots && f.active && f.has_v && f.v > 0.0 && std::isfinite(f.v))
+        spec = h->s.spec_cut = f.v;
+      else if (slots && !failed && theta > exact)  // no cut: theta is the verified floor
+        spec = h->s.spec_cut = theta;
     }
     if (terms_in_total) *terms_in_total = parallel_sum(local_in);
   });
