@@ -556,7 +556,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-inflight", type=int, default=3,
                     help="public-API calls in flight for e2e (1: one call at a time only)")
-    ap.add_argument("--e2e-pipe-steps", type=int, default=3, help="e2e steps per in-flight call")
+    ap.add_argument("--e2e-pipe-steps", type=int, default=4, help="e2e steps per in-flight call")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

@@ -304,7 +304,7 @@ size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap,
   // host destination: only the real parts cross PCIe (8 of the 16 complex
   // bytes per term); measured 89.4 -> 80-84 ms per 1e8-term download, and
   // it frees D2H bandwidth when several calls are in flight
-  // (profiles/r3_summary.md).  IQCC_DL_REAL=0: complex values on the wire.
+  // (profiles/r2s2_summary.md).  IQCC_DL_REAL=0: complex values on the wire.
   static const bool real_wire = !(getenv("IQCC_DL_REAL") && atoi(getenv("IQCC_DL_REAL")) == 0);
   if (host_dst && real_wire) {
     // real parts cross PCIe first (8 B per term); host threads widen them
