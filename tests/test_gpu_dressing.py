@@ -435,3 +435,61 @@ def test_c5_shape_uncapped_growth_then_cap(eng, port):
     d.compress(1e-10, cap, cs)
     check_same(d.download(), want)
     assert cs.dropped_terms == st["dropped_terms"]
+
+
+def test_concurrent_contexts_match_checker(eng, port):
+    """bench.py's e2e path: several host threads, each with its own engine
+    context (native.init_thread), upload / dress_sequence / download at the
+    same time on one device (small readbacks through mapped memory, the
+    real-part download); every thread's result equals the checker's."""
+    import threading
+    from paper_2603_08883_b200 import native
+    n, terms, eps, cap = 124, 60_000, 1e-8, 50_000
+    jobs = []
+    for t in range(3):
+        h = port.gen_mol(n, terms, 40 + t)
+        rs = np.random.default_rng(90 + t)
+        B = (n + 63) // 64
+        ps, taus = [], []
+        for _ in range(4):
+            w = int(rs.integers(2, 5))
+            qs, ys = rs.choice(n, w, replace=False), rs.integers(0, 2, w)
+            if ys.sum() % 2 == 0:
+                ys[-1] ^= 1
+            p = eng.PauliWord(n)
+            for q, y in zip(qs, ys):
+                p.row[q // 64] |= np.uint64(1 << int(q % 64))
+                if y:
+                    p.row[B + q // 64] |= np.uint64(1 << int(q % 64))
+            ps.append(p)
+            taus.append(float(rs.uniform(-0.3, 0.3)))
+        want, _ = port.dress_sequence(h, np.stack([p.row for p in ps]), taus, eps, cap)
+        jobs.append((host(eng, h), eng.Ansatz(ps, taus), want))
+    got, errs = [None] * len(jobs), []
+    start = threading.Barrier(len(jobs))
+
+    def run(i):
+        try:
+            native.init_thread(0)
+            try:
+                hh, ans, _ = jobs[i]
+                start.wait()
+                for _ in range(2):  # the second round reuses the context's caches
+                    d = eng.DeviceSum.upload(hh)
+                    d.dress_sequence(ans, eps, cap)
+                    got[i] = d.download()
+                    del d
+            finally:
+                native.finalize_thread()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            errs.append(e)
+            start.abort()
+
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for g, (_, _, want) in zip(got, jobs):
+        check_same(g, want)
