@@ -78,6 +78,7 @@ struct Ctx {
 };
 
 static thread_local Ctx* g_ctx = nullptr;
+static Ctx* g_comm_ctx = nullptr;  // the context that initialised the NCCL communicator
 static thread_local std::string g_err;
 static std::atomic<uint64_t> g_launches{0};  // every engine kernel launch, all contexts
 
@@ -549,7 +550,12 @@ int iqcc_gpu_finalize(void) {
   return guarded([&] {
     if (!g_ctx) return;
     cudaStreamSynchronize(g_ctx->cur);
-    multi_shutdown();
+    // the process-wide communicator goes with the context that created it
+    // (a worker thread's context finalizing leaves it alone)
+    if (g_comm_ctx == g_ctx) {
+      multi_shutdown();
+      g_comm_ctx = nullptr;
+    }
     ctx_free(g_ctx);
     g_ctx = nullptr;
   });
@@ -1006,11 +1012,15 @@ int iqcc_gpu_comm_init(const void* uid, int rank, int world) {
   return guarded([&] {
     ctx();
     multi_init(uid, rank, world);
+    g_comm_ctx = g_ctx;
   });
 }
 
 int iqcc_gpu_comm_destroy(void) {
-  return guarded([&] { multi_shutdown(); });
+  return guarded([&] {
+    multi_shutdown();
+    g_comm_ctx = nullptr;
+  });
 }
 
 int iqcc_gpu_parallel_dress(iqcc_gpu_sum* h, size_t m, const size_t* bits, const size_t* owner,
