@@ -16,7 +16,9 @@ step (the reference's dress_single input size).
            the dressed sum, every step; --e2e-inflight (default 3) calls in
            flight from as many host threads (one engine context each), so
            one call's H2D overlaps others' dressing and D2H; the one-call-
-           at-a-time figure is kept under e2e.sequential
+           at-a-time figure is kept under e2e.sequential; at N > 1 every
+           rank uploads / dresses (partitioned) / downloads its shard, one
+           call at a time, max over ranks
   roofline the merge kernel (dominant) against MEASURED_PEAKS.json hbm_gbs,
            algorithmic bytes (M_in + M_out) * (16 B + 8) per launch
   cpu_baseline  the UNMODIFIED reference (oracle/_ref, parallel_dress kThreaded)
