@@ -493,3 +493,32 @@ def test_concurrent_contexts_match_checker(eng, port):
     assert not errs, errs
     for g, (_, _, want) in zip(got, jobs):
         check_same(g, want)
+
+
+def test_download_complex_wire_matches():
+    """IQCC_DL_REAL=0 (complex coefficients on the download wire instead of
+    real parts widened on the host) gives the same downloaded sum as the
+    default, after a dressing sequence (124 and 200 qubits)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import hashlib, sys, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2603_08883_b200 import iqcc, native\n"
+        "native.init(0)\n"
+        "out = []\n"
+        "for n in (124, 200):\n"
+        "    d = iqcc.DeviceSum.generate_mol(n, 300000, 3)\n"
+        "    p = iqcc.PauliWord(n); p.row[0] |= np.uint64(0b1011)\n"
+        "    p.row[(n + 63) // 64] |= np.uint64(0b0010)\n"
+        "    d.dress_sequence(iqcc.Ansatz([p], [0.17]), 1e-9, 350000)\n"
+        "    h = d.download()\n"
+        "    assert np.all(h.coeffs.imag == 0.0)\n"
+        "    out.append(hashlib.sha256(h.rows.tobytes() + h.coeffs.tobytes()).hexdigest())\n"
+        "print('DIGEST', ' '.join(out))\n" % root)
+    dig = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=600,
+                           cwd=root, env=dict(os.environ, IQCC_DL_REAL=v))
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        dig.append([ln for ln in r.stdout.splitlines() if ln.startswith("DIGEST")][-1])
+    assert dig[0] == dig[1]
