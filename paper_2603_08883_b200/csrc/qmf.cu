@@ -858,6 +858,146 @@ __global__ void __launch_bounds__(256) k_dis_nib(const ull* __restrict__ keys, c
   if (cid < K) g_part[blockIdx.y * K + cid] = g;
 }
 
+// The generic-Omega gradient by factor ratios (default when no factor of
+// Omega is zero).  T^P differs from T only in the nibble groups P touches
+// (a DIS candidate touches at most 4), so
+//   <omega|T^P|omega> = E_T * prod_{g in G(P)} f_g((T^P)_g) / f_g(T_g),
+// with E_T = prod_g f_g(T_g) and the reciprocals 1/f_g(T_g) computed once
+// per staged term and shared by the block's 256 candidates: about 2|G(P)|
+// table reads and multiplies per anticommuting pair instead of n/4.  A term
+// whose E_T could lose precision (|E_T| < 1e-280) or a candidate touching
+// more than 4 groups takes the full nibble product.  Rounding differs from
+// expect_word's ascending product by a few ulps per term (the gradient is
+// specified to 1e-10; tests pin 1e-13).
+constexpr int kRatioTT = 128;  // staged terms per tile
+template <int B>
+__global__ void __launch_bounds__(256) k_dis_ratio(const ull* __restrict__ keys, const double* __restrict__ coef,
+                                                   size_t M, Filter filt, const double* __restrict__ tab_g, int ng,
+                                                   const ull* __restrict__ cands, size_t K,
+                                                   double* __restrict__ g_part) {
+  constexpr int TT = kRatioTT;
+  extern __shared__ double smd[];
+  double* tab = smd;                     // [ng][256]
+  double* rinv = tab + (size_t)ng * 256;  // [TT][ng]
+  double* te = rinv + (size_t)TT * ng;    // [TT]
+  double* tc = te + TT;                   // [TT]
+  ull* tk = reinterpret_cast<ull*>(tc + TT);  // [TT][2B]
+  int* tslow = reinterpret_cast<int*>(tk + (size_t)TT * 2 * B);  // [TT]
+  unsigned char* tcode = reinterpret_cast<unsigned char*>(tslow + TT);  // [TT][ng] group codes of T
+  for (int i = threadIdx.x; i < ng * 256; i += blockDim.x) tab[i] = tab_g[i];
+  const size_t cid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t per = ((M + gridDim.y - 1) / gridDim.y + TT - 1) / TT * TT;
+  const size_t lo = blockIdx.y * per, hi = min(M, lo + per);
+  Key<B> P;
+#pragma unroll
+  for (int w = 0; w < 2 * B; ++w) P.w[w] = 0;
+  if (cid < K) P = load_key<B>(cands, cid);
+  // the candidate's touched groups: (group, word, shift, code) packed
+  unsigned e[4] = {0u, 0u, 0u, 0u};
+  int mg = 0;
+#pragma unroll
+  for (int w = 0; w < B; ++w)
+#pragma unroll
+    for (int h = 1; h >= 0; --h)
+#pragma unroll
+      for (int nn = 7; nn >= 0; --nn) {
+        const int q = 16 * w + 8 * (1 - h) + (7 - nn);
+        const int sh = 32 * h + 4 * nn;
+        const unsigned code = (unsigned)(((P.w[B + w] >> sh) & 15u) | (((P.w[w] >> sh) & 15u) << 4));
+        if (q < ng && code) {
+          const unsigned ent = (unsigned)q | ((unsigned)w << 6) | ((unsigned)sh << 8) | (code << 16);
+          if (mg == 0) e[0] = ent;
+          else if (mg == 1) e[1] = ent;
+          else if (mg == 2) e[2] = ent;
+          else if (mg == 3) e[3] = ent;
+          ++mg;
+        }
+      }
+  const bool general = mg > 4;
+  double g = 0.0;
+  for (size_t base = lo; base < hi; base += TT) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < TT; i += blockDim.x) {
+      const size_t ti = base + i;
+      Key<B> k;
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) k.w[w] = 0;
+      double c = 0.0;
+      if (ti < hi) {
+        k = load_key<B>(keys, ti);
+        c = coef[ti];
+        if (!filter_keep(filt, ti, c, ti == 0 && key_is_identity<B>(k))) c = 0.0;
+      }
+      double E = 1.0;
+#pragma unroll
+      for (int w = 0; w < B; ++w)
+#pragma unroll
+        for (int h = 1; h >= 0; --h)
+#pragma unroll
+          for (int nn = 7; nn >= 0; --nn) {
+            const int q = 16 * w + 8 * (1 - h) + (7 - nn);
+            if (q < ng) {
+              const int sh = 32 * h + 4 * nn;
+              const unsigned co = (unsigned)(((k.w[B + w] >> sh) & 15u) | (((k.w[w] >> sh) & 15u) << 4));
+              const double f = tab[q * 256 + (int)co];
+              E = __dmul_rn(E, f);
+              rinv[(size_t)i * ng + q] = __drcp_rn(f);
+              tcode[(size_t)i * ng + q] = (unsigned char)co;
+            }
+          }
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) tk[(size_t)i * 2 * B + w] = k.w[w];
+      tc[i] = c;
+      te[i] = E;
+      tslow[i] = !(fabs(E) >= 1e-280);
+    }
+    __syncthreads();
+    const int n = (int)min((size_t)TT, hi - base);
+    for (int j = 0; j < n; ++j) {
+      const ull* kj = tk + (size_t)j * 2 * B;
+      const double c = tc[j];
+      Key<B> k;
+#pragma unroll
+      for (int w = 0; w < 2 * B; ++w) k.w[w] = kj[w];
+      const bool anti = cid < K && c != 0.0 && anticommutes<B>(k, P);
+      if (!anti) continue;
+      double val;
+      if (general || tslow[j]) {  // full nibble product of T^P
+        val = 1.0;
+#pragma unroll
+        for (int w = 0; w < B; ++w)
+#pragma unroll
+          for (int h = 1; h >= 0; --h)
+#pragma unroll
+            for (int nn = 7; nn >= 0; --nn) {
+              const int q = 16 * w + 8 * (1 - h) + (7 - nn);
+              if (q < ng) {
+                const int sh = 32 * h + 4 * nn;
+                const ull xw = k.w[w] ^ P.w[w], zw = k.w[B + w] ^ P.w[B + w];
+                val = __dmul_rn(val, tab[q * 256 + (int)(((zw >> sh) & 15u) | (((xw >> sh) & 15u) << 4))]);
+              }
+            }
+      } else {
+        val = te[j];
+        const double* rj = rinv + (size_t)j * ng;
+        const unsigned char* cj = tcode + (size_t)j * ng;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          if (m < mg) {
+            const unsigned ent = e[m];
+            const int q = (int)(ent & 63u);
+            const unsigned co = cj[q];
+            val = __dmul_rn(__dmul_rn(val, tab[q * 256 + (int)(co ^ (ent >> 16))]), rj[q]);
+          }
+        }
+      }
+      const double im = product_phase<B>(k, P) == 1 ? c : -c;
+      g = __dadd_rn(g, __dmul_rn(im, val));
+    }
+  }
+  if (cid < K) g_part[blockIdx.y * K + cid] = g;
+}
+
 /// g[k] = the slices' partial sums in slice order.
 __global__ void k_dis_fold(const double* __restrict__ g_part, size_t K, int S, double* __restrict__ g) {
   const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
@@ -954,6 +1094,14 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
     double* gpart = f4d + f4.size();
     IQCC_CUDA(cudaMemcpyAsync(f4d, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
     const char* ex = getenv("IQCC_DIS_EXACT");
+    const char* nib_env = getenv("IQCC_DIS_NIB");
+    const int ngr = std::max(1, (nq + 3) / 4);
+    const size_t smem_ratio = ((size_t)ngr * 256 + (size_t)kRatioTT * ngr + 2 * (size_t)kRatioTT) * sizeof(double) +
+                              (size_t)kRatioTT * 2 * B * sizeof(ull) + (size_t)kRatioTT * sizeof(int) +
+                              (size_t)kRatioTT * ngr;
+    bool zero_factor = false;  // a zero factor makes the ratios undefined
+    for (size_t i = 0; i < f4.size(); ++i) zero_factor = zero_factor || f4[i] == 0.0;
+    const bool ratio = !(nib_env && atoi(nib_env)) && !zero_factor && smem_ratio <= (size_t)220 * 1024;
     if (exact || (ex && atoi(ex))) {
       KernelScope ks("dis_gradient");
       k_dis_full<B><<<(unsigned)((K + 127) / 128), 128, 0, st>>>(s.keys(), s.coef(), s.M, s.filt, f4d, dc,
@@ -964,6 +1112,17 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
       double* nibt = ws.misc2.as<double>((size_t)ng * 256);
       k_nibble_table<<<(unsigned)((ng * 256 + 255) / 256), 256, 0, st>>>(f4d, ng, nibt);
       const size_t smem = (size_t)ng * 256 * sizeof(double);
+      if (ratio) {
+        if (func_attr_once((const void*)k_dis_ratio<B>, ctx_device(ctx_current())))
+          IQCC_CUDA(cudaFuncSetAttribute(k_dis_ratio<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024));
+        KernelScope ks("dis_gradient");
+        k_dis_ratio<B><<<dim3(cb, (unsigned)S), 256, smem_ratio, st>>>(s.keys(), s.coef(), s.M, s.filt, nibt, ng,
+                                                                       dc, K, gpart);
+        k_dis_fold<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(gpart, K, S, dg);
+        count_launch("dis_gradient");
+        count_launch("dis_gradient");
+      } else {
       if (func_attr_once((const void*)k_dis_nib<B>, ctx_device(ctx_current())))
         IQCC_CUDA(cudaFuncSetAttribute(k_dis_nib<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(16 * B * 256 * sizeof(double))));
@@ -973,6 +1132,7 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
       k_dis_fold<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(gpart, K, S, dg);
       count_launch("dis_gradient");
       count_launch("dis_gradient");
+      }
     }
   }
   IQCC_CUDA(cudaMemcpyAsync(g, dg, K * sizeof(double), cudaMemcpyDeviceToHost, st));

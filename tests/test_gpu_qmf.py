@@ -150,9 +150,9 @@ def test_gradient_known_answer(eng):  # test_dis.cpp:108-114
 
 @pytest.mark.parametrize("n", [5, 64, 124, 200])
 def test_gradient_bit_exact(eng, port, monkeypatch, n):
-    """DIS gradients at a generic Omega: the nibble-table kernel (default)
-    within 1e-13 of the reference, the ascending-qubit kernel
-    (IQCC_DIS_EXACT=1) bit for bit."""
+    """DIS gradients at a generic Omega: the factor-ratio kernel (default)
+    and the nibble-table kernel (IQCC_DIS_NIB=1) within 1e-13 of the
+    reference, the ascending-qubit kernel (IQCC_DIS_EXACT=1) bit for bit."""
     rng = port.rng(419 + n)
     h = rng.sum(n, 2000)
     th, ph = rng.qmf(n)
@@ -161,6 +161,10 @@ def test_gradient_bit_exact(eng, port, monkeypatch, n):
     want = np.array([port.gradient(h, th, ph, c) for c in cands])
     g = d.gradients(eng.QmfState(th, ph), cands)
     assert np.abs(g - want).max() <= 1e-13 * max(1.0, np.abs(want).max())
+    monkeypatch.setenv("IQCC_DIS_NIB", "1")
+    g = d.gradients(eng.QmfState(th, ph), cands)
+    assert np.abs(g - want).max() <= 1e-13 * max(1.0, np.abs(want).max())
+    monkeypatch.delenv("IQCC_DIS_NIB")
     monkeypatch.setenv("IQCC_DIS_EXACT", "1")
     g = d.gradients(eng.QmfState(th, ph), cands)
     for k in range(len(cands)):
@@ -385,7 +389,7 @@ def test_c4_shape_gradients_bit_exact(eng, port, monkeypatch):
     th, ph = rs.uniform(-3, 3, n), rs.uniform(-3, 3, n)
     sel = [0, 1, 9, 17, 40, 63]
     want = {k: port.gradient(h, th, ph, cands[k]) for k in sel}
-    g = d.gradients(eng.QmfState(th, ph), cands)  # nibble tables (default)
+    g = d.gradients(eng.QmfState(th, ph), cands)  # factor ratios (default)
     for k in sel:
         assert abs(g[k] - want[k]) <= 1e-13 * max(1.0, abs(want[k])), k
     monkeypatch.setenv("IQCC_DIS_EXACT", "1")  # ascending-qubit products: bit-exact
