@@ -869,7 +869,10 @@ __global__ void __launch_bounds__(256) k_dis_nib(const ull* __restrict__ keys, c
 // more than 4 groups takes the full nibble product.  Rounding differs from
 // expect_word's ascending product by a few ulps per term (the gradient is
 // specified to 1e-10; tests pin 1e-13).
-constexpr int kRatioTT = 128;  // staged terms per tile
+#ifndef IQCC_RATIO_TT
+#define IQCC_RATIO_TT 64
+#endif
+constexpr int kRatioTT = IQCC_RATIO_TT;  // staged terms per tile
 template <int B>
 __global__ void __launch_bounds__(256) k_dis_ratio(const ull* __restrict__ keys, const double* __restrict__ coef,
                                                    size_t M, Filter filt, const double* __restrict__ tab_g, int ng,
