@@ -863,18 +863,21 @@ __global__ void __launch_bounds__(256) k_dis_nib(const ull* __restrict__ keys, c
 // (a DIS candidate touches at most 4), so
 //   <omega|T^P|omega> = E_T * prod_{g in G(P)} f_g((T^P)_g) / f_g(T_g),
 // with E_T = prod_g f_g(T_g) and the reciprocals 1/f_g(T_g) computed once
-// per staged term and shared by the block's 256 candidates: about 2|G(P)|
+// per staged term and shared by the block's candidates: about 2|G(P)|
 // table reads and multiplies per anticommuting pair instead of n/4.  A term
 // whose E_T could lose precision (|E_T| < 1e-280) or a candidate touching
 // more than 4 groups takes the full nibble product.  Rounding differs from
 // expect_word's ascending product by a few ulps per term (the gradient is
 // specified to 1e-10; tests pin 1e-13).
-#ifndef IQCC_RATIO_TT
-#define IQCC_RATIO_TT 64
-#endif
-constexpr int kRatioTT = IQCC_RATIO_TT;  // staged terms per tile
+// 128 staged terms per tile; 1024 candidates (threads) per block share the
+// staged E_T / reciprocals and the tables (512 at 200-256 qubits, whose
+// wider rows need more than 64 registers).  Measured on C4 (100 qubits):
+// 256 threads x 64 / 128 / 256 terms 8.0 / 10.2 / 19.1 s, 512 x 64 6.3 s,
+// 1024 x 32 / 64 / 128 6.1 / 5.8 / 5.6 s (profiles/r2s2_summary.md).
+constexpr int kRatioTT = 128;
+__host__ __device__ constexpr int ratio_nt(int B) { return B >= 4 ? 512 : 1024; }
 template <int B>
-__global__ void __launch_bounds__(256) k_dis_ratio(const ull* __restrict__ keys, const double* __restrict__ coef,
+__global__ void __launch_bounds__(ratio_nt(B)) k_dis_ratio(const ull* __restrict__ keys, const double* __restrict__ coef,
                                                    size_t M, Filter filt, const double* __restrict__ tab_g, int ng,
                                                    const ull* __restrict__ cands, size_t K,
                                                    double* __restrict__ g_part) {
@@ -1093,7 +1096,7 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
     // (the table limits a SM to a few resident blocks); partials after f4
     const unsigned cb = (unsigned)((K + 255) / 256);
     const int S = (int)std::max<size_t>(1, std::min<size_t>({8, (148 * 4 + cb - 1) / cb, (s.M + 4095) / 4096}));
-    double* f4d = ws.grad_part.as<double>(f4.size() + (size_t)S * K);
+    double* f4d = ws.grad_part.as<double>(f4.size() + (size_t)8 * K);  // slices <= 8 on every path
     double* gpart = f4d + f4.size();
     IQCC_CUDA(cudaMemcpyAsync(f4d, f4.data(), f4.size() * sizeof(double), cudaMemcpyHostToDevice, st));
     const char* ex = getenv("IQCC_DIS_EXACT");
@@ -1120,9 +1123,12 @@ static void gradients_impl(DeviceStore& s, const double* factors, const uint64_t
           IQCC_CUDA(cudaFuncSetAttribute(k_dis_ratio<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024));
         KernelScope ks("dis_gradient");
-        k_dis_ratio<B><<<dim3(cb, (unsigned)S), 256, smem_ratio, st>>>(s.keys(), s.coef(), s.M, s.filt, nibt, ng,
-                                                                       dc, K, gpart);
-        k_dis_fold<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(gpart, K, S, dg);
+        constexpr int kRatioNT = ratio_nt(B);
+        const unsigned cbr = (unsigned)((K + kRatioNT - 1) / kRatioNT);
+        const int Sr = (int)std::max<size_t>(1, std::min<size_t>({8, (148 * 4 + cbr - 1) / cbr, (s.M + 4095) / 4096}));
+        k_dis_ratio<B><<<dim3(cbr, (unsigned)Sr), kRatioNT, smem_ratio, st>>>(s.keys(), s.coef(), s.M, s.filt, nibt,
+                                                                              ng, dc, K, gpart);
+        k_dis_fold<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(gpart, K, Sr, dg);
         count_launch("dis_gradient");
         count_launch("dis_gradient");
       } else {
