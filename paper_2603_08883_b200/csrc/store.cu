@@ -313,16 +313,20 @@ size_t store_download(DeviceStore& s, uint64_t* rows, double* coeff, size_t cap,
     if (n != n_log) throw std::runtime_error("download: filtered count mismatch");
     double* hre = static_cast<double*>(host_staging(n * sizeof(double)));
     IQCC_CUDA(cudaMemcpyAsync(hre, d_coef, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    cudaEvent_t ev;
-    IQCC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    IQCC_CUDA(cudaEventRecord(ev, st));
+    struct Ev {  // destroyed on every exit path
+      cudaEvent_t e = nullptr;
+      ~Ev() {
+        if (e) cudaEventDestroy(e);
+      }
+    } ev;
+    IQCC_CUDA(cudaEventCreateWithFlags(&ev.e, cudaEventDisableTiming));
+    IQCC_CUDA(cudaEventRecord(ev.e, st));
     IQCC_CUDA(cudaMemcpyAsync(rows, d_rows, n * 2 * Bref * sizeof(ull), cudaMemcpyDeviceToHost, st));
-    for (;;) {
-      const cudaError_t e = cudaEventQuery(ev);
+    for (;;) {  // the real parts have landed: widen them while the rows move
+      const cudaError_t e = cudaEventQuery(ev.e);
       if (e == cudaSuccess) break;
       if (e != cudaErrorNotReady) IQCC_CUDA(e);
     }
-    cudaEventDestroy(ev);
     host_parallel(n, [&](size_t lo, size_t hi, size_t) {
       for (size_t i = lo; i < hi; ++i) {
         coeff[2 * i] = hre[i];
