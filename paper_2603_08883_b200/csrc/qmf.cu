@@ -736,30 +736,49 @@ __global__ void __launch_bounds__(128) k_dis_full(const ull* __restrict__ keys,
     }
     __syncthreads();
     const int n = (int)min((size_t)TT, M - base);
-    for (int j = 0; j < n; ++j) {
-      Key<B> k;
+    // two terms per iteration: their products walk the union of both
+    // supports (and U) in ascending order, a term multiplying by the exact
+    // 1.0 of code 0 where it has no letter, so each chain is the
+    // single-term chain (bit-identical) and the two run side by side; the
+    // sum still adds term j before term j + 1
+    for (int j = 0; j < n; j += 2) {
+      Key<B> k[2];
+      double c[2];
+      bool anti[2], any[2];
 #pragma unroll
-      for (int w = 0; w < 2 * B; ++w) k.w[w] = tk[(size_t)j * 2 * B + w];
-      const double c = tc[j];
-      const bool anti = cid < K && c != 0.0 && anticommutes<B>(k, P);
-      if (!__any_sync(0xffffffffu, anti)) continue;  // warp-uniform
-      const Key<B> kp = key_xor<B>(k, P);
-      double val = 1.0;
+      for (int t = 0; t < 2; ++t) {
+        const int jj = min(j + t, n - 1);
+#pragma unroll
+        for (int w = 0; w < 2 * B; ++w) k[t].w[w] = tk[(size_t)jj * 2 * B + w];
+        c[t] = j + t < n ? tc[jj] : 0.0;
+        anti[t] = cid < K && c[t] != 0.0 && anticommutes<B>(k[t], P);
+        any[t] = __any_sync(0xffffffffu, anti[t]);  // warp-uniform
+      }
+      if (!any[0] && !any[1]) continue;
+      const Key<B> kp0 = key_xor<B>(k[0], P), kp1 = key_xor<B>(k[1], P);
+      double v0 = 1.0, v1 = 1.0;
 #pragma unroll
       for (int w = 0; w < B; ++w) {
-        ull s = k.w[w] | k.w[B + w] | up[w];
+        ull s = (any[0] ? k[0].w[w] | k[0].w[B + w] : 0ull) | (any[1] ? k[1].w[w] | k[1].w[B + w] : 0ull) | up[w];
         while (s) {
           const int lz = __clzll((long long)s);
           const int bit = 63 - lz;
-          const unsigned code =
-              (unsigned)((kp.w[w] >> bit) & 1ull) | ((unsigned)((kp.w[B + w] >> bit) & 1ull) << 1);
-          val = __dmul_rn(val, f4[4 * (64 * w + lz) + code]);
+          const unsigned c0 =
+              (unsigned)((kp0.w[w] >> bit) & 1ull) | ((unsigned)((kp0.w[B + w] >> bit) & 1ull) << 1);
+          const unsigned c1 =
+              (unsigned)((kp1.w[w] >> bit) & 1ull) | ((unsigned)((kp1.w[B + w] >> bit) & 1ull) << 1);
+          v0 = __dmul_rn(v0, f4[4 * (64 * w + lz) + c0]);
+          v1 = __dmul_rn(v1, f4[4 * (64 * w + lz) + c1]);
           s &= ~(1ull << bit);
         }
       }
-      if (anti) {
-        const double im = product_phase<B>(k, P) == 1 ? c : -c;
-        g = __dadd_rn(g, __dmul_rn(im, val));
+      if (anti[0]) {
+        const double im = product_phase<B>(k[0], P) == 1 ? c[0] : -c[0];
+        g = __dadd_rn(g, __dmul_rn(im, v0));
+      }
+      if (anti[1]) {
+        const double im = product_phase<B>(k[1], P) == 1 ? c[1] : -c[1];
+        g = __dadd_rn(g, __dmul_rn(im, v1));
       }
     }
   }
